@@ -1,0 +1,443 @@
+"""bench.py -- headline benchmark of the JACC B200 hot path.
+
+Workload (BASELINE.json configs[1]): Jacobi-2D fp64 16384 x 16384, 100
+timesteps = 200 `parallel loop` launches per step, owned row blocks over N
+devices with HALO (boundary-row dirty-range) merge.  Metric: algorithmic
+loop GB/s (8 B read per src element + 8 B written per interior dst element
+per launch), whole job.  Inputs (2 x 2 GiB) are far larger than L2, so no
+explicit flush is needed between timed iterations.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl jacc|reference]
+
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (the
+only reference this tier has) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GRID = 16384
+TSTEPS = 100
+METRIC = "loop GB/s (Jacobi-2D fp64 16384^2, 100 timesteps, HALO merge)"
+UNIT = "GB/s"
+
+
+def algo_bytes_per_sweep(N, n):
+    """Algorithmic HBM bytes of one Jacobi launch summed over devices: each
+    device reads its owned rows plus one halo row each side (8 B/element)
+    and writes its interior elements (8 B/element)."""
+    tot = 0
+    for d in range(n):
+        q, r = divmod(N, n)
+        lo = d * q + min(d, r)
+        hi = (d + 1) * q + min(d + 1, r)
+        i0, i1 = max(lo, 1), min(hi, N - 1)
+        if i1 <= i0:
+            continue
+        tot += 8 * N * (i1 - i0 + 2) + 8 * (i1 - i0) * (N - 2)
+    return tot
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(kernel="jacobi2d"):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")), reverse=True):
+        try:
+            with open(p) as f:
+                j = json.load(f)
+            k = j.get("kernels", {}).get(kernel)
+            if k and k.get("dram_bytes_per_launch"):
+                return float(k["dram_bytes_per_launch"]), os.path.basename(p)
+        except Exception:
+            pass
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for s in self.samples:
+            try:
+                util = float(s[6])
+                if util > 50:
+                    sm.append(float(s[0]))
+                mx = float(s[1])
+            except ValueError:
+                continue
+            for k, name in enumerate(names):
+                if s[2 + k].lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+# reference arm / cpu baseline: the CPU oracle on a bounded sample
+# ----------------------------------------------------------------------------
+def oracle_sample(sweeps):
+    """Time `sweeps` oracle launches of the J16K sweep on the full 16384^2
+    grid (single thread).  Returns (GB/s algorithmic, seconds, sample text)."""
+    import __graft_entry__ as ge
+    ge.build_oracle()
+    ge.build_synth()
+    import oracle as orc
+    import synth
+    A, B = synth.polybench_jacobi2d(N_GRID)
+    t0 = time.perf_counter()
+    src, dst = A, B
+    for _ in range(sweeps):
+        orc.jacobi2d_sweep(src, dst)
+        src, dst = dst, src
+    dt = time.perf_counter() - t0
+    gbs = sweeps * algo_bytes_per_sweep(N_GRID, 1) / dt / 1e9
+    return gbs, dt, f"{sweeps} oracle sweeps of the 16384^2 grid (of 200 per step), 1 thread"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sweeps = 2
+    for _ in range(args.warmup):
+        oracle_sample(1)
+    vals, times = [], []
+    for _ in range(args.steps):
+        g, dt, sample = oracle_sample(sweeps)
+        vals.append(g)
+        times.append(dt)
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(times) * 1e3 * (2 * TSTEPS / sweeps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (PolyBench jacobi-2d init)",
+        "config": {"workload": "J16K: Jacobi-2D fp64 16384x16384, 100 timesteps",
+                   "sample": sample, "l2": "inputs 2x2 GiB >> 126 MB L2"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# the CUDA path
+# ----------------------------------------------------------------------------
+def run_jacc(args):
+    import torch
+    import __graft_entry__ as ge
+    ge.build_synth()
+    ge.build_jacc()
+    import synth
+    from paper_2110_14340_b200 import jacc as J
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    n = args.gpus
+    if world > 1:
+        # Single-process runtime (the paper's one-driver-many-GPUs model,
+        # P:570): rank 0 drives all N GPUs through the C-ABI; the other
+        # ranks only hold the barrier.
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+    ngpu = torch.cuda.device_count()
+    if ngpu >= n:
+        ords = list(range(n))
+        virtual = False
+    else:
+        ords = [0] * n  # virtual devices on one GPU (parity/plumbing only)
+        virtual = True
+
+    N = N_GRID
+    A, B = synth.polybench_jacobi2d(N)
+    J.jacc_init(n, ords)
+    J.jacc_set_merge_policy(J.JACC_MERGE_HALO if args.merge == "halo" else J.JACC_MERGE_EAGER)
+    J.jacc_data_create(A)
+    J.jacc_data_create(B)
+    J.jacc_update_device(A)
+    J.jacc_update_device(B)
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    args_ab = [J.arg(IN, A), J.arg(OUT, B)]
+    args_ba = [J.arg(IN, B), J.arg(OUT, A)]
+
+    def step():
+        for _ in range(TSTEPS):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ab, 0)
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ba, 0)
+
+    streams = []
+    for d in range(n):
+        sp, ordv = J.jacc_get_stream(d)
+        streams.append((torch.cuda.ExternalStream(sp, device=f"cuda:{ordv}"), ordv))
+
+    def sync():
+        for o in sorted(set(ords)):
+            torch.cuda.synchronize(o)
+
+    for _ in range(args.warmup):
+        step()
+    J.jacc_wait()
+    sync()
+    J.jacc_set_profiling(1)
+    J.jacc_profile_reset()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    with ClockSampler(ords[0]) as clk:
+        for d, (s, o) in enumerate(streams):
+            with torch.cuda.device(o):
+                starts[d].record(s)
+        for _ in range(args.steps):
+            step()
+        for d, (s, o) in enumerate(streams):
+            with torch.cuda.device(o):
+                ends[d].record(s)
+        J.jacc_wait()
+        sync()
+    t = max(starts[d].elapsed_time(ends[d]) for d in range(n)) / 1e3   # max over devices
+    kern = [J.jacc_profile_totals(d) for d in range(n)]
+    J.jacc_set_profiling(0)
+    bytes_step = 2 * TSTEPS * algo_bytes_per_sweep(N, n)
+    value = bytes_step * args.steps / t / 1e9
+    launches_dev = [k[2] for k in kern]
+    # dominant kernel: jacobi2d on device 0; algorithmic bytes per launch on it
+    k_avg = kern[0][0] / max(kern[0][2], 1)
+    per_dev_bytes = algo_bytes_per_sweep_dev(N, n, 0)
+    achieved = per_dev_bytes / k_avg / 1e9
+    peak, peak_src = load_peaks()
+    traffic, tsrc = load_traffic("jacobi2d")
+
+    # ---- e2e through the public API with host buffers ----
+    e2e_times = []
+    for it in range(max(1, min(args.steps, 3)) + 1):
+        sync()
+        t0 = time.perf_counter()
+        J.jacc_update_device(A)
+        J.jacc_update_device(B)
+        step()
+        J.jacc_update_host(A)
+        t1 = time.perf_counter()
+        if it > 0:
+            e2e_times.append(t1 - t0)
+    e2e = bytes_step / statistics.median(e2e_times) / 1e9
+
+    extra = {}
+    if args.extra:
+        extra = run_extra_loops(J, torch, n, streams, peak)
+    J.jacc_finalize()
+
+    cpu = None
+    if args.cpu_baseline and n == 1:
+        g, dt, sample = oracle_sample(args.cpu_sweeps)
+        cpu = {"value": g, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+               "seconds": dt}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (PolyBench jacobi-2d init, seeded generators in synth/)",
+        "config": {"workload": "J16K: Jacobi-2D fp64 16384x16384, 100 timesteps (200 launches/step)",
+                   "merge": args.merge, "devices": ords, "virtual_devices": virtual,
+                   "l2": "no flush: inputs 2x2 GiB >> 126 MB L2",
+                   "parallelism": f"row-block owner partition over {n} device(s)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "jacobi2d_kernel<2>", "kernel_avg_us": k_avg * 1e6,
+                     "algo_bytes_per_launch": per_dev_bytes, "peak_source": peak_src,
+                     "traffic_source": tsrc},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * A.nbytes,
+                "d2h_bytes_per_step": A.nbytes},
+        "gpu_launches": int(sum(launches_dev)),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    if extra:
+        line["loops"] = extra
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def algo_bytes_per_sweep_dev(N, n, d):
+    q, r = divmod(N, n)
+    lo = d * q + min(d, r)
+    hi = (d + 1) * q + min(d + 1, r)
+    i0, i1 = max(lo, 1), min(hi, N - 1)
+    if i1 <= i0:
+        return 0
+    return 8 * N * (i1 - i0 + 2) + 8 * (i1 - i0) * (N - 2)
+
+
+def _time_loop(J, torch, streams, fn, reps):
+    """Device time (max over devices) of `reps` calls of fn, plus the
+    profiled average kernel time on device 0."""
+    fn()
+    J.jacc_wait()
+    J.jacc_set_profiling(1)
+    J.jacc_profile_reset()
+    n = len(streams)
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    for d, (s, o) in enumerate(streams):
+        with torch.cuda.device(o):
+            st[d].record(s)
+    for _ in range(reps):
+        fn()
+    for d, (s, o) in enumerate(streams):
+        with torch.cuda.device(o):
+            en[d].record(s)
+    J.jacc_wait()
+    t = max(st[d].elapsed_time(en[d]) for d in range(n)) / 1e3 / reps
+    k, m, nl, _ = J.jacc_profile_totals(0)
+    J.jacc_set_profiling(0)
+    return t, k / max(nl, 1), m / max(nl, 1)
+
+
+def run_extra_loops(J, torch, n, streams, peak):
+    """The other BASELINE configs (DOT 2^30, GEMM 8192^3, SCAT 2^28) timed
+    through the same C-ABI: kernel-level roofline evidence, not bench lines."""
+    import synth
+    out = {}
+    IN, OUT, INOUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT, J.JACC_ARG_ARRAY_INOUT
+    # DOT 2^30
+    L = 2**30
+    x = synth.uniform_f64(L, 1, synth.AID["x"])
+    y = synth.uniform_f64(L, 1, synth.AID["y"])
+    s = np.zeros(1)
+    for a in (x, y):
+        J.jacc_data_create(a)
+        J.jacc_update_device(a)
+    dargs = [J.arg(IN, x), J.arg(IN, y), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s)]
+    rng = J.make_range(0, L)
+    t, k, _ = _time_loop(J, torch, streams, lambda: J.jacc_launch(J.JACC_LOOP_DOT_F64, rng, dargs), 10)
+    byts = 16 * L
+    out["dot_2^30"] = {"loop_gbs": byts / t / 1e9, "kernel_us": k * 1e6,
+                       "kernel_gbs": byts / n / k / 1e9, "frac_of_peak": byts / n / k / 1e9 / peak,
+                       "launch_ms": t * 1e3}
+    J.jacc_data_delete(x)
+    J.jacc_data_delete(y)
+    del x, y
+    # GEMM 8192^3
+    G = 8192
+    A = synth.uniform_f64(G * G, 2, synth.AID["A"]).reshape(G, G)
+    B = synth.uniform_f64(G * G, 2, synth.AID["B"]).reshape(G, G)
+    C = np.zeros((G, G))
+    for a in (A, B, C):
+        J.jacc_data_create(a)
+        J.jacc_update_device(a)
+    gargs = [J.arg(IN, A), J.arg(IN, B), J.arg(OUT, C)]
+    t, k, m = _time_loop(J, torch, streams, lambda: J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, gargs, 0), 3)
+    fl = 2 * G**3
+    out["gemm_8192"] = {"loop_tflops": fl / t / 1e12, "kernel_ms": k * 1e3,
+                        "kernel_tflops": fl / n / k / 1e12, "merge_ms": m * 1e3,
+                        "launch_ms": t * 1e3}
+    for a in (A, B, C):
+        J.jacc_data_delete(a)
+    del A, B, C
+    # SCAT 2^28 f64
+    S = 2**28
+    idx = synth.index_i32(S, S, 3, synth.AID["idx"])
+    b = synth.dyadic_f64(S, 3, synth.AID["b"])
+    a = synth.dyadic_f64(S, 3, synth.AID["a0"])
+    for arr in (idx, b, a):
+        J.jacc_data_create(arr)
+        J.jacc_update_device(arr)
+    sargs = [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)]
+    srng = J.make_range(0, S)
+    t, k, m = _time_loop(J, torch, streams,
+                         lambda: J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, srng, sargs, 0), 5)
+    byts = S * (4 + 8 + 16)
+    out["scatter_f64_2^28"] = {"loop_gbs": byts / t / 1e9, "kernel_us": k * 1e6,
+                               "kernel_alg_gbs": byts / k / 1e9 if n == 1 else None,
+                               "merge_us": m * 1e6, "launch_ms": t * 1e3}
+    for arr in (idx, b, a):
+        J.jacc_data_delete(arr)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="jacc", choices=["jacc", "reference"])
+    ap.add_argument("--merge", default="halo", choices=["halo", "eager"])
+    ap.add_argument("--no-extra", dest="extra", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-sweeps", type=int, default=10)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_jacc(args)
+
+
+if __name__ == "__main__":
+    main()

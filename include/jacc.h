@@ -1,0 +1,252 @@
+/*
+ * jacc.h -- C-ABI of the B200-native JACC multi-GPU `parallel loop` runtime
+ * (libjacc.so).  Reimplements, from the paper's statement of the problem,
+ * the hot path of arXiv 2110.14340 (Matsumura, Garcia De Gonzalo, Pena):
+ * one OpenACC `parallel loop` distributed automatically over the GPUs of a
+ * single box by predicate-based filtering (Sec 4).
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, R-k = reading k
+ * in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *   - Return codes only; no exceptions cross the ABI.  JACC_OK == 0,
+ *     errors are negative; jacc_error_string() gives stable text.
+ *   - A CUDA error poisons the runtime: every later call returns
+ *     JACC_ERR_STATE until jacc_finalize() + jacc_init().
+ *   - One host thread drives the API (not thread-safe).
+ *   - "host" pointers are caller-owned host memory; the caller keeps them
+ *     valid between jacc_data_create() and jacc_data_delete(); the library
+ *     never frees them.  The library owns device replicas, dirty records,
+ *     streams, events and communicators.
+ *   - Index ranges are half-open [lo, hi) (R-3); recorded dirty ranges are
+ *     inclusive [min, max] in flat element indices, empty <=> min > max,
+ *     reported as (UINT64_MAX, 0).
+ *   - Devices are LOGICAL devices 0..n-1 (device 0 is the primary, R-13);
+ *     each maps to a CUDA ordinal.  Several logical devices may share one
+ *     ordinal ("virtual devices": separate replicas on one GPU) so the
+ *     multi-device path can be exercised on a single B200.
+ */
+#ifndef JACC_H
+#define JACC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int jacc_status;
+
+enum {
+    JACC_OK = 0,
+    JACC_ERR_INVALID = -1,      /* bad argument, size, extent or loop shape */
+    JACC_ERR_OVERLAP = -2,      /* data_create overlaps a present region */
+    JACC_ERR_NOT_PRESENT = -3,  /* pointer not inside any present region (P:209 `present`) */
+    JACC_ERR_UNKNOWN_LOOP = -4, /* loop_id not in the descriptor table */
+    JACC_ERR_OOM = -5,          /* device allocation failed */
+    JACC_ERR_CUDA = -6,         /* CUDA runtime error (runtime is now poisoned) */
+    JACC_ERR_NCCL = -7,         /* NCCL error (runtime is now poisoned) */
+    JACC_ERR_STATE = -8         /* not initialised, double init, or poisoned */
+};
+
+/* ---------------------------------------------------------------------- */
+/* Lifetime                                                                */
+/* ---------------------------------------------------------------------- */
+
+/* Initialise n_devices logical devices.  device_ids[d] is the CUDA ordinal
+ * of logical device d (NULL = 0..n-1).  Repeated ordinals create virtual
+ * devices on one GPU.  Peer access is enabled between distinct ordinals
+ * (NVLink/NVSwitch P2P); an NCCL communicator is created when n > 1 and all
+ * ordinals are distinct (reduction combine).  The paper drives its
+ * GPUs from OpenMP threads inside the library; here each logical
+ * device has its own CUDA stream and the runtime enqueues asynchronously.
+ * Errors: JACC_ERR_STATE if already initialised, JACC_ERR_INVALID for
+ * n_devices < 1 or > JACC_MAX_DEVICES or a bad ordinal. */
+#define JACC_MAX_DEVICES 16
+jacc_status jacc_init(int n_devices, const int *device_ids);
+
+/* Synchronise, free every replica and runtime object.  Present regions
+ * still registered are dropped (host memory untouched). */
+jacc_status jacc_finalize(void);
+
+/* Number of logical devices (0 if not initialised). */
+int jacc_num_devices(void);
+
+/* Merge policy for loops that write arrays (R-5):
+ *   JACC_MERGE_EAGER: after each launch every device pushes its recorded
+ *     dirty region of every written array to all other replicas
+ *     ("Updated data are sent to all other GPUs after each kernel
+ *     execution"; sync at start and end).
+ *   JACC_MERGE_HALO: push only the dirty rows the neighbouring devices read
+ *     in a launch of the same loop shape (the config's boundary-row
+ *     dirty-range merge; the paper's manual halo comparison P:909,
+ *     P:933-939).  Replicas stay stale elsewhere; stale intervals are
+ *     pulled on demand before a launch that reads them and by
+ *     jacc_update_host().  Results are identical under both policies. */
+enum { JACC_MERGE_EAGER = 0, JACC_MERGE_HALO = 1 };
+jacc_status jacc_set_merge_policy(int policy);
+
+/* Execution mode: JACC_MODE_MULTI splits by owned blocks
+ * (default); JACC_MODE_DUP runs the full loop on every device with no
+ * exchange ("duplicating computation on all GPUs and performing no
+ * GPU-to-GPU communication").  The alias rule (R-12) forces DUP per launch. */
+enum { JACC_MODE_MULTI = 0, JACC_MODE_DUP = 1 };
+jacc_status jacc_set_mode(int mode);
+
+/* Owned block [lo, hi) of logical device d when an extent E is split over
+ * n devices: "equally dividing parallel dimensions among GPUs",
+ * the first E mod n blocks one element larger (R-2).  Pure host
+ * logic; needs no GPU and no jacc_init.  Errors: JACC_ERR_INVALID for
+ * E < 0, n < 1, d outside [0, n) or NULL outputs. */
+jacc_status jacc_partition(int64_t E, int n, int d, int64_t *lo, int64_t *hi);
+
+/* ---------------------------------------------------------------------- */
+/* Present table ("managed in a red-black tree ... to accept any */
+/* address of declared data")                       */
+/* ---------------------------------------------------------------------- */
+
+/* Register [host, host+bytes) and allocate one replica of `bytes` on every
+ * logical device ("Device-memory allocations ... are replicated on
+ * all the GPUs").  No copy is made (OpenACC `create`).  elem_size is the
+ * element size in bytes; extents[0..ndims) the row-major shape (ndims 1..3)
+ * whose product times elem_size must equal bytes.
+ * Errors: JACC_ERR_INVALID (bytes == 0, bad shape, host NULL),
+ * JACC_ERR_OVERLAP, JACC_ERR_OOM. */
+jacc_status jacc_data_create(void *host, size_t bytes, size_t elem_size,
+                             int ndims, const int64_t *extents);
+
+/* Unregister the region containing `host` (any interior address) and free
+ * its replicas.  Errors: JACC_ERR_NOT_PRESENT. */
+jacc_status jacc_data_delete(void *host);
+
+/* Copy host bytes [offset, offset+bytes) of the region containing `host`
+ * into EVERY replica ("host-to-GPU communications are replicated")
+ * and mark them valid.  `host` may be any interior address; offset is
+ * relative to it.  Synchronous w.r.t. the host buffer (it may be reused on
+ * return).  Errors: JACC_ERR_NOT_PRESENT, JACC_ERR_INVALID (out of range). */
+jacc_status jacc_update_device(void *host, size_t offset_bytes, size_t bytes);
+
+/* Make the primary replica coherent over the range (pull stale intervals
+ * from their owners over P2P) and copy it to host ("the primary
+ * GPU is used for GPU-to-host transfers").  Waits for all outstanding work.
+ * Errors as jacc_update_device. */
+jacc_status jacc_update_host(void *host, size_t offset_bytes, size_t bytes);
+
+/* ---------------------------------------------------------------------- */
+/* Loop launch (jacc_kernel_push)                    */
+/* ---------------------------------------------------------------------- */
+
+/* Precompiled loop bodies (the paper's experiments embed pre-filtered
+ * kernel strings).  Argument order per loop:
+ *   JACC_LOOP_SQUARE_F32      (Listing 1): y IN f32[n], x OUT f32[n];
+ *       for i in range: x[i] = y[i]*y[i].  range: 1-D over [0,n).
+ *   JACC_LOOP_JACOBI2D_F64    (R-1): src IN f64[N][N], dst OUT f64[N][N];
+ *       for i,j in range: dst[i][j] = 0.2*(src[i][j]+src[i][j-1]+src[i][j+1]
+ *       +src[i+1][j]+src[i-1][j]).  range: 2-D within [1,N-1)^2 (NULL = all).
+ *   JACC_LOOP_DOT_F64         : x IN f64, y IN f64, s REDUCE_SUM_F64;
+ *       s = s + sum_{i in range} x[i]*y[i].
+ *   JACC_LOOP_SUM_F64         : x IN f64, s REDUCE_SUM_F64; s = s + sum x[i].
+ *   JACC_LOOP_GEMM_F64        (R-11): A IN f64[M][K], B IN f64[K][N],
+ *       C OUT f64[M][N]; C = A*B.  range: 2-D over [0,M)x[0,N) (NULL = all).
+ *   JACC_LOOP_SCATTER_ADD_F64 (R-6..R-8): idx IN i32[n], b IN f64[n],
+ *       a INOUT f64[M]; for i in range: a[idx[i]] += b[i] (atomic).
+ *   JACC_LOOP_SCATTER_ADD_I32 : idx IN i32[n], b IN i32[n], a INOUT i32[M].
+ * 1-D array arguments may point inside a region (the loop's array starts
+ * there); 2-D arguments must point at the region base. */
+enum {
+    JACC_LOOP_SQUARE_F32 = 1,
+    JACC_LOOP_JACOBI2D_F64 = 2,
+    JACC_LOOP_DOT_F64 = 3,
+    JACC_LOOP_SUM_F64 = 4,
+    JACC_LOOP_GEMM_F64 = 5,
+    JACC_LOOP_SCATTER_ADD_F64 = 6,
+    JACC_LOOP_SCATTER_ADD_I32 = 7
+};
+
+/* Iteration range, half-open per dimension (R-3). */
+typedef struct {
+    int ndims;
+    int64_t lo[3];
+    int64_t hi[3];
+} jacc_range;
+
+typedef enum {
+    JACC_ARG_ARRAY_IN = 0,
+    JACC_ARG_ARRAY_OUT = 1,
+    JACC_ARG_ARRAY_INOUT = 2,
+    JACC_ARG_SCALAR_F64 = 3,
+    JACC_ARG_SCALAR_I64 = 4,
+    /* reduction(+:s): ptr is a host double* holding s_in on entry and
+     * s_out = s_in + sum on return (R-9); the launch is synchronous
+     * (obligatory sync). */
+    JACC_ARG_REDUCE_SUM_F64 = 5
+} jacc_arg_kind;
+
+typedef struct {
+    int kind;      /* jacc_arg_kind */
+    void *ptr;     /* host address inside a present region (arrays), or host double* (reductions) */
+    double f64;    /* scalar value (SCALAR_F64) */
+    int64_t i64;   /* scalar value (SCALAR_I64) */
+} jacc_arg;
+
+/* Distribute one loop over the logical devices:
+ * resolve every array argument in the present table, apply the alias rule
+ * (R-12), partition the written array's split dimension into n contiguous
+ * owned blocks (dim 0; remainder rule R-2) -- or, for
+ * reductions, the outermost iteration range -- clip each
+ * device's iterations to its block, pull stale input intervals, run the
+ * device kernel with fused write-set tracking (dirty min/max range, or a
+ * dirty bitmap for the scatter, R-15), merge the recorded dirty regions
+ * into the other replicas per the merge policy, and combine reductions
+ * (NCCL allreduce when the devices are distinct GPUs).
+ * async_id: -1 = synchronous (returns after completion); >= 0 = returns
+ * after enqueue (reductions are always synchronous).
+ * Errors: JACC_ERR_UNKNOWN_LOOP, JACC_ERR_INVALID (arg count/kind/shape,
+ * in-place stencil or GEMM), JACC_ERR_NOT_PRESENT, JACC_ERR_CUDA/NCCL. */
+jacc_status jacc_launch(int loop_id, const jacc_range *range,
+                        const jacc_arg *args, int nargs, int async_id);
+
+/* Wait for outstanding work (async_id -1 = all queues). */
+jacc_status jacc_wait(int async_id);
+
+/* ---------------------------------------------------------------------- */
+/* Introspection (parity tests and measurement)                            */
+/* ---------------------------------------------------------------------- */
+
+/* Dirty range recorded on device `dev` for the region containing `host`
+ * by the most recent launch that wrote it (inclusive flat element
+ * indices; empty = (UINT64_MAX, 0)).  Waits for outstanding work. */
+jacc_status jacc_get_dirty_range(void *host, int dev, uint64_t *min, uint64_t *max);
+
+/* Dirty bitmap of device `dev` for the region (bit k of word w <-> element
+ * 32w+k), recorded by the most recent scatter launch; nwords must be
+ * >= ceil(elements/32).  JACC_ERR_INVALID if no bitmap was recorded. */
+jacc_status jacc_get_dirty_bitmap(void *host, int dev, uint32_t *out, size_t nwords);
+
+/* D2H copy of `bytes` from the start of device `dev`'s replica of the
+ * region containing `host` (no coherence action).  Waits for all work. */
+jacc_status jacc_get_replica(void *host, int dev, void *out, size_t bytes);
+
+/* Timing of the most recent launch (requires jacc_set_profiling(1)):
+ * max over devices of kernel time and of merge time (seconds), and the
+ * bytes moved device-to-device by its merge and pulls. */
+jacc_status jacc_last_timing(double *t_kernel_s, double *t_merge_s, uint64_t *bytes_merged);
+
+/* Record CUDA events around every loop kernel and merge (D13 timing
+ * records).  Accumulated totals since the last reset: */
+jacc_status jacc_set_profiling(int on);
+jacc_status jacc_profile_totals(int dev, double *kernel_s, double *merge_s,
+                                uint64_t *launches, uint64_t *bytes_merged);
+jacc_status jacc_profile_reset(void);
+
+/* The CUDA stream (cudaStream_t) logical device `dev` runs on, and its
+ * CUDA ordinal, so callers can time the path with their own events. */
+jacc_status jacc_get_stream(int dev, void **stream, int *cuda_ordinal);
+
+const char *jacc_error_string(jacc_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JACC_H */

@@ -1,0 +1,60 @@
+"""In-tree build of libjacc.so (sm_100a SASS; no PTX JIT needed on the box).
+
+nvcc compiles the device kernels, g++ the host runtime; the shared library
+links CUDA's static runtime and the NCCL that ships with the torch wheel
+(one libnccl.so.2 per process, found through an rpath)."""
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libjacc.so")
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "runtime.cpp", "kernels.cuh")] + [
+    os.path.join(INCLUDE, "jacc.h")]
+
+
+def nccl_paths():
+    import nvidia.nccl as nn  # the wheel torch itself loads
+    base = os.path.dirname(nn.__file__) if getattr(nn, "__file__", None) else list(nn.__path__)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"libjacc build failed at {os.path.basename(cmd[0])}")
+    return r
+
+
+def build(force=False, verbose=False):
+    if not force and os.path.exists(LIB):
+        t = os.path.getmtime(LIB)
+        if all(os.path.getmtime(s) <= t for s in SOURCES):
+            return LIB
+    nccl_inc, nccl_lib = nccl_paths()
+    bdir = os.path.join(PKG, "_build")
+    os.makedirs(bdir, exist_ok=True)
+    ko = os.path.join(bdir, "kernels.o")
+    ro = os.path.join(bdir, "runtime.o")
+    _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+          "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-c",
+          os.path.join(CSRC, "kernels.cu"), "-o", ko])
+    _run(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE,
+          "-I", os.path.join(CUDA_HOME, "include"), "-I", nccl_inc, "-c",
+          os.path.join(CSRC, "runtime.cpp"), "-o", ro])
+    tmp = LIB + ".tmp"
+    _run([NVCC, *ARCH, "-shared", "-o", tmp, ko, ro, "-cudart", "static",
+          "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}"])
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose="-v" in sys.argv))

@@ -1,0 +1,722 @@
+// kernels.cu -- sm_100a device kernels of the JACC hot path.
+//
+// Each loop body runs over the calling device's owned block only (the
+// paper's predicate-based filtering, with the predicated-off
+// iterations clipped from the grid instead of launched idle) and records
+// the elements it actually stores (north_star; DESIGN R-15) in the same
+// pass: a min/max flat-index range reduced per warp and per CTA and
+// published with one 64-bit atomicMin pair per CTA, or a dirty bitmap with
+// warp-aggregated atomicOr for scattered writes.  No extra HBM pass.
+//
+// Element-wise bodies use __dadd_rn/__dmul_rn/__fmul_rn so no FMA is
+// contracted (DESIGN R-14): results are bit-identical to the oracle.
+#include "kernels.cuh"
+
+#include <cstdint>
+
+namespace jk {
+namespace {
+
+constexpr u64 kU64Max = ~0ull;
+
+__device__ __forceinline__ u64 warp_min_u64(u64 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        u64 t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ u64 warp_max_u64(u64 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        u64 t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+// CTA-wide min/max of per-thread stored indices -> one atomic pair per CTA.
+// Must be called by every thread of the CTA (contains __syncthreads).
+template <int NWARPS>
+__device__ __forceinline__ void publish_dirty(u64 mn, u64 mx, u64 *dirty) {
+    __shared__ u64 smn[NWARPS], smx[NWARPS];
+    mn = warp_min_u64(mn);
+    mx = warp_max_u64(mx);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        smn[w] = mn;
+        smx[w] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 a = smn[0], b = smx[0];
+#pragma unroll
+        for (int i = 1; i < NWARPS; i++) {
+            a = smn[i] < a ? smn[i] : a;
+            b = smx[i] > b ? smx[i] : b;
+        }
+        if (a != kU64Max) {
+            atomicMin(&dirty[0], a);
+            atomicMin(&dirty[1], ~b);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// BK6  square_f32 (Listing 1)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) square_f32_kernel(const float *__restrict__ y,
+                                                         float *__restrict__ x, int64_t i0,
+                                                         int64_t i1, int64_t x_off, u64 *dirty) {
+    u64 mn = kU64Max, mx = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < i1; i += stride) {
+        const float v = __ldg(y + i);
+        __stcs(x + i, __fmul_rn(v, v));
+        const u64 f = (u64)(x_off + i);
+        mn = f < mn ? f : mn;
+        mx = f > mx ? f : mx;
+    }
+    publish_dirty<8>(mn, mx, dirty);
+}
+
+// ---------------------------------------------------------------------------
+// BK1  Jacobi-2D register-marching stencil.
+//
+// A warp owns a slab of 32*V consecutive columns (V doubles per lane, 128-bit
+// loads when V == 2) and marches down JR rows keeping rows i-1, i, i+1 in
+// registers plus JPF rows of prefetch; horizontal neighbours come from the
+// adjacent lane by shuffle, the two slab-edge columns by one extra load in
+// lanes 0 and 31 (L1/L2 hits: the neighbouring slab reads the same lines).
+// Each src element is read from HBM once per sweep (halo rows between row
+// tiles are L2 hits), each dst element written once: 16 B/point.
+// ---------------------------------------------------------------------------
+constexpr int JW = 4;    // warps per CTA (side by side in columns)
+constexpr int JR = 32;   // rows per tile
+constexpr int JPF = 3;   // rows of prefetch beyond i+1
+
+template <int V>
+struct JRow {
+    double v[V];
+    double l, r;
+};
+
+template <int V>
+__device__ __forceinline__ void jload(JRow<V> &o, const double *__restrict__ src, int64_t N,
+                                      int64_t row, int64_t j0, int64_t cs, int lane, bool ok) {
+    const double *p = src + row * N;
+    if (ok && j0 < N) {
+        if constexpr (V == 2) {
+            const double2 t = __ldg(reinterpret_cast<const double2 *>(p + j0));
+            o.v[0] = t.x;
+            o.v[1] = t.y;
+        } else {
+            o.v[0] = __ldg(p + j0);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < V; k++) o.v[k] = 0.0;
+    }
+    o.l = (ok && lane == 0 && cs >= 1) ? __ldg(p + cs - 1) : 0.0;
+    o.r = (ok && lane == 31 && cs + 32 * V < N) ? __ldg(p + cs + 32 * V) : 0.0;
+}
+
+template <int V>
+__global__ void __launch_bounds__(JW * 32)
+    jacobi2d_kernel(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t r0,
+                    int64_t r1, int64_t c0, int64_t c1, int64_t cs_base, int64_t ntiles_y,
+                    u64 *dirty, double *push_top, double *push_bot) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t cs = cs_base + ((int64_t)blockIdx.x * JW + warp) * (32 * V);
+    const int64_t j0 = cs + lane * V;
+    u64 mn = kU64Max, mx = 0;
+
+    for (int64_t ty = blockIdx.y; ty < ntiles_y; ty += gridDim.y) {
+        const int64_t rs = r0 + ty * JR;
+        const int64_t re = rs + JR < r1 ? rs + JR : r1;
+        // rows needed: rs-1 .. re (re <= r1 <= N-1 exists)
+        JRow<V> q[JPF + 3];
+#pragma unroll
+        for (int t = 0; t < JPF + 3; t++)
+            jload<V>(q[t], src, N, rs - 1 + t, j0, cs, lane, rs - 1 + t <= re);
+
+#pragma unroll
+        for (int k = 0; k < JR; k++) {
+            const int64_t i = rs + k;
+            if (i >= re) break;
+            const JRow<V> &U = q[0], &C = q[1], &D = q[2];
+            // neighbours across the lane boundary (all lanes shuffle)
+            const double fromL = __shfl_up_sync(0xffffffffu, C.v[V - 1], 1);
+            const double fromR = __shfl_down_sync(0xffffffffu, C.v[0], 1);
+            double out[V];
+#pragma unroll
+            for (int e = 0; e < V; e++) {
+                const double left = e > 0 ? C.v[e - 1] : (lane > 0 ? fromL : C.l);
+                const double right = e < V - 1 ? C.v[e + 1] : (lane < 31 ? fromR : C.r);
+                // PolyBench order: ((((c + l) + r) + dn) + up) then * 0.2
+                double acc = __dadd_rn(C.v[e], left);
+                acc = __dadd_rn(acc, right);
+                acc = __dadd_rn(acc, D.v[e]);
+                acc = __dadd_rn(acc, U.v[e]);
+                out[e] = __dmul_rn(0.2, acc);
+            }
+            const int64_t base = i * N;
+            const bool full = (j0 >= c0) && (j0 + V <= c1);
+            double *tp = (i == r0) ? push_top : nullptr;
+            double *bp = (i == r1 - 1) ? push_bot : nullptr;
+            if (full) {
+                if constexpr (V == 2) {
+                    const double2 o2 = make_double2(out[0], out[1]);
+                    __stcs(reinterpret_cast<double2 *>(dst + base + j0), o2);
+                    if (tp) *reinterpret_cast<double2 *>(tp + base + j0) = o2;
+                    if (bp) *reinterpret_cast<double2 *>(bp + base + j0) = o2;
+                } else {
+                    __stcs(dst + base + j0, out[0]);
+                    if (tp) tp[base + j0] = out[0];
+                    if (bp) bp[base + j0] = out[0];
+                }
+                const u64 f0 = (u64)(base + j0), f1 = (u64)(base + j0 + V - 1);
+                mn = f0 < mn ? f0 : mn;
+                mx = f1 > mx ? f1 : mx;
+            } else {
+#pragma unroll
+                for (int e = 0; e < V; e++) {
+                    const int64_t j = j0 + e;
+                    if (j >= c0 && j < c1) {
+                        dst[base + j] = out[e];
+                        if (tp) tp[base + j] = out[e];
+                        if (bp) bp[base + j] = out[e];
+                        const u64 f = (u64)(base + j);
+                        mn = f < mn ? f : mn;
+                        mx = f > mx ? f : mx;
+                    }
+                }
+            }
+            // rotate the register ring, prefetch row i + JPF + 2
+#pragma unroll
+            for (int t = 0; t < JPF + 2; t++) q[t] = q[t + 1];
+            const int64_t nr = i + JPF + 2;
+            jload<V>(q[JPF + 2], src, N, nr, j0, cs, lane, nr <= re);
+        }
+    }
+    publish_dirty<JW>(mn, mx, dirty);
+}
+
+// ---------------------------------------------------------------------------
+// BK2  fixed-order fp64 reduction (dot / sum) with last-block finish.
+// The per-thread assignment depends only on the fixed grid, so the result is
+// deterministic run to run.
+// ---------------------------------------------------------------------------
+constexpr int RT = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < RT / 32 ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    }
+    return t;  // valid in thread 0
+}
+
+template <bool DOT, bool VEC>
+__global__ void __launch_bounds__(RT) reduce_kernel(const double *__restrict__ x,
+                                                    const double *__restrict__ y, int64_t n,
+                                                    double *partials, unsigned *ticket,
+                                                    double *out) {
+    __shared__ double sh[RT / 32];
+    __shared__ bool last;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int64_t tid = (int64_t)blockIdx.x * RT + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * RT;
+    if (VEC) {
+        // x (and y) 16-byte aligned: pairs of doubles, 4 pairs in flight per thread
+        const int64_t np = n >> 1;
+        const double2 *x2 = reinterpret_cast<const double2 *>(x);
+        const double2 *y2 = reinterpret_cast<const double2 *>(y);
+        int64_t p = tid;
+        for (; p + 3 * nth < np; p += 4 * nth) {
+            double2 xv[4], yv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                xv[u] = __ldcs(x2 + p + u * nth);
+                if (DOT) yv[u] = __ldcs(y2 + p + u * nth);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (DOT) {
+                    a0 = fma(xv[u].x, yv[u].x, a0);
+                    a1 = fma(xv[u].y, yv[u].y, a1);
+                } else {
+                    a0 += xv[u].x;
+                    a1 += xv[u].y;
+                }
+            }
+        }
+        for (; p < np; p += nth) {
+            const double2 xv = __ldcs(x2 + p);
+            if (DOT) {
+                const double2 yv = __ldcs(y2 + p);
+                a2 = fma(xv.x, yv.x, a2);
+                a3 = fma(xv.y, yv.y, a3);
+            } else {
+                a2 += xv.x;
+                a3 += xv.y;
+            }
+        }
+        if ((n & 1) && tid == 0) a3 += DOT ? x[n - 1] * y[n - 1] : x[n - 1];
+    } else {
+        for (int64_t i = tid; i < n; i += nth) a0 += DOT ? x[i] * y[i] : x[i];
+    }
+    double v = block_sum((a0 + a1) + (a2 + a3), sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = v;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double t = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += RT) t += __ldcg(partials + i);
+        t = block_sum(t, sh);
+        if (threadIdx.x == 0) {
+            *out = t;
+            *ticket = 0u;
+        }
+    }
+}
+
+__global__ void combine_kernel(PeerPtrs parts, double s_in, double *out) {
+    double t = 0.0;
+    for (int d = 0; d < parts.n; d++) t += *static_cast<const volatile double *>(parts.p[d]);
+    *out = s_in + t;
+}
+
+// ---------------------------------------------------------------------------
+// BK3  fp64 GEMM on the DMMA tensor pipe.
+// CTA tile 64x64, K tile 16, 3-stage cp.async pipeline, 4 warps (2x2) each
+// owning a 32x32 warp tile = 4x4 mma.sync.m8n8k4.f64 fragments.
+// ---------------------------------------------------------------------------
+constexpr int GBM = 64, GBN = 64, GBK = 16, GST = 3;
+constexpr int GAP = GBK + 4;  // A smem row stride (doubles): conflict-free fragment loads
+constexpr int GBP = GBN + 8;  // B smem row stride (doubles)
+constexpr int GSMEM = GST * (GBM * GAP + GBK * GBP) * 8;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, int bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+    asm volatile(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+template <bool V16>
+__device__ __forceinline__ void gemm_load_tile(double *As, double *Bs, const double *A,
+                                               const double *B, int64_t M, int64_t Nb, int64_t N,
+                                               int64_t K, int64_t m0, int64_t n0, int64_t k0) {
+    // A rows < M (bound), B cols < Nb (bound); N is B's row stride
+    const int tid = threadIdx.x;
+    if (V16) {
+#pragma unroll
+        for (int it = 0; it < (GBM * GBK / 2) / 128; it++) {
+            const int c = tid + it * 128;
+            const int row = c / (GBK / 2), cp = c % (GBK / 2);
+            const int64_t gm = m0 + row, gk = k0 + 2 * cp;
+            int bytes = 0;
+            const double *src = A;
+            if (gm < M && gk < K) {
+                bytes = (K - gk >= 2) ? 16 : 8;
+                src = A + gm * K + gk;
+            }
+            cp_async16(As + row * GAP + 2 * cp, src, bytes);
+        }
+#pragma unroll
+        for (int it = 0; it < (GBK * GBN / 2) / 128; it++) {
+            const int c = tid + it * 128;
+            const int row = c / (GBN / 2), cp = c % (GBN / 2);
+            const int64_t gk = k0 + row, gn = n0 + 2 * cp;
+            int bytes = 0;
+            const double *src = B;
+            if (gk < K && gn < Nb) {
+                bytes = (Nb - gn >= 2) ? 16 : 8;
+                src = B + gk * N + gn;
+            }
+            cp_async16(Bs + row * GBP + 2 * cp, src, bytes);
+        }
+    } else {
+#pragma unroll
+        for (int it = 0; it < (GBM * GBK) / 128; it++) {
+            const int c = tid + it * 128;
+            const int row = c / GBK, cc = c % GBK;
+            const int64_t gm = m0 + row, gk = k0 + cc;
+            const bool ok = gm < M && gk < K;
+            cp_async8(As + row * GAP + cc, ok ? A + gm * K + gk : A, ok ? 8 : 0);
+        }
+#pragma unroll
+        for (int it = 0; it < (GBK * GBN) / 128; it++) {
+            const int c = tid + it * 128;
+            const int row = c / GBN, cc = c % GBN;
+            const int64_t gk = k0 + row, gn = n0 + cc;
+            const bool ok = gk < K && gn < Nb;
+            cp_async8(Bs + row * GBP + cc, ok ? B + gk * N + gn : B, ok ? 8 : 0);
+        }
+    }
+}
+
+template <bool V16>
+__global__ void __launch_bounds__(128) gemm_f64_kernel(const double *__restrict__ A,
+                                                       const double *__restrict__ B,
+                                                       double *__restrict__ C, int64_t M,
+                                                       int64_t N, int64_t K, int64_t r0, int64_t r1,
+                                                       int64_t c0, int64_t c1, u64 *dirty) {
+    extern __shared__ __align__(16) double gsm[];
+    double *As = gsm;                        // [GST][GBM][GAP]
+    double *Bs = gsm + GST * GBM * GAP;      // [GST][GBK][GBP]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int64_t m0 = r0 + (int64_t)blockIdx.y * GBM;
+    const int64_t n0 = c0 + (int64_t)blockIdx.x * GBN;
+    const int64_t Mb = r1, Nb = c1;  // loads beyond the owned block are never needed
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int64_t KT = (K + GBK - 1) / GBK;
+#pragma unroll
+    for (int s = 0; s < GST - 1; s++) {
+        if (s < KT)
+            gemm_load_tile<V16>(As + s * GBM * GAP, Bs + s * GBK * GBP, A, B, Mb, Nb, N, K, m0,
+                                n0, (int64_t)s * GBK);
+        cp_commit();
+    }
+    const int ar = lane >> 2, ac = lane & 3;
+    for (int64_t kt = 0; kt < KT; kt++) {
+        cp_wait<GST - 2>();
+        __syncthreads();
+        const int64_t nk = kt + GST - 1;
+        if (nk < KT) {
+            const int s = (int)(nk % GST);
+            gemm_load_tile<V16>(As + s * GBM * GAP, Bs + s * GBK * GBP, A, B, Mb, Nb, N, K, m0,
+                                n0, nk * GBK);
+        }
+        cp_commit();
+        const int s = (int)(kt % GST);
+        const double *as = As + s * GBM * GAP + (wm * 32 + ar) * GAP + ac;
+        const double *bs = Bs + s * GBK * GBP + ac * GBP + wn * 32 + ar;
+#pragma unroll
+        for (int kk = 0; kk < GBK; kk += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) a[i] = as[i * 8 * GAP + kk];
+#pragma unroll
+            for (int j = 0; j < 4; j++) b[j] = bs[kk * GBP + j * 8];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+    }
+    cp_wait<0>();
+
+    // epilogue: store C rows in [r0, r1), cols in [c0, c1); track dirty
+    u64 mn = kU64Max, mx = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int64_t m = m0 + wm * 32 + i * 8 + ar;
+        if (m >= r1) continue;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int64_t n = n0 + wn * 32 + j * 8 + ac * 2;
+            const int64_t f = m * N + n;
+            if (V16 && n + 1 < c1) {
+                *reinterpret_cast<double2 *>(C + f) = make_double2(acc[i][j][0], acc[i][j][1]);
+                mn = (u64)f < mn ? (u64)f : mn;
+                mx = (u64)(f + 1) > mx ? (u64)(f + 1) : mx;
+            } else {
+                if (n < c1) {
+                    C[f] = acc[i][j][0];
+                    mn = (u64)f < mn ? (u64)f : mn;
+                    mx = (u64)f > mx ? (u64)f : mx;
+                }
+                if (n + 1 < c1) {
+                    C[f + 1] = acc[i][j][1];
+                    mx = (u64)(f + 1) > mx ? (u64)(f + 1) : mx;
+                }
+            }
+        }
+    }
+    publish_dirty<4>(mn, mx, dirty);
+}
+
+// ---------------------------------------------------------------------------
+// BK4  owner-filtered scatter-add with warp-aggregated dirty bitmap
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void scat_one(int32_t k, int64_t i, const T *__restrict__ b, T *a,
+                                         int64_t lo, int64_t hi, uint32_t *bitmap, u64 &mn,
+                                         u64 &mx, bool valid) {
+    const bool own = valid && k >= lo && k < hi;
+    if (own) {
+        atomicAdd(a + k, __ldg(b + i));  // RED.ADD: predicated atomic
+        mn = (u64)k < mn ? (u64)k : mn;
+        mx = (u64)k > mx ? (u64)k : mx;
+    }
+    // warp-aggregated bitmap update: lanes hitting the same 32-bit word
+    // combine their bits; the group's lowest lane issues one atomicOr.
+    const uint32_t word = own ? ((uint32_t)k >> 5) : 0xffffffffu;
+    const uint32_t bit = own ? (1u << (k & 31)) : 0u;
+    const unsigned grp = __match_any_sync(0xffffffffu, word);
+    const uint32_t bits = __reduce_or_sync(grp, bit);
+    if (own && (threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1)) atomicOr(bitmap + word, bits);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restrict__ idx,
+                                                          const T *__restrict__ b, T *a, int64_t n,
+                                                          int64_t lo, int64_t hi, uint32_t *bitmap,
+                                                          u64 *dirty) {
+    u64 mn = kU64Max, mx = 0;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n4 = n >> 2;
+    const int4 *idx4 = reinterpret_cast<const int4 *>(idx);
+    // whole warps iterate together (match/reduce need full warps)
+    const int64_t iters = (n4 + nth - 1) / nth;
+    for (int64_t it = 0; it < iters; it++) {
+        const int64_t q = tid + it * nth;
+        const bool v = q < n4;
+        int4 k4 = make_int4(0, 0, 0, 0);
+        if (v) k4 = __ldcs(idx4 + q);
+        scat_one<T>(k4.x, 4 * q + 0, b, a, lo, hi, bitmap, mn, mx, v);
+        scat_one<T>(k4.y, 4 * q + 1, b, a, lo, hi, bitmap, mn, mx, v);
+        scat_one<T>(k4.z, 4 * q + 2, b, a, lo, hi, bitmap, mn, mx, v);
+        scat_one<T>(k4.w, 4 * q + 3, b, a, lo, hi, bitmap, mn, mx, v);
+    }
+    // tail (n % 4), handled by the first warp
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const int64_t i = 4 * n4 + threadIdx.x;
+        const bool v = i < n;
+        scat_one<T>(v ? idx[i] : 0, v ? i : 0, b, a, lo, hi, bitmap, mn, mx, v);
+    }
+    publish_dirty<8>(mn, mx, dirty);
+}
+
+// ---------------------------------------------------------------------------
+// BK5  merges over peer memory (NVLink P2P stores; plain stores for virtual
+// devices that share one GPU)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) merge_range_kernel(const char *__restrict__ src,
+                                                          PeerPtrs dsts, const u64 *dirty,
+                                                          int64_t elem, int64_t lo, int64_t hi) {
+    u64 dmin = dirty[0], dmax = ~dirty[1];
+    if (dmin > dmax) return;
+    int64_t a = (int64_t)dmin > lo ? (int64_t)dmin : lo;
+    int64_t b = (int64_t)dmax + 1 < hi ? (int64_t)dmax + 1 : hi;
+    if (a >= b) return;
+    int64_t s = a * elem, e = b * elem;  // byte span
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    // 16-byte aligned body (replicas share alignment: cudaMalloc bases)
+    int64_t vs = (s + 15) & ~(int64_t)15, ve = e & ~(int64_t)15;
+    if (vs > ve) vs = ve = e;
+    for (int64_t p = s + tid; p < vs; p += nth)
+        for (int d = 0; d < dsts.n; d++) static_cast<char *>(dsts.p[d])[p] = src[p];
+    for (int64_t p = ve + tid; p < e; p += nth)
+        for (int d = 0; d < dsts.n; d++) static_cast<char *>(dsts.p[d])[p] = src[p];
+    const int64_t nv = (ve - vs) >> 4;
+    const int4 *s4 = reinterpret_cast<const int4 *>(src + vs);
+    int64_t q = tid;
+    for (; q + 3 * nth < nv; q += 4 * nth) {
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = __ldcs(s4 + q + u * nth);
+        for (int d = 0; d < dsts.n; d++) {
+            int4 *d4 = reinterpret_cast<int4 *>(static_cast<char *>(dsts.p[d]) + vs);
+#pragma unroll
+            for (int u = 0; u < 4; u++) d4[q + u * nth] = v[u];
+        }
+    }
+    for (; q < nv; q += nth) {
+        const int4 v = __ldcs(s4 + q);
+        for (int d = 0; d < dsts.n; d++)
+            reinterpret_cast<int4 *>(static_cast<char *>(dsts.p[d]) + vs)[q] = v;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) merge_bitmap_kernel(const T *__restrict__ src, PeerPtrs dsts,
+                                                           const uint32_t *__restrict__ bitmap,
+                                                           int64_t lo, int64_t hi) {
+    // one warp per group of 32 words: lane l reads word w0+l, then the warp
+    // walks the words; each dirty element is stored by its own lane, so the
+    // 32 elements of a word go out as one coalesced 128/256-byte segment.
+    const int lane = threadIdx.x & 31;
+    const int64_t wlo = lo >> 5, whi = (hi + 31) >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w0 = wlo + gw * 32; w0 < whi; w0 += nw * 32) {
+        const uint32_t mine = (w0 + lane < whi) ? __ldg(bitmap + w0 + lane) : 0u;
+        unsigned any = __ballot_sync(0xffffffffu, mine != 0u);
+        while (any) {
+            const int j = __ffs(any) - 1;
+            any &= any - 1;
+            const uint32_t bits = __shfl_sync(0xffffffffu, mine, j);
+            if ((bits >> lane) & 1u) {
+                const int64_t e = ((w0 + j) << 5) + lane;
+                const T v = src[e];
+                for (int d = 0; d < dsts.n; d++) static_cast<T *>(dsts.p[d])[e] = v;
+            }
+        }
+    }
+}
+
+inline int grid_for(int64_t work, int per_block, int max_blocks) {
+    int64_t g = (work + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (int)g;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------
+cudaError_t square_f32(cudaStream_t s, const float *y, float *x, int64_t i0, int64_t i1,
+                       int64_t x_off, u64 *dirty) {
+    if (i1 <= i0) return cudaSuccess;
+    square_f32_kernel<<<grid_for(i1 - i0, 256 * 4, 148 * 16), 256, 0, s>>>(y, x, i0, i1, x_off,
+                                                                           dirty);
+    return cudaGetLastError();
+}
+
+cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N, int64_t r0,
+                     int64_t r1, int64_t c0, int64_t c1, u64 *dirty, double *push_top,
+                     double *push_bot) {
+    if (r1 <= r0 || c1 <= c0) return cudaSuccess;
+    const bool v2 = (N % 2 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0) &&
+                    (!push_top || (uintptr_t)push_top % 16 == 0) &&
+                    (!push_bot || (uintptr_t)push_bot % 16 == 0);
+    const int V = v2 ? 2 : 1;
+    const int64_t cs_base = c0 & ~(int64_t)(V - 1);
+    const int64_t slab = 32 * V * JW;
+    const int64_t gx = (c1 - cs_base + slab - 1) / slab;
+    const int64_t ty = (r1 - r0 + JR - 1) / JR;
+    dim3 grid((unsigned)gx, (unsigned)(ty < 65535 ? ty : 65535));
+    if (v2)
+        jacobi2d_kernel<2><<<grid, JW * 32, 0, s>>>(src, dst, N, r0, r1, c0, c1, cs_base, ty, dirty,
+                                                    push_top, push_bot);
+    else
+        jacobi2d_kernel<1><<<grid, JW * 32, 0, s>>>(src, dst, N, r0, r1, c0, c1, cs_base, ty, dirty,
+                                                    push_top, push_bot);
+    return cudaGetLastError();
+}
+
+cudaError_t reduce_f64(cudaStream_t s, const double *x, const double *y, int64_t n,
+                       double *partials, unsigned *ticket, double *out) {
+    const bool vec = ((uintptr_t)x % 16 == 0) && (!y || (uintptr_t)y % 16 == 0);
+    if (y) {
+        if (vec) reduce_kernel<true, true><<<kReduceGrid, RT, 0, s>>>(x, y, n, partials, ticket, out);
+        else reduce_kernel<true, false><<<kReduceGrid, RT, 0, s>>>(x, y, n, partials, ticket, out);
+    } else {
+        if (vec) reduce_kernel<false, true><<<kReduceGrid, RT, 0, s>>>(x, y, n, partials, ticket, out);
+        else reduce_kernel<false, false><<<kReduceGrid, RT, 0, s>>>(x, y, n, partials, ticket, out);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t combine(cudaStream_t s, PeerPtrs parts, double s_in, double *out) {
+    combine_kernel<<<1, 1, 0, s>>>(parts, s_in, out);
+    return cudaGetLastError();
+}
+
+cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C, int64_t M,
+                     int64_t N, int64_t K, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                     u64 *dirty) {
+    if (r1 <= r0 || c1 <= c0 || K <= 0) return cudaSuccess;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gemm_f64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GSMEM);
+        cudaFuncSetAttribute(gemm_f64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GSMEM);
+        attr = true;
+    }
+    const bool v16 = (K % 2 == 0) && (N % 2 == 0) && (c0 % 2 == 0) && ((uintptr_t)A % 16 == 0) &&
+                     ((uintptr_t)B % 16 == 0) && ((uintptr_t)C % 16 == 0);
+    dim3 grid((unsigned)((c1 - c0 + GBN - 1) / GBN), (unsigned)((r1 - r0 + GBM - 1) / GBM));
+    if (v16)
+        gemm_f64_kernel<true><<<grid, 128, GSMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    else
+        gemm_f64_kernel<false><<<grid, 128, GSMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    return cudaGetLastError();
+}
+
+cudaError_t scatter_add_f64(cudaStream_t s, const int32_t *idx, const double *b, double *a,
+                            int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty) {
+    if (n <= 0) return cudaSuccess;
+    if ((uintptr_t)idx % 16 != 0) return cudaErrorInvalidValue;  // runtime guarantees alignment
+    scatter_add_kernel<double><<<grid_for(n, 256 * 4, 148 * 8), 256, 0, s>>>(idx, b, a, n, lo, hi,
+                                                                            bitmap, dirty);
+    return cudaGetLastError();
+}
+
+cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b, int32_t *a,
+                            int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty) {
+    if (n <= 0) return cudaSuccess;
+    if ((uintptr_t)idx % 16 != 0) return cudaErrorInvalidValue;
+    scatter_add_kernel<int32_t><<<grid_for(n, 256 * 4, 148 * 8), 256, 0, s>>>(idx, b, a, n, lo, hi,
+                                                                             bitmap, dirty);
+    return cudaGetLastError();
+}
+
+cudaError_t merge_range(cudaStream_t s, const void *src, PeerPtrs dsts, const u64 *dirty,
+                        int64_t elem, int64_t lo, int64_t hi) {
+    if (hi <= lo || dsts.n == 0) return cudaSuccess;
+    merge_range_kernel<<<grid_for((hi - lo) * elem, 256 * 16 * 4, 148 * 8), 256, 0, s>>>(
+        static_cast<const char *>(src), dsts, dirty, elem, lo, hi);
+    return cudaGetLastError();
+}
+
+cudaError_t merge_bitmap(cudaStream_t s, const void *src, PeerPtrs dsts, const uint32_t *bitmap,
+                         int64_t elem, int64_t lo, int64_t hi) {
+    if (hi <= lo || dsts.n == 0) return cudaSuccess;
+    const int64_t words = ((hi + 31) >> 5) - (lo >> 5);
+    const int g = grid_for(words, 8 * 32, 148 * 8);  // 8 warps x 32 words per block
+    if (elem == 8)
+        merge_bitmap_kernel<double><<<g, 256, 0, s>>>(static_cast<const double *>(src), dsts,
+                                                      bitmap, lo, hi);
+    else if (elem == 4)
+        merge_bitmap_kernel<int32_t><<<g, 256, 0, s>>>(static_cast<const int32_t *>(src), dsts,
+                                                       bitmap, lo, hi);
+    else
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+}  // namespace jk

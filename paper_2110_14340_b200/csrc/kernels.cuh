@@ -1,0 +1,69 @@
+// kernels.cuh -- launch wrappers of the sm_100a device kernels (internal to
+// libjacc.so; not part of the C-ABI).  Every wrapper enqueues on `s` and
+// returns the launch error.  Dirty records are two u64 in device memory:
+// d[0] = min stored flat index, d[1] = ~max stored flat index; both reset to
+// all-ones (one 16-byte memset) before a launch, so an untouched record
+// reads back as the empty set (UINT64_MAX, 0)  (DESIGN R-3, R-15).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace jk {
+
+using u64 = unsigned long long;
+constexpr int kMaxPeers = 16;
+
+struct PeerPtrs {
+    void *p[kMaxPeers];
+    int n;
+};
+
+// BK6  Listing 1: x[i] = y[i]*y[i] for i in [i0, i1); x and y
+// are the loop's arrays (already offset); dirty indices are x_off + i.
+cudaError_t square_f32(cudaStream_t s, const float *y, float *x, int64_t i0, int64_t i1,
+                       int64_t x_off, u64 *dirty);
+
+// BK1  PolyBench jacobi-2d sweep (DESIGN R-1) over rows [r0,r1) x cols
+// [c0,c1) of an N x N grid, with fused dirty-range tracking and fused HALO
+// push: row r0 is also stored into push_top, row r1-1 into push_bot (peer
+// replicas of dst, same layout; nullptr = no push).
+cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N,
+                     int64_t r0, int64_t r1, int64_t c0, int64_t c1, u64 *dirty,
+                     double *push_top, double *push_bot);
+
+// BK2  Fixed-order reduction of sum x[i]*y[i] (y != nullptr) or sum x[i]
+// over [0, n); result written to *out.  `partials` holds kReduceGrid
+// doubles, `ticket` one zeroed u32 (left zeroed on exit).
+constexpr int kReduceGrid = 148 * 4;
+cudaError_t reduce_f64(cudaStream_t s, const double *x, const double *y, int64_t n,
+                       double *partials, unsigned *ticket, double *out);
+
+// c8 combine on one device: *out = s_in + sum_d *parts[d] (device order).
+cudaError_t combine(cudaStream_t s, PeerPtrs parts, double s_in, double *out);
+
+// BK3  C[r0:r1, c0:c1] = A[r0:r1, :] * B[:, c0:c1] on the fp64 tensor pipe
+// (DMMA via mma.sync m8n8k4 f64), dirty-range tracking fused.
+cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C,
+                     int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1,
+                     int64_t c0, int64_t c1, u64 *dirty);
+
+// BK4  Owner-filtered scatter: for i in [0,n):
+// k = idx[i]; if lo <= k < hi: a[k] += b[i] (atomic); bitmap bit k set
+// (warp-aggregated atomicOr), dirty min/max of k.  a, bitmap indexed by
+// element of the whole region.
+cudaError_t scatter_add_f64(cudaStream_t s, const int32_t *idx, const double *b, double *a,
+                            int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty);
+cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b, int32_t *a,
+                            int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty);
+
+// BK5  Dirty-region merge over peer memory.  merge_range copies the
+// recorded span [dirty min, dirty max] (clamped to [lo, hi)) of src into
+// every peer replica; `max_elems` bounds the grid (host-known write bound).
+cudaError_t merge_range(cudaStream_t s, const void *src, PeerPtrs dsts, const u64 *dirty,
+                        int64_t elem, int64_t lo, int64_t hi);
+// merge_bitmap copies exactly the elements whose dirty bit is set within
+// [lo, hi) into every peer replica (elem = 4 or 8 bytes).
+cudaError_t merge_bitmap(cudaStream_t s, const void *src, PeerPtrs dsts, const uint32_t *bitmap,
+                         int64_t elem, int64_t lo, int64_t hi);
+
+}  // namespace jk

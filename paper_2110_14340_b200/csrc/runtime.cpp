@@ -1,0 +1,1145 @@
+// runtime.cpp -- host runtime of libjacc.so: the C-ABI of include/jacc.h.
+//
+//   a1  present table (ordered map, interior-address lookup)
+//   a2  update_device: H2D into every replica
+//   a3  launch planning: alias rule, owned blocks of the written
+//       array's split dimension (remainder rule S:266), clipped
+//       per-device iteration ranges, stale-input pulls (validity tracker)
+//   a4  device kernels with fused write tracking (kernels.cu)
+//   a5  reduction combine (NCCL allreduce across distinct GPUs)
+//   a6  dirty-region merge (EAGER P:471/P:527, or HALO)
+//   a7  update_host: gather stale owned intervals into the primary, D2H
+//   a8  wait
+//
+// Ordering between logical devices uses one CUDA event per device per launch
+// generation: launch k on device d waits for launch k-1 of every device it
+// exchanged data with in launch k-1 or exchanges with in launch k ("we
+// synchronize GPUs at the beginning and ending of the communication",
+// P:527).  That covers RAW on pushed/pulled data and WAR on peer replicas.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "jacc.h"
+#include "kernels.cuh"
+
+namespace {
+
+using u64 = unsigned long long;
+constexpr u64 kEmptyMin = ~0ull;
+
+// ---------------------------------------------------------------------------
+// Interval set over element indices (half-open), used for replica validity.
+// ---------------------------------------------------------------------------
+struct IntervalSet {
+    std::map<int64_t, int64_t> iv;  // start -> end
+
+    void add(int64_t a, int64_t b) {
+        if (a >= b) return;
+        auto it = iv.upper_bound(a);
+        if (it != iv.begin()) {
+            auto p = std::prev(it);
+            if (p->second >= a) {
+                a = p->first;
+                b = std::max(b, p->second);
+                it = iv.erase(p);
+            }
+        }
+        while (it != iv.end() && it->first <= b) {
+            b = std::max(b, it->second);
+            it = iv.erase(it);
+        }
+        iv[a] = b;
+    }
+    void remove(int64_t a, int64_t b) {
+        if (a >= b) return;
+        auto it = iv.upper_bound(a);
+        if (it != iv.begin()) --it;
+        std::vector<std::pair<int64_t, int64_t>> keep;
+        while (it != iv.end() && it->first < b) {
+            if (it->second <= a) {
+                ++it;
+                continue;
+            }
+            if (it->first < a) keep.push_back({it->first, a});
+            if (it->second > b) keep.push_back({b, it->second});
+            it = iv.erase(it);
+        }
+        for (auto &k : keep) iv[k.first] = k.second;
+    }
+    // sub-intervals of [a,b) NOT covered
+    std::vector<std::pair<int64_t, int64_t>> missing(int64_t a, int64_t b) const {
+        std::vector<std::pair<int64_t, int64_t>> out;
+        if (a >= b) return out;
+        int64_t cur = a;
+        auto it = iv.upper_bound(a);
+        if (it != iv.begin()) --it;
+        for (; it != iv.end() && it->first < b; ++it) {
+            if (it->second <= cur) continue;
+            if (it->first > cur) out.push_back({cur, std::min(it->first, b)});
+            cur = std::max(cur, it->second);
+            if (cur >= b) break;
+        }
+        if (cur < b) out.push_back({cur, b});
+        return out;
+    }
+    bool covers(int64_t a, int64_t b) const { return missing(a, b).empty(); }
+};
+
+// ---------------------------------------------------------------------------
+struct Device {
+    int ord = 0;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    double *partials = nullptr;  // kReduceGrid
+    unsigned *ticket = nullptr;
+    double *part = nullptr;      // this device's reduction partial
+    double *res = nullptr;       // allreduce result / combine output
+    double *hscal = nullptr;     // pinned host scalar
+    ncclComm_t comm = nullptr;
+    // profiling
+    double kernel_s = 0, merge_s = 0;
+    uint64_t launches = 0, bytes_merged = 0;
+};
+
+struct Region {
+    uintptr_t base = 0;
+    size_t bytes = 0, elem = 0;
+    int ndims = 0;
+    int64_t ext[3] = {1, 1, 1};
+    int64_t nelem = 0;
+    bool pinned = false;
+    std::vector<char *> rep;           // per device replica
+    std::vector<u64 *> dirty;          // per device [min, ~max]
+    std::vector<uint32_t *> bitmap;    // per device, lazily allocated
+    std::vector<IntervalSet> valid;    // per device
+};
+
+struct ProfRec {
+    int dev;
+    cudaEvent_t k0, k1, m1;
+};
+
+struct Runtime {
+    bool init = false;
+    bool poisoned = false;
+    int n = 0;
+    std::vector<Device> dev;
+    std::map<uintptr_t, std::unique_ptr<Region>> table;
+    int policy = JACC_MERGE_EAGER;
+    int mode = JACC_MODE_MULTI;
+    int gen = 0;
+    bool distinct = true;
+    bool use_nccl = false;
+    std::vector<std::vector<char>> comm_prev;  // [d][q]
+    bool profiling = false;
+    std::vector<ProfRec> prof;                 // unresolved event records
+    size_t last_start = 0;                     // first record of the last launch
+    std::vector<cudaEvent_t> evpool;
+    double last_k = 0, last_m = 0;
+    uint64_t last_bytes = 0;
+    bool last_valid = false;
+};
+
+Runtime R;
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+struct Fail {
+    jacc_status st;
+};
+
+void cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) {
+        if (getenv("JACC_DEBUG")) fprintf(stderr, "[jacc] %s: %s\n", what, cudaGetErrorString(e));
+        R.poisoned = true;
+        throw Fail{JACC_ERR_CUDA};
+    }
+}
+#define CK(x) cuda_check((x), #x)
+
+void nccl_check(ncclResult_t e, const char *what) {
+    if (e != ncclSuccess) {
+        if (getenv("JACC_DEBUG")) fprintf(stderr, "[jacc] %s: %s\n", what, ncclGetErrorString(e));
+        R.poisoned = true;
+        throw Fail{JACC_ERR_NCCL};
+    }
+}
+#define NK(x) nccl_check((x), #x)
+
+template <typename F>
+jacc_status guard(F &&f, bool need_init = true) {
+    if (need_init && (!R.init || R.poisoned)) return JACC_ERR_STATE;
+    try {
+        return f();
+    } catch (Fail &e) {
+        return e.st;
+    } catch (std::bad_alloc &) {
+        return JACC_ERR_OOM;
+    }
+}
+
+Region *lookup(const void *p) {
+    uintptr_t a = (uintptr_t)p;
+    auto it = R.table.upper_bound(a);
+    if (it == R.table.begin()) return nullptr;
+    --it;
+    Region *r = it->second.get();
+    return (a >= r->base && a < r->base + r->bytes) ? r : nullptr;
+}
+
+void set_dev(int d) { CK(cudaSetDevice(R.dev[d].ord)); }
+
+void sync_all() {
+    for (int d = 0; d < R.n; d++) {
+        set_dev(d);
+        CK(cudaStreamSynchronize(R.dev[d].s));
+    }
+}
+
+cudaEvent_t pool_event() {
+    if (!R.evpool.empty()) {
+        cudaEvent_t e = R.evpool.back();
+        R.evpool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+}
+
+// resolve the accumulated profiling records into totals (syncs on them;
+// called only on query, so timing never adds a host sync per launch)
+void flush_prof() {
+    if (R.prof.empty()) return;
+    double kmax = 0, mmax = 0;
+    for (size_t i = 0; i < R.prof.size(); i++) {
+        auto &p = R.prof[i];
+        set_dev(p.dev);
+        CK(cudaEventSynchronize(p.m1));
+        float k = 0, m = 0;
+        CK(cudaEventElapsedTime(&k, p.k0, p.k1));
+        CK(cudaEventElapsedTime(&m, p.k1, p.m1));
+        R.dev[p.dev].kernel_s += k * 1e-3;
+        R.dev[p.dev].merge_s += m * 1e-3;
+        if (i >= R.last_start) {
+            kmax = std::max(kmax, (double)k * 1e-3);
+            mmax = std::max(mmax, (double)m * 1e-3);
+        }
+        R.evpool.push_back(p.k0);
+        R.evpool.push_back(p.k1);
+        R.evpool.push_back(p.m1);
+    }
+    if (R.last_start < R.prof.size()) {
+        R.last_k = kmax;
+        R.last_m = mmax;
+        R.last_valid = true;
+    }
+    R.prof.clear();
+    R.last_start = 0;
+}
+
+void free_region(Region *r) {
+    for (int d = 0; d < (int)r->rep.size(); d++) {
+        set_dev(d);
+        if (r->rep[d]) cudaFree(r->rep[d]);
+        if (r->dirty[d]) cudaFree(r->dirty[d]);
+        if (r->bitmap[d]) cudaFree(r->bitmap[d]);
+    }
+    if (r->pinned) cudaHostUnregister((void *)r->base);
+}
+
+// c4 partition ("equally dividing"; S:266 remainder rule)
+void partition(int64_t E, int n, int d, int64_t &lo, int64_t &hi) {
+    const int64_t q = E / n, r = E % n;
+    lo = (int64_t)d * q + std::min<int64_t>(d, r);
+    hi = (int64_t)(d + 1) * q + std::min<int64_t>(d + 1, r);
+}
+
+// ---------------------------------------------------------------------------
+// loop descriptors (D12) and per-device plans
+// ---------------------------------------------------------------------------
+struct ArgInfo {
+    Region *reg = nullptr;
+    int64_t off = 0;  // element offset of the loop's array inside the region
+    int kind = 0;
+};
+
+struct Foot {  // read footprint: region, element interval
+    Region *reg;
+    int64_t lo, hi;
+};
+
+struct DevPlan {
+    bool active = false;
+    int64_t i0 = 0, i1 = 0, j0 = 0, j1 = 0;  // iteration sub-range
+    int64_t wlo = 0, whi = 0;                // write bound (elements of written region), [wlo,whi)
+    int64_t own_lo = 0, own_hi = 0;          // owned block of the split extent
+    std::vector<Foot> reads;
+};
+
+struct Desc {
+    int id;
+    const char *name;
+    int nargs;
+    int kinds[3];
+    size_t elems[3];   // required element sizes (0 = n/a)
+    int out_arg;       // index of written array (-1 none)
+    bool reduction;
+    int halo_rows;     // stencil radius along the split dim (HALO prediction)
+};
+
+const Desc kDescs[] = {
+    {JACC_LOOP_SQUARE_F32, "square_f32", 2, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT, 0}, {4, 4, 0}, 1, false, 0},
+    {JACC_LOOP_JACOBI2D_F64, "jacobi2d_f64", 2, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT, 0}, {8, 8, 0}, 1, false, 1},
+    {JACC_LOOP_DOT_F64, "dot_f64", 3, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_REDUCE_SUM_F64}, {8, 8, 0}, -1, true, 0},
+    {JACC_LOOP_SUM_F64, "sum_f64", 2, {JACC_ARG_ARRAY_IN, JACC_ARG_REDUCE_SUM_F64, 0}, {8, 0, 0}, -1, true, 0},
+    {JACC_LOOP_GEMM_F64, "gemm_f64", 3, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT}, {8, 8, 8}, 2, false, 0},
+    {JACC_LOOP_SCATTER_ADD_F64, "scatter_add_f64", 3, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_INOUT}, {4, 8, 8}, 2, false, 0},
+    {JACC_LOOP_SCATTER_ADD_I32, "scatter_add_i32", 3, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_INOUT}, {4, 4, 4}, 2, false, 0},
+};
+
+const Desc *find_desc(int id) {
+    for (auto &d : kDescs)
+        if (d.id == id) return &d;
+    return nullptr;
+}
+
+void invalid_if(bool c) {
+    if (c) throw Fail{JACC_ERR_INVALID};
+}
+
+// ---------------------------------------------------------------------------
+// the launch
+// ---------------------------------------------------------------------------
+struct Launch {
+    const Desc *D;
+    std::vector<ArgInfo> a;
+    jacc_range rg;
+    bool dup = false;
+    std::vector<DevPlan> plan;
+    double *red_ptr = nullptr;
+    // loop-specific shapes
+    int64_t n1 = 0;            // 1-D length (square, dot, sum, scatter iterations)
+    int64_t N = 0;             // jacobi grid
+    int64_t M = 0, Nn = 0, K = 0;  // gemm
+};
+
+void plan_launch(Launch &L) {
+    const int n = R.n;
+    L.plan.assign(n, DevPlan{});
+    const int id = L.D->id;
+    for (int d = 0; d < n; d++) {
+        DevPlan &p = L.plan[d];
+        const int nd = L.dup ? 1 : n, dd = L.dup ? 0 : d;
+        if (id == JACC_LOOP_SQUARE_F32) {
+            // x written: split x's dim 0 (its whole region extent)
+            Region *xr = L.a[1].reg;
+            partition(xr->nelem, nd, dd, p.own_lo, p.own_hi);
+            const int64_t xo = L.a[1].off;
+            p.i0 = std::max(L.rg.lo[0], p.own_lo - xo);
+            p.i1 = std::min(L.rg.hi[0], p.own_hi - xo);
+            p.active = p.i1 > p.i0;
+            if (p.active) {
+                p.wlo = xo + p.i0;
+                p.whi = xo + p.i1;
+                p.reads.push_back({L.a[0].reg, L.a[0].off + p.i0, L.a[0].off + p.i1});
+            }
+        } else if (id == JACC_LOOP_JACOBI2D_F64) {
+            const int64_t N = L.N;
+            partition(N, nd, dd, p.own_lo, p.own_hi);  // rows of dst
+            p.i0 = std::max(L.rg.lo[0], p.own_lo);
+            p.i1 = std::min(L.rg.hi[0], p.own_hi);
+            p.j0 = L.rg.lo[1];
+            p.j1 = L.rg.hi[1];
+            p.active = p.i1 > p.i0 && p.j1 > p.j0;
+            if (p.active) {
+                p.wlo = p.i0 * N + p.j0;
+                p.whi = (p.i1 - 1) * N + p.j1;
+                p.reads.push_back({L.a[0].reg, (p.i0 - 1) * N, (p.i1 + 1) * N});
+            }
+        } else if (id == JACC_LOOP_DOT_F64 || id == JACC_LOOP_SUM_F64) {
+            // reductions: filter by the outermost parallel iterator
+            int64_t lo, hi;
+            partition(L.rg.hi[0] - L.rg.lo[0], nd, dd, lo, hi);
+            p.i0 = L.rg.lo[0] + lo;
+            p.i1 = L.rg.lo[0] + hi;
+            p.active = p.i1 > p.i0;
+            const int narr = id == JACC_LOOP_DOT_F64 ? 2 : 1;
+            if (p.active)
+                for (int k = 0; k < narr; k++)
+                    p.reads.push_back({L.a[k].reg, L.a[k].off + p.i0, L.a[k].off + p.i1});
+        } else if (id == JACC_LOOP_GEMM_F64) {
+            partition(L.M, nd, dd, p.own_lo, p.own_hi);  // rows of C
+            p.i0 = std::max(L.rg.lo[0], p.own_lo);
+            p.i1 = std::min(L.rg.hi[0], p.own_hi);
+            p.j0 = L.rg.lo[1];
+            p.j1 = L.rg.hi[1];
+            p.active = p.i1 > p.i0 && p.j1 > p.j0;
+            if (p.active) {
+                p.wlo = p.i0 * L.Nn + p.j0;
+                p.whi = (p.i1 - 1) * L.Nn + p.j1;
+                p.reads.push_back({L.a[0].reg, p.i0 * L.K, p.i1 * L.K});
+                p.reads.push_back({L.a[1].reg, 0, L.K * L.Nn});
+            }
+        } else {  // scatter: owned slice of a; every device scans all i
+            Region *ar = L.a[2].reg;
+            partition(ar->nelem, nd, dd, p.own_lo, p.own_hi);
+            p.i0 = L.rg.lo[0];
+            p.i1 = L.rg.hi[0];
+            p.active = p.i1 > p.i0 && p.own_hi > p.own_lo;
+            if (p.active) {
+                p.wlo = p.own_lo;
+                p.whi = p.own_hi;
+                p.reads.push_back({L.a[0].reg, L.a[0].off + p.i0, L.a[0].off + p.i1});
+                p.reads.push_back({L.a[1].reg, L.a[1].off + p.i0, L.a[1].off + p.i1});
+                p.reads.push_back({ar, p.own_lo, p.own_hi});
+            }
+        }
+    }
+}
+
+// HALO: which rows of device d's written block do neighbour p's next
+// footprint (its written rows +- halo radius) cover?  Returns the push
+// targets for the first and last written row (Jacobi).
+void halo_targets(const Launch &L, int d, int &top, int &bot) {
+    top = bot = -1;
+    const DevPlan &me = L.plan[d];
+    if (!me.active) return;
+    for (int p = 0; p < R.n; p++) {
+        if (p == d || !L.plan[p].active) continue;
+        const int64_t flo = L.plan[p].i0 - L.D->halo_rows, fhi = L.plan[p].i1 + L.D->halo_rows;
+        if (me.i0 >= flo && me.i0 < fhi) top = p;
+        if (me.i1 - 1 >= flo && me.i1 - 1 < fhi) bot = p;
+    }
+}
+
+struct Pull {
+    int dst, src;
+    Region *reg;
+    int64_t lo, hi;
+};
+
+jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args, int nargs,
+                      int async_id) {
+    const Desc *D = find_desc(loop_id);
+    if (!D) return JACC_ERR_UNKNOWN_LOOP;
+    invalid_if(nargs != D->nargs || (nargs > 0 && !args));
+    Launch L;
+    L.D = D;
+    L.a.resize(nargs);
+    for (int k = 0; k < nargs; k++) {
+        invalid_if(args[k].kind != D->kinds[k]);
+        L.a[k].kind = args[k].kind;
+        if (args[k].kind == JACC_ARG_REDUCE_SUM_F64) {
+            invalid_if(!args[k].ptr);
+            L.red_ptr = static_cast<double *>(args[k].ptr);
+            continue;
+        }
+        Region *r = lookup(args[k].ptr);
+        if (!r) throw Fail{JACC_ERR_NOT_PRESENT};
+        invalid_if(r->elem != D->elems[k]);
+        const uintptr_t boff = (uintptr_t)args[k].ptr - r->base;
+        invalid_if(boff % r->elem != 0);
+        L.a[k].reg = r;
+        L.a[k].off = (int64_t)(boff / r->elem);
+    }
+    // ---- shapes and ranges -------------------------------------------------
+    jacc_range rg{};
+    const int id = D->id;
+    if (id == JACC_LOOP_JACOBI2D_F64) {
+        Region *s = L.a[0].reg, *t = L.a[1].reg;
+        invalid_if(s->ndims != 2 || t->ndims != 2 || L.a[0].off || L.a[1].off);
+        invalid_if(s->ext[0] != s->ext[1] || t->ext[0] != s->ext[0] || t->ext[1] != s->ext[1]);
+        invalid_if(s == t);  // in-place stencil: a race in OpenACC (R-12)
+        L.N = s->ext[0];
+        rg.ndims = 2;
+        rg.lo[0] = rg.lo[1] = 1;
+        rg.hi[0] = rg.hi[1] = L.N - 1;
+        if (range) {
+            invalid_if(range->ndims != 2);
+            for (int k = 0; k < 2; k++) {
+                invalid_if(range->lo[k] < 1 || range->hi[k] > L.N - 1);
+                rg.lo[k] = range->lo[k];
+                rg.hi[k] = std::max(range->lo[k], range->hi[k]);
+            }
+        }
+    } else if (id == JACC_LOOP_GEMM_F64) {
+        Region *A = L.a[0].reg, *B = L.a[1].reg, *C = L.a[2].reg;
+        invalid_if(A->ndims != 2 || B->ndims != 2 || C->ndims != 2);
+        invalid_if(L.a[0].off || L.a[1].off || L.a[2].off);
+        L.M = A->ext[0];
+        L.K = A->ext[1];
+        L.Nn = B->ext[1];
+        invalid_if(B->ext[0] != L.K || C->ext[0] != L.M || C->ext[1] != L.Nn);
+        invalid_if(C == A || C == B);  // in-place GEMM is a race (R-12)
+        rg.ndims = 2;
+        rg.lo[0] = rg.lo[1] = 0;
+        rg.hi[0] = L.M;
+        rg.hi[1] = L.Nn;
+        if (range) {
+            invalid_if(range->ndims != 2);
+            invalid_if(range->lo[0] < 0 || range->hi[0] > L.M || range->lo[1] < 0 ||
+                       range->hi[1] > L.Nn);
+            for (int k = 0; k < 2; k++) {
+                rg.lo[k] = range->lo[k];
+                rg.hi[k] = std::max(range->lo[k], range->hi[k]);
+            }
+        }
+    } else {
+        // 1-D loops: range over i; arrays must hold [off+lo, off+hi)
+        invalid_if(!range || range->ndims != 1 || range->lo[0] < 0 || range->hi[0] < range->lo[0]);
+        rg = *range;
+        for (int k = 0; k < nargs; k++) {
+            if (!L.a[k].reg) continue;
+            if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
+                if (k == 2) continue;  // a is indexed by idx values
+            }
+            invalid_if(L.a[k].off + rg.hi[0] > L.a[k].reg->nelem);
+        }
+        if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
+            invalid_if(L.a[2].off != 0);
+            invalid_if(L.a[2].reg == L.a[0].reg || L.a[2].reg == L.a[1].reg);  // race (R-12)
+            invalid_if(((L.a[0].off * 4) % 16) != 0);  // idx 16-byte aligned for int4 loads
+        }
+        if (id == JACC_LOOP_SQUARE_F32 && L.a[0].reg == L.a[1].reg) {
+            // two pointers to one array, one read and one written:
+            // duplicate computation, no communication (R-12)
+            L.dup = true;
+        }
+    }
+    L.rg = rg;
+    if (R.mode == JACC_MODE_DUP) L.dup = true;
+    plan_launch(L);
+
+    const int n = R.n;
+    const int out = D->out_arg;
+    Region *W = out >= 0 ? L.a[out].reg : nullptr;
+    // elements of the write block the kernel may leave untouched must be
+    // current on the owner before it is declared valid there (normally a
+    // no-op: an owner is the only writer of its block)
+    if (W && id != JACC_LOOP_SCATTER_ADD_F64 && id != JACC_LOOP_SCATTER_ADD_I32)
+        for (int d = 0; d < n; d++)
+            if (L.plan[d].active) L.plan[d].reads.push_back({W, L.plan[d].wlo, L.plan[d].whi});
+
+    // ---- pulls: stale input intervals (validity tracker) -------------------
+    std::vector<Pull> pulls;
+    std::vector<std::vector<char>> comm(n, std::vector<char>(n, 0));
+    for (int d = 0; d < n; d++) {
+        for (const Foot &f : L.plan[d].reads) {
+            for (auto &m : f.reg->valid[d].missing(f.lo, f.hi)) {
+                int64_t a = m.first;
+                while (a < m.second) {
+                    int src = -1;
+                    int64_t b = m.second;
+                    for (int q = 0; q < n && src < 0; q++) {
+                        if (q == d) continue;
+                        auto &vi = f.reg->valid[q].iv;
+                        auto it = vi.upper_bound(a);
+                        if (it == vi.begin()) continue;
+                        --it;
+                        if (it->first <= a && it->second > a) {
+                            src = q;
+                            b = std::min(b, it->second);
+                        }
+                    }
+                    if (src < 0) {
+                        // never written anywhere valid (uninitialised data): nothing to pull
+                        break;
+                    }
+                    pulls.push_back({d, src, f.reg, a, b});
+                    comm[d][src] = comm[src][d] = 1;
+                    a = b;
+                }
+            }
+        }
+    }
+
+    // ---- merge pattern ------------------------------------------------------
+    std::vector<int> top(n, -1), bot(n, -1);
+    const bool writes = W && !L.dup;
+    if (writes) {
+        for (int d = 0; d < n; d++) {
+            if (!L.plan[d].active) continue;
+            if (R.policy == JACC_MERGE_EAGER) {
+                for (int p = 0; p < n; p++)
+                    if (p != d) comm[d][p] = comm[p][d] = 1;
+            } else if (D->halo_rows > 0) {
+                halo_targets(L, d, top[d], bot[d]);
+                if (top[d] >= 0) comm[d][top[d]] = comm[top[d]][d] = 1;
+                if (bot[d] >= 0) comm[d][bot[d]] = comm[bot[d]][d] = 1;
+            }
+        }
+    }
+    if (R.comm_prev.empty()) R.comm_prev.assign(n, std::vector<char>(n, 0));
+
+    // ---- enqueue per device -------------------------------------------------
+    if (R.prof.size() > 30000) flush_prof();
+    R.last_start = R.prof.size();
+    const int cur = R.gen & 1, prev = cur ^ 1;
+    const bool prof = R.profiling;
+    uint64_t merged_bytes = 0;
+    if (W && !L.dup && (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32)) {
+        const size_t words = (size_t)((W->nelem + 31) / 32);
+        for (int d = 0; d < n; d++)
+            if (!W->bitmap[d]) {
+                set_dev(d);
+                CK(cudaMalloc(&W->bitmap[d], words * 4));
+                CK(cudaMemsetAsync(W->bitmap[d], 0, words * 4, R.dev[d].s));
+            }
+    }
+    for (int d = 0; d < n; d++) {
+        Device &dv = R.dev[d];
+        const DevPlan &p = L.plan[d];
+        set_dev(d);
+        for (int q = 0; q < n; q++)
+            if (q != d && (comm[d][q] || R.comm_prev[d][q]))
+                CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
+        for (const Pull &pl : pulls) {
+            if (pl.dst != d) continue;
+            const size_t e = pl.reg->elem;
+            CK(cudaMemcpyPeerAsync(pl.reg->rep[d] + pl.lo * e, dv.ord, pl.reg->rep[pl.src] + pl.lo * e,
+                                   R.dev[pl.src].ord, (size_t)(pl.hi - pl.lo) * e, dv.s));
+            merged_bytes += (uint64_t)(pl.hi - pl.lo) * e;
+        }
+        ProfRec pr{d, nullptr, nullptr, nullptr};
+        if (prof) {
+            pr.k0 = pool_event();
+            pr.k1 = pool_event();
+            pr.m1 = pool_event();
+            CK(cudaEventRecord(pr.k0, dv.s));
+        }
+        if (W) CK(cudaMemsetAsync(W->dirty[d], 0xff, 16, dv.s));
+        if (p.active) {
+            switch (id) {
+            case JACC_LOOP_SQUARE_F32: {
+                const float *y = reinterpret_cast<const float *>(L.a[0].reg->rep[d]) + L.a[0].off;
+                float *x = reinterpret_cast<float *>(L.a[1].reg->rep[d]) + L.a[1].off;
+                CK(jk::square_f32(dv.s, y, x, p.i0, p.i1, L.a[1].off, W->dirty[d]));
+                break;
+            }
+            case JACC_LOOP_JACOBI2D_F64: {
+                double *pt = top[d] >= 0 ? reinterpret_cast<double *>(W->rep[top[d]]) : nullptr;
+                double *pb = bot[d] >= 0 ? reinterpret_cast<double *>(W->rep[bot[d]]) : nullptr;
+                CK(jk::jacobi2d(dv.s, reinterpret_cast<const double *>(L.a[0].reg->rep[d]),
+                                reinterpret_cast<double *>(W->rep[d]), L.N, p.i0, p.i1, p.j0, p.j1,
+                                W->dirty[d], pt, pb));
+                int64_t rowb = (p.j1 - p.j0) * 8;
+                if (pt) merged_bytes += rowb;
+                if (pb) merged_bytes += rowb;
+                break;
+            }
+            case JACC_LOOP_DOT_F64:
+            case JACC_LOOP_SUM_F64: {
+                const double *x = reinterpret_cast<const double *>(L.a[0].reg->rep[d]) + L.a[0].off;
+                const double *y = id == JACC_LOOP_DOT_F64
+                                      ? reinterpret_cast<const double *>(L.a[1].reg->rep[d]) + L.a[1].off
+                                      : nullptr;
+                CK(jk::reduce_f64(dv.s, x + p.i0, y ? y + p.i0 : nullptr, p.i1 - p.i0, dv.partials,
+                                  dv.ticket, dv.part));
+                break;
+            }
+            case JACC_LOOP_GEMM_F64:
+                CK(jk::gemm_f64(dv.s, reinterpret_cast<const double *>(L.a[0].reg->rep[d]),
+                                reinterpret_cast<const double *>(L.a[1].reg->rep[d]),
+                                reinterpret_cast<double *>(W->rep[d]), L.M, L.Nn, L.K, p.i0, p.i1,
+                                p.j0, p.j1, W->dirty[d]));
+                break;
+            case JACC_LOOP_SCATTER_ADD_F64:
+            case JACC_LOOP_SCATTER_ADD_I32: {
+                const int32_t *ix = reinterpret_cast<const int32_t *>(L.a[0].reg->rep[d]) + L.a[0].off + p.i0;
+                uint32_t *bm = W->bitmap[d];
+                if (!L.dup) {
+                    const int64_t w0 = p.own_lo >> 5, w1 = (p.own_hi + 31) >> 5;
+                    CK(cudaMemsetAsync(bm + w0, 0, (size_t)(w1 - w0) * 4, dv.s));
+                }
+                if (id == JACC_LOOP_SCATTER_ADD_F64) {
+                    const double *b = reinterpret_cast<const double *>(L.a[1].reg->rep[d]) + L.a[1].off + p.i0;
+                    CK(jk::scatter_add_f64(dv.s, ix, b, reinterpret_cast<double *>(W->rep[d]),
+                                           p.i1 - p.i0, p.own_lo, p.own_hi, bm, W->dirty[d]));
+                } else {
+                    const int32_t *b = reinterpret_cast<const int32_t *>(L.a[1].reg->rep[d]) + L.a[1].off + p.i0;
+                    CK(jk::scatter_add_i32(dv.s, ix, b, reinterpret_cast<int32_t *>(W->rep[d]),
+                                           p.i1 - p.i0, p.own_lo, p.own_hi, bm, W->dirty[d]));
+                }
+                break;
+            }
+            }
+        } else if (D->reduction) {
+            CK(cudaMemsetAsync(dv.part, 0, 8, dv.s));
+        }
+        if (prof) CK(cudaEventRecord(pr.k1, dv.s));
+        // ---- EAGER merge: push the recorded dirty region to every peer ----
+        if (writes && p.active && R.policy == JACC_MERGE_EAGER && n > 1) {
+            jk::PeerPtrs pp{};
+            for (int q = 0; q < n; q++)
+                if (q != d) pp.p[pp.n++] = W->rep[q];
+            if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
+                CK(jk::merge_bitmap(dv.s, W->rep[d], pp, W->bitmap[d], (int64_t)W->elem, p.wlo, p.whi));
+            } else {
+                CK(jk::merge_range(dv.s, W->rep[d], pp, W->dirty[d], (int64_t)W->elem, p.wlo, p.whi));
+            }
+            merged_bytes += (uint64_t)(p.whi - p.wlo) * W->elem * (n - 1);  // upper bound (host view)
+        }
+        if (prof) {
+            CK(cudaEventRecord(pr.m1, dv.s));
+            R.prof.push_back(pr);
+        }
+        CK(cudaEventRecord(dv.ev[cur], dv.s));
+        dv.launches++;
+    }
+
+    // ---- validity bookkeeping ---------------------------------------------
+    for (const Pull &pl : pulls) pl.reg->valid[pl.dst].add(pl.lo, pl.hi);
+    if (writes) {
+        for (int d = 0; d < n; d++) {
+            const DevPlan &p = L.plan[d];
+            if (!p.active) continue;
+            W->valid[d].add(p.wlo, p.whi);
+            if (R.policy == JACC_MERGE_EAGER) continue;  // every peer received the dirty set
+            for (int q = 0; q < n; q++) {
+                if (q == d) continue;
+                // q keeps validity only on the rows pushed to it (HALO)
+                std::vector<std::pair<int64_t, int64_t>> keep;
+                if (id == JACC_LOOP_JACOBI2D_F64) {
+                    if (top[d] == q) keep.push_back({p.i0 * L.N, (p.i0 + 1) * L.N});
+                    if (bot[d] == q) keep.push_back({(p.i1 - 1) * L.N, p.i1 * L.N});
+                }
+                std::vector<std::pair<int64_t, int64_t>> had;
+                for (auto &k : keep) {
+                    // only what q already had valid stays valid
+                    IntervalSet tmp;
+                    tmp.add(k.first, k.second);
+                    for (auto &m : W->valid[q].missing(k.first, k.second)) tmp.remove(m.first, m.second);
+                    for (auto &iv : tmp.iv) had.push_back(iv);
+                }
+                W->valid[q].remove(p.wlo, p.whi);
+                for (auto &h : had) W->valid[q].add(h.first, h.second);
+            }
+        }
+    }
+    R.dev[0].bytes_merged += merged_bytes;
+    R.last_bytes = merged_bytes;
+    R.comm_prev = comm;
+    R.gen++;
+
+    // ---- reduction combine (obligatory sync) -------------------
+    if (D->reduction) {
+        Device &d0 = R.dev[0];
+        const double s_in = *L.red_ptr;
+        if (R.use_nccl) {
+            NK(ncclGroupStart());
+            for (int d = 0; d < n; d++)
+                NK(ncclAllReduce(R.dev[d].part, R.dev[d].res, 1, ncclDouble, ncclSum, R.dev[d].comm,
+                                 R.dev[d].s));
+            NK(ncclGroupEnd());
+            set_dev(0);
+            jk::PeerPtrs pp{};
+            pp.p[0] = d0.res;
+            pp.n = 1;
+            CK(jk::combine(d0.s, pp, s_in, d0.res));
+        } else {
+            set_dev(0);
+            for (int d = 1; d < n; d++) CK(cudaStreamWaitEvent(d0.s, R.dev[d].ev[cur], 0));
+            jk::PeerPtrs pp{};
+            for (int d = 0; d < n; d++) pp.p[pp.n++] = R.dev[d].part;
+            CK(jk::combine(d0.s, pp, s_in, d0.res));
+        }
+        CK(cudaMemcpyAsync(d0.hscal, d0.res, 8, cudaMemcpyDeviceToHost, d0.s));
+        CK(cudaStreamSynchronize(d0.s));
+        *L.red_ptr = *d0.hscal;
+        if (R.use_nccl) {
+            // the combine ran after each device's allreduce: refresh events
+            for (int d = 0; d < n; d++) {
+                set_dev(d);
+                CK(cudaEventRecord(R.dev[d].ev[cur], R.dev[d].s));
+            }
+        }
+    }
+    if (async_id < 0) sync_all();
+    return JACC_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+jacc_status jacc_init(int n_devices, const int *device_ids) {
+    if (R.init) return JACC_ERR_STATE;
+    return guard(
+        [&]() -> jacc_status {
+            int count = 0;
+            if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1) return JACC_ERR_CUDA;
+            if (n_devices < 1 || n_devices > JACC_MAX_DEVICES) return JACC_ERR_INVALID;
+            std::vector<int> ords(n_devices);
+            for (int d = 0; d < n_devices; d++) {
+                ords[d] = device_ids ? device_ids[d] : d;
+                if (ords[d] < 0 || ords[d] >= count) return JACC_ERR_INVALID;
+            }
+            R = Runtime{};
+            R.n = n_devices;
+            R.dev.resize(n_devices);
+            for (int d = 0; d < n_devices; d++)
+                for (int q = 0; q < d; q++)
+                    if (ords[q] == ords[d]) R.distinct = false;
+            const char *pol = getenv("JACC_MERGE");
+            if (pol && !strcmp(pol, "halo")) R.policy = JACC_MERGE_HALO;
+            R.init = true;
+            for (int d = 0; d < n_devices; d++) {
+                Device &dv = R.dev[d];
+                dv.ord = ords[d];
+                set_dev(d);
+                CK(cudaStreamCreateWithFlags(&dv.s, cudaStreamNonBlocking));
+                CK(cudaEventCreateWithFlags(&dv.ev[0], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&dv.ev[1], cudaEventDisableTiming));
+                CK(cudaEventRecord(dv.ev[0], dv.s));
+                CK(cudaEventRecord(dv.ev[1], dv.s));
+                CK(cudaMalloc(&dv.partials, jk::kReduceGrid * sizeof(double)));
+                CK(cudaMalloc(&dv.ticket, 64));
+                CK(cudaMemset(dv.ticket, 0, 64));
+                CK(cudaMalloc(&dv.part, 8));
+                CK(cudaMalloc(&dv.res, 8));
+                CK(cudaMemset(dv.part, 0, 8));
+                CK(cudaMallocHost(&dv.hscal, 8));
+            }
+            // peer access between distinct GPUs (NVLink / NVSwitch P2P)
+            for (int d = 0; d < n_devices; d++)
+                for (int q = 0; q < n_devices; q++) {
+                    if (ords[d] == ords[q]) continue;
+                    int ok = 0;
+                    CK(cudaDeviceCanAccessPeer(&ok, ords[d], ords[q]));
+                    if (!ok) {
+                        R.poisoned = true;
+                        return JACC_ERR_INVALID;
+                    }
+                    set_dev(d);
+                    cudaError_t e = cudaDeviceEnablePeerAccess(ords[q], 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else CK(e);
+                }
+            if (n_devices > 1 && R.distinct) {
+                std::vector<ncclComm_t> comms(n_devices);
+                NK(ncclCommInitAll(comms.data(), n_devices, ords.data()));
+                for (int d = 0; d < n_devices; d++) R.dev[d].comm = comms[d];
+                R.use_nccl = true;
+            }
+            R.comm_prev.assign(n_devices, std::vector<char>(n_devices, 0));
+            return JACC_OK;
+        },
+        false);
+}
+
+jacc_status jacc_finalize(void) {
+    if (!R.init) return JACC_ERR_STATE;
+    for (int d = 0; d < R.n; d++) {
+        cudaSetDevice(R.dev[d].ord);
+        cudaStreamSynchronize(R.dev[d].s);
+    }
+    for (auto &kv : R.table) free_region(kv.second.get());
+    R.table.clear();
+    for (auto &p : R.prof) {
+        R.evpool.push_back(p.k0);
+        R.evpool.push_back(p.k1);
+        R.evpool.push_back(p.m1);
+    }
+    for (auto e : R.evpool) cudaEventDestroy(e);
+    for (int d = 0; d < R.n; d++) {
+        Device &dv = R.dev[d];
+        cudaSetDevice(dv.ord);
+        if (dv.comm) ncclCommDestroy(dv.comm);
+        cudaFree(dv.partials);
+        cudaFree(dv.ticket);
+        cudaFree(dv.part);
+        cudaFree(dv.res);
+        cudaFreeHost(dv.hscal);
+        cudaEventDestroy(dv.ev[0]);
+        cudaEventDestroy(dv.ev[1]);
+        cudaStreamDestroy(dv.s);
+    }
+    cudaGetLastError();
+    R = Runtime{};
+    return JACC_OK;
+}
+
+int jacc_num_devices(void) { return R.init ? R.n : 0; }
+
+jacc_status jacc_partition(int64_t E, int n, int d, int64_t *lo, int64_t *hi) {
+    if (E < 0 || n < 1 || d < 0 || d >= n || !lo || !hi) return JACC_ERR_INVALID;
+    partition(E, n, d, *lo, *hi);
+    return JACC_OK;
+}
+
+jacc_status jacc_set_merge_policy(int policy) {
+    if (!R.init || R.poisoned) return JACC_ERR_STATE;
+    if (policy != JACC_MERGE_EAGER && policy != JACC_MERGE_HALO) return JACC_ERR_INVALID;
+    R.policy = policy;
+    return JACC_OK;
+}
+
+jacc_status jacc_set_mode(int mode) {
+    if (!R.init || R.poisoned) return JACC_ERR_STATE;
+    if (mode != JACC_MODE_MULTI && mode != JACC_MODE_DUP) return JACC_ERR_INVALID;
+    R.mode = mode;
+    return JACC_OK;
+}
+
+jacc_status jacc_data_create(void *host, size_t bytes, size_t elem_size, int ndims,
+                             const int64_t *extents) {
+    return guard([&]() -> jacc_status {
+        if (!host || bytes == 0 || elem_size == 0 || ndims < 1 || ndims > 3 || !extents)
+            return JACC_ERR_INVALID;
+        int64_t prod = 1;
+        for (int k = 0; k < ndims; k++) {
+            if (extents[k] < 1) return JACC_ERR_INVALID;
+            prod *= extents[k];
+        }
+        if ((size_t)prod * elem_size != bytes) return JACC_ERR_INVALID;
+        const uintptr_t a = (uintptr_t)host;
+        // overlap with a present region
+        auto it = R.table.lower_bound(a);
+        if (it != R.table.end() && it->first < a + bytes) return JACC_ERR_OVERLAP;
+        if (it != R.table.begin()) {
+            auto p = std::prev(it);
+            if (p->second->base + p->second->bytes > a) return JACC_ERR_OVERLAP;
+        }
+        auto r = std::make_unique<Region>();
+        r->base = a;
+        r->bytes = bytes;
+        r->elem = elem_size;
+        r->ndims = ndims;
+        for (int k = 0; k < ndims; k++) r->ext[k] = extents[k];
+        r->nelem = prod;
+        r->rep.assign(R.n, nullptr);
+        r->dirty.assign(R.n, nullptr);
+        r->bitmap.assign(R.n, nullptr);
+        r->valid.assign(R.n, IntervalSet{});
+        for (int d = 0; d < R.n; d++) {
+            set_dev(d);
+            if (cudaMalloc(&r->rep[d], bytes) != cudaSuccess ||
+                cudaMalloc(&r->dirty[d], 16) != cudaSuccess) {
+                cudaGetLastError();
+                free_region(r.get());
+                return JACC_ERR_OOM;
+            }
+            CK(cudaMemset(r->dirty[d], 0xff, 16));
+        }
+        // pin large host buffers so update_device/update_host are DMA-direct
+        if (bytes >= (1u << 20) && !getenv("JACC_NO_PIN")) {
+            cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterPortable);
+            if (e == cudaSuccess) r->pinned = true;
+            else cudaGetLastError();
+        }
+        R.table[a] = std::move(r);
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_data_delete(void *host) {
+    return guard([&]() -> jacc_status {
+        Region *r = lookup(host);
+        if (!r) return JACC_ERR_NOT_PRESENT;
+        sync_all();
+        free_region(r);
+        R.table.erase(r->base);
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_update_device(void *host, size_t off, size_t bytes) {
+    return guard([&]() -> jacc_status {
+        Region *r = lookup(host);
+        if (!r) return JACC_ERR_NOT_PRESENT;
+        const size_t start = ((uintptr_t)host - r->base) + off;
+        if (start + bytes > r->bytes || start % r->elem || bytes % r->elem) return JACC_ERR_INVALID;
+        if (bytes == 0) return JACC_OK;
+        sync_all();
+        for (int d = 0; d < R.n; d++) {
+            set_dev(d);
+            CK(cudaMemcpyAsync(r->rep[d] + start, (const char *)r->base + start, bytes,
+                               cudaMemcpyHostToDevice, R.dev[d].s));
+        }
+        sync_all();
+        const int64_t e0 = (int64_t)(start / r->elem), e1 = (int64_t)((start + bytes) / r->elem);
+        for (int d = 0; d < R.n; d++) r->valid[d].add(e0, e1);
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_update_host(void *host, size_t off, size_t bytes) {
+    return guard([&]() -> jacc_status {
+        Region *r = lookup(host);
+        if (!r) return JACC_ERR_NOT_PRESENT;
+        const size_t start = ((uintptr_t)host - r->base) + off;
+        if (start + bytes > r->bytes || start % r->elem || bytes % r->elem) return JACC_ERR_INVALID;
+        if (bytes == 0) return JACC_OK;
+        sync_all();
+        const int64_t e0 = (int64_t)(start / r->elem), e1 = (int64_t)((start + bytes) / r->elem);
+        // gather: pull stale intervals into the primary from a valid replica
+        Device &d0 = R.dev[0];
+        set_dev(0);
+        for (auto &m : r->valid[0].missing(e0, e1)) {
+            int64_t a = m.first;
+            while (a < m.second) {
+                int src = -1;
+                int64_t b = m.second;
+                for (int q = 1; q < R.n && src < 0; q++) {
+                    auto &vi = r->valid[q].iv;
+                    auto it = vi.upper_bound(a);
+                    if (it == vi.begin()) continue;
+                    --it;
+                    if (it->first <= a && it->second > a) {
+                        src = q;
+                        b = std::min(b, it->second);
+                    }
+                }
+                if (src < 0) break;  // never initialised anywhere
+                CK(cudaStreamWaitEvent(d0.s, R.dev[src].ev[(R.gen - 1) & 1], 0));
+                CK(cudaMemcpyPeerAsync(r->rep[0] + a * r->elem, d0.ord, r->rep[src] + a * r->elem,
+                                       R.dev[src].ord, (size_t)(b - a) * r->elem, d0.s));
+                r->valid[0].add(a, b);
+                a = b;
+            }
+        }
+        CK(cudaMemcpyAsync((char *)r->base + start, r->rep[0] + start, bytes, cudaMemcpyDeviceToHost,
+                           d0.s));
+        CK(cudaStreamSynchronize(d0.s));
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_launch(int loop_id, const jacc_range *range, const jacc_arg *args, int nargs,
+                        int async_id) {
+    return guard([&]() { return do_launch(loop_id, range, args, nargs, async_id); });
+}
+
+jacc_status jacc_wait(int async_id) {
+    (void)async_id;
+    return guard([&]() -> jacc_status {
+        sync_all();
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_get_dirty_range(void *host, int dev, uint64_t *mn, uint64_t *mx) {
+    return guard([&]() -> jacc_status {
+        Region *r = lookup(host);
+        if (!r) return JACC_ERR_NOT_PRESENT;
+        if (dev < 0 || dev >= R.n || !mn || !mx) return JACC_ERR_INVALID;
+        sync_all();
+        u64 h[2];
+        set_dev(dev);
+        CK(cudaMemcpy(h, r->dirty[dev], 16, cudaMemcpyDeviceToHost));
+        *mn = h[0];
+        *mx = ~h[1];
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_get_dirty_bitmap(void *host, int dev, uint32_t *out, size_t nwords) {
+    return guard([&]() -> jacc_status {
+        Region *r = lookup(host);
+        if (!r) return JACC_ERR_NOT_PRESENT;
+        if (dev < 0 || dev >= R.n || !out) return JACC_ERR_INVALID;
+        const size_t words = (size_t)((r->nelem + 31) / 32);
+        if (nwords < words || !r->bitmap[dev]) return JACC_ERR_INVALID;
+        sync_all();
+        set_dev(dev);
+        CK(cudaMemcpy(out, r->bitmap[dev], words * 4, cudaMemcpyDeviceToHost));
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_get_replica(void *host, int dev, void *out, size_t bytes) {
+    return guard([&]() -> jacc_status {
+        Region *r = lookup(host);
+        if (!r) return JACC_ERR_NOT_PRESENT;
+        if (dev < 0 || dev >= R.n || !out || bytes > r->bytes) return JACC_ERR_INVALID;
+        sync_all();
+        set_dev(dev);
+        CK(cudaMemcpy(out, r->rep[dev], bytes, cudaMemcpyDeviceToHost));
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_last_timing(double *tk, double *tm, uint64_t *bytes) {
+    return guard([&]() -> jacc_status {
+        flush_prof();
+        if (tk) *tk = R.last_valid ? R.last_k : 0.0;
+        if (tm) *tm = R.last_valid ? R.last_m : 0.0;
+        if (bytes) *bytes = R.last_bytes;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_set_profiling(int on) {
+    return guard([&]() -> jacc_status {
+        flush_prof();
+        R.profiling = on != 0;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_profile_totals(int dev, double *ks, double *ms, uint64_t *launches,
+                                uint64_t *bytes) {
+    return guard([&]() -> jacc_status {
+        if (dev < 0 || dev >= R.n) return JACC_ERR_INVALID;
+        flush_prof();
+        const Device &dv = R.dev[dev];
+        if (ks) *ks = dv.kernel_s;
+        if (ms) *ms = dv.merge_s;
+        if (launches) *launches = dv.launches;
+        if (bytes) *bytes = dv.bytes_merged;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_profile_reset(void) {
+    return guard([&]() -> jacc_status {
+        flush_prof();
+        for (auto &dv : R.dev) {
+            dv.kernel_s = dv.merge_s = 0;
+            dv.launches = dv.bytes_merged = 0;
+        }
+        R.last_valid = false;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_get_stream(int dev, void **stream, int *ord) {
+    return guard([&]() -> jacc_status {
+        if (dev < 0 || dev >= R.n) return JACC_ERR_INVALID;
+        if (stream) *stream = (void *)R.dev[dev].s;
+        if (ord) *ord = R.dev[dev].ord;
+        return JACC_OK;
+    });
+}
+
+const char *jacc_error_string(jacc_status s) {
+    switch (s) {
+    case JACC_OK: return "JACC_OK";
+    case JACC_ERR_INVALID: return "JACC_ERR_INVALID: invalid argument";
+    case JACC_ERR_OVERLAP: return "JACC_ERR_OVERLAP: region overlaps a present region";
+    case JACC_ERR_NOT_PRESENT: return "JACC_ERR_NOT_PRESENT: address not in any present region";
+    case JACC_ERR_UNKNOWN_LOOP: return "JACC_ERR_UNKNOWN_LOOP: no such loop id";
+    case JACC_ERR_OOM: return "JACC_ERR_OOM: device allocation failed";
+    case JACC_ERR_CUDA: return "JACC_ERR_CUDA: CUDA error (runtime poisoned)";
+    case JACC_ERR_NCCL: return "JACC_ERR_NCCL: NCCL error (runtime poisoned)";
+    case JACC_ERR_STATE: return "JACC_ERR_STATE: not initialised or poisoned";
+    default: return "JACC: unknown status";
+    }
+}
+
+}  // extern "C"

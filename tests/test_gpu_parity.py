@@ -1,0 +1,493 @@
+"""GPU parity (-m gpu): the CUDA path, called through the C-ABI, against the
+CPU oracle on the same seeded inputs.  Bit-exact for element-wise, integer
+and index work and for the dirty sets; fp64 reductions within 1e-12 of the
+Neumaier reference and GEMM within 1e-12*(|A||B|)_ij (north_star; DESIGN
+R-8, R-10, R-11).  Multi-device runs use virtual devices (several logical
+devices on one B200, separate replicas), with both merge policies.
+"""
+from contextlib import contextmanager
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import synth
+
+pytestmark = pytest.mark.gpu
+U64MAX = 2**64 - 1
+
+
+@pytest.fixture(scope="module")
+def J():
+    import __graft_entry__ as ge
+    ge.build_jacc()
+    from paper_2110_14340_b200 import jacc
+    return jacc
+
+
+@contextmanager
+def runtime(J, n=1, policy=0, mode=0):
+    J.jacc_init(n, [0] * n)
+    try:
+        J.jacc_set_merge_policy(policy)
+        J.jacc_set_mode(mode)
+        yield
+    finally:
+        J.jacc_finalize()
+
+
+def _in(J, x):
+    return J.arg(J.JACC_ARG_ARRAY_IN, x)
+
+
+def _out(J, x):
+    return J.arg(J.JACC_ARG_ARRAY_OUT, x)
+
+
+def _inout(J, x):
+    return J.arg(J.JACC_ARG_ARRAY_INOUT, x)
+
+
+def _create(J, *arrs, upload=True):
+    for a in arrs:
+        J.jacc_data_create(a)
+        if upload:
+            J.jacc_update_device(a)
+
+
+# --------------------------------------------------------------------------
+# K1 Listing 1
+# --------------------------------------------------------------------------
+def test_square_listing1(J):
+    y = np.array([1, 2, 3], dtype=np.float32)
+    x = np.zeros(3, dtype=np.float32)
+    with runtime(J):
+        _create(J, y, x)
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(0, 3), [_in(J, y), _out(J, x)])
+        J.jacc_update_host(x)
+        assert J.jacc_get_dirty_range(x, 0) == (0, 2)
+    assert x.tolist() == [1, 4, 9]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+@pytest.mark.parametrize("size", [1, 5, 1000, 123457])
+def test_square_multi(J, n, size):
+    y = synth.uniform_f32(size, 31, 3) * 8 - 4
+    x = np.full(size, -1.0, dtype=np.float32)
+    ref = orc.square_f32(y)
+    with runtime(J, n):
+        _create(J, y, x)
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(0, size), [_in(J, y), _out(J, x)])
+        for d in range(n):
+            lo, hi = orc.partition(size, n, d)
+            xd = np.zeros_like(y)
+            exp = orc.square_f32_filtered(y, xd, lo, hi - 1)
+            assert J.jacc_get_dirty_range(x, d) == exp
+            assert np.array_equal(J.jacc_get_replica(x, d), ref)   # EAGER: coherent
+        J.jacc_update_host(x)
+    assert np.array_equal(x, ref)
+
+
+def test_square_interior_pointer_subrange(J):
+    """1-D args may point inside a region (present lookup of any address)."""
+    y = synth.uniform_f32(1000, 32, 3)
+    x = np.zeros(1000, dtype=np.float32)
+    with runtime(J, 2):
+        _create(J, y, x)
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(10, 300),
+                      [_in(J, y[100:]), _out(J, x[200:])])
+        J.jacc_update_host(x)
+    ref = np.zeros(1000, dtype=np.float32)
+    ref[210:500] = orc.square_f32(np.ascontiguousarray(y[110:400]))
+    assert np.array_equal(x, ref)
+
+
+def test_square_alias_is_duplicated(J):
+    """x and y the same array (read and written): duplicate mode."""
+    y = synth.uniform_f32(777, 33, 3)
+    ref = orc.square_f32(y)
+    with runtime(J, 3):
+        _create(J, y)
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(0, 777), [_in(J, y), _out(J, y)])
+        for d in range(3):
+            assert np.array_equal(J.jacc_get_replica(y, d), ref)
+        J.jacc_update_host(y)
+    assert np.array_equal(y, ref)
+
+
+# --------------------------------------------------------------------------
+# c1 Jacobi-2D
+# --------------------------------------------------------------------------
+def _jacobi_gpu(J, A0, B0, T, n, policy, rng=None, check_dirty=True):
+    A, B = A0.copy(), B0.copy()
+    N = A.shape[0]
+    dirt = []
+    with runtime(J, n, policy):
+        _create(J, A, B)
+        for t in range(T):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, rng, [_in(J, A), _out(J, B)], async_id=0)
+            if check_dirty and t == 0:
+                dirt.append([J.jacc_get_dirty_range(B, d) for d in range(n)])
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, rng, [_in(J, B), _out(J, A)], async_id=0)
+        J.jacc_wait()
+        reps = None
+        if policy == J.JACC_MERGE_EAGER:
+            reps = [(J.jacc_get_replica(A, d), J.jacc_get_replica(B, d)) for d in range(n)]
+        J.jacc_update_host(A)
+        J.jacc_update_host(B)
+    return A, B, dirt, reps
+
+
+def test_jacobi_J256_bit_exact(J):
+    """BASELINE config 1: 256^2, 10 timesteps, 1 GPU, bit-exact vs oracle."""
+    N, T = 256, 10
+    A0, B0 = synth.polybench_jacobi2d(N)
+    # PolyBench init is (nearly) harmonic; also a seeded random field
+    for A0_, B0_ in ((A0, B0), (synth.uniform_f64(N * N, 41, 1).reshape(N, N),
+                                synth.uniform_f64(N * N, 41, 2).reshape(N, N))):
+        Ar, Br = A0_.copy(), B0_.copy()
+        orc.jacobi2d(T, Ar, Br)
+        A, B, dirt, _ = _jacobi_gpu(J, A0_, B0_, T, 1, J.JACC_MERGE_EAGER)
+        assert np.array_equal(A, Ar) and np.array_equal(B, Br)
+        assert dirt[0] == [(257, 65278)]
+
+
+@pytest.mark.parametrize("N", [3, 4, 5, 17, 64, 258, 301])
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_jacobi_multi_device(J, N, n, policy):
+    T = 3
+    A0 = synth.uniform_f64(N * N, 42 + N, 1).reshape(N, N)
+    B0 = synth.uniform_f64(N * N, 42 + N, 2).reshape(N, N)
+    Ar, Br = A0.copy(), B0.copy()
+    orc.jacobi2d(T, Ar, Br)
+    A, B, dirt, reps = _jacobi_gpu(J, A0, B0, T, n, policy)
+    assert np.array_equal(A, Ar) and np.array_equal(B, Br)
+    # dirty sets == oracle write log of the filtered first sweep
+    for d in range(n):
+        lo, hi = orc.partition(N, n, d)
+        tmp = B0.copy()
+        assert dirt[0][d] == orc.jacobi2d_sweep_filtered(A0, tmp, lo, hi - 1)
+    if reps is not None:  # EAGER: every replica coherent after every launch
+        for a, b in reps:
+            assert np.array_equal(a, Ar) and np.array_equal(b, Br)
+
+
+@pytest.mark.parametrize("n", [1, 3])
+def test_jacobi_subrange(J, n):
+    N = 50
+    A0 = synth.uniform_f64(N * N, 43, 1).reshape(N, N)
+    B0 = synth.uniform_f64(N * N, 43, 2).reshape(N, N)
+    rng = J.make_range([7, 3], [40, 33])
+    A, B, _, _ = _jacobi_gpu(J, A0, B0, 1, n, 0, rng=rng, check_dirty=False)
+    # oracle: the loop nest restricted to the same range
+    Ar, Br = A0.copy(), B0.copy()
+    for (s, t) in ((Ar, Br), (Br, Ar)):
+        full = t.copy()
+        orc.jacobi2d_sweep(s, full)
+        t[7:40, 3:33] = full[7:40, 3:33]
+    assert np.array_equal(A, Ar) and np.array_equal(B, Br)
+
+
+def test_jacobi_rejects_in_place(J):
+    A = np.zeros((8, 8))
+    with runtime(J):
+        _create(J, A)
+        st = J.jacc_launch_status(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, A)])
+        assert st == J.JACC_ERR_INVALID
+
+
+def test_jacobi_full_size_sampled(J):
+    """BASELINE config 2 at full size (16384^2, n=1, the bench launch
+    configuration): one sweep checked on sampled windows recomputed by the
+    oracle, then 200 launches on an exact harmonic field (a fixed point of
+    the fp64 sweep at any size) must leave it unchanged bit for bit."""
+    N = 16384
+    A = synth.uniform_f64(N * N, 44, 1).reshape(N, N)
+    B = np.zeros((N, N))
+    rs = np.random.default_rng(5)
+    with runtime(J):
+        _create(J, A, B)
+        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)])
+        J.jacc_update_host(B)
+        for (i, j) in [(1, 1), (N - 2, N - 2), (1, N - 2), (N - 2, 1), (8191, 8192)] + \
+                [tuple(rs.integers(1, N - 1, 2)) for _ in range(20)]:
+            i0, j0 = max(i - 3, 0), max(j - 3, 0)
+            i1, j1 = min(i + 4, N), min(j + 4, N)
+            w = np.ascontiguousarray(A[i0:i1, j0:j1])
+            # pad to a square window for the oracle (N x N signature)
+            m = max(w.shape)
+            src = np.zeros((m, m)); src[:w.shape[0], :w.shape[1]] = w
+            dst = np.zeros((m, m))
+            orc.jacobi2d_sweep(src, dst)
+            assert B[i, j] == dst[i - i0, j - j0], (i, j)
+        assert J.jacc_get_dirty_range(B, 0) == (N + 1, (N - 2) * N + N - 2)
+        ii, jj = np.meshgrid(np.arange(N, dtype=np.float64), np.arange(N, dtype=np.float64),
+                             indexing="ij")
+        H = 3 * ii + 7 * jj + 11
+        A[:] = H
+        B[:] = H
+        del ii, jj
+        J.jacc_update_device(A)
+        J.jacc_update_device(B)
+        for t in range(100):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)], async_id=0)
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, B), _out(J, A)], async_id=0)
+        J.jacc_update_host(A)
+        assert np.array_equal(A, H)
+
+
+# --------------------------------------------------------------------------
+# c2 / c8 reductions
+# --------------------------------------------------------------------------
+def _reduce(J, x, y, s_in, n, lo=0, hi=None, xoff=0, yoff=0):
+    hi = x.size - xoff if hi is None else hi
+    s = np.array([s_in])
+    with runtime(J, n):
+        _create(J, x)
+        if y is not None:
+            _create(J, y)
+        args = [_in(J, x[xoff:])]
+        if y is not None:
+            args.append(_in(J, y[yoff:]))
+        args.append(J.arg(J.JACC_ARG_REDUCE_SUM_F64, s))
+        loop = J.JACC_LOOP_DOT_F64 if y is not None else J.JACC_LOOP_SUM_F64
+        J.jacc_launch(loop, J.make_range(lo, hi), args)
+    return s[0]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+@pytest.mark.parametrize("size", [0, 1, 7, 4096, 1_000_003])
+def test_dot_sum_dyadic_exact(J, n, size):
+    x = synth.dyadic_f64(max(size, 1), 51, 3)[:size].copy() if size else np.zeros(1)
+    y = synth.dyadic_f64(max(size, 1), 51, 4)[:size].copy() if size else np.zeros(1)
+    hi = size
+    assert _reduce(J, x, y, 1.5, n, 0, hi) == orc.dot_f64(x[:hi], y[:hi], 1.5)
+    assert _reduce(J, x, None, -2.0, n, 0, hi) == orc.sum_f64(x[:hi], -2.0)
+
+
+@pytest.mark.parametrize("n", [1, 3])
+def test_dot_uniform_tolerance(J, n):
+    size = 3_000_001
+    x = synth.uniform_f64(size, 52, 3)
+    y = synth.uniform_f64(size, 52, 4) - 0.5
+    ref = orc.dot_neumaier(x, y, 0.25)
+    got = _reduce(J, x, y, 0.25, n)
+    assert abs(got - ref) <= 1e-12 * abs(ref)
+    ref = orc.sum_neumaier(x, 0.0)
+    assert abs(_reduce(J, x, None, 0.0, n) - ref) <= 1e-12 * abs(ref)
+
+
+@pytest.mark.parametrize("xoff,yoff", [(1, 1), (1, 2), (3, 0)])
+def test_dot_misaligned_interior_pointers(J, xoff, yoff):
+    size = 100_001
+    x = synth.dyadic_f64(size, 53, 3)
+    y = synth.dyadic_f64(size, 53, 4)
+    m = size - 3
+    got = _reduce(J, x, y, 0.0, 2, 0, m, xoff, yoff)
+    assert got == orc.dot_f64(np.ascontiguousarray(x[xoff:xoff + m]),
+                              np.ascontiguousarray(y[yoff:yoff + m]), 0.0)
+
+
+def test_dot_full_size(J):
+    """BASELINE config 3 at full size: 2^30 fp64, n=1, dyadic (exact)."""
+    size = 2**30
+    x = synth.dyadic_f64(size, 54, 3)
+    y = synth.dyadic_f64(size, 54, 4)
+    assert _reduce(J, x, y, 0.0, 1) == orc.dot_f64(x, y, 0.0)
+
+
+# --------------------------------------------------------------------------
+# c3 GEMM
+# --------------------------------------------------------------------------
+def _gemm(J, A, B, n, rng=None, dirty=False):
+    M, N = A.shape[0], B.shape[1]
+    C = np.full((M, N), -3.0)
+    with runtime(J, n):
+        _create(J, A, B)
+        _create(J, C, upload=True)
+        J.jacc_launch(J.JACC_LOOP_GEMM_F64, rng, [_in(J, A), _in(J, B), _out(J, C)])
+        dr = [J.jacc_get_dirty_range(C, d) for d in range(n)] if dirty else None
+        reps = [J.jacc_get_replica(C, d) for d in range(n)]
+        J.jacc_update_host(C)
+    return C, dr, reps
+
+
+def _gemm_bound(A, B):
+    return 1e-12 * (np.abs(A) @ np.abs(B))
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 64), (37, 53, 71), (130, 67, 16), (1, 1, 1),
+                                   (200, 256, 33)])
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_gemm_random_tolerance(J, shape, n):
+    M, N, K = shape
+    A = synth.uniform_f64(M * K, 61, 1).reshape(M, K)
+    B = synth.uniform_f64(K * N, 61, 2).reshape(K, N)
+    ref = orc.gemm_f64(A, B)
+    C, dr, reps = _gemm(J, A, B, n, dirty=True)
+    assert (np.abs(C - ref) <= _gemm_bound(A, B)).all()
+    for d in range(n):
+        lo, hi = orc.partition(M, n, d)
+        Cd = np.zeros((M, N))
+        assert dr[d] == orc.gemm_f64_filtered(A, B, Cd, lo, hi - 1)
+        assert np.array_equal(reps[d], C)
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_gemm_exact_cases(J, n):
+    M = N = K = 96
+    B = synth.uniform_f64(K * N, 62, 2).reshape(K, N)
+    C, _, _ = _gemm(J, np.eye(M), B, n)
+    assert np.array_equal(C, B)
+    C, _, _ = _gemm(J, np.ones((M, K)), np.ones((K, N)), n)
+    assert (C == K).all()
+    u = synth.int_i32(M, -9, 9, 62, 3).astype(np.float64)
+    v = synth.int_i32(N, -9, 9, 62, 4).astype(np.float64)
+    A1 = np.ascontiguousarray(np.repeat(u[:, None], K, axis=1))
+    B1 = np.ascontiguousarray(np.repeat(v[None, :], K, axis=0))
+    C, _, _ = _gemm(J, A1, B1, n)
+    assert np.array_equal(C, K * np.outer(u, v))
+
+
+def test_gemm_subrange(J):
+    M, N, K = 70, 90, 20
+    A = synth.uniform_f64(M * K, 63, 1).reshape(M, K)
+    B = synth.uniform_f64(K * N, 63, 2).reshape(K, N)
+    C, _, _ = _gemm(J, A, B, 2, rng=J.make_range([5, 10], [60, 81]))
+    ref = np.full((M, N), -3.0)
+    ref[5:60, 10:81] = orc.gemm_f64(A, B)[5:60, 10:81]
+    m = np.abs(C - ref) <= 1e-12 * np.abs(ref)
+    assert m.all()
+
+
+def test_gemm_full_size_sampled(J):
+    """BASELINE config 4 at full size: 8192^3 fp64 (n=1, bench launch
+    configuration); sampled rows recomputed by the oracle; identity exact."""
+    Nn = 8192
+    A = synth.uniform_f64(Nn * Nn, 64, 1).reshape(Nn, Nn)
+    B = synth.uniform_f64(Nn * Nn, 64, 2).reshape(Nn, Nn)
+    C, dr, _ = _gemm(J, A, B, 1, dirty=True)
+    assert dr[0] == (0, Nn * Nn - 1)
+    for i in (0, 1, 4095, 8191, 1234):
+        row = orc.gemm_f64(np.ascontiguousarray(A[i:i + 1]), B)
+        bound = 1e-12 * (np.abs(A[i:i + 1]) @ np.abs(B))
+        assert (np.abs(C[i:i + 1] - row) <= bound).all(), i
+
+
+# --------------------------------------------------------------------------
+# c5 scatter
+# --------------------------------------------------------------------------
+def _scatter(J, idx, b, a0, n, policy=0):
+    a = a0.copy()
+    loop = J.JACC_LOOP_SCATTER_ADD_F64 if a.dtype == np.float64 else J.JACC_LOOP_SCATTER_ADD_I32
+    with runtime(J, n, policy):
+        _create(J, idx, b, a)
+        J.jacc_launch(loop, J.make_range(0, idx.size), [_in(J, idx), _in(J, b), _inout(J, a)])
+        bms = [J.jacc_get_dirty_bitmap(a, d, a.size) for d in range(n)]
+        drs = [J.jacc_get_dirty_range(a, d) for d in range(n)]
+        reps = [J.jacc_get_replica(a, d) for d in range(n)] if policy == 0 else None
+        J.jacc_update_host(a)
+    return a, bms, drs, reps
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+@pytest.mark.parametrize("sizes", [(1, 1), (100, 37), (100_003, 5000), (1_000_000, 1_000_000)])
+@pytest.mark.parametrize("dtype", ["f64", "i32"])
+def test_scatter_exact(J, n, sizes, dtype):
+    N, M = sizes
+    idx = synth.index_i32(N, M, 71, 5)
+    if dtype == "f64":
+        b = synth.dyadic_f64(N, 71, 6)
+        a0 = synth.dyadic_f64(M, 71, 7)
+    else:
+        b = synth.int_i32(N, -1000, 1000, 71, 6)
+        a0 = synth.int_i32(M, -10**6, 10**6, 71, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, bms, drs, reps = _scatter(J, idx, b, a0, n)
+    assert np.array_equal(a, ref)
+    for d in range(n):
+        lo, hi = orc.partition(M, n, d)
+        bm, mn, mx = orc.scatter_add_filtered(idx, b, a0.copy(), lo, hi - 1)
+        assert np.array_equal(bms[d], bm)
+        assert drs[d] == (mn, mx)
+        assert np.array_equal(reps[d], ref)
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_scatter_halo_policy_and_uniform_tolerance(J, n):
+    N, M = 200_000, 30_000
+    idx = synth.index_i32(N, M, 72, 5)
+    b = synth.uniform_f64(N, 72, 6)
+    a0 = synth.uniform_f64(M, 72, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, _, _, _ = _scatter(J, idx, b, a0, n, policy=1)
+    # per-element bound |d| <= 1e-12 * sum |contributions| (R-8)
+    mag = np.abs(a0).copy()
+    np.add.at(mag, idx, np.abs(b))
+    assert (np.abs(a - ref) <= 1e-12 * mag).all()
+
+
+def test_scatter_permutation_exact(J):
+    M = 1 << 16
+    idx = synth.permutation_i32(M, 73, 5)
+    b = synth.uniform_f64(M, 73, 6)
+    a0 = synth.uniform_f64(M, 73, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, _, _, _ = _scatter(J, idx, b, a0, 4)
+    assert np.array_equal(a, ref)
+
+
+def test_scatter_full_size(J):
+    """BASELINE config 5 at full size: 2^28 updates into 2^28 elements,
+    random idx, dyadic b (exact in any order), n=1."""
+    N = M = 2**28
+    idx = synth.index_i32(N, M, 74, 5)
+    b = synth.dyadic_f64(N, 74, 6)
+    a0 = synth.dyadic_f64(M, 74, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, bms, drs, _ = _scatter(J, idx, b, a0, 1)
+    assert np.array_equal(a, ref)
+    pop = int(np.unpackbits(bms[0].view(np.uint8)).sum())
+    assert pop == np.unique(idx).size
+    assert drs[0] == (int(idx.min()), int(idx.max()))
+
+
+# --------------------------------------------------------------------------
+# runtime behaviour
+# --------------------------------------------------------------------------
+def test_present_table_errors(J):
+    a = np.zeros(1000)
+    with runtime(J):
+        J.jacc_data_create(a)
+        with pytest.raises(J.JaccError) as e:
+            J.jacc_data_create(a[10:20])
+        assert e.value.status == J.JACC_ERR_OVERLAP
+        # any interior address resolves
+        J.jacc_update_device(a[500:], 0, 80)
+        b = np.zeros(10)
+        st = J.jacc_launch_status(J.JACC_LOOP_SUM_F64, J.make_range(0, 10),
+                                  [_in(J, b), J.arg(J.JACC_ARG_REDUCE_SUM_F64, np.zeros(1))])
+        assert st == J.JACC_ERR_NOT_PRESENT
+        assert J.jacc_launch_status(99, None, []) == J.JACC_ERR_UNKNOWN_LOOP
+        J.jacc_data_delete(a[999:])
+        with pytest.raises(J.JaccError):
+            J.jacc_data_delete(a)
+
+
+def test_profiling_records(J):
+    N = 512
+    A, B = synth.polybench_jacobi2d(N)
+    with runtime(J, 2):
+        J.jacc_set_profiling(1)
+        _create(J, A, B)
+        for _ in range(4):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)], async_id=0)
+        tk, tm, nb = J.jacc_last_timing()
+        assert tk > 0 and tm >= 0 and nb > 0
+        k, m, nl, _ = J.jacc_profile_totals(0)
+        assert nl == 4 and k >= tk
