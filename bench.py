@@ -135,15 +135,21 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 # reference arm / cpu baseline: the CPU oracle on a bounded sample
 # ----------------------------------------------------------------------------
+_ORC_GRID = None
+
+
 def oracle_sample(sweeps):
     """Time `sweeps` oracle launches of the J16K sweep on the full 16384^2
     grid (single thread).  Returns (GB/s algorithmic, seconds, sample text)."""
+    global _ORC_GRID
     import __graft_entry__ as ge
     ge.build_oracle()
     ge.build_synth()
     import oracle as orc
     import synth
-    A, B = synth.polybench_jacobi2d(N_GRID)
+    if _ORC_GRID is None:
+        _ORC_GRID = synth.polybench_jacobi2d(N_GRID)
+    A, B = _ORC_GRID
     t0 = time.perf_counter()
     src, dst = A, B
     for _ in range(sweeps):
@@ -171,7 +177,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(times) * 1e3 * (2 * TSTEPS / sweeps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (PolyBench jacobi-2d init)",
         "config": {"workload": "J16K: Jacobi-2D fp64 16384x16384, 100 timesteps",
                    "sample": sample, "l2": "inputs 2x2 GiB >> 126 MB L2"},
@@ -184,6 +190,93 @@ def run_reference(args):
 # ----------------------------------------------------------------------------
 # the CUDA path
 # ----------------------------------------------------------------------------
+class Ctx:
+    """Launch context: single process (N logical devices, real or virtual
+    GPUs) or one process per GPU under torch.distributed.run (C-ABI
+    multi-process mode: CUDA-IPC peer replicas, NCCL for reductions)."""
+
+    def __init__(self, J, torch, n):
+        self.J, self.torch, self.n = J, torch, n
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.mp = self.world > 1
+        ngpu = torch.cuda.device_count()
+        if self.mp:
+            import torch.distributed as dist
+            from paper_2110_14340_b200 import dist as jd
+            self.dist, self.jd = dist, jd
+            if self.world != n:
+                raise SystemExit(f"--gpus {n} must equal WORLD_SIZE {self.world}")
+            dist.init_process_group("gloo", init_method="env://")
+            lr = int(os.environ.get("LOCAL_RANK", str(self.rank)))
+            ordv = lr % ngpu
+            torch.cuda.set_device(ordv)
+            _, _, distinct = jd.init_rank(ordv)
+            self.virtual = not distinct
+            self.local = [self.rank]
+            self.ords = [ordv]
+        else:
+            self.virtual = ngpu < n
+            self.ords = list(range(n)) if not self.virtual else [0] * n
+            J.jacc_init(n, self.ords)
+            self.local = list(range(n))
+        self.streams = {}
+        for d in self.local:
+            sp, o = J.jacc_get_stream(d)
+            self.streams[d] = (torch.cuda.ExternalStream(sp, device=f"cuda:{o}"), o)
+
+    def create(self, arr):
+        if self.mp:
+            self.jd.data_create(arr)
+        else:
+            self.J.jacc_data_create(arr)
+
+    def sync(self):
+        for o in sorted(set(o for _, o in self.streams.values())):
+            self.torch.cuda.synchronize(o)
+
+    def barrier(self):
+        if self.mp:
+            self.dist.barrier()
+
+    def reduce(self, x, op="max"):
+        if not self.mp:
+            return x
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def timed(self, fn, reps):
+        """Device time of reps x fn (CUDA events on every local stream, max
+        over local devices, then max over ranks)."""
+        torch = self.torch
+        self.J.jacc_wait()
+        self.sync()
+        self.barrier()
+        st, en = {}, {}
+        for d, (s, o) in self.streams.items():
+            with torch.cuda.device(o):
+                st[d] = torch.cuda.Event(enable_timing=True)
+                en[d] = torch.cuda.Event(enable_timing=True)
+                st[d].record(s)
+        for _ in range(reps):
+            fn()
+        for d, (s, o) in self.streams.items():
+            with torch.cuda.device(o):
+                en[d].record(s)
+        self.J.jacc_wait()
+        self.sync()
+        t = max(st[d].elapsed_time(en[d]) for d in self.streams) / 1e3
+        return self.reduce(t, "max")
+
+    def finalize(self):
+        if self.mp:
+            self.jd.finalize()
+            self.dist.destroy_process_group()
+        else:
+            self.J.jacc_finalize()
+
+
 def run_jacc(args):
     import torch
     import __graft_entry__ as ge
@@ -192,35 +285,14 @@ def run_jacc(args):
     import synth
     from paper_2110_14340_b200 import jacc as J
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     n = args.gpus
-    if world > 1:
-        # Single-process runtime (the paper's one-driver-many-GPUs model,
-        # P:570): rank 0 drives all N GPUs through the C-ABI; the other
-        # ranks only hold the barrier.
-        import torch.distributed as dist
-        dist.init_process_group("gloo", init_method="env://")
-        if rank != 0:
-            dist.barrier()
-            dist.destroy_process_group()
-            return
-    ngpu = torch.cuda.device_count()
-    if ngpu >= n:
-        ords = list(range(n))
-        virtual = False
-    else:
-        ords = [0] * n  # virtual devices on one GPU (parity/plumbing only)
-        virtual = True
-
+    C = Ctx(J, torch, n)
     N = N_GRID
     A, B = synth.polybench_jacobi2d(N)
-    J.jacc_init(n, ords)
     J.jacc_set_merge_policy(J.JACC_MERGE_HALO if args.merge == "halo" else J.JACC_MERGE_EAGER)
-    J.jacc_data_create(A)
-    J.jacc_data_create(B)
-    J.jacc_update_device(A)
-    J.jacc_update_device(B)
+    for arr in (A, B):
+        C.create(arr)
+        J.jacc_update_device(arr)
     IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
     args_ab = [J.arg(IN, A), J.arg(OUT, B)]
     args_ba = [J.arg(IN, B), J.arg(OUT, A)]
@@ -230,51 +302,31 @@ def run_jacc(args):
             J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ab, 0)
             J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ba, 0)
 
-    streams = []
-    for d in range(n):
-        sp, ordv = J.jacc_get_stream(d)
-        streams.append((torch.cuda.ExternalStream(sp, device=f"cuda:{ordv}"), ordv))
-
-    def sync():
-        for o in sorted(set(ords)):
-            torch.cuda.synchronize(o)
-
     for _ in range(args.warmup):
         step()
-    J.jacc_wait()
-    sync()
     J.jacc_set_profiling(1)
     J.jacc_profile_reset()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
-    with ClockSampler(ords[0]) as clk:
-        for d, (s, o) in enumerate(streams):
-            with torch.cuda.device(o):
-                starts[d].record(s)
-        for _ in range(args.steps):
-            step()
-        for d, (s, o) in enumerate(streams):
-            with torch.cuda.device(o):
-                ends[d].record(s)
-        J.jacc_wait()
-        sync()
-    t = max(starts[d].elapsed_time(ends[d]) for d in range(n)) / 1e3   # max over devices
-    kern = [J.jacc_profile_totals(d) for d in range(n)]
+    with ClockSampler(C.ords[0]) as clk:
+        t = C.timed(step, args.steps)
+    kern = {d: J.jacc_profile_totals(d) for d in C.local}
     J.jacc_set_profiling(0)
     bytes_step = 2 * TSTEPS * algo_bytes_per_sweep(N, n)
     value = bytes_step * args.steps / t / 1e9
-    launches_dev = [k[2] for k in kern]
-    # dominant kernel: jacobi2d on device 0; algorithmic bytes per launch on it
-    k_avg = kern[0][0] / max(kern[0][2], 1)
+    launches = C.reduce(sum(k[2] for k in kern.values()), "sum")
+    # dominant kernel: jacobi2d; average launch duration on the slowest device
+    k_avg = C.reduce(max(k[0] / max(k[2], 1) for k in kern.values()), "max")
     per_dev_bytes = algo_bytes_per_sweep_dev(N, n, 0)
     achieved = per_dev_bytes / k_avg / 1e9
     peak, peak_src = load_peaks()
     traffic, tsrc = load_traffic("jacobi2d")
+    if traffic is not None and n > 1:
+        traffic = None  # the committed capture is of the n=1 launch
 
     # ---- e2e through the public API with host buffers ----
     e2e_times = []
     for it in range(max(1, min(args.steps, 3)) + 1):
-        sync()
+        C.sync()
+        C.barrier()
         t0 = time.perf_counter()
         J.jacc_update_device(A)
         J.jacc_update_device(B)
@@ -282,27 +334,29 @@ def run_jacc(args):
         J.jacc_update_host(A)
         t1 = time.perf_counter()
         if it > 0:
-            e2e_times.append(t1 - t0)
+            e2e_times.append(C.reduce(t1 - t0, "max"))
     e2e = bytes_step / statistics.median(e2e_times) / 1e9
 
     extra = {}
-    if args.extra:
-        extra = run_extra_loops(J, torch, n, streams, peak)
-    J.jacc_finalize()
+    if args.extra and not C.mp:
+        extra = run_extra_loops(J, C, n, peak)
+    C.finalize()
 
     cpu = None
-    if args.cpu_baseline and n == 1:
+    if args.cpu_baseline and n == 1 and C.rank == 0:
         g, dt, sample = oracle_sample(args.cpu_sweeps)
         cpu = {"value": g, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
                "seconds": dt}
-
+    if C.rank != 0:
+        return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (PolyBench jacobi-2d init, seeded generators in synth/)",
         "config": {"workload": "J16K: Jacobi-2D fp64 16384x16384, 100 timesteps (200 launches/step)",
-                   "merge": args.merge, "devices": ords, "virtual_devices": virtual,
+                   "merge": args.merge, "launch": "one process per GPU" if C.mp else "single process",
+                   "virtual_devices": C.virtual,
                    "l2": "no flush: inputs 2x2 GiB >> 126 MB L2",
                    "parallelism": f"row-block owner partition over {n} device(s)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -312,17 +366,13 @@ def run_jacc(args):
                      "traffic_source": tsrc},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * A.nbytes,
                 "d2h_bytes_per_step": A.nbytes},
-        "gpu_launches": int(sum(launches_dev)),
+        "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
     if extra:
         line["loops"] = extra
     print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 def algo_bytes_per_sweep_dev(N, n, d):
@@ -335,32 +385,19 @@ def algo_bytes_per_sweep_dev(N, n, d):
     return 8 * N * (i1 - i0 + 2) + 8 * (i1 - i0) * (N - 2)
 
 
-def _time_loop(J, torch, streams, fn, reps):
-    """Device time (max over devices) of `reps` calls of fn, plus the
-    profiled average kernel time on device 0."""
+def _time_loop(J, C, fn, reps):
+    """Device time per call (max over devices/ranks) of fn, plus the
+    profiled average kernel and merge time per launch on device 0."""
     fn()
-    J.jacc_wait()
     J.jacc_set_profiling(1)
     J.jacc_profile_reset()
-    n = len(streams)
-    st = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
-    en = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
-    for d, (s, o) in enumerate(streams):
-        with torch.cuda.device(o):
-            st[d].record(s)
-    for _ in range(reps):
-        fn()
-    for d, (s, o) in enumerate(streams):
-        with torch.cuda.device(o):
-            en[d].record(s)
-    J.jacc_wait()
-    t = max(st[d].elapsed_time(en[d]) for d in range(n)) / 1e3 / reps
-    k, m, nl, _ = J.jacc_profile_totals(0)
+    t = C.timed(fn, reps) / reps
+    k, m, nl, _ = J.jacc_profile_totals(C.local[0])
     J.jacc_set_profiling(0)
     return t, k / max(nl, 1), m / max(nl, 1)
 
 
-def run_extra_loops(J, torch, n, streams, peak):
+def run_extra_loops(J, C, n, peak):
     """The other BASELINE configs (DOT 2^30, GEMM 8192^3, SCAT 2^28) timed
     through the same C-ABI: kernel-level roofline evidence, not bench lines."""
     import synth
@@ -376,7 +413,7 @@ def run_extra_loops(J, torch, n, streams, peak):
         J.jacc_update_device(a)
     dargs = [J.arg(IN, x), J.arg(IN, y), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s)]
     rng = J.make_range(0, L)
-    t, k, _ = _time_loop(J, torch, streams, lambda: J.jacc_launch(J.JACC_LOOP_DOT_F64, rng, dargs), 10)
+    t, k, _ = _time_loop(J, C, lambda: J.jacc_launch(J.JACC_LOOP_DOT_F64, rng, dargs), 10)
     byts = 16 * L
     out["dot_2^30"] = {"loop_gbs": byts / t / 1e9, "kernel_us": k * 1e6,
                        "kernel_gbs": byts / n / k / 1e9, "frac_of_peak": byts / n / k / 1e9 / peak,
@@ -386,21 +423,21 @@ def run_extra_loops(J, torch, n, streams, peak):
     del x, y
     # GEMM 8192^3
     G = 8192
-    A = synth.uniform_f64(G * G, 2, synth.AID["A"]).reshape(G, G)
-    B = synth.uniform_f64(G * G, 2, synth.AID["B"]).reshape(G, G)
-    C = np.zeros((G, G))
-    for a in (A, B, C):
+    Ag = synth.uniform_f64(G * G, 2, synth.AID["A"]).reshape(G, G)
+    Bg = synth.uniform_f64(G * G, 2, synth.AID["B"]).reshape(G, G)
+    Cg = np.zeros((G, G))
+    for a in (Ag, Bg, Cg):
         J.jacc_data_create(a)
         J.jacc_update_device(a)
-    gargs = [J.arg(IN, A), J.arg(IN, B), J.arg(OUT, C)]
-    t, k, m = _time_loop(J, torch, streams, lambda: J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, gargs, 0), 3)
+    gargs = [J.arg(IN, Ag), J.arg(IN, Bg), J.arg(OUT, Cg)]
+    t, k, m = _time_loop(J, C, lambda: J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, gargs, 0), 3)
     fl = 2 * G**3
     out["gemm_8192"] = {"loop_tflops": fl / t / 1e12, "kernel_ms": k * 1e3,
                         "kernel_tflops": fl / n / k / 1e12, "merge_ms": m * 1e3,
                         "launch_ms": t * 1e3}
-    for a in (A, B, C):
+    for a in (Ag, Bg, Cg):
         J.jacc_data_delete(a)
-    del A, B, C
+    del Ag, Bg, Cg
     # SCAT 2^28 f64
     S = 2**28
     idx = synth.index_i32(S, S, 3, synth.AID["idx"])
@@ -411,7 +448,7 @@ def run_extra_loops(J, torch, n, streams, peak):
         J.jacc_update_device(arr)
     sargs = [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)]
     srng = J.make_range(0, S)
-    t, k, m = _time_loop(J, torch, streams,
+    t, k, m = _time_loop(J, C,
                          lambda: J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, srng, sargs, 0), 5)
     byts = S * (4 + 8 + 16)
     out["scatter_f64_2^28"] = {"loop_gbs": byts / t / 1e9, "kernel_us": k * 1e6,

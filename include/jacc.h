@@ -244,6 +244,62 @@ jacc_status jacc_profile_reset(void);
  * CUDA ordinal, so callers can time the path with their own events. */
 jacc_status jacc_get_stream(int dev, void **stream, int *cuda_ordinal);
 
+/* ---------------------------------------------------------------------- */
+/* One process per GPU (the launch model of bench.py under torchrun)       */
+/* ---------------------------------------------------------------------- */
+/* In this mode each process ("rank") owns ONE logical device (d = rank)
+ * of `world`, every rank issues the same API calls in the same order
+ * (SPMD), and the runtime reaches the other devices' replicas through
+ * CUDA IPC mappings of their memory (NVLink P2P loads/stores on distinct
+ * GPUs; plain device memory when ranks share one GPU).  Cross-device
+ * ordering uses CUDA IPC events plus per-rank progress counters in POSIX
+ * shared memory (no rank enqueues launch k before every rank has enqueued
+ * launch k-1).  The caller moves the opaque byte blobs below between ranks
+ * with any transport (bench.py uses torch.distributed): that is plumbing,
+ * no data-path bytes travel through it.
+ *
+ * Protocol:
+ *   rank 0: jacc_unique_id(id)            (optional: NCCL reduction combine,
+ *                                          only when ranks are distinct GPUs)
+ *   all:    jacc_init_rank(rank, world, ordinal, id or NULL, shm_name)
+ *   all:    jacc_export_runtime(blob) -> all-gather -> jacc_import_runtime(peer, blob_peer)
+ *   per array, all ranks in the same order:
+ *           jacc_data_create(...); jacc_export_region(host, blob) -> all-gather
+ *           -> jacc_import_region(host, peer, blob_peer) for every peer
+ * Then the ordinary API applies.  jacc_update_device/update_host/wait/
+ * data_delete/finalize and reductions are collective; update_host makes
+ * the caller's own replica coherent and copies it to the caller's host
+ * buffer.  Introspection calls accept only the caller's device. */
+#define JACC_UNIQUE_ID_BYTES 128
+#define JACC_RUNTIME_HANDLE_BYTES 192
+#define JACC_REGION_HANDLE_BYTES 64
+
+/* NCCL unique id for the reduction communicator (out: >= 128 bytes). */
+jacc_status jacc_unique_id(void *out, size_t bytes);
+
+/* Initialise this process as logical device `rank` of `world` on CUDA
+ * ordinal `cuda_ordinal`.  unique_id: NULL = combine reductions over CUDA
+ * IPC (required when ranks share a GPU), else the NCCL id from rank 0.
+ * shm_name: name of the POSIX shared-memory segment for progress counters,
+ * identical on all ranks and unique per job.  Errors: JACC_ERR_STATE if
+ * initialised, JACC_ERR_INVALID, JACC_ERR_CUDA, JACC_ERR_NCCL. */
+jacc_status jacc_init_rank(int rank, int world, int cuda_ordinal, const void *unique_id,
+                           const char *shm_name);
+
+/* Opaque handle blob of this rank's events and reduction buffer
+ * (>= JACC_RUNTIME_HANDLE_BYTES) / import a peer's. */
+jacc_status jacc_export_runtime(void *out, size_t bytes);
+jacc_status jacc_import_runtime(int peer, const void *in, size_t bytes);
+
+/* Opaque handle of this rank's replica of the region containing `host`
+ * (>= JACC_REGION_HANDLE_BYTES) / map a peer's replica.  A launch that uses
+ * a region before every peer replica is imported fails with JACC_ERR_STATE. */
+jacc_status jacc_export_region(void *host, void *out, size_t bytes);
+jacc_status jacc_import_region(void *host, int peer, const void *in, size_t bytes);
+
+/* This process's logical device (0 in single-process mode, -1 before init). */
+int jacc_rank(void);
+
 const char *jacc_error_string(jacc_status s);
 
 #ifdef __cplusplus

@@ -17,9 +17,15 @@
 // synchronize GPUs at the beginning and ending of the communication",
 // P:527).  That covers RAW on pushed/pulled data and WAR on peer replicas.
 #include <cuda_runtime.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -148,6 +154,19 @@ struct Runtime {
     double last_k = 0, last_m = 0;
     uint64_t last_bytes = 0;
     bool last_valid = false;
+    // one-process-per-GPU mode (jacc_init_rank): this process owns logical
+    // device `me`; peers' replicas and events are CUDA-IPC mapped; host
+    // progress counters live in POSIX shared memory.
+    bool mp = false;
+    int me = 0;
+    struct Slot {
+        uint64_t launches;
+        uint64_t barrier;
+        uint64_t pad[6];
+    };
+    Slot *shm = nullptr;
+    std::string shm_name;
+    uint64_t barrier_gen = 0;
 };
 
 Runtime R;
@@ -198,13 +217,66 @@ Region *lookup(const void *p) {
     return (a >= r->base && a < r->base + r->bytes) ? r : nullptr;
 }
 
+bool local(int d) { return !R.mp || d == R.me; }
+
 void set_dev(int d) { CK(cudaSetDevice(R.dev[d].ord)); }
 
-void sync_all() {
+// spin on a shared-memory predicate with a generous timeout (a dead peer
+// must not hang the caller forever)
+template <typename P>
+void spin_until(P pred) {
+    auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t it = 0; !pred(); it++) {
+        if ((it & 1023) == 1023) {
+            sched_yield();
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(300)) {
+                R.poisoned = true;
+                throw Fail{JACC_ERR_STATE};
+            }
+        }
+    }
+}
+
+uint64_t shm_load(const uint64_t *p) { return __atomic_load_n(p, __ATOMIC_ACQUIRE); }
+void shm_store(uint64_t *p, uint64_t v) { __atomic_store_n(p, v, __ATOMIC_RELEASE); }
+
+// host barrier across ranks (multi-process mode only)
+void rank_barrier() {
+    if (!R.mp) return;
+    const uint64_t b = ++R.barrier_gen;
+    shm_store(&R.shm[R.me].barrier, b);
+    spin_until([&] {
+        for (int q = 0; q < R.n; q++)
+            if (shm_load(&R.shm[q].barrier) < b) return false;
+        return true;
+    });
+}
+
+// wait until every rank has enqueued `k` launches (multi-process lockstep:
+// no rank runs more than one launch ahead, so the two-slot event ring of a
+// peer is never re-recorded before this rank has waited on it)
+void wait_launches(uint64_t k) {
+    if (!R.mp) return;
+    spin_until([&] {
+        for (int q = 0; q < R.n; q++)
+            if (shm_load(&R.shm[q].launches) < k) return false;
+        return true;
+    });
+}
+
+// drain this process's device streams
+void local_sync() {
     for (int d = 0; d < R.n; d++) {
+        if (!local(d)) continue;
         set_dev(d);
         CK(cudaStreamSynchronize(R.dev[d].s));
     }
+}
+
+// drain every device's work (collective across ranks in multi-process mode)
+void sync_all() {
+    local_sync();
+    rank_barrier();
 }
 
 cudaEvent_t pool_event() {
@@ -251,6 +323,10 @@ void flush_prof() {
 
 void free_region(Region *r) {
     for (int d = 0; d < (int)r->rep.size(); d++) {
+        if (!local(d)) {
+            if (r->rep[d]) cudaIpcCloseMemHandle(r->rep[d]);
+            continue;
+        }
         set_dev(d);
         if (r->rep[d]) cudaFree(r->rep[d]);
         if (r->dirty[d]) cudaFree(r->dirty[d]);
@@ -520,6 +596,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     }
     L.rg = rg;
     if (R.mode == JACC_MODE_DUP) L.dup = true;
+    for (auto &ai : L.a)
+        if (ai.reg)
+            for (int d = 0; d < R.n; d++)
+                if (!ai.reg->rep[d]) return JACC_ERR_STATE;  // peer replica not imported yet
     plan_launch(L);
 
     const int n = R.n;
@@ -589,16 +669,18 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     const int cur = R.gen & 1, prev = cur ^ 1;
     const bool prof = R.profiling;
     uint64_t merged_bytes = 0;
+    wait_launches(R.gen);
     if (W && !L.dup && (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32)) {
         const size_t words = (size_t)((W->nelem + 31) / 32);
         for (int d = 0; d < n; d++)
-            if (!W->bitmap[d]) {
+            if (local(d) && !W->bitmap[d]) {
                 set_dev(d);
                 CK(cudaMalloc(&W->bitmap[d], words * 4));
                 CK(cudaMemsetAsync(W->bitmap[d], 0, words * 4, R.dev[d].s));
             }
     }
     for (int d = 0; d < n; d++) {
+        if (!local(d)) continue;
         Device &dv = R.dev[d];
         const DevPlan &p = L.plan[d];
         set_dev(d);
@@ -608,8 +690,9 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         for (const Pull &pl : pulls) {
             if (pl.dst != d) continue;
             const size_t e = pl.reg->elem;
-            CK(cudaMemcpyPeerAsync(pl.reg->rep[d] + pl.lo * e, dv.ord, pl.reg->rep[pl.src] + pl.lo * e,
-                                   R.dev[pl.src].ord, (size_t)(pl.hi - pl.lo) * e, dv.s));
+            // UVA: peer device pointer or CUDA-IPC mapped peer replica
+            CK(cudaMemcpyAsync(pl.reg->rep[d] + pl.lo * e, pl.reg->rep[pl.src] + pl.lo * e,
+                               (size_t)(pl.hi - pl.lo) * e, cudaMemcpyDefault, dv.s));
             merged_bytes += (uint64_t)(pl.hi - pl.lo) * e;
         }
         ProfRec pr{d, nullptr, nullptr, nullptr};
@@ -698,6 +781,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         CK(cudaEventRecord(dv.ev[cur], dv.s));
         dv.launches++;
     }
+    if (R.mp) shm_store(&R.shm[R.me].launches, R.gen + 1);
 
     // ---- validity bookkeeping ---------------------------------------------
     for (const Pull &pl : pulls) pl.reg->valid[pl.dst].add(pl.lo, pl.hi);
@@ -728,29 +812,36 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             }
         }
     }
-    R.dev[0].bytes_merged += merged_bytes;
+    R.dev[R.mp ? R.me : 0].bytes_merged += merged_bytes;
     R.last_bytes = merged_bytes;
     R.comm_prev = comm;
     R.gen++;
 
     // ---- reduction combine (obligatory sync) -------------------
     if (D->reduction) {
-        Device &d0 = R.dev[0];
+        // the device that finishes the combine: device 0, or this rank's own
+        const int h = R.mp ? R.me : 0;
+        Device &d0 = R.dev[h];
         const double s_in = *L.red_ptr;
         if (R.use_nccl) {
             NK(ncclGroupStart());
             for (int d = 0; d < n; d++)
-                NK(ncclAllReduce(R.dev[d].part, R.dev[d].res, 1, ncclDouble, ncclSum, R.dev[d].comm,
-                                 R.dev[d].s));
+                if (local(d))
+                    NK(ncclAllReduce(R.dev[d].part, R.dev[d].res, 1, ncclDouble, ncclSum,
+                                     R.dev[d].comm, R.dev[d].s));
             NK(ncclGroupEnd());
-            set_dev(0);
+            set_dev(h);
             jk::PeerPtrs pp{};
             pp.p[0] = d0.res;
             pp.n = 1;
             CK(jk::combine(d0.s, pp, s_in, d0.res));
         } else {
-            set_dev(0);
-            for (int d = 1; d < n; d++) CK(cudaStreamWaitEvent(d0.s, R.dev[d].ev[cur], 0));
+            // virtual devices / no NCCL: fixed-order sum of the partials read
+            // over peer memory (same GPU, P2P or CUDA-IPC mapped)
+            wait_launches(R.gen);
+            set_dev(h);
+            for (int d = 0; d < n; d++)
+                if (d != h) CK(cudaStreamWaitEvent(d0.s, R.dev[d].ev[cur], 0));
             jk::PeerPtrs pp{};
             for (int d = 0; d < n; d++) pp.p[pp.n++] = R.dev[d].part;
             CK(jk::combine(d0.s, pp, s_in, d0.res));
@@ -758,13 +849,9 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         CK(cudaMemcpyAsync(d0.hscal, d0.res, 8, cudaMemcpyDeviceToHost, d0.s));
         CK(cudaStreamSynchronize(d0.s));
         *L.red_ptr = *d0.hscal;
-        if (R.use_nccl) {
-            // the combine ran after each device's allreduce: refresh events
-            for (int d = 0; d < n; d++) {
-                set_dev(d);
-                CK(cudaEventRecord(R.dev[d].ev[cur], R.dev[d].s));
-            }
-        }
+        // peers read this rank's partial: nobody overwrites it before all
+        // combines are done
+        if (R.mp && !R.use_nccl) rank_barrier();
     }
     if (async_id < 0) sync_all();
     return JACC_OK;
@@ -845,8 +932,15 @@ jacc_status jacc_init(int n_devices, const int *device_ids) {
 jacc_status jacc_finalize(void) {
     if (!R.init) return JACC_ERR_STATE;
     for (int d = 0; d < R.n; d++) {
+        if (!local(d)) continue;
         cudaSetDevice(R.dev[d].ord);
         cudaStreamSynchronize(R.dev[d].s);
+    }
+    if (R.mp && !R.poisoned) {
+        try {
+            rank_barrier();  // no peer still reads or writes our memory
+        } catch (Fail &) {
+        }
     }
     for (auto &kv : R.table) free_region(kv.second.get());
     R.table.clear();
@@ -858,6 +952,12 @@ jacc_status jacc_finalize(void) {
     for (auto e : R.evpool) cudaEventDestroy(e);
     for (int d = 0; d < R.n; d++) {
         Device &dv = R.dev[d];
+        if (!local(d)) {
+            if (dv.ev[0]) cudaEventDestroy(dv.ev[0]);
+            if (dv.ev[1]) cudaEventDestroy(dv.ev[1]);
+            if (dv.part) cudaIpcCloseMemHandle(dv.part);
+            continue;
+        }
         cudaSetDevice(dv.ord);
         if (dv.comm) ncclCommDestroy(dv.comm);
         cudaFree(dv.partials);
@@ -870,6 +970,10 @@ jacc_status jacc_finalize(void) {
         cudaStreamDestroy(dv.s);
     }
     cudaGetLastError();
+    if (R.shm) {
+        munmap(R.shm, sizeof(Runtime::Slot) * JACC_MAX_DEVICES);
+        if (R.me == 0) shm_unlink(R.shm_name.c_str());
+    }
     R = Runtime{};
     return JACC_OK;
 }
@@ -927,6 +1031,7 @@ jacc_status jacc_data_create(void *host, size_t bytes, size_t elem_size, int ndi
         r->bitmap.assign(R.n, nullptr);
         r->valid.assign(R.n, IntervalSet{});
         for (int d = 0; d < R.n; d++) {
+            if (!local(d)) continue;  // peers' replicas arrive via jacc_import_region
             set_dev(d);
             if (cudaMalloc(&r->rep[d], bytes) != cudaSuccess ||
                 cudaMalloc(&r->dirty[d], 16) != cudaSuccess) {
@@ -967,6 +1072,7 @@ jacc_status jacc_update_device(void *host, size_t off, size_t bytes) {
         if (bytes == 0) return JACC_OK;
         sync_all();
         for (int d = 0; d < R.n; d++) {
+            if (!local(d)) continue;
             set_dev(d);
             CK(cudaMemcpyAsync(r->rep[d] + start, (const char *)r->base + start, bytes,
                                cudaMemcpyHostToDevice, R.dev[d].s));
@@ -987,35 +1093,51 @@ jacc_status jacc_update_host(void *host, size_t off, size_t bytes) {
         if (bytes == 0) return JACC_OK;
         sync_all();
         const int64_t e0 = (int64_t)(start / r->elem), e1 = (int64_t)((start + bytes) / r->elem);
-        // gather: pull stale intervals into the primary from a valid replica
-        Device &d0 = R.dev[0];
-        set_dev(0);
-        for (auto &m : r->valid[0].missing(e0, e1)) {
-            int64_t a = m.first;
-            while (a < m.second) {
-                int src = -1;
-                int64_t b = m.second;
-                for (int q = 1; q < R.n && src < 0; q++) {
-                    auto &vi = r->valid[q].iv;
-                    auto it = vi.upper_bound(a);
-                    if (it == vi.begin()) continue;
-                    --it;
-                    if (it->first <= a && it->second > a) {
-                        src = q;
-                        b = std::min(b, it->second);
+        // gather: pull stale intervals into the primary from a valid replica.
+        // Multi-process mode: every rank's device is its own primary; all
+        // ranks plan every device's pulls so the validity trackers agree.
+        struct GP {
+            int t, src;
+            int64_t a, b;
+        };
+        std::vector<GP> gp;
+        for (int t = 0; t < R.n; t++) {
+            if (!R.mp && t != 0) continue;
+            for (auto &m : r->valid[t].missing(e0, e1)) {
+                int64_t a = m.first;
+                while (a < m.second) {
+                    int src = -1;
+                    int64_t b = m.second;
+                    for (int q = 0; q < R.n && src < 0; q++) {
+                        if (q == t) continue;
+                        auto &vi = r->valid[q].iv;
+                        auto it = vi.upper_bound(a);
+                        if (it == vi.begin()) continue;
+                        --it;
+                        if (it->first <= a && it->second > a) {
+                            src = q;
+                            b = std::min(b, it->second);
+                        }
                     }
+                    if (src < 0) break;  // never initialised anywhere
+                    gp.push_back({t, src, a, b});
+                    a = b;
                 }
-                if (src < 0) break;  // never initialised anywhere
-                CK(cudaStreamWaitEvent(d0.s, R.dev[src].ev[(R.gen - 1) & 1], 0));
-                CK(cudaMemcpyPeerAsync(r->rep[0] + a * r->elem, d0.ord, r->rep[src] + a * r->elem,
-                                       R.dev[src].ord, (size_t)(b - a) * r->elem, d0.s));
-                r->valid[0].add(a, b);
-                a = b;
             }
         }
-        CK(cudaMemcpyAsync((char *)r->base + start, r->rep[0] + start, bytes, cudaMemcpyDeviceToHost,
+        const int h = R.mp ? R.me : 0;
+        Device &d0 = R.dev[h];
+        set_dev(h);
+        for (auto &g : gp) {
+            if (g.t == h)
+                CK(cudaMemcpyAsync(r->rep[h] + g.a * r->elem, r->rep[g.src] + g.a * r->elem,
+                                   (size_t)(g.b - g.a) * r->elem, cudaMemcpyDefault, d0.s));
+        }
+        for (auto &g : gp) r->valid[g.t].add(g.a, g.b);
+        CK(cudaMemcpyAsync((char *)r->base + start, r->rep[h] + start, bytes, cudaMemcpyDeviceToHost,
                            d0.s));
         CK(cudaStreamSynchronize(d0.s));
+        rank_barrier();  // peers may have read this rank's replica
         return JACC_OK;
     });
 }
@@ -1038,7 +1160,8 @@ jacc_status jacc_get_dirty_range(void *host, int dev, uint64_t *mn, uint64_t *mx
         Region *r = lookup(host);
         if (!r) return JACC_ERR_NOT_PRESENT;
         if (dev < 0 || dev >= R.n || !mn || !mx) return JACC_ERR_INVALID;
-        sync_all();
+        if (!local(dev)) return JACC_ERR_INVALID;
+        local_sync();
         u64 h[2];
         set_dev(dev);
         CK(cudaMemcpy(h, r->dirty[dev], 16, cudaMemcpyDeviceToHost));
@@ -1055,7 +1178,8 @@ jacc_status jacc_get_dirty_bitmap(void *host, int dev, uint32_t *out, size_t nwo
         if (dev < 0 || dev >= R.n || !out) return JACC_ERR_INVALID;
         const size_t words = (size_t)((r->nelem + 31) / 32);
         if (nwords < words || !r->bitmap[dev]) return JACC_ERR_INVALID;
-        sync_all();
+        if (!local(dev)) return JACC_ERR_INVALID;
+        local_sync();
         set_dev(dev);
         CK(cudaMemcpy(out, r->bitmap[dev], words * 4, cudaMemcpyDeviceToHost));
         return JACC_OK;
@@ -1067,7 +1191,8 @@ jacc_status jacc_get_replica(void *host, int dev, void *out, size_t bytes) {
         Region *r = lookup(host);
         if (!r) return JACC_ERR_NOT_PRESENT;
         if (dev < 0 || dev >= R.n || !out || bytes > r->bytes) return JACC_ERR_INVALID;
-        sync_all();
+        if (!local(dev)) return JACC_ERR_INVALID;
+        local_sync();
         set_dev(dev);
         CK(cudaMemcpy(out, r->rep[dev], bytes, cudaMemcpyDeviceToHost));
         return JACC_OK;
@@ -1120,12 +1245,161 @@ jacc_status jacc_profile_reset(void) {
 
 jacc_status jacc_get_stream(int dev, void **stream, int *ord) {
     return guard([&]() -> jacc_status {
-        if (dev < 0 || dev >= R.n) return JACC_ERR_INVALID;
+        if (dev < 0 || dev >= R.n || !local(dev)) return JACC_ERR_INVALID;
         if (stream) *stream = (void *)R.dev[dev].s;
         if (ord) *ord = R.dev[dev].ord;
         return JACC_OK;
     });
 }
+
+// ---------------------------------------------------------------------------
+// one process per GPU
+// ---------------------------------------------------------------------------
+jacc_status jacc_unique_id(void *out, size_t bytes) {
+    if (!out || bytes < JACC_UNIQUE_ID_BYTES) return JACC_ERR_INVALID;
+    static_assert(sizeof(ncclUniqueId) <= JACC_UNIQUE_ID_BYTES, "nccl id size");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return JACC_ERR_NCCL;
+    memset(out, 0, bytes);
+    memcpy(out, &id, sizeof(id));
+    return JACC_OK;
+}
+
+jacc_status jacc_init_rank(int rank, int world, int cuda_ordinal, const void *unique_id,
+                           const char *shm_name) {
+    if (R.init) return JACC_ERR_STATE;
+    return guard(
+        [&]() -> jacc_status {
+            int count = 0;
+            if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1) return JACC_ERR_CUDA;
+            if (world < 1 || world > JACC_MAX_DEVICES || rank < 0 || rank >= world ||
+                cuda_ordinal < 0 || cuda_ordinal >= count || !shm_name || !*shm_name)
+                return JACC_ERR_INVALID;
+            R = Runtime{};
+            R.n = world;
+            R.mp = true;
+            R.me = rank;
+            R.dev.resize(world);
+            R.init = true;
+            const char *pol = getenv("JACC_MERGE");
+            if (pol && !strcmp(pol, "halo")) R.policy = JACC_MERGE_HALO;
+            // host progress counters (zero-filled on creation)
+            R.shm_name = shm_name[0] == '/' ? shm_name : std::string("/") + shm_name;
+            int fd = shm_open(R.shm_name.c_str(), O_CREAT | O_RDWR, 0600);
+            if (fd < 0) return JACC_ERR_INVALID;
+            const size_t sz = sizeof(Runtime::Slot) * JACC_MAX_DEVICES;
+            if (ftruncate(fd, (off_t)sz) != 0) {
+                close(fd);
+                return JACC_ERR_INVALID;
+            }
+            void *m = mmap(nullptr, sz, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+            close(fd);
+            if (m == MAP_FAILED) return JACC_ERR_INVALID;
+            R.shm = static_cast<Runtime::Slot *>(m);
+            Device &dv = R.dev[rank];
+            dv.ord = cuda_ordinal;
+            set_dev(rank);
+            CK(cudaStreamCreateWithFlags(&dv.s, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; k++) {
+                CK(cudaEventCreateWithFlags(&dv.ev[k], cudaEventDisableTiming | cudaEventInterprocess));
+                CK(cudaEventRecord(dv.ev[k], dv.s));
+            }
+            CK(cudaMalloc(&dv.partials, jk::kReduceGrid * sizeof(double)));
+            CK(cudaMalloc(&dv.ticket, 64));
+            CK(cudaMemset(dv.ticket, 0, 64));
+            CK(cudaMalloc(&dv.part, 8));
+            CK(cudaMalloc(&dv.res, 8));
+            CK(cudaMemset(dv.part, 0, 8));
+            CK(cudaMallocHost(&dv.hscal, 8));
+            CK(cudaStreamSynchronize(dv.s));
+            if (unique_id && world > 1) {
+                ncclUniqueId id;
+                memcpy(&id, unique_id, sizeof(id));
+                NK(ncclCommInitRank(&dv.comm, world, id, rank));
+                R.use_nccl = true;
+            }
+            R.comm_prev.assign(world, std::vector<char>(world, 0));
+            return JACC_OK;
+        },
+        false);
+}
+
+jacc_status jacc_export_runtime(void *out, size_t bytes) {
+    return guard([&]() -> jacc_status {
+        if (!R.mp || !out || bytes < JACC_RUNTIME_HANDLE_BYTES) return JACC_ERR_INVALID;
+        static_assert(3 * sizeof(cudaIpcMemHandle_t) <= JACC_RUNTIME_HANDLE_BYTES, "handle size");
+        Device &dv = R.dev[R.me];
+        set_dev(R.me);
+        char *o = static_cast<char *>(out);
+        memset(o, 0, bytes);
+        cudaIpcEventHandle_t e0, e1;
+        cudaIpcMemHandle_t mp;
+        CK(cudaIpcGetEventHandle(&e0, dv.ev[0]));
+        CK(cudaIpcGetEventHandle(&e1, dv.ev[1]));
+        CK(cudaIpcGetMemHandle(&mp, dv.part));
+        memcpy(o, &e0, sizeof(e0));
+        memcpy(o + 64, &e1, sizeof(e1));
+        memcpy(o + 128, &mp, sizeof(mp));
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_import_runtime(int peer, const void *in, size_t bytes) {
+    return guard([&]() -> jacc_status {
+        if (!R.mp || !in || bytes < JACC_RUNTIME_HANDLE_BYTES || peer < 0 || peer >= R.n ||
+            peer == R.me)
+            return JACC_ERR_INVALID;
+        const char *p = static_cast<const char *>(in);
+        Device &pv = R.dev[peer];
+        set_dev(R.me);
+        cudaIpcEventHandle_t e0, e1;
+        cudaIpcMemHandle_t mp;
+        memcpy(&e0, p, sizeof(e0));
+        memcpy(&e1, p + 64, sizeof(e1));
+        memcpy(&mp, p + 128, sizeof(mp));
+        CK(cudaIpcOpenEventHandle(&pv.ev[0], e0));
+        CK(cudaIpcOpenEventHandle(&pv.ev[1], e1));
+        void *ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, mp, cudaIpcMemLazyEnablePeerAccess));
+        pv.part = static_cast<double *>(ptr);
+        pv.ord = -1;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_export_region(void *host, void *out, size_t bytes) {
+    return guard([&]() -> jacc_status {
+        if (!R.mp || !out || bytes < JACC_REGION_HANDLE_BYTES) return JACC_ERR_INVALID;
+        Region *r = lookup(host);
+        if (!r) return JACC_ERR_NOT_PRESENT;
+        set_dev(R.me);
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, r->rep[R.me]));
+        memset(out, 0, bytes);
+        memcpy(out, &h, sizeof(h));
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_import_region(void *host, int peer, const void *in, size_t bytes) {
+    return guard([&]() -> jacc_status {
+        if (!R.mp || !in || bytes < JACC_REGION_HANDLE_BYTES || peer < 0 || peer >= R.n ||
+            peer == R.me)
+            return JACC_ERR_INVALID;
+        Region *r = lookup(host);
+        if (!r) return JACC_ERR_NOT_PRESENT;
+        if (r->rep[peer]) return JACC_ERR_STATE;
+        set_dev(R.me);
+        cudaIpcMemHandle_t h;
+        memcpy(&h, in, sizeof(h));
+        void *ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        r->rep[peer] = static_cast<char *>(ptr);
+        return JACC_OK;
+    });
+}
+
+int jacc_rank(void) { return R.init ? (R.mp ? R.me : 0) : -1; }
 
 const char *jacc_error_string(jacc_status s) {
     switch (s) {

@@ -50,7 +50,12 @@ EXPORTS = [
     "jacc_launch", "jacc_wait", "jacc_get_dirty_range", "jacc_get_dirty_bitmap",
     "jacc_get_replica", "jacc_last_timing", "jacc_set_profiling", "jacc_profile_totals",
     "jacc_profile_reset", "jacc_get_stream", "jacc_error_string",
+    "jacc_unique_id", "jacc_init_rank", "jacc_export_runtime", "jacc_import_runtime",
+    "jacc_export_region", "jacc_import_region", "jacc_rank",
 ]
+JACC_UNIQUE_ID_BYTES = 128
+JACC_RUNTIME_HANDLE_BYTES = 192
+JACC_REGION_HANDLE_BYTES = 64
 
 
 class jacc_range(ctypes.Structure):
@@ -88,10 +93,18 @@ for _name, _args in {
     "jacc_get_stream": [_I, ctypes.POINTER(_P), ctypes.POINTER(_I)],
     "jacc_partition": [ctypes.c_int64, _I, _I, ctypes.POINTER(ctypes.c_int64),
                        ctypes.POINTER(ctypes.c_int64)],
+    "jacc_unique_id": [_P, _SZ],
+    "jacc_init_rank": [_I, _I, _I, _P, ctypes.c_char_p],
+    "jacc_export_runtime": [_P, _SZ],
+    "jacc_import_runtime": [_I, _P, _SZ],
+    "jacc_export_region": [_P, _P, _SZ],
+    "jacc_import_region": [_P, _I, _P, _SZ],
 }.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = ctypes.c_int
+lib.jacc_rank.argtypes = []
+lib.jacc_rank.restype = ctypes.c_int
 lib.jacc_num_devices.argtypes = []
 lib.jacc_num_devices.restype = ctypes.c_int
 lib.jacc_error_string.argtypes = [ctypes.c_int]
@@ -258,3 +271,46 @@ def jacc_get_stream(dev):
 
 def jacc_error_string(status):
     return lib.jacc_error_string(status).decode()
+
+
+# ---- one process per GPU ------------------------------------------------------
+def _blob(n):
+    return ctypes.create_string_buffer(n)
+
+
+def jacc_unique_id():
+    b = _blob(JACC_UNIQUE_ID_BYTES)
+    _ck(lib.jacc_unique_id(b, len(b)), "jacc_unique_id")
+    return bytes(b.raw)
+
+
+def jacc_init_rank(rank, world, cuda_ordinal, unique_id, shm_name):
+    uid = ctypes.create_string_buffer(unique_id, JACC_UNIQUE_ID_BYTES) if unique_id else None
+    return _ck(lib.jacc_init_rank(rank, world, cuda_ordinal, uid, shm_name.encode()),
+               "jacc_init_rank")
+
+
+def jacc_export_runtime():
+    b = _blob(JACC_RUNTIME_HANDLE_BYTES)
+    _ck(lib.jacc_export_runtime(b, len(b)), "jacc_export_runtime")
+    return bytes(b.raw)
+
+
+def jacc_import_runtime(peer, blob):
+    b = ctypes.create_string_buffer(blob, len(blob))
+    return _ck(lib.jacc_import_runtime(peer, b, len(blob)), "jacc_import_runtime")
+
+
+def jacc_export_region(arr):
+    b = _blob(JACC_REGION_HANDLE_BYTES)
+    _ck(lib.jacc_export_region(_addr(arr), b, len(b)), "jacc_export_region")
+    return bytes(b.raw)
+
+
+def jacc_import_region(arr, peer, blob):
+    b = ctypes.create_string_buffer(blob, len(blob))
+    return _ck(lib.jacc_import_region(_addr(arr), peer, b, len(blob)), "jacc_import_region")
+
+
+def jacc_rank():
+    return lib.jacc_rank()
