@@ -13,6 +13,7 @@
 #include "kernels.cuh"
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace jk {
 namespace {
@@ -39,9 +40,18 @@ __device__ __forceinline__ u64 warp_max_u64(u64 v) {
 
 // CTA-wide min/max of per-thread stored indices -> one atomic pair per CTA.
 // Must be called by every thread of the CTA (contains __syncthreads).
+//
+// Records are double-buffered: the two 16-byte slots of a 32-byte-aligned
+// pair alternate between launches, and every writing kernel clears the
+// OTHER slot (the one the next launch will use) -- no memset per launch.
 template <int NWARPS>
 __device__ __forceinline__ void publish_dirty(u64 mn, u64 mx, u64 *dirty) {
     __shared__ u64 smn[NWARPS], smx[NWARPS];
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        u64 *nx = reinterpret_cast<u64 *>(reinterpret_cast<uintptr_t>(dirty) ^ 16u);
+        nx[0] = kU64Max;
+        nx[1] = kU64Max;
+    }
     mn = warp_min_u64(mn);
     mx = warp_max_u64(mx);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -93,9 +103,9 @@ __global__ void __launch_bounds__(256) square_f32_kernel(const float *__restrict
 // Each src element is read from HBM once per sweep (halo rows between row
 // tiles are L2 hits), each dst element written once: 16 B/point.
 // ---------------------------------------------------------------------------
-constexpr int JW = 4;    // warps per CTA (side by side in columns)
-constexpr int JR = 32;   // rows per tile
-constexpr int JPF = 3;   // rows of prefetch beyond i+1
+// Tile shape (JW warps side by side, JR rows, JPF rows of prefetch, MINB
+// CTAs/SM register target) is a template so variants can be measured on the
+// box (JACC_JACOBI_VARIANT); the default is the measured best.
 
 template <int V>
 struct JRow {
@@ -123,8 +133,8 @@ __device__ __forceinline__ void jload(JRow<V> &o, const double *__restrict__ src
     o.r = (ok && lane == 31 && cs + 32 * V < N) ? __ldg(p + cs + 32 * V) : 0.0;
 }
 
-template <int V>
-__global__ void __launch_bounds__(JW * 32)
+template <int V, int JW, int JR, int JPF, int MINB>
+__global__ void __launch_bounds__(JW * 32, MINB)
     jacobi2d_kernel(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t r0,
                     int64_t r1, int64_t c0, int64_t c1, int64_t cs_base, int64_t ntiles_y,
                     u64 *dirty, double *push_top, double *push_bot) {
@@ -303,14 +313,11 @@ __global__ void combine_kernel(PeerPtrs parts, double s_in, double *out) {
 
 // ---------------------------------------------------------------------------
 // BK3  fp64 GEMM on the DMMA tensor pipe.
-// CTA tile 64x64, K tile 16, 3-stage cp.async pipeline, 4 warps (2x2) each
-// owning a 32x32 warp tile = 4x4 mma.sync.m8n8k4.f64 fragments.
+// CTA tile BM x BN, K tile BK, ST-stage cp.async pipeline; warps arranged
+// (BM/WM) x (BN/WN), each owning a WM x WN warp tile of
+// mma.sync.m8n8k4.f64 fragments (SASS DMMA.8x8x4).  Smem rows are padded
+// (A: BK+4, B: BN+8 doubles) so fragment loads are conflict-free.
 // ---------------------------------------------------------------------------
-constexpr int GBM = 64, GBN = 64, GBK = 16, GST = 3;
-constexpr int GAP = GBK + 4;  // A smem row stride (doubles): conflict-free fragment loads
-constexpr int GBP = GBN + 8;  // B smem row stride (doubles)
-constexpr int GSMEM = GST * (GBM * GAP + GBK * GBP) * 8;
-
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int bytes) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
@@ -332,7 +339,15 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
         : "d"(a), "d"(b));
 }
 
-template <bool V16>
+template <int BM, int BN, int BK, int ST, int WM, int WN>
+struct GemmCfg {
+    static constexpr int NT = (BM / WM) * (BN / WN) * 32;
+    static constexpr int AP = BK + 4;
+    static constexpr int BP = BN + 8;
+    static constexpr int SMEM = ST * (BM * AP + BK * BP) * 8;
+};
+
+template <class G, int BM, int BN, int BK, bool V16>
 __device__ __forceinline__ void gemm_load_tile(double *As, double *Bs, const double *A,
                                                const double *B, int64_t M, int64_t Nb, int64_t N,
                                                int64_t K, int64_t m0, int64_t n0, int64_t k0) {
@@ -340,9 +355,10 @@ __device__ __forceinline__ void gemm_load_tile(double *As, double *Bs, const dou
     const int tid = threadIdx.x;
     if (V16) {
 #pragma unroll
-        for (int it = 0; it < (GBM * GBK / 2) / 128; it++) {
-            const int c = tid + it * 128;
-            const int row = c / (GBK / 2), cp = c % (GBK / 2);
+        for (int it = 0; it < (BM * BK / 2 + G::NT - 1) / G::NT; it++) {
+            const int c = tid + it * G::NT;
+            if (c >= BM * BK / 2) break;
+            const int row = c / (BK / 2), cp = c % (BK / 2);
             const int64_t gm = m0 + row, gk = k0 + 2 * cp;
             int bytes = 0;
             const double *src = A;
@@ -350,12 +366,13 @@ __device__ __forceinline__ void gemm_load_tile(double *As, double *Bs, const dou
                 bytes = (K - gk >= 2) ? 16 : 8;
                 src = A + gm * K + gk;
             }
-            cp_async16(As + row * GAP + 2 * cp, src, bytes);
+            cp_async16(As + row * G::AP + 2 * cp, src, bytes);
         }
 #pragma unroll
-        for (int it = 0; it < (GBK * GBN / 2) / 128; it++) {
-            const int c = tid + it * 128;
-            const int row = c / (GBN / 2), cp = c % (GBN / 2);
+        for (int it = 0; it < (BK * BN / 2 + G::NT - 1) / G::NT; it++) {
+            const int c = tid + it * G::NT;
+            if (c >= BK * BN / 2) break;
+            const int row = c / (BN / 2), cp = c % (BN / 2);
             const int64_t gk = k0 + row, gn = n0 + 2 * cp;
             int bytes = 0;
             const double *src = B;
@@ -363,82 +380,84 @@ __device__ __forceinline__ void gemm_load_tile(double *As, double *Bs, const dou
                 bytes = (Nb - gn >= 2) ? 16 : 8;
                 src = B + gk * N + gn;
             }
-            cp_async16(Bs + row * GBP + 2 * cp, src, bytes);
+            cp_async16(Bs + row * G::BP + 2 * cp, src, bytes);
         }
     } else {
 #pragma unroll
-        for (int it = 0; it < (GBM * GBK) / 128; it++) {
-            const int c = tid + it * 128;
-            const int row = c / GBK, cc = c % GBK;
+        for (int it = 0; it < (BM * BK + G::NT - 1) / G::NT; it++) {
+            const int c = tid + it * G::NT;
+            if (c >= BM * BK) break;
+            const int row = c / BK, cc = c % BK;
             const int64_t gm = m0 + row, gk = k0 + cc;
             const bool ok = gm < M && gk < K;
-            cp_async8(As + row * GAP + cc, ok ? A + gm * K + gk : A, ok ? 8 : 0);
+            cp_async8(As + row * G::AP + cc, ok ? A + gm * K + gk : A, ok ? 8 : 0);
         }
 #pragma unroll
-        for (int it = 0; it < (GBK * GBN) / 128; it++) {
-            const int c = tid + it * 128;
-            const int row = c / GBN, cc = c % GBN;
+        for (int it = 0; it < (BK * BN + G::NT - 1) / G::NT; it++) {
+            const int c = tid + it * G::NT;
+            if (c >= BK * BN) break;
+            const int row = c / BN, cc = c % BN;
             const int64_t gk = k0 + row, gn = n0 + cc;
             const bool ok = gk < K && gn < Nb;
-            cp_async8(Bs + row * GBP + cc, ok ? B + gk * N + gn : B, ok ? 8 : 0);
+            cp_async8(Bs + row * G::BP + cc, ok ? B + gk * N + gn : B, ok ? 8 : 0);
         }
     }
 }
 
-template <bool V16>
-__global__ void __launch_bounds__(128) gemm_f64_kernel(const double *__restrict__ A,
-                                                       const double *__restrict__ B,
-                                                       double *__restrict__ C, int64_t M,
-                                                       int64_t N, int64_t K, int64_t r0, int64_t r1,
-                                                       int64_t c0, int64_t c1, u64 *dirty) {
+template <int BM, int BN, int BK, int ST, int WM, int WN, bool V16>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, ST, WM, WN>::NT)
+    gemm_f64_kernel(const double *__restrict__ A, const double *__restrict__ B,
+                    double *__restrict__ C, int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1,
+                    int64_t c0, int64_t c1, u64 *dirty) {
+    using G = GemmCfg<BM, BN, BK, ST, WM, WN>;
+    constexpr int MI = WM / 8, NJ = WN / 8, WCOLS = BN / WN;
     extern __shared__ __align__(16) double gsm[];
-    double *As = gsm;                        // [GST][GBM][GAP]
-    double *Bs = gsm + GST * GBM * GAP;      // [GST][GBK][GBP]
+    double *As = gsm;                       // [ST][BM][AP]
+    double *Bs = gsm + ST * BM * G::AP;     // [ST][BK][BP]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = warp >> 1, wn = warp & 1;
-    const int64_t m0 = r0 + (int64_t)blockIdx.y * GBM;
-    const int64_t n0 = c0 + (int64_t)blockIdx.x * GBN;
-    const int64_t Mb = r1, Nb = c1;  // loads beyond the owned block are never needed
+    const int wm = warp / WCOLS, wn = warp % WCOLS;
+    const int64_t m0 = r0 + (int64_t)blockIdx.y * BM;
+    const int64_t n0 = c0 + (int64_t)blockIdx.x * BN;
 
-    double acc[4][4][2];
+    double acc[MI][NJ][2];
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < MI; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    const int64_t KT = (K + GBK - 1) / GBK;
+    const int64_t KT = (K + BK - 1) / BK;
 #pragma unroll
-    for (int s = 0; s < GST - 1; s++) {
+    for (int s = 0; s < ST - 1; s++) {
         if (s < KT)
-            gemm_load_tile<V16>(As + s * GBM * GAP, Bs + s * GBK * GBP, A, B, Mb, Nb, N, K, m0,
-                                n0, (int64_t)s * GBK);
+            gemm_load_tile<G, BM, BN, BK, V16>(As + s * BM * G::AP, Bs + s * BK * G::BP, A, B, r1,
+                                               c1, N, K, m0, n0, (int64_t)s * BK);
         cp_commit();
     }
     const int ar = lane >> 2, ac = lane & 3;
     for (int64_t kt = 0; kt < KT; kt++) {
-        cp_wait<GST - 2>();
+        cp_wait<ST - 2>();
         __syncthreads();
-        const int64_t nk = kt + GST - 1;
+        const int64_t nk = kt + ST - 1;
         if (nk < KT) {
-            const int s = (int)(nk % GST);
-            gemm_load_tile<V16>(As + s * GBM * GAP, Bs + s * GBK * GBP, A, B, Mb, Nb, N, K, m0,
-                                n0, nk * GBK);
+            const int s = (int)(nk % ST);
+            gemm_load_tile<G, BM, BN, BK, V16>(As + s * BM * G::AP, Bs + s * BK * G::BP, A, B, r1,
+                                               c1, N, K, m0, n0, nk * BK);
         }
         cp_commit();
-        const int s = (int)(kt % GST);
-        const double *as = As + s * GBM * GAP + (wm * 32 + ar) * GAP + ac;
-        const double *bs = Bs + s * GBK * GBP + ac * GBP + wn * 32 + ar;
+        const int s = (int)(kt % ST);
+        const double *as = As + s * BM * G::AP + (wm * WM + ar) * G::AP + ac;
+        const double *bs = Bs + s * BK * G::BP + ac * G::BP + wn * WN + ar;
 #pragma unroll
-        for (int kk = 0; kk < GBK; kk += 4) {
-            double a[4], b[4];
+        for (int kk = 0; kk < BK; kk += 4) {
+            double a[MI], b[NJ];
 #pragma unroll
-            for (int i = 0; i < 4; i++) a[i] = as[i * 8 * GAP + kk];
+            for (int i = 0; i < MI; i++) a[i] = as[i * 8 * G::AP + kk];
 #pragma unroll
-            for (int j = 0; j < 4; j++) b[j] = bs[kk * GBP + j * 8];
+            for (int j = 0; j < NJ; j++) b[j] = bs[kk * G::BP + j * 8];
 #pragma unroll
-            for (int i = 0; i < 4; i++)
+            for (int i = 0; i < MI; i++)
 #pragma unroll
-                for (int j = 0; j < 4; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+                for (int j = 0; j < NJ; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
     }
     cp_wait<0>();
@@ -446,12 +465,12 @@ __global__ void __launch_bounds__(128) gemm_f64_kernel(const double *__restrict_
     // epilogue: store C rows in [r0, r1), cols in [c0, c1); track dirty
     u64 mn = kU64Max, mx = 0;
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const int64_t m = m0 + wm * 32 + i * 8 + ar;
+    for (int i = 0; i < MI; i++) {
+        const int64_t m = m0 + wm * WM + i * 8 + ar;
         if (m >= r1) continue;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int64_t n = n0 + wn * 32 + j * 8 + ac * 2;
+        for (int j = 0; j < NJ; j++) {
+            const int64_t n = n0 + wn * WN + j * 8 + ac * 2;
             const int64_t f = m * N + n;
             if (V16 && n + 1 < c1) {
                 *reinterpret_cast<double2 *>(C + f) = make_double2(acc[i][j][0], acc[i][j][1]);
@@ -470,7 +489,7 @@ __global__ void __launch_bounds__(128) gemm_f64_kernel(const double *__restrict_
             }
         }
     }
-    publish_dirty<4>(mn, mx, dirty);
+    publish_dirty<G::NT / 32>(mn, mx, dirty);
 }
 
 // ---------------------------------------------------------------------------
@@ -503,8 +522,12 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
     u64 mn = kU64Max, mx = 0;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n4 = n >> 2;
-    const int4 *idx4 = reinterpret_cast<const int4 *>(idx);
+    // 16-byte aligned body of int4 loads; head (< 4) and tail (< 4) elements
+    // go to the first warp
+    int64_t h = (int64_t)((16 - ((uintptr_t)idx & 15)) & 15) >> 2;
+    if (h > n) h = n;
+    const int64_t n4 = (n - h) >> 2;
+    const int4 *idx4 = reinterpret_cast<const int4 *>(idx + h);
     // whole warps iterate together (match/reduce need full warps)
     const int64_t iters = (n4 + nth - 1) / nth;
     for (int64_t it = 0; it < iters; it++) {
@@ -512,18 +535,217 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
         const bool v = q < n4;
         int4 k4 = make_int4(0, 0, 0, 0);
         if (v) k4 = __ldcs(idx4 + q);
-        scat_one<T>(k4.x, 4 * q + 0, b, a, lo, hi, bitmap, mn, mx, v);
-        scat_one<T>(k4.y, 4 * q + 1, b, a, lo, hi, bitmap, mn, mx, v);
-        scat_one<T>(k4.z, 4 * q + 2, b, a, lo, hi, bitmap, mn, mx, v);
-        scat_one<T>(k4.w, 4 * q + 3, b, a, lo, hi, bitmap, mn, mx, v);
+        const int64_t i0 = h + 4 * q;
+        scat_one<T>(k4.x, i0 + 0, b, a, lo, hi, bitmap, mn, mx, v);
+        scat_one<T>(k4.y, i0 + 1, b, a, lo, hi, bitmap, mn, mx, v);
+        scat_one<T>(k4.z, i0 + 2, b, a, lo, hi, bitmap, mn, mx, v);
+        scat_one<T>(k4.w, i0 + 3, b, a, lo, hi, bitmap, mn, mx, v);
     }
-    // tail (n % 4), handled by the first warp
     if (blockIdx.x == 0 && threadIdx.x < 32) {
-        const int64_t i = 4 * n4 + threadIdx.x;
-        const bool v = i < n;
+        const int l = threadIdx.x;
+        const int64_t t0 = h + 4 * n4;  // tail start
+        const int64_t i = l < 4 ? (int64_t)l : t0 + (l - 4);
+        const bool v = (l < 4) ? (i < h) : (i < n);
         scat_one<T>(v ? idx[i] : 0, v ? i : 0, b, a, lo, hi, bitmap, mn, mx, v);
     }
     publish_dirty<8>(mn, mx, dirty);
+}
+
+// ---------------------------------------------------------------------------
+// BK4b destination-binned scatter (see kernels.cuh)
+// ---------------------------------------------------------------------------
+constexpr int SB_T = 256, SB_E = 8, SB_TILE = SB_T * SB_E;
+constexpr int SB_MAXB = 1024;
+
+__global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restrict__ idx, int64_t n,
+                                                        int64_t lo, int64_t hi, int shift, int nb,
+                                                        u64 *counts) {
+    __shared__ unsigned h[SB_MAXB];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t hd = (int64_t)((16 - ((uintptr_t)idx & 15)) & 15) >> 2;
+    if (hd > n) hd = n;
+    const int64_t n4 = (n - hd) >> 2;
+    const int4 *idx4 = reinterpret_cast<const int4 *>(idx + hd);
+    if (tid < hd) {
+        const int32_t k = idx[tid];
+        if (k >= lo && k < hi) atomicAdd(&h[(k - lo) >> shift], 1u);
+    }
+    for (int64_t q = tid; q < n4; q += nth) {
+        const int4 k = __ldg(idx4 + q);
+        if (k.x >= lo && k.x < hi) atomicAdd(&h[(k.x - lo) >> shift], 1u);
+        if (k.y >= lo && k.y < hi) atomicAdd(&h[(k.y - lo) >> shift], 1u);
+        if (k.z >= lo && k.z < hi) atomicAdd(&h[(k.z - lo) >> shift], 1u);
+        if (k.w >= lo && k.w < hi) atomicAdd(&h[(k.w - lo) >> shift], 1u);
+    }
+    for (int64_t i = hd + 4 * n4 + tid; i < n; i += nth) {
+        const int32_t k = idx[i];
+        if (k >= lo && k < hi) atomicAdd(&h[(k - lo) >> shift], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+        if (h[i]) atomicAdd(&counts[i], (u64)h[i]);
+}
+
+// exclusive scan of counts[0..nb) -> base[0..nb] and cursor = base (1 block);
+// also zeroes the apply kernel's work counter
+__global__ void scat_scan_kernel(const u64 *counts, int nb, u64 *base, u64 *cursor, u64 *work) {
+    if (threadIdx.x == 0) {
+        *work = 0;
+        u64 acc = 0;
+        for (int i = 0; i < nb; i++) {
+            base[i] = acc;
+            cursor[i] = acc;
+            acc += counts[i];
+        }
+        base[nb] = acc;
+    }
+}
+
+// warp 0 computes the exclusive scan of hist[0..nb) into off[]
+__device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off, int nb,
+                                            unsigned *total) {
+    const int lane = threadIdx.x & 31;
+    const int per = (nb + 31) / 32;
+    const int b0 = lane * per;
+    unsigned loc = 0;
+    for (int i = 0; i < per; i++)
+        if (b0 + i < nb) loc += hist[b0 + i];
+    unsigned inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    unsigned run = inc - loc;
+    for (int i = 0; i < per; i++)
+        if (b0 + i < nb) {
+            off[b0 + i] = run;
+            run += hist[b0 + i];
+        }
+    if (lane == 31) *total = inc;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restrict__ idx,
+                                                         const T *__restrict__ b, int64_t n,
+                                                         int64_t lo, int64_t hi, int shift, int nb,
+                                                         u64 *cursor, int32_t *__restrict__ pidx,
+                                                         T *__restrict__ pval) {
+    __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB];
+    __shared__ u64 gbase[SB_MAXB];
+    __shared__ int32_t sk[SB_TILE];
+    __shared__ T sv[SB_TILE];
+    __shared__ uint16_t sbk[SB_TILE];
+    __shared__ unsigned total;
+    const int tid = threadIdx.x;
+    const int64_t ntiles = (n + SB_TILE - 1) / SB_TILE;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int i = tid; i < nb; i += SB_T) hist[i] = 0;
+        __syncthreads();
+        int32_t k[SB_E];
+        T v[SB_E];
+        int bk[SB_E];
+        unsigned rk[SB_E];
+#pragma unroll
+        for (int j = 0; j < SB_E; j++) {
+            const int64_t i = t * SB_TILE + j * SB_T + tid;
+            bk[j] = -1;
+            if (i < n) {
+                k[j] = __ldcs(idx + i);
+                if (k[j] >= lo && k[j] < hi) {
+                    bk[j] = (int)((k[j] - lo) >> shift);
+                    v[j] = __ldcs(b + i);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < SB_E; j++)
+            if (bk[j] >= 0) rk[j] = atomicAdd(&hist[bk[j]], 1u);
+        __syncthreads();
+        if (tid < 32) warp_exscan(hist, loff, nb, &total);
+        for (int i = tid; i < nb; i += SB_T)
+            gbase[i] = hist[i] ? atomicAdd(&cursor[i], (u64)hist[i]) : 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < SB_E; j++)
+            if (bk[j] >= 0) {
+                const unsigned pos = loff[bk[j]] + rk[j];
+                sk[pos] = k[j];
+                sv[pos] = v[j];
+                sbk[pos] = (uint16_t)bk[j];
+            }
+        __syncthreads();
+        const unsigned cnt = total;
+        for (unsigned pos = tid; pos < cnt; pos += SB_T) {
+            const int bb = sbk[pos];
+            const u64 g = gbase[bb] + (pos - loff[bb]);
+            pidx[g] = sk[pos];
+            pval[g] = sv[pos];
+        }
+        __syncthreads();
+    }
+}
+
+// Pairs are applied in global order through a dynamic chunk counter, so
+// the chunks in flight at any moment span ~one bucket of `a` (static
+// grid-stride lets CTAs drift apart and the working set spill out of L2).
+constexpr int SA_CH = 4096;
+
+// The write log is kept as an epoch byte-map (one plain byte store per
+// update, no L2 atomic) and packed into the dirty bitmap afterwards: the
+// bitmap atomics would otherwise double the L2 atomic traffic of the pass.
+template <typename T>
+__global__ void __launch_bounds__(256) scat_apply_kernel(const int32_t *__restrict__ pidx,
+                                                         const T *__restrict__ pval, const u64 *base,
+                                                         int nb, u64 *work, T *a, uint8_t *bytemap,
+                                                         uint8_t epoch, u64 *dirty) {
+    __shared__ u64 chunk;
+    const int64_t m = (int64_t)base[nb];
+    const int64_t nchunks = (m + SA_CH - 1) / SA_CH;
+    u64 mn = kU64Max, mx = 0;
+    for (;;) {
+        if (threadIdx.x == 0) chunk = atomicAdd(work, 1ull);
+        __syncthreads();
+        const int64_t c = (int64_t)chunk;
+        __syncthreads();
+        if (c >= nchunks) break;
+        const int64_t p0 = c * SA_CH;
+        const int64_t p1 = p0 + SA_CH < m ? p0 + SA_CH : m;
+#pragma unroll 4
+        for (int64_t p = p0 + threadIdx.x; p < p1; p += 256) {
+            const int32_t k = __ldcs(pidx + p);
+            const T v = __ldcs(pval + p);
+            atomicAdd(a + k, v);
+            bytemap[k] = epoch;
+            mn = (u64)k < mn ? (u64)k : mn;
+            mx = (u64)k > mx ? (u64)k : mx;
+        }
+    }
+    publish_dirty<8>(mn, mx, dirty);
+}
+
+// bitmap word w <- bits of bytemap[32w .. 32w+31] == epoch, for words
+// covering [lo, hi) (elements outside [lo, hi) are never marked)
+__global__ void __launch_bounds__(256) scat_pack_kernel(const uint8_t *__restrict__ bytemap,
+                                                        uint8_t epoch, int64_t lo, int64_t hi,
+                                                        uint32_t *bitmap) {
+    const int64_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w = w0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w1; w += nth) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(bytemap + (w << 5));
+        const uint4 q0 = __ldcs(p), q1 = __ldcs(p + 1);
+        const uint32_t wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        uint32_t bits = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+#pragma unroll
+            for (int b = 0; b < 4; b++)
+                if (((wd[i] >> (8 * b)) & 0xffu) == epoch) bits |= 1u << (4 * i + b);
+        bitmap[w] = bits;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -615,13 +837,10 @@ cudaError_t square_f32(cudaStream_t s, const float *y, float *x, int64_t i0, int
     return cudaGetLastError();
 }
 
-cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N, int64_t r0,
-                     int64_t r1, int64_t c0, int64_t c1, u64 *dirty, double *push_top,
-                     double *push_bot) {
-    if (r1 <= r0 || c1 <= c0) return cudaSuccess;
-    const bool v2 = (N % 2 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0) &&
-                    (!push_top || (uintptr_t)push_top % 16 == 0) &&
-                    (!push_bot || (uintptr_t)push_bot % 16 == 0);
+template <int JW, int JR, int JPF, int MINB>
+static cudaError_t jacobi2d_launch(cudaStream_t s, bool v2, const double *src, double *dst,
+                                   int64_t N, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                                   u64 *dirty, double *push_top, double *push_bot) {
     const int V = v2 ? 2 : 1;
     const int64_t cs_base = c0 & ~(int64_t)(V - 1);
     const int64_t slab = 32 * V * JW;
@@ -629,12 +848,36 @@ cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N, 
     const int64_t ty = (r1 - r0 + JR - 1) / JR;
     dim3 grid((unsigned)gx, (unsigned)(ty < 65535 ? ty : 65535));
     if (v2)
-        jacobi2d_kernel<2><<<grid, JW * 32, 0, s>>>(src, dst, N, r0, r1, c0, c1, cs_base, ty, dirty,
-                                                    push_top, push_bot);
+        jacobi2d_kernel<2, JW, JR, JPF, MINB><<<grid, JW * 32, 0, s>>>(
+            src, dst, N, r0, r1, c0, c1, cs_base, ty, dirty, push_top, push_bot);
     else
-        jacobi2d_kernel<1><<<grid, JW * 32, 0, s>>>(src, dst, N, r0, r1, c0, c1, cs_base, ty, dirty,
-                                                    push_top, push_bot);
+        jacobi2d_kernel<1, JW, JR, JPF, MINB><<<grid, JW * 32, 0, s>>>(
+            src, dst, N, r0, r1, c0, c1, cs_base, ty, dirty, push_top, push_bot);
     return cudaGetLastError();
+}
+
+cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N, int64_t r0,
+                     int64_t r1, int64_t c0, int64_t c1, u64 *dirty, double *push_top,
+                     double *push_bot) {
+    if (r1 <= r0 || c1 <= c0) return cudaSuccess;
+    const bool v2 = (N % 2 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0) &&
+                    (!push_top || (uintptr_t)push_top % 16 == 0) &&
+                    (!push_bot || (uintptr_t)push_bot % 16 == 0);
+    static int variant = -1;
+    if (variant < 0) {
+        const char *e = getenv("JACC_JACOBI_VARIANT");
+        variant = e ? atoi(e) : 0;
+    }
+    switch (variant) {
+    case 1: return jacobi2d_launch<4, 32, 3, 6>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 2: return jacobi2d_launch<4, 64, 3, 7>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 3: return jacobi2d_launch<4, 32, 4, 6>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 4: return jacobi2d_launch<4, 16, 2, 8>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 5: return jacobi2d_launch<8, 32, 3, 3>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 6: return jacobi2d_launch<2, 32, 3, 12>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 7: return jacobi2d_launch<4, 32, 6, 4>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    default: return jacobi2d_launch<4, 32, 3, 7>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    }
 }
 
 cudaError_t reduce_f64(cudaStream_t s, const double *x, const double *y, int64_t n,
@@ -655,32 +898,52 @@ cudaError_t combine(cudaStream_t s, PeerPtrs parts, double s_in, double *out) {
     return cudaGetLastError();
 }
 
+template <int BM, int BN, int BK, int ST, int WM, int WN>
+static cudaError_t gemm_launch(cudaStream_t s, bool v16, const double *A, const double *B,
+                               double *C, int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1,
+                               int64_t c0, int64_t c1, u64 *dirty) {
+    using G = GemmCfg<BM, BN, BK, ST, WM, WN>;
+    auto kt = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, true>;
+    auto kf = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, false>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        attr = true;
+    }
+    dim3 grid((unsigned)((c1 - c0 + BN - 1) / BN), (unsigned)((r1 - r0 + BM - 1) / BM));
+    if (v16)
+        kt<<<grid, G::NT, G::SMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    else
+        kf<<<grid, G::NT, G::SMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    return cudaGetLastError();
+}
+
 cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C, int64_t M,
                      int64_t N, int64_t K, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
                      u64 *dirty) {
     if (r1 <= r0 || c1 <= c0 || K <= 0) return cudaSuccess;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(gemm_f64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             GSMEM);
-        cudaFuncSetAttribute(gemm_f64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             GSMEM);
-        attr = true;
-    }
     const bool v16 = (K % 2 == 0) && (N % 2 == 0) && (c0 % 2 == 0) && ((uintptr_t)A % 16 == 0) &&
                      ((uintptr_t)B % 16 == 0) && ((uintptr_t)C % 16 == 0);
-    dim3 grid((unsigned)((c1 - c0 + GBN - 1) / GBN), (unsigned)((r1 - r0 + GBM - 1) / GBM));
-    if (v16)
-        gemm_f64_kernel<true><<<grid, 128, GSMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    else
-        gemm_f64_kernel<false><<<grid, 128, GSMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    return cudaGetLastError();
+    static int variant = -1;
+    if (variant < 0) {
+        const char *e = getenv("JACC_GEMM_VARIANT");
+        variant = e ? atoi(e) : 0;
+    }
+    switch (variant) {
+    case 1: return gemm_launch<64, 64, 32, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 2: return gemm_launch<128, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 3: return gemm_launch<128, 128, 16, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 4: return gemm_launch<64, 128, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 5: return gemm_launch<64, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 6: return gemm_launch<128, 128, 32, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    default: return gemm_launch<64, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    }
 }
 
 cudaError_t scatter_add_f64(cudaStream_t s, const int32_t *idx, const double *b, double *a,
                             int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty) {
     if (n <= 0) return cudaSuccess;
-    if ((uintptr_t)idx % 16 != 0) return cudaErrorInvalidValue;  // runtime guarantees alignment
     scatter_add_kernel<double><<<grid_for(n, 256 * 4, 148 * 8), 256, 0, s>>>(idx, b, a, n, lo, hi,
                                                                             bitmap, dirty);
     return cudaGetLastError();
@@ -689,9 +952,65 @@ cudaError_t scatter_add_f64(cudaStream_t s, const int32_t *idx, const double *b,
 cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b, int32_t *a,
                             int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty) {
     if (n <= 0) return cudaSuccess;
-    if ((uintptr_t)idx % 16 != 0) return cudaErrorInvalidValue;
     scatter_add_kernel<int32_t><<<grid_for(n, 256 * 4, 148 * 8), 256, 0, s>>>(idx, b, a, n, lo, hi,
                                                                              bitmap, dirty);
+    return cudaGetLastError();
+}
+
+
+ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
+    ScatterPlan p{false, 0, 1, 0, 0};
+    const int64_t span = hi - lo;
+    const char *force = getenv("JACC_SCATTER_BINNED");  // "0" never, "1" always (tests)
+    if (span <= 0 || n <= 0 || (force && force[0] == '0')) return p;
+    if (!(force && force[0] == '1') && (n < (1 << 22) || span * elem <= (int64_t)96 << 20))
+        return p;  // a fits in L2: the direct kernel is already L2-resident
+    int shift = 0;
+    while (((int64_t)elem << shift) < ((int64_t)16 << 20)) shift++;  // 16 MiB buckets
+    while (((span + ((int64_t)1 << shift) - 1) >> shift) > SB_MAXB) shift++;
+    p.binned = true;
+    p.shift = shift;
+    p.nb = (int)((span + ((int64_t)1 << shift) - 1) >> shift);
+    const size_t hdr = ((size_t)(3 * p.nb + 2) * 8 + 255) & ~(size_t)255;
+    p.scratch = hdr + (((size_t)n * 4 + 255) & ~(size_t)255) + (size_t)n * elem;
+    p.bytemap = (size_t)(((hi + 31) >> 5) << 5);
+    return p;
+}
+
+cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
+                               void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
+                               u64 *dirty, const ScatterPlan &pl, void *scratch, uint8_t *bytemap,
+                               uint8_t epoch) {
+    char *sc = static_cast<char *>(scratch);
+    u64 *counts = reinterpret_cast<u64 *>(sc);
+    u64 *cursor = counts + pl.nb;
+    u64 *base = cursor + pl.nb;  // nb + 1
+    u64 *work = base + pl.nb + 1;
+    const size_t hdr = ((size_t)(3 * pl.nb + 2) * 8 + 255) & ~(size_t)255;
+    int32_t *pidx = reinterpret_cast<int32_t *>(sc + hdr);
+    char *pv = sc + hdr + (((size_t)n * 4 + 255) & ~(size_t)255);
+    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)pl.nb * 8, s);
+    if (e != cudaSuccess) return e;
+    scat_hist_kernel<<<148 * 8, 256, 0, s>>>(idx, n, lo, hi, pl.shift, pl.nb, counts);
+    scat_scan_kernel<<<1, 32, 0, s>>>(counts, pl.nb, base, cursor, work);
+    const int64_t tiles = (n + SB_TILE - 1) / SB_TILE;
+    const int pg = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
+    if (is_f64) {
+        scat_part_kernel<double><<<pg, SB_T, 0, s>>>(idx, static_cast<const double *>(b), n, lo, hi,
+                                                     pl.shift, pl.nb, cursor, pidx,
+                                                     reinterpret_cast<double *>(pv));
+        scat_apply_kernel<double><<<148 * 8, 256, 0, s>>>(
+            pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
+            static_cast<double *>(a), bytemap, epoch, dirty);
+    } else {
+        scat_part_kernel<int32_t><<<pg, SB_T, 0, s>>>(idx, static_cast<const int32_t *>(b), n, lo,
+                                                      hi, pl.shift, pl.nb, cursor, pidx,
+                                                      reinterpret_cast<int32_t *>(pv));
+        scat_apply_kernel<int32_t><<<148 * 8, 256, 0, s>>>(
+            pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
+            static_cast<int32_t *>(a), bytemap, epoch, dirty);
+    }
+    scat_pack_kernel<<<148 * 8, 256, 0, s>>>(bytemap, epoch, lo, hi, bitmap);
     return cudaGetLastError();
 }
 

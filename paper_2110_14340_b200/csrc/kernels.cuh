@@ -1,9 +1,10 @@
 // kernels.cuh -- launch wrappers of the sm_100a device kernels (internal to
 // libjacc.so; not part of the C-ABI).  Every wrapper enqueues on `s` and
 // returns the launch error.  Dirty records are two u64 in device memory:
-// d[0] = min stored flat index, d[1] = ~max stored flat index; both reset to
-// all-ones (one 16-byte memset) before a launch, so an untouched record
-// reads back as the empty set (UINT64_MAX, 0)  (DESIGN R-3, R-15).
+// d[0] = min stored flat index, d[1] = ~max stored flat index; all-ones is
+// the empty set (UINT64_MAX, 0) (DESIGN R-3, R-15).  Each record is one
+// slot of a 32-byte-aligned pair; a writing kernel fills its slot and
+// clears the other one (slot address ^ 16) for the next launch.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -55,6 +56,25 @@ cudaError_t scatter_add_f64(cudaStream_t s, const int32_t *idx, const double *b,
                             int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty);
 cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b, int32_t *a,
                             int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty);
+
+// BK4b Same loop, executed as a destination-binned pipeline for arrays far
+// larger than L2: (1) histogram of owned updates per 16 MiB bucket of a,
+// (2) scan, (3) stable-per-CTA partition of (k, b[i]) pairs into bucket
+// order through shared memory (coalesced writes), (4) apply the pairs
+// bucket by bucket, so the read-modify-writes of a hit L2 and every line of
+// a moves to/from HBM about once.  Write tracking (bitmap + range) is fused
+// into (4).  is_f64: T = double, else int32.
+struct ScatterPlan {
+    bool binned;
+    int shift, nb;
+    size_t scratch;   // bytes of pair scratch
+    size_t bytemap;   // bytes of the epoch byte-map (elements of a, rounded to 32)
+};
+ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem);
+cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
+                               void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
+                               u64 *dirty, const ScatterPlan &pl, void *scratch, uint8_t *bytemap,
+                               uint8_t epoch);
 
 // BK5  Dirty-region merge over peer memory.  merge_range copies the
 // recorded span [dirty min, dirty max] (clamped to [lo, hi)) of src into

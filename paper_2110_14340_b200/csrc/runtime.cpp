@@ -112,6 +112,8 @@ struct Device {
     double *res = nullptr;       // allreduce result / combine output
     double *hscal = nullptr;     // pinned host scalar
     ncclComm_t comm = nullptr;
+    void *scratch = nullptr;     // binned-scatter pairs (grown on demand)
+    size_t scratch_bytes = 0;
     // profiling
     double kernel_s = 0, merge_s = 0;
     uint64_t launches = 0, bytes_merged = 0;
@@ -125,8 +127,11 @@ struct Region {
     int64_t nelem = 0;
     bool pinned = false;
     std::vector<char *> rep;           // per device replica
-    std::vector<u64 *> dirty;          // per device [min, ~max]
+    std::vector<u64 *> dirty;          // per device: 2 slots of [min, ~max] (32 B)
+    std::vector<int> dslot;            // per device: slot of the most recent launch
     std::vector<uint32_t *> bitmap;    // per device, lazily allocated
+    std::vector<uint8_t *> bytemap;    // per device epoch byte-map (binned scatter)
+    std::vector<uint8_t> epoch;
     std::vector<IntervalSet> valid;    // per device
 };
 
@@ -331,6 +336,7 @@ void free_region(Region *r) {
         if (r->rep[d]) cudaFree(r->rep[d]);
         if (r->dirty[d]) cudaFree(r->dirty[d]);
         if (r->bitmap[d]) cudaFree(r->bitmap[d]);
+        if (r->bytemap[d]) cudaFree(r->bytemap[d]);
     }
     if (r->pinned) cudaHostUnregister((void *)r->base);
 }
@@ -586,7 +592,6 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
             invalid_if(L.a[2].off != 0);
             invalid_if(L.a[2].reg == L.a[0].reg || L.a[2].reg == L.a[1].reg);  // race (R-12)
-            invalid_if(((L.a[0].off * 4) % 16) != 0);  // idx 16-byte aligned for int4 loads
         }
         if (id == JACC_LOOP_SQUARE_F32 && L.a[0].reg == L.a[1].reg) {
             // two pointers to one array, one read and one written:
@@ -670,7 +675,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     const bool prof = R.profiling;
     uint64_t merged_bytes = 0;
     wait_launches(R.gen);
-    if (W && !L.dup && (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32)) {
+    if (W && (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32)) {
         const size_t words = (size_t)((W->nelem + 31) / 32);
         for (int d = 0; d < n; d++)
             if (local(d) && !W->bitmap[d]) {
@@ -702,13 +707,18 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             pr.m1 = pool_event();
             CK(cudaEventRecord(pr.k0, dv.s));
         }
-        if (W) CK(cudaMemsetAsync(W->dirty[d], 0xff, 16, dv.s));
+        u64 *drec = nullptr;  // this launch's dirty-record slot (cleared by the previous one)
+        if (W) {
+            W->dslot[d] ^= 1;
+            drec = W->dirty[d] + 2 * W->dslot[d];
+            if (!p.active) CK(cudaMemsetAsync(drec, 0xff, 16, dv.s));  // nothing will write it
+        }
         if (p.active) {
             switch (id) {
             case JACC_LOOP_SQUARE_F32: {
                 const float *y = reinterpret_cast<const float *>(L.a[0].reg->rep[d]) + L.a[0].off;
                 float *x = reinterpret_cast<float *>(L.a[1].reg->rep[d]) + L.a[1].off;
-                CK(jk::square_f32(dv.s, y, x, p.i0, p.i1, L.a[1].off, W->dirty[d]));
+                CK(jk::square_f32(dv.s, y, x, p.i0, p.i1, L.a[1].off, drec));
                 break;
             }
             case JACC_LOOP_JACOBI2D_F64: {
@@ -716,7 +726,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 double *pb = bot[d] >= 0 ? reinterpret_cast<double *>(W->rep[bot[d]]) : nullptr;
                 CK(jk::jacobi2d(dv.s, reinterpret_cast<const double *>(L.a[0].reg->rep[d]),
                                 reinterpret_cast<double *>(W->rep[d]), L.N, p.i0, p.i1, p.j0, p.j1,
-                                W->dirty[d], pt, pb));
+                                drec, pt, pb));
                 int64_t rowb = (p.j1 - p.j0) * 8;
                 if (pt) merged_bytes += rowb;
                 if (pb) merged_bytes += rowb;
@@ -736,24 +746,56 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 CK(jk::gemm_f64(dv.s, reinterpret_cast<const double *>(L.a[0].reg->rep[d]),
                                 reinterpret_cast<const double *>(L.a[1].reg->rep[d]),
                                 reinterpret_cast<double *>(W->rep[d]), L.M, L.Nn, L.K, p.i0, p.i1,
-                                p.j0, p.j1, W->dirty[d]));
+                                p.j0, p.j1, drec));
                 break;
             case JACC_LOOP_SCATTER_ADD_F64:
             case JACC_LOOP_SCATTER_ADD_I32: {
                 const int32_t *ix = reinterpret_cast<const int32_t *>(L.a[0].reg->rep[d]) + L.a[0].off + p.i0;
                 uint32_t *bm = W->bitmap[d];
-                if (!L.dup) {
+                {
                     const int64_t w0 = p.own_lo >> 5, w1 = (p.own_hi + 31) >> 5;
                     CK(cudaMemsetAsync(bm + w0, 0, (size_t)(w1 - w0) * 4, dv.s));
                 }
-                if (id == JACC_LOOP_SCATTER_ADD_F64) {
-                    const double *b = reinterpret_cast<const double *>(L.a[1].reg->rep[d]) + L.a[1].off + p.i0;
-                    CK(jk::scatter_add_f64(dv.s, ix, b, reinterpret_cast<double *>(W->rep[d]),
-                                           p.i1 - p.i0, p.own_lo, p.own_hi, bm, W->dirty[d]));
+                const bool f64 = id == JACC_LOOP_SCATTER_ADD_F64;
+                const char *b = L.a[1].reg->rep[d] + (L.a[1].off + p.i0) * (int64_t)W->elem;
+                const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
+                const jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
+                if (sp.binned) {
+                    if (dv.scratch_bytes < sp.scratch) {
+                        CK(cudaStreamSynchronize(dv.s));
+                        if (dv.scratch) CK(cudaFree(dv.scratch));
+                        dv.scratch = nullptr;
+                        dv.scratch_bytes = 0;
+                        if (cudaMalloc(&dv.scratch, sp.scratch) != cudaSuccess) {
+                            cudaGetLastError();
+                            throw Fail{JACC_ERR_OOM};
+                        }
+                        dv.scratch_bytes = sp.scratch;
+                    }
+                    if (!W->bytemap[d]) {
+                        if (cudaMalloc(&W->bytemap[d], sp.bytemap) != cudaSuccess) {
+                            cudaGetLastError();
+                            throw Fail{JACC_ERR_OOM};
+                        }
+                        CK(cudaMemsetAsync(W->bytemap[d], 0, sp.bytemap, dv.s));
+                        W->epoch[d] = 0;
+                    }
+                    if (W->epoch[d] == 255) {  // wrap: clear stale epochs
+                        CK(cudaMemsetAsync(W->bytemap[d], 0, sp.bytemap, dv.s));
+                        W->epoch[d] = 0;
+                    }
+                    W->epoch[d]++;
+                    CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
+                                              drec, sp, dv.scratch, W->bytemap[d],
+                                              W->epoch[d]));
+                } else if (f64) {
+                    CK(jk::scatter_add_f64(dv.s, ix, reinterpret_cast<const double *>(b),
+                                           reinterpret_cast<double *>(W->rep[d]), p.i1 - p.i0, lo,
+                                           hi, bm, drec));
                 } else {
-                    const int32_t *b = reinterpret_cast<const int32_t *>(L.a[1].reg->rep[d]) + L.a[1].off + p.i0;
-                    CK(jk::scatter_add_i32(dv.s, ix, b, reinterpret_cast<int32_t *>(W->rep[d]),
-                                           p.i1 - p.i0, p.own_lo, p.own_hi, bm, W->dirty[d]));
+                    CK(jk::scatter_add_i32(dv.s, ix, reinterpret_cast<const int32_t *>(b),
+                                           reinterpret_cast<int32_t *>(W->rep[d]), p.i1 - p.i0, lo,
+                                           hi, bm, drec));
                 }
                 break;
             }
@@ -770,7 +812,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
                 CK(jk::merge_bitmap(dv.s, W->rep[d], pp, W->bitmap[d], (int64_t)W->elem, p.wlo, p.whi));
             } else {
-                CK(jk::merge_range(dv.s, W->rep[d], pp, W->dirty[d], (int64_t)W->elem, p.wlo, p.whi));
+                CK(jk::merge_range(dv.s, W->rep[d], pp, drec, (int64_t)W->elem, p.wlo, p.whi));
             }
             merged_bytes += (uint64_t)(p.whi - p.wlo) * W->elem * (n - 1);  // upper bound (host view)
         }
@@ -960,6 +1002,7 @@ jacc_status jacc_finalize(void) {
         }
         cudaSetDevice(dv.ord);
         if (dv.comm) ncclCommDestroy(dv.comm);
+        if (dv.scratch) cudaFree(dv.scratch);
         cudaFree(dv.partials);
         cudaFree(dv.ticket);
         cudaFree(dv.part);
@@ -1029,17 +1072,20 @@ jacc_status jacc_data_create(void *host, size_t bytes, size_t elem_size, int ndi
         r->rep.assign(R.n, nullptr);
         r->dirty.assign(R.n, nullptr);
         r->bitmap.assign(R.n, nullptr);
+        r->dslot.assign(R.n, 0);
+        r->bytemap.assign(R.n, nullptr);
+        r->epoch.assign(R.n, 0);
         r->valid.assign(R.n, IntervalSet{});
         for (int d = 0; d < R.n; d++) {
             if (!local(d)) continue;  // peers' replicas arrive via jacc_import_region
             set_dev(d);
             if (cudaMalloc(&r->rep[d], bytes) != cudaSuccess ||
-                cudaMalloc(&r->dirty[d], 16) != cudaSuccess) {
+                cudaMalloc(&r->dirty[d], 32) != cudaSuccess) {
                 cudaGetLastError();
                 free_region(r.get());
                 return JACC_ERR_OOM;
             }
-            CK(cudaMemset(r->dirty[d], 0xff, 16));
+            CK(cudaMemset(r->dirty[d], 0xff, 32));
         }
         // pin large host buffers so update_device/update_host are DMA-direct
         if (bytes >= (1u << 20) && !getenv("JACC_NO_PIN")) {
@@ -1164,7 +1210,7 @@ jacc_status jacc_get_dirty_range(void *host, int dev, uint64_t *mn, uint64_t *mx
         local_sync();
         u64 h[2];
         set_dev(dev);
-        CK(cudaMemcpy(h, r->dirty[dev], 16, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(h, r->dirty[dev] + 2 * r->dslot[dev], 16, cudaMemcpyDeviceToHost));
         *mn = h[0];
         *mx = ~h[1];
         return JACC_OK;

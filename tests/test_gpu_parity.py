@@ -441,6 +441,75 @@ def test_scatter_permutation_exact(J):
     assert np.array_equal(a, ref)
 
 
+@pytest.mark.parametrize("binned", ["0", "1"])
+@pytest.mark.parametrize("n", [1, 3])
+@pytest.mark.parametrize("lo", [0, 1, 2, 3, 5])
+def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, n, lo):
+    """Direct and destination-binned scatter pipelines, iteration ranges
+    starting at any element (int4 head/tail handling)."""
+    monkeypatch.setenv("JACC_SCATTER_BINNED", binned)
+    N, M = 30_011, 4099
+    idx = synth.index_i32(N, M, 75, 5)
+    b = synth.dyadic_f64(N, 75, 6)
+    a0 = synth.dyadic_f64(M, 75, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx[lo:N - 2], b[lo:N - 2], ref)
+    a = a0.copy()
+    with runtime(J, n):
+        _create(J, idx, b, a)
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, J.make_range(lo, N - 2),
+                      [_in(J, idx), _in(J, b), _inout(J, a)])
+        for d in range(n):
+            plo, phi = orc.partition(M, n, d)
+            bm, mn, mx = orc.scatter_add_filtered(np.ascontiguousarray(idx[lo:N - 2]),
+                                                  np.ascontiguousarray(b[lo:N - 2]), a0.copy(),
+                                                  plo, phi - 1)
+            assert np.array_equal(J.jacc_get_dirty_bitmap(a, d, M), bm)
+            assert J.jacc_get_dirty_range(a, d) == (mn, mx)
+        J.jacc_update_host(a)
+    assert np.array_equal(a, ref)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "i32"])
+@pytest.mark.parametrize("n", [1, 2])
+def test_scatter_binned_large(J, dtype, n):
+    """Arrays larger than L2 take the binned pipeline by default."""
+    M = 2**25 if dtype == "f64" else 2**26
+    N = 2**23
+    idx = synth.index_i32(N, M, 76, 5)
+    if dtype == "f64":
+        b, a0 = synth.dyadic_f64(N, 76, 6), synth.dyadic_f64(M, 76, 7)
+    else:
+        b, a0 = synth.int_i32(N, -1000, 1000, 76, 6), synth.int_i32(M, -10**6, 10**6, 76, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, bms, drs, reps = _scatter(J, idx, b, a0, n)
+    assert np.array_equal(a, ref)
+    for d in range(n):
+        lo, hi = orc.partition(M, n, d)
+        bm, mn, mx = orc.scatter_add_filtered(idx, b, a0.copy(), lo, hi - 1)
+        assert np.array_equal(bms[d], bm) and drs[d] == (mn, mx)
+        assert np.array_equal(reps[d], ref)
+
+
+def test_scatter_dup_mode(J):
+    N, M = 10_000, 999
+    idx = synth.index_i32(N, M, 77, 5)
+    b = synth.int_i32(N, -9, 9, 77, 6)
+    a0 = synth.int_i32(M, -9, 9, 77, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a = a0.copy()
+    with runtime(J, 3, mode=1):
+        _create(J, idx, b, a)
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_I32, J.make_range(0, N),
+                      [_in(J, idx), _in(J, b), _inout(J, a)])
+        for d in range(3):
+            assert np.array_equal(J.jacc_get_replica(a, d), ref)
+        J.jacc_update_host(a)
+    assert np.array_equal(a, ref)
+
+
 def test_scatter_full_size(J):
     """BASELINE config 5 at full size: 2^28 updates into 2^28 elements,
     random idx, dyadic b (exact in any order), n=1."""
