@@ -90,8 +90,14 @@ jacc_status jacc_set_merge_policy(int policy);
 /* Execution mode: JACC_MODE_MULTI splits by owned blocks
  * (default); JACC_MODE_DUP runs the full loop on every device with no
  * exchange ("duplicating computation on all GPUs and performing no
- * GPU-to-GPU communication").  The alias rule (R-12) forces DUP per launch. */
-enum { JACC_MODE_MULTI = 0, JACC_MODE_DUP = 1 };
+ * GPU-to-GPU communication").  The alias rule (R-12) forces DUP per launch.
+ * JACC_MODE_ADAPTIVE (single-process mode only): every kernel
+ * identity (loop, argument regions, range) starts duplicated, is profiled
+ * with CUDA events, switches to multi-GPU after Eq. (1) has held five
+ * times, and back to duplication for good after Eq. (2) or (3) has held
+ * five times with a positive mean margin (controller below; DESIGN R-16).
+ * peak_P2P defaults to 770 GB/s (env JACC_PEAK_P2P_GBS). */
+enum { JACC_MODE_MULTI = 0, JACC_MODE_DUP = 1, JACC_MODE_ADAPTIVE = 2 };
 jacc_status jacc_set_mode(int mode);
 
 /* Owned block [lo, hi) of logical device d when an extent E is split over
@@ -299,6 +305,25 @@ jacc_status jacc_import_region(void *host, int peer, const void *in, size_t byte
 
 /* This process's logical device (0 in single-process mode, -1 before init). */
 int jacc_rank(void);
+
+/* ---------------------------------------------------------------------- */
+/* Adaptive utilization controller (NEXT-1)                     */
+/* ---------------------------------------------------------------------- */
+/* Controller states: 0 DUP_WARMUP, 1 DUP_PROFILING, 2 MULTI, 3 DUP_FINAL. */
+/* Pure host logic, no GPU: feed `len` observations (kernel time, comm time
+ * [s], WriteSize [bytes] -- WriteSize = bytes the busiest device sends in
+ * a multi-GPU merge) to a fresh controller for n devices and peak_p2p
+ * [B/s]; states_out[i] = state before observation i, states_out[len] =
+ * final state (len + 1 entries).  Errors: JACC_ERR_INVALID. */
+jacc_status jacc_adaptive_replay(int n, double peak_p2p, int len, const double *t_kernel,
+                                 const double *t_comm, const double *write_size, int *states_out);
+
+/* Observations fed so far to the controller of the most recent kernel
+ * identity launched with `loop_id` under JACC_MODE_ADAPTIVE (waits for
+ * outstanding observations): up to `cap` entries, *len = total count,
+ * *state_now = current state (-1 if none). */
+jacc_status jacc_adaptive_history(int loop_id, int cap, double *t_kernel, double *t_comm,
+                                  double *write_size, int *states, int *len, int *state_now);
 
 const char *jacc_error_string(jacc_status s);
 

@@ -102,6 +102,54 @@ struct IntervalSet {
 };
 
 // ---------------------------------------------------------------------------
+// NEXT-1: adaptive utilization controller (DESIGN R-16), one per
+// kernel identity.  Starts duplicated; after the warm-up run profiles
+// eff_dup (time per written byte) until Eq. (1) has held five times, then
+// runs multi-GPU; switches back for good once Eq. (2) or Eq. (3) has held
+// five times with a positive mean margin.
+// ---------------------------------------------------------------------------
+struct AdaptiveCtl {
+    enum { DUP_WARMUP = 0, DUP_PROFILING = 1, MULTI = 2, DUP_FINAL = 3 };
+    int state = DUP_WARMUP;
+    double eff_sum = 0;
+    int eff_cnt = 0, c1 = 0, c23 = 0;
+    double margin_sum = 0;
+    int margin_cnt = 0;
+    bool dup() const { return state != MULTI; }
+    // observations fed so far (for introspection / replay tests)
+    std::vector<double> h_tk, h_tc, h_ws;
+    std::vector<int> h_state;
+    void observe(double tk, double tc, double ws, int n, double peak) {
+        switch (state) {
+        case DUP_WARMUP:
+            state = DUP_PROFILING;  // warm-up run is not profiled
+            break;
+        case DUP_PROFILING:
+            if (ws > 0) {
+                eff_sum += tk / ws;
+                eff_cnt++;
+            }
+            if (tk > tk / n + ws / peak) c1++;  // Eq. (1)
+            if (c1 >= 5) state = MULTI;
+            break;
+        case MULTI: {
+            const double left = tk + tc;
+            const double r2 = tk * n;  // Eq. (2)
+            const double r3 = (eff_cnt > 0 && ws > 0) ? (eff_sum / eff_cnt) * ws
+                                                      : __builtin_inf();  // Eq. (3)
+            if (left > r2 || left > r3) c23++;
+            margin_sum += left - std::min(r2, r3);
+            margin_cnt++;
+            if (c23 >= 5 && margin_sum / margin_cnt > 0) state = DUP_FINAL;
+            break;
+        }
+        default:
+            break;
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
 struct Device {
     int ord = 0;
     cudaStream_t s = nullptr;
@@ -140,6 +188,15 @@ struct ProfRec {
     cudaEvent_t k0, k1, m1;
 };
 
+// one adaptive observation in flight: a launch's per-device events
+struct AdaptRec {
+    std::string key;
+    int n_dev;
+    bool dup;
+    double ws;
+    std::vector<ProfRec> ev;
+};
+
 struct Runtime {
     bool init = false;
     bool poisoned = false;
@@ -172,6 +229,11 @@ struct Runtime {
     Slot *shm = nullptr;
     std::string shm_name;
     uint64_t barrier_gen = 0;
+    // adaptive utilization (JACC_MODE_ADAPTIVE)
+    std::map<std::string, AdaptiveCtl> adapt;
+    std::map<int, std::string> adapt_last_key;  // loop_id -> most recent key
+    std::vector<AdaptRec> adapt_pending;
+    double peak_p2p = 770e9;  // B/s per GPU egress (measured peer copy, B200_PROFILING.md)
 };
 
 Runtime R;
@@ -506,6 +568,50 @@ void halo_targets(const Launch &L, int d, int &top, int &bot) {
     }
 }
 
+// Feed completed adaptive observations (FIFO) to their controllers.  An
+// observation made in a mode the controller has since left is dropped.
+void poll_adaptive(bool block) {
+    size_t done = 0;
+    for (; done < R.adapt_pending.size(); done++) {
+        AdaptRec &ar = R.adapt_pending[done];
+        bool ready = true;
+        for (auto &e : ar.ev) {
+            if (block) {
+                set_dev(e.dev);
+                CK(cudaEventSynchronize(e.m1));
+            } else {
+                cudaError_t q = cudaEventQuery(e.m1);
+                if (q == cudaErrorNotReady) {
+                    ready = false;
+                    break;
+                }
+                CK(q);
+            }
+        }
+        if (!ready) break;
+        double tk = 0, tc = 0;
+        for (auto &e : ar.ev) {
+            float k = 0, m = 0;
+            CK(cudaEventElapsedTime(&k, e.k0, e.k1));
+            CK(cudaEventElapsedTime(&m, e.k1, e.m1));
+            tk = std::max(tk, (double)k * 1e-3);
+            tc = std::max(tc, (double)m * 1e-3);
+            R.evpool.push_back(e.k0);
+            R.evpool.push_back(e.k1);
+            R.evpool.push_back(e.m1);
+        }
+        AdaptiveCtl &c = R.adapt[ar.key];
+        if (ar.dup == c.dup() && c.state != AdaptiveCtl::DUP_FINAL) {
+            c.h_tk.push_back(tk);
+            c.h_tc.push_back(tc);
+            c.h_ws.push_back(ar.ws);
+            c.h_state.push_back(c.state);
+            c.observe(tk, tc, ar.ws, ar.n_dev, R.peak_p2p);
+        }
+    }
+    R.adapt_pending.erase(R.adapt_pending.begin(), R.adapt_pending.begin() + done);
+}
+
 struct Pull {
     int dst, src;
     Region *reg;
@@ -537,7 +643,8 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         L.a[k].off = (int64_t)(boff / r->elem);
     }
     // ---- shapes and ranges -------------------------------------------------
-    jacc_range rg{};
+    jacc_range rg;
+    memset(&rg, 0, sizeof(rg));
     const int id = D->id;
     if (id == JACC_LOOP_JACOBI2D_F64) {
         Region *s = L.a[0].reg, *t = L.a[1].reg;
@@ -581,7 +688,9 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     } else {
         // 1-D loops: range over i; arrays must hold [off+lo, off+hi)
         invalid_if(!range || range->ndims != 1 || range->lo[0] < 0 || range->hi[0] < range->lo[0]);
-        rg = *range;
+        rg.ndims = 1;
+        rg.lo[0] = range->lo[0];
+        rg.hi[0] = range->hi[0];
         for (int k = 0; k < nargs; k++) {
             if (!L.a[k].reg) continue;
             if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
@@ -601,6 +710,41 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     }
     L.rg = rg;
     if (R.mode == JACC_MODE_DUP) L.dup = true;
+    // ---- NEXT-1 adaptive utilization (single process, n > 1) ---------------
+    const bool adaptive = R.mode == JACC_MODE_ADAPTIVE && R.n > 1 && !R.mp && !L.dup;
+    std::string akey;
+    double adapt_ws = 0;
+    if (adaptive) {
+        poll_adaptive(false);
+        // kernel identity: loop, argument regions/offsets, iteration range
+        akey.assign((const char *)&loop_id, sizeof(loop_id));
+        for (auto &ai : L.a) {
+            akey.append((const char *)&ai.reg, sizeof(ai.reg));
+            akey.append((const char *)&ai.off, sizeof(ai.off));
+        }
+        akey.append((const char *)&L.rg.ndims, sizeof(L.rg.ndims));
+        akey.append((const char *)L.rg.lo, sizeof(L.rg.lo));
+        akey.append((const char *)L.rg.hi, sizeof(L.rg.hi));
+        R.adapt_last_key[loop_id] = akey;
+        // WriteSize: bytes the busiest device would send in a multi-GPU merge
+        plan_launch(L);
+        if (D->out_arg >= 0) {
+            Region *Wr = L.a[D->out_arg].reg;
+            for (int d = 0; d < R.n; d++) {
+                const DevPlan &pp = L.plan[d];
+                if (!pp.active) continue;
+                double b;
+                if (R.policy == JACC_MERGE_EAGER)
+                    b = (double)(pp.whi - pp.wlo) * Wr->elem * (R.n - 1);
+                else if (D->halo_rows > 0)
+                    b = 2.0 * D->halo_rows * (double)(pp.j1 - pp.j0) * Wr->elem;
+                else
+                    b = 0;
+                adapt_ws = std::max(adapt_ws, b);
+            }
+        }
+        L.dup = R.adapt[akey].dup();
+    }
     for (auto &ai : L.a)
         if (ai.reg)
             for (int d = 0; d < R.n; d++)
@@ -675,6 +819,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     const bool prof = R.profiling;
     uint64_t merged_bytes = 0;
     wait_launches(R.gen);
+    std::vector<ProfRec> adapt_evs;
     if (W && (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32)) {
         const size_t words = (size_t)((W->nelem + 31) / 32);
         for (int d = 0; d < n; d++)
@@ -706,6 +851,13 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             pr.k1 = pool_event();
             pr.m1 = pool_event();
             CK(cudaEventRecord(pr.k0, dv.s));
+        }
+        ProfRec ap{d, nullptr, nullptr, nullptr};
+        if (adaptive) {
+            ap.k0 = pool_event();
+            ap.k1 = pool_event();
+            ap.m1 = pool_event();
+            CK(cudaEventRecord(ap.k0, dv.s));
         }
         u64 *drec = nullptr;  // this launch's dirty-record slot (cleared by the previous one)
         if (W) {
@@ -804,6 +956,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             CK(cudaMemsetAsync(dv.part, 0, 8, dv.s));
         }
         if (prof) CK(cudaEventRecord(pr.k1, dv.s));
+        if (adaptive) CK(cudaEventRecord(ap.k1, dv.s));
         // ---- EAGER merge: push the recorded dirty region to every peer ----
         if (writes && p.active && R.policy == JACC_MERGE_EAGER && n > 1) {
             jk::PeerPtrs pp{};
@@ -820,10 +973,15 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             CK(cudaEventRecord(pr.m1, dv.s));
             R.prof.push_back(pr);
         }
+        if (adaptive) {
+            CK(cudaEventRecord(ap.m1, dv.s));
+            adapt_evs.push_back(ap);
+        }
         CK(cudaEventRecord(dv.ev[cur], dv.s));
         dv.launches++;
     }
     if (R.mp) shm_store(&R.shm[R.me].launches, R.gen + 1);
+    if (adaptive) R.adapt_pending.push_back({akey, n, L.dup, adapt_ws, adapt_evs});
 
     // ---- validity bookkeeping ---------------------------------------------
     for (const Pull &pl : pulls) pl.reg->valid[pl.dst].add(pl.lo, pl.hi);
@@ -926,6 +1084,7 @@ jacc_status jacc_init(int n_devices, const int *device_ids) {
                     if (ords[q] == ords[d]) R.distinct = false;
             const char *pol = getenv("JACC_MERGE");
             if (pol && !strcmp(pol, "halo")) R.policy = JACC_MERGE_HALO;
+            if (const char *pk = getenv("JACC_PEAK_P2P_GBS")) R.peak_p2p = atof(pk) * 1e9;
             R.init = true;
             for (int d = 0; d < n_devices; d++) {
                 Device &dv = R.dev[d];
@@ -991,6 +1150,12 @@ jacc_status jacc_finalize(void) {
         R.evpool.push_back(p.k1);
         R.evpool.push_back(p.m1);
     }
+    for (auto &ar : R.adapt_pending)
+        for (auto &e : ar.ev) {
+            R.evpool.push_back(e.k0);
+            R.evpool.push_back(e.k1);
+            R.evpool.push_back(e.m1);
+        }
     for (auto e : R.evpool) cudaEventDestroy(e);
     for (int d = 0; d < R.n; d++) {
         Device &dv = R.dev[d];
@@ -1038,7 +1203,9 @@ jacc_status jacc_set_merge_policy(int policy) {
 
 jacc_status jacc_set_mode(int mode) {
     if (!R.init || R.poisoned) return JACC_ERR_STATE;
-    if (mode != JACC_MODE_MULTI && mode != JACC_MODE_DUP) return JACC_ERR_INVALID;
+    if (mode != JACC_MODE_MULTI && mode != JACC_MODE_DUP && mode != JACC_MODE_ADAPTIVE)
+        return JACC_ERR_INVALID;
+    if (mode == JACC_MODE_ADAPTIVE && R.mp) return JACC_ERR_INVALID;  // needs every device's timing
     R.mode = mode;
     return JACC_OK;
 }
@@ -1446,6 +1613,45 @@ jacc_status jacc_import_region(void *host, int peer, const void *in, size_t byte
 }
 
 int jacc_rank(void) { return R.init ? (R.mp ? R.me : 0) : -1; }
+
+jacc_status jacc_adaptive_replay(int n, double peak_p2p, int len, const double *t_kernel,
+                                 const double *t_comm, const double *write_size, int *states_out) {
+    if (n < 1 || peak_p2p <= 0 || len < 0 || (len > 0 && (!t_kernel || !t_comm || !write_size)) ||
+        !states_out)
+        return JACC_ERR_INVALID;
+    AdaptiveCtl c;
+    for (int i = 0; i < len; i++) {
+        states_out[i] = c.state;
+        c.observe(t_kernel[i], t_comm[i], write_size[i], n, peak_p2p);
+    }
+    states_out[len] = c.state;
+    return JACC_OK;
+}
+
+jacc_status jacc_adaptive_history(int loop_id, int cap, double *t_kernel, double *t_comm,
+                                  double *write_size, int *states, int *len, int *state_now) {
+    return guard([&]() -> jacc_status {
+        if (cap < 0 || !len) return JACC_ERR_INVALID;
+        poll_adaptive(true);
+        auto it = R.adapt_last_key.find(loop_id);
+        if (it == R.adapt_last_key.end()) {
+            *len = 0;
+            if (state_now) *state_now = -1;
+            return JACC_OK;
+        }
+        const AdaptiveCtl &c = R.adapt[it->second];
+        const int m = (int)c.h_tk.size();
+        *len = m;
+        if (state_now) *state_now = c.state;
+        for (int i = 0; i < m && i < cap; i++) {
+            if (t_kernel) t_kernel[i] = c.h_tk[i];
+            if (t_comm) t_comm[i] = c.h_tc[i];
+            if (write_size) write_size[i] = c.h_ws[i];
+            if (states) states[i] = c.h_state[i];
+        }
+        return JACC_OK;
+    });
+}
 
 const char *jacc_error_string(jacc_status s) {
     switch (s) {

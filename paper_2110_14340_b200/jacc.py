@@ -52,7 +52,9 @@ EXPORTS = [
     "jacc_profile_reset", "jacc_get_stream", "jacc_error_string",
     "jacc_unique_id", "jacc_init_rank", "jacc_export_runtime", "jacc_import_runtime",
     "jacc_export_region", "jacc_import_region", "jacc_rank",
+    "jacc_adaptive_replay", "jacc_adaptive_history",
 ]
+JACC_MODE_ADAPTIVE = 2
 JACC_UNIQUE_ID_BYTES = 128
 JACC_RUNTIME_HANDLE_BYTES = 192
 JACC_REGION_HANDLE_BYTES = 64
@@ -99,6 +101,8 @@ for _name, _args in {
     "jacc_import_runtime": [_I, _P, _SZ],
     "jacc_export_region": [_P, _P, _SZ],
     "jacc_import_region": [_P, _I, _P, _SZ],
+    "jacc_adaptive_replay": [_I, ctypes.c_double, _I, _P, _P, _P, _P],
+    "jacc_adaptive_history": [_I, _I, _P, _P, _P, _P, ctypes.POINTER(_I), ctypes.POINTER(_I)],
 }.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
@@ -314,3 +318,27 @@ def jacc_import_region(arr, peer, blob):
 
 def jacc_rank():
     return lib.jacc_rank()
+
+
+# ---- adaptive utilization controller (NEXT-1) --------------------------------
+def jacc_adaptive_replay(n, peak_p2p, trace):
+    """States before each observation + final state (pure host logic)."""
+    m = len(trace)
+    tk = np.ascontiguousarray([t[0] for t in trace], dtype=np.float64)
+    tc = np.ascontiguousarray([t[1] for t in trace], dtype=np.float64)
+    ws = np.ascontiguousarray([t[2] for t in trace], dtype=np.float64)
+    out = np.zeros(m + 1, dtype=np.int32)
+    _ck(lib.jacc_adaptive_replay(n, peak_p2p, m, tk.ctypes.data, tc.ctypes.data, ws.ctypes.data,
+                                 out.ctypes.data), "jacc_adaptive_replay")
+    return out.tolist()
+
+
+def jacc_adaptive_history(loop_id, cap=4096):
+    tk, tc, ws = (np.zeros(cap) for _ in range(3))
+    st = np.zeros(cap, dtype=np.int32)
+    ln, now = ctypes.c_int(), ctypes.c_int()
+    _ck(lib.jacc_adaptive_history(loop_id, cap, tk.ctypes.data, tc.ctypes.data, ws.ctypes.data,
+                                  st.ctypes.data, ctypes.byref(ln), ctypes.byref(now)),
+        "jacc_adaptive_history")
+    m = min(ln.value, cap)
+    return list(zip(tk[:m], tc[:m], ws[:m])), st[:m].tolist(), now.value

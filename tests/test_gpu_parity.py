@@ -560,3 +560,33 @@ def test_profiling_records(J):
         assert tk > 0 and tm >= 0 and nb > 0
         k, m, nl, _ = J.jacc_profile_totals(0)
         assert nl == 4 and k >= tk
+
+
+# --------------------------------------------------------------------------
+# NEXT-1 adaptive utilization
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("policy", [0, 1])
+def test_adaptive_mode_parity_and_controller_replay(J, policy):
+    """Under JACC_MODE_ADAPTIVE every launch runs duplicated or multi-GPU as
+    the controller decides; results stay bit-exact, and the runtime's state
+    sequence equals the oracle controller replayed on the same measured
+    observations."""
+    from oracle import adaptive as ad
+    N, T = 514, 20
+    A0 = synth.uniform_f64(N * N, 91, 1).reshape(N, N)
+    B0 = synth.uniform_f64(N * N, 91, 2).reshape(N, N)
+    Ar, Br = A0.copy(), B0.copy()
+    orc.jacobi2d(T, Ar, Br)
+    A, B = A0.copy(), B0.copy()
+    with runtime(J, 2, policy, mode=J.JACC_MODE_ADAPTIVE):
+        _create(J, A, B)
+        for _ in range(T):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)])
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, B), _out(J, A)])
+        trace, states, now = J.jacc_adaptive_history(J.JACC_LOOP_JACOBI2D_F64)
+        J.jacc_update_host(A)
+        J.jacc_update_host(B)
+    assert np.array_equal(A, Ar) and np.array_equal(B, Br)
+    assert len(trace) >= 2
+    rep = ad.replay(trace, 2, 770e9)
+    assert states == rep[:-1] and now == rep[-1]
