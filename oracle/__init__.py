@@ -47,6 +47,10 @@ def _load():
             "orc_scatter_add_f64_filtered": ([I, P, P, P, I, I, P, PU, PU], None),
             "orc_scatter_add_i32_filtered": ([I, P, P, P, I, I, P, PU, PU], None),
             "orc_exchange_range": ([ctypes.c_int, P, ctypes.c_size_t, PU, PU], None),
+            "orc_himeno_stencil": ([I, I, I, P, P, P, P, P, P, P, ctypes.c_float, I, I,
+                                    ctypes.c_float, ctypes.POINTER(ctypes.c_double), PU, PU],
+                                   ctypes.c_float),
+            "orc_himeno_copy": ([I, I, I, P, P, I, I, PU, PU], None),
             "orc_exchange_bitmap": ([ctypes.c_int, P, ctypes.c_size_t, I, P], None),
         }
         for name, (args, res) in sig.items():
@@ -187,3 +191,35 @@ def exchange_bitmap(replicas, bitmaps):
     ptrs = (ctypes.c_void_p * n)(*[r.ctypes.data for r in replicas])
     bms = (ctypes.c_void_p * n)(*[b.ctypes.data for b in bitmaps])
     _load().orc_exchange_bitmap(n, ptrs, replicas[0].itemsize, replicas[0].size, bms)
+
+
+# ---- NEXT-2 Himeno ------------------------------------------
+def himeno_stencil(p, a, b, c, wrk1, bnd, wrk2, omega=0.8, planes=None, gosa_in=0.0):
+    """Stencil loop of one Himeno iteration (in place on wrk2).  Returns
+    (gosa fp32 as written, gosa_ref compensated fp64 sum of the same fp32
+    terms, (wmin, wmax)).  planes = inclusive (lb, ub) filter or None."""
+    I, J, K = p.shape
+    lb, ub = planes if planes is not None else (0, I)
+    ref = ctypes.c_double()
+    mn, mx = _range_out()
+    g = _load().orc_himeno_stencil(I, J, K, _p(p), _p(a), _p(b), _p(c), _p(wrk1), _p(bnd),
+                                   _p(wrk2), omega, lb, ub, gosa_in, ctypes.byref(ref),
+                                   ctypes.byref(mn), ctypes.byref(mx))
+    return g, ref.value, (mn.value, mx.value)
+
+
+def himeno_copy(wrk2, p, planes=None):
+    I, J, K = p.shape
+    lb, ub = planes if planes is not None else (0, I)
+    mn, mx = _range_out()
+    _load().orc_himeno_copy(I, J, K, _p(wrk2), _p(p), lb, ub, ctypes.byref(mn), ctypes.byref(mx))
+    return mn.value, mx.value
+
+
+def himeno_iterations(nn, p, a, b, c, wrk1, bnd, wrk2, omega=0.8):
+    """nn Jacobi iterations (stencil + copy); returns the last gosa pair."""
+    g = None
+    for _ in range(nn):
+        g = himeno_stencil(p, a, b, c, wrk1, bnd, wrk2, omega)
+        himeno_copy(wrk2, p)
+    return g

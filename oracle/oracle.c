@@ -363,3 +363,93 @@ void orc_exchange_bitmap(int n, void **replicas, size_t elem, int64_t nelem,
                         memcpy((char *)replicas[p] + e * elem,
                                (char *)replicas[d] + e * elem, elem);
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-2 workload: Himeno benchmark (Table 1 "Himeno   */
+/* 19-point Jacobian Stencil Computation", Size XL 1024x512x512 fp32;  */
+/* P:704 "Himeno iteratively updates a 19-point stencil grid according */
+/* to Jacobi's method"; Fig. 10).  The loop bodies follow   */
+/* the benchmark's public source (DESIGN R-17): one Jacobi iteration =  */
+/* the stencil loop (writes wrk2, reduces gosa) then the copy loop      */
+/* (p = wrk2), both over the interior i in [1,I-1), j in [1,J-1),       */
+/* k in [1,K-1) of row-major [I][J][K] fp32 arrays.  a holds 4 arrays,  */
+/* b and c 3 each, [m][I][J][K].  Expression order exactly as written,  */
+/* fp32 arithmetic (FLT_EVAL_METHOD 0), no contraction.                */
+/* ------------------------------------------------------------------ */
+#define HI(m, i, j, k) ((((int64_t)(m) * I + (i)) * J + (j)) * K + (k))
+
+static float himeno_point(int64_t I, int64_t J, int64_t K, const float *p, const float *a,
+                          const float *b, const float *c, const float *wrk1, const float *bnd,
+                          int64_t i, int64_t j, int64_t k, float *ss_out)
+{
+    float s0 = a[HI(0, i, j, k)] * p[HI(0, i + 1, j, k)]
+             + a[HI(1, i, j, k)] * p[HI(0, i, j + 1, k)]
+             + a[HI(2, i, j, k)] * p[HI(0, i, j, k + 1)]
+             + b[HI(0, i, j, k)]
+               * (p[HI(0, i + 1, j + 1, k)] - p[HI(0, i + 1, j - 1, k)]
+                  - p[HI(0, i - 1, j + 1, k)] + p[HI(0, i - 1, j - 1, k)])
+             + b[HI(1, i, j, k)]
+               * (p[HI(0, i, j + 1, k + 1)] - p[HI(0, i, j - 1, k + 1)]
+                  - p[HI(0, i, j + 1, k - 1)] + p[HI(0, i, j - 1, k - 1)])
+             + b[HI(2, i, j, k)]
+               * (p[HI(0, i + 1, j, k + 1)] - p[HI(0, i - 1, j, k + 1)]
+                  - p[HI(0, i + 1, j, k - 1)] + p[HI(0, i - 1, j, k - 1)])
+             + c[HI(0, i, j, k)] * p[HI(0, i - 1, j, k)]
+             + c[HI(1, i, j, k)] * p[HI(0, i, j - 1, k)]
+             + c[HI(2, i, j, k)] * p[HI(0, i, j, k - 1)]
+             + wrk1[HI(0, i, j, k)];
+    float ss = (s0 * a[HI(3, i, j, k)] - p[HI(0, i, j, k)]) * bnd[HI(0, i, j, k)];
+    *ss_out = ss;
+    return ss;
+}
+
+/* stencil loop over planes [i_lb, i_ub] (inclusive; the whole interior
+ * for the sequential oracle), writes wrk2, returns gosa_in + sum ss*ss
+ * accumulated in fp32 in loop order; *gosa_ref (if non-NULL) receives the
+ * Neumaier-compensated fp64 sum of the same fp32 terms (accuracy
+ * reference, DESIGN R-17).  Records the write log min/max. */
+float orc_himeno_stencil(int64_t I, int64_t J, int64_t K, const float *p, const float *a,
+                         const float *b, const float *c, const float *wrk1, const float *bnd,
+                         float *wrk2, float omega, int64_t i_lb, int64_t i_ub, float gosa_in,
+                         double *gosa_ref, uint64_t *wmin, uint64_t *wmax)
+{
+    float gosa = gosa_in;
+    double s = 0.0, cmp = 0.0;
+    uint64_t mn = UINT64_MAX, mx = 0;
+    for (int64_t i = 1; i < I - 1; i++)
+        for (int64_t j = 1; j < J - 1; j++)
+            for (int64_t k = 1; k < K - 1; k++) {
+                if (!(i_lb <= i && i_ub >= i)) continue;   /* filter */
+                float ss;
+                himeno_point(I, J, K, p, a, b, c, wrk1, bnd, i, j, k, &ss);
+                gosa += ss * ss;
+                neu_add(&s, &cmp, (double)(ss * ss));
+                wrk2[HI(0, i, j, k)] = p[HI(0, i, j, k)] + omega * ss;
+                uint64_t f = (uint64_t)HI(0, i, j, k);
+                if (f < mn) mn = f;
+                if (f > mx) mx = f;
+            }
+    if (gosa_ref) *gosa_ref = (double)gosa_in + (s + cmp);
+    if (wmin) *wmin = mn;
+    if (wmax) *wmax = mx;
+    return gosa;
+}
+
+/* copy loop p = wrk2 over interior planes [i_lb, i_ub] */
+void orc_himeno_copy(int64_t I, int64_t J, int64_t K, const float *wrk2, float *p,
+                     int64_t i_lb, int64_t i_ub, uint64_t *wmin, uint64_t *wmax)
+{
+    uint64_t mn = UINT64_MAX, mx = 0;
+    for (int64_t i = 1; i < I - 1; i++)
+        for (int64_t j = 1; j < J - 1; j++)
+            for (int64_t k = 1; k < K - 1; k++) {
+                if (!(i_lb <= i && i_ub >= i)) continue;
+                p[HI(0, i, j, k)] = wrk2[HI(0, i, j, k)];
+                uint64_t f = (uint64_t)HI(0, i, j, k);
+                if (f < mn) mn = f;
+                if (f > mx) mx = f;
+            }
+    if (wmin) *wmin = mn;
+    if (wmax) *wmax = mx;
+}
+#undef HI

@@ -985,6 +985,11 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
 
     // ---- validity bookkeeping ---------------------------------------------
     for (const Pull &pl : pulls) pl.reg->valid[pl.dst].add(pl.lo, pl.hi);
+    if (W && L.dup) {
+        // duplicated: every device computed (after pulling) the whole block
+        for (int d = 0; d < n; d++)
+            if (L.plan[d].active) W->valid[d].add(L.plan[d].wlo, L.plan[d].whi);
+    }
     if (writes) {
         for (int d = 0; d < n; d++) {
             const DevPlan &p = L.plan[d];
