@@ -304,12 +304,26 @@ def run_jacc(args):
 
     for _ in range(args.warmup):
         step()
+    # kernel-level timing (CUDA events around every launch on its stream)
     J.jacc_set_profiling(1)
     J.jacc_profile_reset()
-    with ClockSampler(C.ords[0]) as clk:
-        t = C.timed(step, args.steps)
+    t_plain = C.timed(step, 1)
     kern = {d: J.jacc_profile_totals(d) for d in C.local}
     J.jacc_set_profiling(0)
+    # the timed steps replay one CUDA graph of the 200-launch step (captured
+    # at steady state: identical device work, host planning amortised);
+    # multi-process mode has no graphs and issues the launches directly
+    use_graph = not C.mp and not args.no_graph
+    if use_graph:
+        J.jacc_graph_begin()
+        step()
+        gid = J.jacc_graph_end()
+        J.jacc_graph_replay(gid, 1)  # warm the graph
+        timed_step = lambda: J.jacc_graph_replay(gid, 1)
+    else:
+        timed_step = step
+    with ClockSampler(C.ords[0]) as clk:
+        t = C.timed(timed_step, args.steps)
     bytes_step = 2 * TSTEPS * algo_bytes_per_sweep(N, n)
     value = bytes_step * args.steps / t / 1e9
     launches = C.reduce(sum(k[2] for k in kern.values()), "sum")
@@ -356,6 +370,8 @@ def run_jacc(args):
         "data": "synthetic (PolyBench jacobi-2d init, seeded generators in synth/)",
         "config": {"workload": "J16K: Jacobi-2D fp64 16384x16384, 100 timesteps (200 launches/step)",
                    "merge": args.merge, "launch": "one process per GPU" if C.mp else "single process",
+                   "issue": "CUDA graph replay of the captured step" if use_graph else "jacc_launch x200",
+                   "ms_per_step_plain_launches": t_plain * 1e3,
                    "virtual_devices": C.virtual,
                    "l2": "no flush: inputs 2x2 GiB >> 126 MB L2",
                    "parallelism": f"row-block owner partition over {n} device(s)"},
@@ -456,6 +472,29 @@ def run_extra_loops(J, C, n, peak):
                                "merge_us": m * 1e6, "launch_ms": t * 1e3}
     for arr in (idx, b, a):
         J.jacc_data_delete(arr)
+    del idx, b, a
+    # Himeno XL (NEXT-2 workload): stencil + gosa, then copy, fp32
+    I, Jd, K = 1025, 513, 513
+    hp, ha, hb, hc, hw1, hbd = synth.himeno_init(I, Jd, K)
+    hw2 = np.zeros_like(hp)
+    for arr in (hp, ha, hb, hc, hw1, hbd, hw2):
+        J.jacc_data_create(arr)
+        J.jacc_update_device(arr)
+    g = np.zeros(1)
+    hargs = [J.arg(IN, hp), J.arg(IN, ha), J.arg(IN, hb), J.arg(IN, hc), J.arg(IN, hw1),
+             J.arg(IN, hbd), J.arg(OUT, hw2), J.arg(J.JACC_ARG_REDUCE_SUM_F64, g),
+             J.arg(J.JACC_ARG_SCALAR_F64, f64=0.8)]
+    cargs = [J.arg(IN, hw2), J.arg(OUT, hp)]
+    ts, ks, _ = _time_loop(J, C, lambda: J.jacc_launch(J.JACC_LOOP_HIMENO_F32, None, hargs, 0), 5)
+    tc, kc, _ = _time_loop(J, C, lambda: J.jacc_launch(J.JACC_LOOP_HIMENO_COPY_F32, None, cargs, 0), 5)
+    pts = (I - 2) * (Jd - 2) * (K - 2)
+    sb, cb = 56 * pts, 8 * pts   # 12 coefficient/aux arrays + p read, wrk2 written | copy
+    out["himeno_XL_fp32"] = {"stencil_us": ks * 1e6, "stencil_gbs": sb / n / ks / 1e9,
+                             "stencil_frac": sb / n / ks / 1e9 / peak,
+                             "copy_us": kc * 1e6, "copy_gbs": cb / n / kc / 1e9,
+                             "iteration_ms": (ts + tc) * 1e3, "gosa": float(g[0])}
+    for arr in (hp, ha, hb, hc, hw1, hbd, hw2):
+        J.jacc_data_delete(arr)
     return out
 
 
@@ -469,6 +508,7 @@ def main():
     ap.add_argument("--no-extra", dest="extra", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-sweeps", type=int, default=10)
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -115,7 +115,7 @@ jacc_status jacc_partition(int64_t E, int n, int d, int64_t *lo, int64_t *hi);
 /* Register [host, host+bytes) and allocate one replica of `bytes` on every
  * logical device ("Device-memory allocations ... are replicated on
  * all the GPUs").  No copy is made (OpenACC `create`).  elem_size is the
- * element size in bytes; extents[0..ndims) the row-major shape (ndims 1..3)
+ * element size in bytes; extents[0..ndims) the row-major shape (ndims 1..4)
  * whose product times elem_size must equal bytes.
  * Errors: JACC_ERR_INVALID (bytes == 0, bad shape, host NULL),
  * JACC_ERR_OVERLAP, JACC_ERR_OOM. */
@@ -158,8 +158,16 @@ jacc_status jacc_update_host(void *host, size_t offset_bytes, size_t bytes);
  *   JACC_LOOP_SCATTER_ADD_F64 (R-6..R-8): idx IN i32[n], b IN f64[n],
  *       a INOUT f64[M]; for i in range: a[idx[i]] += b[i] (atomic).
  *   JACC_LOOP_SCATTER_ADD_I32 : idx IN i32[n], b IN i32[n], a INOUT i32[M].
+ *   JACC_LOOP_HIMENO_F32      (NEXT-2, Himeno stencil loop, P:654, P:704,
+ *       R-17): p IN f32[I][J][K], a IN f32[4][I][J][K], b IN f32[3][I][J][K],
+ *       c IN f32[3][I][J][K], wrk1 IN, bnd IN, wrk2 OUT (f32[I][J][K]),
+ *       gosa REDUCE_SUM_F64, omega SCALAR_F64 (.f64 field); for the 19-point
+ *       stencil over range (3-D within [1,I-1)x[1,J-1)x[1,K-1), NULL = all):
+ *       ss = (s0*a3 - p)*bnd; gosa += ss*ss; wrk2 = p + omega*ss (fp32 as
+ *       written; gosa accumulated in fp64).
+ *   JACC_LOOP_HIMENO_COPY_F32 : wrk2 IN, p OUT; p = wrk2 over the range.
  * 1-D array arguments may point inside a region (the loop's array starts
- * there); 2-D arguments must point at the region base. */
+ * there); multi-dimensional arguments must point at the region base. */
 enum {
     JACC_LOOP_SQUARE_F32 = 1,
     JACC_LOOP_JACOBI2D_F64 = 2,
@@ -167,7 +175,9 @@ enum {
     JACC_LOOP_SUM_F64 = 4,
     JACC_LOOP_GEMM_F64 = 5,
     JACC_LOOP_SCATTER_ADD_F64 = 6,
-    JACC_LOOP_SCATTER_ADD_I32 = 7
+    JACC_LOOP_SCATTER_ADD_I32 = 7,
+    JACC_LOOP_HIMENO_F32 = 8,
+    JACC_LOOP_HIMENO_COPY_F32 = 9
 };
 
 /* Iteration range, half-open per dimension (R-3). */
@@ -324,6 +334,24 @@ jacc_status jacc_adaptive_replay(int n, double peak_p2p, int len, const double *
  * *state_now = current state (-1 if none). */
 jacc_status jacc_adaptive_history(int loop_id, int cap, double *t_kernel, double *t_comm,
                                   double *write_size, int *states, int *len, int *state_now);
+
+/* ---------------------------------------------------------------------- */
+/* CUDA graphs of launch sequences (single-process mode)                   */
+/* ---------------------------------------------------------------------- */
+/* Capture the device work of the launches issued between
+ * jacc_graph_begin() and jacc_graph_end() (every device's stream, merges
+ * and pulls included) into one CUDA graph; nothing executes during the
+ * capture.  The graph maps the runtime state at begin (replica validity,
+ * dirty-record slots) to the state at end; jacc_graph_replay runs it
+ * `count` times and requires the current state to equal the captured
+ * start state (true for a steady stencil ping-pong), else JACC_ERR_STATE.
+ * Launches with a reduction cannot be captured (obligatory host sync) and
+ * return JACC_ERR_INVALID; synchronous calls during a capture return
+ * JACC_ERR_STATE.  jacc_data_delete() destroys every graph. */
+jacc_status jacc_graph_begin(void);
+jacc_status jacc_graph_end(int *graph_id);
+jacc_status jacc_graph_replay(int graph_id, int count);
+jacc_status jacc_graph_destroy(int graph_id);
 
 const char *jacc_error_string(jacc_status s);
 

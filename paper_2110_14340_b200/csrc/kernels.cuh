@@ -35,7 +35,7 @@ cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N,
 // BK2  Fixed-order reduction of sum x[i]*y[i] (y != nullptr) or sum x[i]
 // over [0, n); result written to *out.  `partials` holds kReduceGrid
 // doubles, `ticket` one zeroed u32 (left zeroed on exit).
-constexpr int kReduceGrid = 148 * 4;
+constexpr int kReduceGrid = 148 * 4;  // (partials buffers hold kHimenoPartials)
 cudaError_t reduce_f64(cudaStream_t s, const double *x, const double *y, int64_t n,
                        double *partials, unsigned *ticket, double *out);
 
@@ -75,6 +75,23 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
                                u64 *dirty, const ScatterPlan &pl, void *scratch, uint8_t *bytemap,
                                uint8_t epoch);
+
+// NEXT-2  Himeno benchmark (DESIGN R-17), fp32, row-major
+// [I][J][K] arrays (a: 4, b and c: 3 stacked arrays).  Stencil loop over
+// planes [i0,i1) x [j0,j1) x [k0,k1): wrk2 = p + omega*ss, partial
+// gosa = sum ss*ss accumulated in fp64 in a fixed order (block partials in
+// `partials`, capacity kHimenoPartials, last block finishes) -> *out;
+// dirty range of wrk2 fused.  Copy loop p = wrk2 over the same box, dirty
+// range of p fused, HALO push of planes i0 / i1-1 into peer replicas of p.
+constexpr int kHimenoPartials = 16384;
+cudaError_t himeno_stencil(cudaStream_t s, const float *p, const float *a, const float *b,
+                           const float *c, const float *wrk1, const float *bnd, float *wrk2,
+                           int64_t I, int64_t J, int64_t K, int64_t i0, int64_t i1, int64_t j0,
+                           int64_t j1, int64_t k0, int64_t k1, float omega, double *partials,
+                           unsigned *ticket, double *out, u64 *dirty);
+cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, int64_t J,
+                        int64_t K, int64_t i0, int64_t i1, int64_t j0, int64_t j1, int64_t k0,
+                        int64_t k1, u64 *dirty, float *push_top, float *push_bot);
 
 // BK5  Dirty-region merge over peer memory.  merge_range copies the
 // recorded span [dirty min, dirty max] (clamped to [lo, hi)) of src into

@@ -171,7 +171,7 @@ struct Region {
     uintptr_t base = 0;
     size_t bytes = 0, elem = 0;
     int ndims = 0;
-    int64_t ext[3] = {1, 1, 1};
+    int64_t ext[4] = {1, 1, 1, 1};
     int64_t nelem = 0;
     bool pinned = false;
     std::vector<char *> rep;           // per device replica
@@ -195,6 +195,17 @@ struct AdaptRec {
     bool dup;
     double ws;
     std::vector<ProfRec> ev;
+};
+
+// A captured launch sequence (CUDA graph over every device's stream) and
+// the host-side runtime state it maps S_start -> S_end.
+struct GraphRec {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+    std::map<Region *, std::vector<IntervalSet>> v_start, v_end;
+    std::map<Region *, std::vector<int>> slot_start, slot_end;
+    std::vector<std::vector<char>> comm_end;
 };
 
 struct Runtime {
@@ -234,6 +245,11 @@ struct Runtime {
     std::map<int, std::string> adapt_last_key;  // loop_id -> most recent key
     std::vector<AdaptRec> adapt_pending;
     double peak_p2p = 770e9;  // B/s per GPU egress (measured peer copy, B200_PROFILING.md)
+    // CUDA graph capture / replay of launch sequences (single process)
+    bool capturing = false;
+    GraphRec cap;
+    std::map<int, GraphRec> graphs;
+    int next_graph = 1;
 };
 
 Runtime R;
@@ -403,6 +419,12 @@ void free_region(Region *r) {
     if (r->pinned) cudaHostUnregister((void *)r->base);
 }
 
+void destroy_graph(GraphRec &g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    g = GraphRec{};
+}
+
 // c4 partition ("equally dividing"; S:266 remainder rule)
 void partition(int64_t E, int n, int d, int64_t &lo, int64_t &hi) {
     const int64_t q = E / n, r = E % n;
@@ -436,8 +458,8 @@ struct Desc {
     int id;
     const char *name;
     int nargs;
-    int kinds[3];
-    size_t elems[3];   // required element sizes (0 = n/a)
+    int kinds[9];
+    size_t elems[9];   // required element sizes (0 = n/a)
     int out_arg;       // index of written array (-1 none)
     bool reduction;
     int halo_rows;     // stencil radius along the split dim (HALO prediction)
@@ -451,6 +473,11 @@ const Desc kDescs[] = {
     {JACC_LOOP_GEMM_F64, "gemm_f64", 3, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT}, {8, 8, 8}, 2, false, 0},
     {JACC_LOOP_SCATTER_ADD_F64, "scatter_add_f64", 3, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_INOUT}, {4, 8, 8}, 2, false, 0},
     {JACC_LOOP_SCATTER_ADD_I32, "scatter_add_i32", 3, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_INOUT}, {4, 4, 4}, 2, false, 0},
+    {JACC_LOOP_HIMENO_F32, "himeno_f32", 9,
+     {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN,
+      JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT, JACC_ARG_REDUCE_SUM_F64, JACC_ARG_SCALAR_F64},
+     {4, 4, 4, 4, 4, 4, 4, 0, 0}, 6, true, 0},
+    {JACC_LOOP_HIMENO_COPY_F32, "himeno_copy_f32", 2, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT}, {4, 4}, 1, false, 1},
 };
 
 const Desc *find_desc(int id) {
@@ -477,6 +504,8 @@ struct Launch {
     int64_t n1 = 0;            // 1-D length (square, dot, sum, scatter iterations)
     int64_t N = 0;             // jacobi grid
     int64_t M = 0, Nn = 0, K = 0;  // gemm
+    int64_t HI = 0, HJ = 0, HK = 0;  // himeno grid
+    double scalar = 0;               // SCALAR_F64 argument (himeno omega)
 };
 
 void plan_launch(Launch &L) {
@@ -535,6 +564,27 @@ void plan_launch(Launch &L) {
                 p.whi = (p.i1 - 1) * L.Nn + p.j1;
                 p.reads.push_back({L.a[0].reg, p.i0 * L.K, p.i1 * L.K});
                 p.reads.push_back({L.a[1].reg, 0, L.K * L.Nn});
+            }
+        } else if (id == JACC_LOOP_HIMENO_F32 || id == JACC_LOOP_HIMENO_COPY_F32) {
+            const int64_t P = L.HJ * L.HK, V = L.HI * P;
+            partition(L.HI, nd, dd, p.own_lo, p.own_hi);  // planes of the written array
+            p.i0 = std::max(L.rg.lo[0], p.own_lo);
+            p.i1 = std::min(L.rg.hi[0], p.own_hi);
+            p.j0 = L.rg.lo[1];
+            p.j1 = L.rg.hi[1];
+            p.active = p.i1 > p.i0 && p.j1 > p.j0 && L.rg.hi[2] > L.rg.lo[2];
+            if (p.active) {
+                p.wlo = p.i0 * P + p.j0 * L.HK + L.rg.lo[2];
+                p.whi = (p.i1 - 1) * P + (p.j1 - 1) * L.HK + L.rg.hi[2];
+                if (id == JACC_LOOP_HIMENO_F32) {
+                    p.reads.push_back({L.a[0].reg, (p.i0 - 1) * P, (p.i1 + 1) * P});  // p +- 1 plane
+                    const int stacks[6] = {1, 4, 3, 3, 1, 1};
+                    for (int k = 1; k < 6; k++)
+                        for (int m = 0; m < stacks[k]; m++)
+                            p.reads.push_back({L.a[k].reg, m * V + p.i0 * P, m * V + p.i1 * P});
+                } else {
+                    p.reads.push_back({L.a[0].reg, p.i0 * P, p.i1 * P});  // wrk2 planes
+                }
             }
         } else {  // scatter: owned slice of a; every device scans all i
             Region *ar = L.a[2].reg;
@@ -622,6 +672,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                       int async_id) {
     const Desc *D = find_desc(loop_id);
     if (!D) return JACC_ERR_UNKNOWN_LOOP;
+    if (R.capturing) {
+        if (D->reduction) return JACC_ERR_INVALID;  // obligatory host sync cannot be captured
+        async_id = 0;
+    }
     invalid_if(nargs != D->nargs || (nargs > 0 && !args));
     Launch L;
     L.D = D;
@@ -632,6 +686,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         if (args[k].kind == JACC_ARG_REDUCE_SUM_F64) {
             invalid_if(!args[k].ptr);
             L.red_ptr = static_cast<double *>(args[k].ptr);
+            continue;
+        }
+        if (args[k].kind == JACC_ARG_SCALAR_F64) {
+            L.scalar = args[k].f64;
             continue;
         }
         Region *r = lookup(args[k].ptr);
@@ -659,6 +717,45 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             invalid_if(range->ndims != 2);
             for (int k = 0; k < 2; k++) {
                 invalid_if(range->lo[k] < 1 || range->hi[k] > L.N - 1);
+                rg.lo[k] = range->lo[k];
+                rg.hi[k] = std::max(range->lo[k], range->hi[k]);
+            }
+        }
+    } else if (id == JACC_LOOP_HIMENO_F32 || id == JACC_LOOP_HIMENO_COPY_F32) {
+        // p, wrk1, bnd, wrk2: [I][J][K]; a: [4][I][J][K]; b, c: [3][I][J][K]
+        Region *P = L.a[0].reg;
+        invalid_if(P->ndims != 3);
+        L.HI = P->ext[0];
+        L.HJ = P->ext[1];
+        L.HK = P->ext[2];
+        invalid_if(L.HI < 3 || L.HJ < 3 || L.HK < 3);
+        for (int k = 0; k < nargs; k++) {
+            if (!L.a[k].reg) continue;
+            Region *r = L.a[k].reg;
+            invalid_if(L.a[k].off != 0);
+            int stack = 0;
+            if (id == JACC_LOOP_HIMENO_F32) stack = k == 1 ? 4 : (k == 2 || k == 3) ? 3 : 0;
+            if (stack) {
+                invalid_if(r->ndims != 4 || r->ext[0] != stack || r->ext[1] != L.HI ||
+                           r->ext[2] != L.HJ || r->ext[3] != L.HK);
+            } else {
+                invalid_if(r->ndims != 3 || r->ext[0] != L.HI || r->ext[1] != L.HJ ||
+                           r->ext[2] != L.HK);
+            }
+        }
+        const int out = D->out_arg;
+        for (int k = 0; k < nargs; k++)  // written array must not alias an input (R-12)
+            if (k != out && L.a[k].reg) invalid_if(L.a[k].reg == L.a[out].reg);
+        rg.ndims = 3;
+        rg.lo[0] = rg.lo[1] = rg.lo[2] = 1;
+        rg.hi[0] = L.HI - 1;
+        rg.hi[1] = L.HJ - 1;
+        rg.hi[2] = L.HK - 1;
+        if (range) {
+            invalid_if(range->ndims != 3);
+            const int64_t ex[3] = {L.HI, L.HJ, L.HK};
+            for (int k = 0; k < 3; k++) {
+                invalid_if(range->lo[k] < 1 || range->hi[k] > ex[k] - 1);
                 rg.lo[k] = range->lo[k];
                 rg.hi[k] = std::max(range->lo[k], range->hi[k]);
             }
@@ -711,7 +808,8 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     L.rg = rg;
     if (R.mode == JACC_MODE_DUP) L.dup = true;
     // ---- NEXT-1 adaptive utilization (single process, n > 1) ---------------
-    const bool adaptive = R.mode == JACC_MODE_ADAPTIVE && R.n > 1 && !R.mp && !L.dup;
+    const bool adaptive =
+        R.mode == JACC_MODE_ADAPTIVE && R.n > 1 && !R.mp && !L.dup && !R.capturing;
     std::string akey;
     double adapt_ws = 0;
     if (adaptive) {
@@ -737,7 +835,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 if (R.policy == JACC_MERGE_EAGER)
                     b = (double)(pp.whi - pp.wlo) * Wr->elem * (R.n - 1);
                 else if (D->halo_rows > 0)
-                    b = 2.0 * D->halo_rows * (double)(pp.j1 - pp.j0) * Wr->elem;
+                    b = 2.0 * D->halo_rows * (double)(Wr->nelem / Wr->ext[0]) * Wr->elem;
                 else
                     b = 0;
                 adapt_ws = std::max(adapt_ws, b);
@@ -816,7 +914,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     if (R.prof.size() > 30000) flush_prof();
     R.last_start = R.prof.size();
     const int cur = R.gen & 1, prev = cur ^ 1;
-    const bool prof = R.profiling;
+    const bool prof = R.profiling && !R.capturing;
     uint64_t merged_bytes = 0;
     wait_launches(R.gen);
     std::vector<ProfRec> adapt_evs;
@@ -900,6 +998,25 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                                 reinterpret_cast<double *>(W->rep[d]), L.M, L.Nn, L.K, p.i0, p.i1,
                                 p.j0, p.j1, drec));
                 break;
+            case JACC_LOOP_HIMENO_F32: {
+                auto F = [&](int k) { return reinterpret_cast<const float *>(L.a[k].reg->rep[d]); };
+                CK(jk::himeno_stencil(dv.s, F(0), F(1), F(2), F(3), F(4), F(5),
+                                      reinterpret_cast<float *>(W->rep[d]), L.HI, L.HJ, L.HK, p.i0,
+                                      p.i1, p.j0, p.j1, L.rg.lo[2], L.rg.hi[2], (float)L.scalar,
+                                      dv.partials, dv.ticket, dv.part, drec));
+                break;
+            }
+            case JACC_LOOP_HIMENO_COPY_F32: {
+                float *pt = top[d] >= 0 ? reinterpret_cast<float *>(W->rep[top[d]]) : nullptr;
+                float *pb = bot[d] >= 0 ? reinterpret_cast<float *>(W->rep[bot[d]]) : nullptr;
+                CK(jk::himeno_copy(dv.s, reinterpret_cast<const float *>(L.a[0].reg->rep[d]),
+                                   reinterpret_cast<float *>(W->rep[d]), L.HI, L.HJ, L.HK, p.i0, p.i1,
+                                   p.j0, p.j1, L.rg.lo[2], L.rg.hi[2], drec, pt, pb));
+                const int64_t planeb = (p.j1 - p.j0) * (L.rg.hi[2] - L.rg.lo[2]) * 4;
+                if (pt) merged_bytes += planeb;
+                if (pb) merged_bytes += planeb;
+                break;
+            }
             case JACC_LOOP_SCATTER_ADD_F64:
             case JACC_LOOP_SCATTER_ADD_I32: {
                 const int32_t *ix = reinterpret_cast<const int32_t *>(L.a[0].reg->rep[d]) + L.a[0].off + p.i0;
@@ -911,7 +1028,8 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 const bool f64 = id == JACC_LOOP_SCATTER_ADD_F64;
                 const char *b = L.a[1].reg->rep[d] + (L.a[1].off + p.i0) * (int64_t)W->elem;
                 const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
-                const jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
+                jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
+                if (R.capturing) sp.binned = false;  // epoch byte-map state is host-side
                 if (sp.binned) {
                     if (dv.scratch_bytes < sp.scratch) {
                         CK(cudaStreamSynchronize(dv.s));
@@ -1000,9 +1118,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 if (q == d) continue;
                 // q keeps validity only on the rows pushed to it (HALO)
                 std::vector<std::pair<int64_t, int64_t>> keep;
-                if (id == JACC_LOOP_JACOBI2D_F64) {
-                    if (top[d] == q) keep.push_back({p.i0 * L.N, (p.i0 + 1) * L.N});
-                    if (bot[d] == q) keep.push_back({(p.i1 - 1) * L.N, p.i1 * L.N});
+                if (D->halo_rows > 0) {
+                    const int64_t unit = W->nelem / W->ext[0];  // elements per split index
+                    if (top[d] == q) keep.push_back({p.i0 * unit, (p.i0 + 1) * unit});
+                    if (bot[d] == q) keep.push_back({(p.i1 - 1) * unit, p.i1 * unit});
                 }
                 std::vector<std::pair<int64_t, int64_t>> had;
                 for (auto &k : keep) {
@@ -1021,6 +1140,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     R.last_bytes = merged_bytes;
     R.comm_prev = comm;
     R.gen++;
+    if (R.capturing) R.cap.launches++;
 
     // ---- reduction combine (obligatory sync) -------------------
     if (D->reduction) {
@@ -1100,7 +1220,7 @@ jacc_status jacc_init(int n_devices, const int *device_ids) {
                 CK(cudaEventCreateWithFlags(&dv.ev[1], cudaEventDisableTiming));
                 CK(cudaEventRecord(dv.ev[0], dv.s));
                 CK(cudaEventRecord(dv.ev[1], dv.s));
-                CK(cudaMalloc(&dv.partials, jk::kReduceGrid * sizeof(double)));
+                CK(cudaMalloc(&dv.partials, jk::kHimenoPartials * sizeof(double)));
                 CK(cudaMalloc(&dv.ticket, 64));
                 CK(cudaMemset(dv.ticket, 0, 64));
                 CK(cudaMalloc(&dv.part, 8));
@@ -1148,6 +1268,15 @@ jacc_status jacc_finalize(void) {
         } catch (Fail &) {
         }
     }
+    if (R.capturing) {
+        cudaGraph_t g = nullptr;
+        cudaSetDevice(R.dev[0].ord);
+        cudaStreamEndCapture(R.dev[0].s, &g);
+        if (g) cudaGraphDestroy(g);
+        R.capturing = false;
+    }
+    for (auto &g : R.graphs) destroy_graph(g.second);
+    R.graphs.clear();
     for (auto &kv : R.table) free_region(kv.second.get());
     R.table.clear();
     for (auto &p : R.prof) {
@@ -1218,7 +1347,8 @@ jacc_status jacc_set_mode(int mode) {
 jacc_status jacc_data_create(void *host, size_t bytes, size_t elem_size, int ndims,
                              const int64_t *extents) {
     return guard([&]() -> jacc_status {
-        if (!host || bytes == 0 || elem_size == 0 || ndims < 1 || ndims > 3 || !extents)
+        if (R.capturing) return JACC_ERR_STATE;
+        if (!host || bytes == 0 || elem_size == 0 || ndims < 1 || ndims > 4 || !extents)
             return JACC_ERR_INVALID;
         int64_t prod = 1;
         for (int k = 0; k < ndims; k++) {
@@ -1274,7 +1404,10 @@ jacc_status jacc_data_delete(void *host) {
     return guard([&]() -> jacc_status {
         Region *r = lookup(host);
         if (!r) return JACC_ERR_NOT_PRESENT;
+        if (R.capturing) return JACC_ERR_STATE;
         sync_all();
+        for (auto &g : R.graphs) destroy_graph(g.second);  // they reference the replicas
+        R.graphs.clear();
         free_region(r);
         R.table.erase(r->base);
         return JACC_OK;
@@ -1283,6 +1416,7 @@ jacc_status jacc_data_delete(void *host) {
 
 jacc_status jacc_update_device(void *host, size_t off, size_t bytes) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         Region *r = lookup(host);
         if (!r) return JACC_ERR_NOT_PRESENT;
         const size_t start = ((uintptr_t)host - r->base) + off;
@@ -1304,6 +1438,7 @@ jacc_status jacc_update_device(void *host, size_t off, size_t bytes) {
 
 jacc_status jacc_update_host(void *host, size_t off, size_t bytes) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         Region *r = lookup(host);
         if (!r) return JACC_ERR_NOT_PRESENT;
         const size_t start = ((uintptr_t)host - r->base) + off;
@@ -1368,6 +1503,7 @@ jacc_status jacc_launch(int loop_id, const jacc_range *range, const jacc_arg *ar
 jacc_status jacc_wait(int async_id) {
     (void)async_id;
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         sync_all();
         return JACC_OK;
     });
@@ -1375,6 +1511,7 @@ jacc_status jacc_wait(int async_id) {
 
 jacc_status jacc_get_dirty_range(void *host, int dev, uint64_t *mn, uint64_t *mx) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         Region *r = lookup(host);
         if (!r) return JACC_ERR_NOT_PRESENT;
         if (dev < 0 || dev >= R.n || !mn || !mx) return JACC_ERR_INVALID;
@@ -1391,6 +1528,7 @@ jacc_status jacc_get_dirty_range(void *host, int dev, uint64_t *mn, uint64_t *mx
 
 jacc_status jacc_get_dirty_bitmap(void *host, int dev, uint32_t *out, size_t nwords) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         Region *r = lookup(host);
         if (!r) return JACC_ERR_NOT_PRESENT;
         if (dev < 0 || dev >= R.n || !out) return JACC_ERR_INVALID;
@@ -1406,6 +1544,7 @@ jacc_status jacc_get_dirty_bitmap(void *host, int dev, uint32_t *out, size_t nwo
 
 jacc_status jacc_get_replica(void *host, int dev, void *out, size_t bytes) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         Region *r = lookup(host);
         if (!r) return JACC_ERR_NOT_PRESENT;
         if (dev < 0 || dev >= R.n || !out || bytes > r->bytes) return JACC_ERR_INVALID;
@@ -1419,6 +1558,7 @@ jacc_status jacc_get_replica(void *host, int dev, void *out, size_t bytes) {
 
 jacc_status jacc_last_timing(double *tk, double *tm, uint64_t *bytes) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         flush_prof();
         if (tk) *tk = R.last_valid ? R.last_k : 0.0;
         if (tm) *tm = R.last_valid ? R.last_m : 0.0;
@@ -1429,6 +1569,7 @@ jacc_status jacc_last_timing(double *tk, double *tm, uint64_t *bytes) {
 
 jacc_status jacc_set_profiling(int on) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         flush_prof();
         R.profiling = on != 0;
         return JACC_OK;
@@ -1438,6 +1579,7 @@ jacc_status jacc_set_profiling(int on) {
 jacc_status jacc_profile_totals(int dev, double *ks, double *ms, uint64_t *launches,
                                 uint64_t *bytes) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         if (dev < 0 || dev >= R.n) return JACC_ERR_INVALID;
         flush_prof();
         const Device &dv = R.dev[dev];
@@ -1451,6 +1593,7 @@ jacc_status jacc_profile_totals(int dev, double *ks, double *ms, uint64_t *launc
 
 jacc_status jacc_profile_reset(void) {
     return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
         flush_prof();
         for (auto &dv : R.dev) {
             dv.kernel_s = dv.merge_s = 0;
@@ -1522,7 +1665,7 @@ jacc_status jacc_init_rank(int rank, int world, int cuda_ordinal, const void *un
                 CK(cudaEventCreateWithFlags(&dv.ev[k], cudaEventDisableTiming | cudaEventInterprocess));
                 CK(cudaEventRecord(dv.ev[k], dv.s));
             }
-            CK(cudaMalloc(&dv.partials, jk::kReduceGrid * sizeof(double)));
+            CK(cudaMalloc(&dv.partials, jk::kHimenoPartials * sizeof(double)));
             CK(cudaMalloc(&dv.ticket, 64));
             CK(cudaMemset(dv.ticket, 0, 64));
             CK(cudaMalloc(&dv.part, 8));
@@ -1618,6 +1761,152 @@ jacc_status jacc_import_region(void *host, int peer, const void *in, size_t byte
 }
 
 int jacc_rank(void) { return R.init ? (R.mp ? R.me : 0) : -1; }
+
+// ---------------------------------------------------------------------------
+// CUDA graphs of launch sequences
+// ---------------------------------------------------------------------------
+namespace {
+void snapshot(std::map<Region *, std::vector<IntervalSet>> &v, std::map<Region *, std::vector<int>> &sl) {
+    v.clear();
+    sl.clear();
+    for (auto &kv : R.table) {
+        v[kv.second.get()] = kv.second->valid;
+        sl[kv.second.get()] = kv.second->dslot;
+    }
+}
+bool same_validity(const std::map<Region *, std::vector<IntervalSet>> &v) {
+    if (v.size() != R.table.size()) return false;
+    for (auto &kv : R.table) {
+        auto it = v.find(kv.second.get());
+        if (it == v.end()) return false;
+        for (int d = 0; d < R.n; d++)
+            if (it->second[d].iv != kv.second->valid[d].iv) return false;
+    }
+    return true;
+}
+// make stream s (on device h) wait for every device's current work
+void join_into(int h) {
+    for (int d = 0; d < R.n; d++) {
+        if (d == h) continue;
+        set_dev(d);
+        cudaEvent_t e = pool_event();
+        CK(cudaEventRecord(e, R.dev[d].s));
+        set_dev(h);
+        CK(cudaStreamWaitEvent(R.dev[h].s, e, 0));
+        R.evpool.push_back(e);  // safe: a recorded event may be re-recorded later
+    }
+}
+}  // namespace
+
+jacc_status jacc_graph_begin(void) {
+    return guard([&]() -> jacc_status {
+        if (R.mp || R.capturing || R.mode == JACC_MODE_ADAPTIVE) return JACC_ERR_INVALID;
+        sync_all();
+        flush_prof();
+        R.cap = GraphRec{};
+        snapshot(R.cap.v_start, R.cap.slot_start);
+        // everything before the capture is complete: no waits on older events
+        R.comm_prev.assign(R.n, std::vector<char>(R.n, 0));
+        set_dev(0);
+        CK(cudaStreamBeginCapture(R.dev[0].s, cudaStreamCaptureModeRelaxed));
+        // fork: every other device stream joins the capture
+        cudaEvent_t fork = pool_event();
+        CK(cudaEventRecord(fork, R.dev[0].s));
+        for (int d = 1; d < R.n; d++) {
+            set_dev(d);
+            CK(cudaStreamWaitEvent(R.dev[d].s, fork, 0));
+        }
+        R.evpool.push_back(fork);
+        R.capturing = true;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_graph_end(int *graph_id) {
+    return guard([&]() -> jacc_status {
+        if (!R.capturing || !graph_id) return JACC_ERR_INVALID;
+        R.capturing = false;
+        join_into(0);
+        set_dev(0);
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamEndCapture(R.dev[0].s, &g));
+        R.cap.graph = g;
+        CK(cudaGraphInstantiate(&R.cap.exec, g, 0));
+        snapshot(R.cap.v_end, R.cap.slot_end);
+        R.cap.comm_end = R.comm_prev;
+        const int id = R.next_graph++;
+        R.graphs[id] = R.cap;
+        R.cap = GraphRec{};
+        // the captured work has NOT run: restore the pre-capture state
+        for (auto &kv : R.table) {
+            Region *r = kv.second.get();
+            r->valid = R.graphs[id].v_start[r];
+            r->dslot = R.graphs[id].slot_start[r];
+        }
+        R.gen -= R.graphs[id].launches;
+        R.comm_prev.assign(R.n, std::vector<char>(R.n, 0));
+        // events last recorded inside the capture: re-record them outside
+        for (int d = 0; d < R.n; d++) {
+            set_dev(d);
+            CK(cudaEventRecord(R.dev[d].ev[0], R.dev[d].s));
+            CK(cudaEventRecord(R.dev[d].ev[1], R.dev[d].s));
+        }
+        *graph_id = id;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_graph_replay(int graph_id, int count) {
+    return guard([&]() -> jacc_status {
+        auto it = R.graphs.find(graph_id);
+        if (it == R.graphs.end() || count < 0 || R.capturing) return JACC_ERR_INVALID;
+        GraphRec &g = it->second;
+        if (!same_validity(g.v_start)) return JACC_ERR_STATE;  // not the captured state
+        if (count == 0) return JACC_OK;
+        // dirty-record slots: the first captured launch of each region writes
+        // slot start^1, which the previous launch must have cleared
+        for (auto &kv : R.table) {
+            Region *r = kv.second.get();
+            for (int d = 0; d < R.n; d++)
+                if (r->dslot[d] != g.slot_start[r][d]) {
+                    set_dev(d);
+                    CK(cudaMemsetAsync(r->dirty[d] + 2 * (g.slot_start[r][d] ^ 1), 0xff, 16,
+                                       R.dev[d].s));
+                }
+        }
+        join_into(0);
+        set_dev(0);
+        for (int k = 0; k < count; k++) CK(cudaGraphLaunch(g.exec, R.dev[0].s));
+        // order every device stream after the replay and refresh its event
+        cudaEvent_t done = pool_event();
+        CK(cudaEventRecord(done, R.dev[0].s));
+        R.gen += g.launches * count;
+        for (int d = 0; d < R.n; d++) {
+            set_dev(d);
+            if (d) CK(cudaStreamWaitEvent(R.dev[d].s, done, 0));
+            CK(cudaEventRecord(R.dev[d].ev[(R.gen - 1) & 1], R.dev[d].s));
+            R.dev[d].launches += (uint64_t)g.launches * count;
+        }
+        R.evpool.push_back(done);
+        for (auto &kv : R.table) {
+            Region *r = kv.second.get();
+            r->valid = g.v_end[r];
+            r->dslot = g.slot_end[r];
+        }
+        R.comm_prev = g.comm_end;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_graph_destroy(int graph_id) {
+    return guard([&]() -> jacc_status {
+        auto it = R.graphs.find(graph_id);
+        if (it == R.graphs.end()) return JACC_ERR_INVALID;
+        destroy_graph(it->second);
+        R.graphs.erase(it);
+        return JACC_OK;
+    });
+}
 
 jacc_status jacc_adaptive_replay(int n, double peak_p2p, int len, const double *t_kernel,
                                  const double *t_comm, const double *write_size, int *states_out) {

@@ -36,6 +36,8 @@ JACC_LOOP_SUM_F64 = 4
 JACC_LOOP_GEMM_F64 = 5
 JACC_LOOP_SCATTER_ADD_F64 = 6
 JACC_LOOP_SCATTER_ADD_I32 = 7
+JACC_LOOP_HIMENO_F32 = 8
+JACC_LOOP_HIMENO_COPY_F32 = 9
 JACC_ARG_ARRAY_IN = 0
 JACC_ARG_ARRAY_OUT = 1
 JACC_ARG_ARRAY_INOUT = 2
@@ -53,6 +55,7 @@ EXPORTS = [
     "jacc_unique_id", "jacc_init_rank", "jacc_export_runtime", "jacc_import_runtime",
     "jacc_export_region", "jacc_import_region", "jacc_rank",
     "jacc_adaptive_replay", "jacc_adaptive_history",
+    "jacc_graph_begin", "jacc_graph_end", "jacc_graph_replay", "jacc_graph_destroy",
 ]
 JACC_MODE_ADAPTIVE = 2
 JACC_UNIQUE_ID_BYTES = 128
@@ -102,6 +105,10 @@ for _name, _args in {
     "jacc_export_region": [_P, _P, _SZ],
     "jacc_import_region": [_P, _I, _P, _SZ],
     "jacc_adaptive_replay": [_I, ctypes.c_double, _I, _P, _P, _P, _P],
+    "jacc_graph_begin": [],
+    "jacc_graph_end": [ctypes.POINTER(_I)],
+    "jacc_graph_replay": [_I, _I],
+    "jacc_graph_destroy": [_I],
     "jacc_adaptive_history": [_I, _I, _P, _P, _P, _P, ctypes.POINTER(_I), ctypes.POINTER(_I)],
 }.items():
     _f = getattr(lib, _name)
@@ -342,3 +349,22 @@ def jacc_adaptive_history(loop_id, cap=4096):
         "jacc_adaptive_history")
     m = min(ln.value, cap)
     return list(zip(tk[:m], tc[:m], ws[:m])), st[:m].tolist(), now.value
+
+
+# ---- CUDA graphs of launch sequences ------------------------------------------
+def jacc_graph_begin():
+    return _ck(lib.jacc_graph_begin(), "jacc_graph_begin")
+
+
+def jacc_graph_end():
+    g = ctypes.c_int()
+    _ck(lib.jacc_graph_end(ctypes.byref(g)), "jacc_graph_end")
+    return g.value
+
+
+def jacc_graph_replay(graph_id, count=1):
+    return _ck(lib.jacc_graph_replay(graph_id, count), "jacc_graph_replay")
+
+
+def jacc_graph_destroy(graph_id):
+    return _ck(lib.jacc_graph_destroy(graph_id), "jacc_graph_destroy")

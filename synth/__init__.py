@@ -32,6 +32,7 @@ def _load():
             "syn_int_i32": [P, I, I, U, U, I, I],
             "syn_permutation_i32": [P, I, U, U],
             "syn_polybench_jacobi2d": [P, P, I, I, I],
+            "syn_himeno_init": [P, P, P, P, P, P, I, I, I],
         }.items():
             f = getattr(lib, name)
             f.argtypes = args
@@ -103,3 +104,28 @@ def polybench_jacobi2d(N, A=None, B=None):
         B = np.empty((N, N), dtype=np.float64)
     _load().syn_polybench_jacobi2d(_ptr(A), _ptr(B), N, 0, N)
     return A, B
+
+
+def himeno_init(I, J, K):
+    """Himeno benchmark initial arrays (p, a[4], b[3], c[3], wrk1, bnd) for an
+    I x J x K grid, fp32 row-major."""
+    p = np.empty((I, J, K), np.float32)
+    a = np.empty((4, I, J, K), np.float32)
+    b = np.empty((3, I, J, K), np.float32)
+    c = np.empty((3, I, J, K), np.float32)
+    wrk1 = np.empty((I, J, K), np.float32)
+    bnd = np.empty((I, J, K), np.float32)
+    _load().syn_himeno_init(_ptr(p), _ptr(a), _ptr(b), _ptr(c), _ptr(wrk1), _ptr(bnd), I, J, K)
+    return p, a, b, c, wrk1, bnd
+
+
+def himeno_random(I, J, K, seed):
+    """Seeded random Himeno arrays (uniform [0,1) fp32) for parity tests."""
+    V = I * J * K
+    p = uniform_f32(V, seed, 20).reshape(I, J, K)
+    a = uniform_f32(4 * V, seed, 21).reshape(4, I, J, K)
+    b = uniform_f32(3 * V, seed, 22).reshape(3, I, J, K)
+    c = uniform_f32(3 * V, seed, 23).reshape(3, I, J, K)
+    wrk1 = uniform_f32(V, seed, 24).reshape(I, J, K)
+    bnd = uniform_f32(V, seed, 25).reshape(I, J, K)
+    return p, a, b, c, wrk1, bnd

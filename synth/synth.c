@@ -98,3 +98,25 @@ void syn_polybench_jacobi2d(double *A, double *B, int64_t N, int64_t row0, int64
         }
     }
 }
+
+/* Himeno benchmark initial state (himenoBMT initmt): a0..a2 = 1, a3 = 1/6,
+ * b = 0, c = 1, p[i][j][k] = (float)(i*i) / (float)((I-1)*(I-1)),
+ * wrk1 = 0, bnd = 1.  a: [4][I][J][K], b, c: [3][I][J][K]. */
+void syn_himeno_init(float *p, float *a, float *b, float *c, float *wrk1, float *bnd,
+                     int64_t I, int64_t J, int64_t K)
+{
+    const int64_t V = I * J * K, P = J * K;
+    const float den = (float)((I - 1) * (I - 1));
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < I; i++) {
+        const float pv = (float)(i * i) / den;
+        for (int64_t x = i * P; x < (i + 1) * P; x++) {
+            p[x] = pv;
+            a[x] = 1.0f; a[V + x] = 1.0f; a[2 * V + x] = 1.0f; a[3 * V + x] = (float)(1.0 / 6.0);
+            b[x] = 0.0f; b[V + x] = 0.0f; b[2 * V + x] = 0.0f;
+            c[x] = 1.0f; c[V + x] = 1.0f; c[2 * V + x] = 1.0f;
+            wrk1[x] = 0.0f;
+            bnd[x] = 1.0f;
+        }
+    }
+}

@@ -590,3 +590,154 @@ def test_adaptive_mode_parity_and_controller_replay(J, policy):
     assert len(trace) >= 2
     rep = ad.replay(trace, 2, 770e9)
     assert states == rep[:-1] and now == rep[-1]
+
+
+# --------------------------------------------------------------------------
+# NEXT-2 Himeno: 19-point stencil + gosa, copy loop
+# --------------------------------------------------------------------------
+def _himeno_gpu(J, arrs, nn, n, policy, omega=0.8, rng=None):
+    p, a, b, c, w1, bd = (x.copy() for x in arrs)
+    wrk2 = np.zeros_like(p)
+    gosas, dirt = [], []
+    with runtime(J, n, policy):
+        _create(J, p, a, b, c, w1, bd, wrk2)
+        IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+        for it in range(nn):
+            g = np.zeros(1)
+            J.jacc_launch(J.JACC_LOOP_HIMENO_F32, rng,
+                          [J.arg(IN, p), J.arg(IN, a), J.arg(IN, b), J.arg(IN, c), J.arg(IN, w1),
+                           J.arg(IN, bd), J.arg(OUT, wrk2), J.arg(J.JACC_ARG_REDUCE_SUM_F64, g),
+                           J.arg(J.JACC_ARG_SCALAR_F64, f64=omega)])
+            gosas.append(g[0])
+            if it == 0:
+                dirt.append([J.jacc_get_dirty_range(wrk2, d) for d in range(n)])
+            J.jacc_launch(J.JACC_LOOP_HIMENO_COPY_F32, rng, [J.arg(IN, wrk2), J.arg(OUT, p)], 0)
+            if it == 0:
+                dirt.append([J.jacc_get_dirty_range(p, d) for d in range(n)])
+        J.jacc_update_host(p)
+        J.jacc_update_host(wrk2)
+    return p, wrk2, gosas, dirt
+
+
+@pytest.mark.parametrize("shape", [(3, 3, 3), (9, 5, 7), (17, 12, 21), (34, 33, 35), (66, 40, 70)])
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_himeno_multi_device(J, shape, n, policy):
+    I, Jd, K = shape
+    arrs = synth.himeno_random(I, Jd, K, 95)
+    nn = 3
+    p, a, b, c, w1, bd = (x.copy() for x in arrs)
+    wrk2 = np.zeros_like(p)
+    refs, logs = [], []
+    for it in range(nn):
+        _, gref, wl = orc.himeno_stencil(p, a, b, c, w1, bd, wrk2)
+        refs.append(gref)
+        cl = orc.himeno_copy(wrk2, p)
+        if it == 0:
+            logs = (wl, cl)
+    gp, gw, gosas, dirt = _himeno_gpu(J, arrs, nn, n, policy)
+    assert np.array_equal(gp, p) and np.array_equal(gw, wrk2)
+    for g, r in zip(gosas, refs):
+        assert abs(g - r) <= 1e-12 * abs(r) + 1e-300
+    # per-device dirty ranges == oracle write logs of the filtered launches
+    p0, a0, b0, c0, w10, bd0 = arrs
+    for d in range(n):
+        lo, hi = orc.partition(I, n, d)
+        tmp = np.zeros_like(p0)
+        _, _, wl = orc.himeno_stencil(p0, a0, b0, c0, w10, bd0, tmp, planes=(lo, hi - 1))
+        assert dirt[0][d] == wl
+        cl = orc.himeno_copy(tmp, p0.copy(), planes=(lo, hi - 1))
+        assert dirt[1][d] == cl
+
+
+def test_himeno_subrange(J):
+    I, Jd, K = 20, 18, 22
+    arrs = synth.himeno_random(I, Jd, K, 96)
+    rng = J.make_range([3, 2, 5], [15, 17, 20])
+    gp, gw, gosas, _ = _himeno_gpu(J, arrs, 1, 2, 0, rng=rng)
+    p, a, b, c, w1, bd = (x.copy() for x in arrs)
+    full = np.zeros_like(p)
+    orc.himeno_stencil(p, a, b, c, w1, bd, full)
+    box = (slice(3, 15), slice(2, 17), slice(5, 20))
+    w_ref = np.zeros_like(p)
+    w_ref[box] = full[box]
+    assert np.array_equal(gw, w_ref)
+    p_ref = p.copy()
+    p_ref[box] = full[box]
+    assert np.array_equal(gp, p_ref)
+
+
+def test_himeno_XL_full_size(J):
+    """The paper's Size XL (1024x512x512) with the benchmark's
+    initial state, one iteration at n=1 (the bench launch configuration):
+    wrk2 and p bit-exact vs the oracle, gosa within 1e-12 of the compensated
+    reference."""
+    I, Jd, K = 1025, 513, 513
+    arrs = synth.himeno_init(I, Jd, K)
+    gp, gw, gosas, _ = _himeno_gpu(J, arrs, 1, 1, 0)
+    p, a, b, c, w1, bd = arrs
+    wrk2 = np.zeros_like(p)
+    g, gref, _ = orc.himeno_stencil(p, a, b, c, w1, bd, wrk2)
+    assert np.array_equal(gw, wrk2)
+    assert abs(gosas[0] - gref) <= 1e-12 * gref
+    orc.himeno_copy(wrk2, p)
+    assert np.array_equal(gp, p)
+
+
+# --------------------------------------------------------------------------
+# CUDA graphs of launch sequences
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [1, 3])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_graph_capture_replay_jacobi(J, n, policy):
+    """Capture one steady timestep (2 launches, merges included) and replay
+    it; interleave with plain launches; results equal the oracle."""
+    N = 301
+    A0 = synth.uniform_f64(N * N, 97, 1).reshape(N, N)
+    B0 = synth.uniform_f64(N * N, 97, 2).reshape(N, N)
+    A, B = A0.copy(), B0.copy()
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    ab, ba = [J.arg(IN, A), J.arg(OUT, B)], [J.arg(IN, B), J.arg(OUT, A)]
+
+    def step():
+        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, ab, 0)
+        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, ba, 0)
+
+    with runtime(J, n, policy):
+        _create(J, A, B)
+        step()                       # steady state
+        J.jacc_graph_begin()
+        step()                       # captured, not executed
+        gid = J.jacc_graph_end()
+        J.jacc_graph_replay(gid, 3)  # timesteps 2..4
+        step()                       # timestep 5 (plain)
+        J.jacc_graph_replay(gid, 1)  # timestep 6
+        J.jacc_update_host(A)
+        J.jacc_update_host(B)
+        J.jacc_graph_destroy(gid)
+    Ar, Br = A0.copy(), B0.copy()
+    orc.jacobi2d(6, Ar, Br)
+    assert np.array_equal(A, Ar) and np.array_equal(B, Br)
+
+
+def test_graph_rules(J):
+    N = 64
+    A = synth.uniform_f64(N * N, 98, 1).reshape(N, N)
+    B = synth.uniform_f64(N * N, 98, 2).reshape(N, N)
+    x = synth.dyadic_f64(1000, 98, 3)
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    with runtime(J, 2, 1):
+        _create(J, A, B, x)
+        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, A), J.arg(OUT, B)])
+        J.jacc_graph_begin()
+        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, B), J.arg(OUT, A)])
+        # reductions cannot be captured; synchronous calls are refused
+        st = J.jacc_launch_status(J.JACC_LOOP_SUM_F64, J.make_range(0, 1000),
+                                  [J.arg(IN, x), J.arg(J.JACC_ARG_REDUCE_SUM_F64, np.zeros(1))])
+        assert st == J.JACC_ERR_INVALID
+        assert J.lib.jacc_wait(-1) == J.JACC_ERR_STATE
+        gid = J.jacc_graph_end()
+        # a fresh upload of B (stale on the peer under HALO) changes the
+        # replica validity: replay refused
+        J.jacc_update_device(B)
+        assert J.lib.jacc_graph_replay(gid, 1) == J.JACC_ERR_STATE
