@@ -751,77 +751,91 @@ __global__ void __launch_bounds__(256) scat_pack_kernel(const uint8_t *__restric
 
 // ---------------------------------------------------------------------------
 // NEXT-2  Himeno (19-point stencil + gosa reduction, and the copy loop)
+//
+// Persistent fixed grid; a tile is 32 consecutive k x 8 j at one plane i,
+// tiles are walked k-fastest then j then i, so the CTAs in flight cover a
+// few consecutive planes and the p neighbours (planes i-1, i, i+1) are L2
+// hits while the 12 coefficient/aux arrays stream from HBM once.  Every
+// point issues its ~31 loads independently (high memory-level
+// parallelism).  gosa: fp32 terms ss*ss accumulated in fp64 per thread,
+// reduced in a fixed order (fixed grid -> deterministic).
 // ---------------------------------------------------------------------------
-constexpr int HX = 32, HY = 8;  // block: 32 k x 8 j, marching over i
+constexpr int HX = 32, HY = 8, HT = HX * HY;
+constexpr int kHimenoGrid = 148 * 8;  // <= kHimenoPartials
 
-__global__ void __launch_bounds__(HX * HY) himeno_stencil_kernel(
+__device__ __forceinline__ void publish_dirty_flat(u64 mn, u64 mx, u64 *dirty) {
+    // publish_dirty for 1-D launches of HT threads (clears the other slot)
+    publish_dirty<HT / 32>(mn, mx, dirty);
+}
+
+__global__ void __launch_bounds__(HT) himeno_stencil_kernel(
     const float *__restrict__ p, const float *__restrict__ a, const float *__restrict__ b,
     const float *__restrict__ c, const float *__restrict__ wrk1, const float *__restrict__ bnd,
     float *__restrict__ wrk2, int64_t I, int64_t J, int64_t K, int64_t i0, int64_t i1, int64_t j0,
     int64_t j1, int64_t k0, int64_t k1, float omega, double *partials, unsigned *ticket,
     double *out, u64 *dirty) {
-    __shared__ double sh[HX * HY / 32];
+    __shared__ double sh[HT / 32];
     __shared__ bool last;
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int tid = ty * HX + tx;
-    const int64_t k = k0 + (int64_t)blockIdx.x * HX + tx;
-    const int64_t j = j0 + (int64_t)blockIdx.y * HY + ty;
-    const int64_t P = J * K, V = I * J * K;  // plane stride, array stride
-    const int64_t ni = i1 - i0;
-    const int64_t chunk = (ni + gridDim.z - 1) / gridDim.z;
-    const int64_t ia = i0 + (int64_t)blockIdx.z * chunk;
-    const int64_t ib = ia + chunk < i1 ? ia + chunk : i1;
+    const int tid = threadIdx.x;
+    const int tx = tid % HX, ty = tid / HX;
+    const int64_t P = J * K, V = I * J * K;
+    const float *a0 = a, *a1 = a + V, *a2 = a + 2 * V, *a3 = a + 3 * V;
+    const float *b0 = b, *b1 = b + V, *b2 = b + 2 * V;
+    const float *c0 = c, *c1 = c + V, *c2 = c + 2 * V;
+    const int64_t nkt = (k1 - k0 + HX - 1) / HX, njt = (j1 - j0 + HY - 1) / HY;
+    const int64_t ntiles = nkt * njt * (i1 - i0);
     double g = 0.0;
     u64 mn = kU64Max, mx = 0;
-    if (k < k1 && j < j1) {
-        for (int64_t i = ia; i < ib; i++) {
-            const int64_t x = i * P + j * K + k;
-            const float *q = p + x;
-            float t;
-            // s0 exactly as written, left to right, no contraction
-            float s0 = __fmul_rn(__ldcs(a + x), __ldg(q + P));
-            s0 = __fadd_rn(s0, __fmul_rn(__ldcs(a + V + x), __ldg(q + K)));
-            s0 = __fadd_rn(s0, __fmul_rn(__ldcs(a + 2 * V + x), __ldg(q + 1)));
-            t = __fadd_rn(__fsub_rn(__fsub_rn(__ldg(q + P + K), __ldg(q + P - K)), __ldg(q - P + K)),
-                          __ldg(q - P - K));
-            s0 = __fadd_rn(s0, __fmul_rn(__ldcs(b + x), t));
-            t = __fadd_rn(__fsub_rn(__fsub_rn(__ldg(q + K + 1), __ldg(q - K + 1)), __ldg(q + K - 1)),
-                          __ldg(q - K - 1));
-            s0 = __fadd_rn(s0, __fmul_rn(__ldcs(b + V + x), t));
-            t = __fadd_rn(__fsub_rn(__fsub_rn(__ldg(q + P + 1), __ldg(q - P + 1)), __ldg(q + P - 1)),
-                          __ldg(q - P - 1));
-            s0 = __fadd_rn(s0, __fmul_rn(__ldcs(b + 2 * V + x), t));
-            s0 = __fadd_rn(s0, __fmul_rn(__ldcs(c + x), __ldg(q - P)));
-            s0 = __fadd_rn(s0, __fmul_rn(__ldcs(c + V + x), __ldg(q - K)));
-            s0 = __fadd_rn(s0, __fmul_rn(__ldcs(c + 2 * V + x), __ldg(q - 1)));
-            s0 = __fadd_rn(s0, __ldcs(wrk1 + x));
-            const float p0 = __ldg(q);
-            const float ss = __fmul_rn(__fsub_rn(__fmul_rn(s0, __ldcs(a + 3 * V + x)), p0), __ldcs(bnd + x));
-            g += (double)__fmul_rn(ss, ss);
-            __stcs(wrk2 + x, __fadd_rn(p0, __fmul_rn(omega, ss)));
-            mn = (u64)x < mn ? (u64)x : mn;
-            mx = (u64)x > mx ? (u64)x : mx;
-        }
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t kt = t % nkt, r = t / nkt;
+        const int64_t jt = r % njt, i = i0 + r / njt;
+        const int64_t k = k0 + kt * HX + tx, j = j0 + jt * HY + ty;
+        if (k >= k1 || j >= j1) continue;
+        const int64_t x = i * P + j * K + k;
+        const float *q = p + x;
+        // all loads independent; arithmetic exactly as written, no contraction
+        const float pip = __ldg(q + P), pjp = __ldg(q + K), pkp = __ldg(q + 1);
+        const float pim = __ldg(q - P), pjm = __ldg(q - K), pkm = __ldg(q - 1), p0 = __ldg(q);
+        const float q1 = __ldg(q + P + K), q2 = __ldg(q + P - K), q3 = __ldg(q - P + K), q4 = __ldg(q - P - K);
+        const float q5 = __ldg(q + K + 1), q6 = __ldg(q - K + 1), q7 = __ldg(q + K - 1), q8 = __ldg(q - K - 1);
+        const float q9 = __ldg(q + P + 1), q10 = __ldg(q - P + 1), q11 = __ldg(q + P - 1), q12 = __ldg(q - P - 1);
+        const float va0 = __ldcs(a0 + x), va1 = __ldcs(a1 + x), va2 = __ldcs(a2 + x), va3 = __ldcs(a3 + x);
+        const float vb0 = __ldcs(b0 + x), vb1 = __ldcs(b1 + x), vb2 = __ldcs(b2 + x);
+        const float vc0 = __ldcs(c0 + x), vc1 = __ldcs(c1 + x), vc2 = __ldcs(c2 + x);
+        const float vw = __ldcs(wrk1 + x), vbnd = __ldcs(bnd + x);
+        float s0 = __fmul_rn(va0, pip);
+        s0 = __fadd_rn(s0, __fmul_rn(va1, pjp));
+        s0 = __fadd_rn(s0, __fmul_rn(va2, pkp));
+        s0 = __fadd_rn(s0, __fmul_rn(vb0, __fadd_rn(__fsub_rn(__fsub_rn(q1, q2), q3), q4)));
+        s0 = __fadd_rn(s0, __fmul_rn(vb1, __fadd_rn(__fsub_rn(__fsub_rn(q5, q6), q7), q8)));
+        s0 = __fadd_rn(s0, __fmul_rn(vb2, __fadd_rn(__fsub_rn(__fsub_rn(q9, q10), q11), q12)));
+        s0 = __fadd_rn(s0, __fmul_rn(vc0, pim));
+        s0 = __fadd_rn(s0, __fmul_rn(vc1, pjm));
+        s0 = __fadd_rn(s0, __fmul_rn(vc2, pkm));
+        s0 = __fadd_rn(s0, vw);
+        const float ss = __fmul_rn(__fsub_rn(__fmul_rn(s0, va3), p0), vbnd);
+        g += (double)__fmul_rn(ss, ss);
+        __stcs(wrk2 + x, __fadd_rn(p0, __fmul_rn(omega, ss)));
+        mn = (u64)x < mn ? (u64)x : mn;
+        mx = (u64)x > mx ? (u64)x : mx;
     }
-    // fixed-order reduction: warp, block, then the last block over all blocks
-    const unsigned nblk = gridDim.x * gridDim.y * gridDim.z;
-    const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    // fixed-order reduction: warp, block, then the last block over the grid
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) g += __shfl_down_sync(0xffffffffu, g, o);
     if ((tid & 31) == 0) sh[tid >> 5] = g;
     __syncthreads();
     if (tid == 0) {
         double v = 0.0;
-        for (int w = 0; w < HX * HY / 32; w++) v += sh[w];
-        partials[bid] = v;
+        for (int w = 0; w < HT / 32; w++) v += sh[w];
+        partials[blockIdx.x] = v;
         __threadfence();
-        last = atomicAdd(ticket, 1u) == nblk - 1;
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (last) {
         __threadfence();
         double v = 0.0;
-        for (unsigned i = tid; i < nblk; i += HX * HY) v += __ldcg(partials + i);
+        for (unsigned i = tid; i < gridDim.x; i += HT) v += __ldcg(partials + i);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
         __syncthreads();
@@ -829,91 +843,52 @@ __global__ void __launch_bounds__(HX * HY) himeno_stencil_kernel(
         __syncthreads();
         if (tid == 0) {
             double tot = 0.0;
-            for (int w = 0; w < HX * HY / 32; w++) tot += sh[w];
+            for (int w = 0; w < HT / 32; w++) tot += sh[w];
             *out = tot;
             *ticket = 0u;
         }
     }
-    // dirty range of wrk2 (1-D block index for publish_dirty's reset)
-    __shared__ u64 smn[HX * HY / 32], smx[HX * HY / 32];
-    mn = warp_min_u64(mn);
-    mx = warp_max_u64(mx);
-    if ((tid & 31) == 0) {
-        smn[tid >> 5] = mn;
-        smx[tid >> 5] = mx;
-    }
-    if (bid == 0 && tid == 0) {
-        u64 *nx = reinterpret_cast<u64 *>(reinterpret_cast<uintptr_t>(dirty) ^ 16u);
-        nx[0] = kU64Max;
-        nx[1] = kU64Max;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        u64 lo = smn[0], hi = smx[0];
-        for (int w = 1; w < HX * HY / 32; w++) {
-            lo = smn[w] < lo ? smn[w] : lo;
-            hi = smx[w] > hi ? smx[w] : hi;
-        }
-        if (lo != kU64Max) {
-            atomicMin(&dirty[0], lo);
-            atomicMin(&dirty[1], ~hi);
-        }
-    }
+    publish_dirty_flat(mn, mx, dirty);
 }
 
-__global__ void __launch_bounds__(HX * HY) himeno_copy_kernel(
+// copy loop: one warp per (i, j) row of the box, 4 independent loads in
+// flight per lane
+__global__ void __launch_bounds__(HT) himeno_copy_kernel(
     const float *__restrict__ wrk2, float *__restrict__ p, int64_t J, int64_t K, int64_t i0,
     int64_t i1, int64_t j0, int64_t j1, int64_t k0, int64_t k1, u64 *dirty, float *push_top,
     float *push_bot) {
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t k = k0 + (int64_t)blockIdx.x * HX + tx;
-    const int64_t j = j0 + (int64_t)blockIdx.y * HY + ty;
+    const int lane = threadIdx.x & 31;
     const int64_t P = J * K;
-    const int64_t ni = i1 - i0;
-    const int64_t chunk = (ni + gridDim.z - 1) / gridDim.z;
-    const int64_t ia = i0 + (int64_t)blockIdx.z * chunk;
-    const int64_t ib = ia + chunk < i1 ? ia + chunk : i1;
+    const int64_t nj = j1 - j0, rows = (i1 - i0) * nj, len = k1 - k0;
+    const int64_t wg = ((int64_t)blockIdx.x * HT + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * HT) >> 5;
     u64 mn = kU64Max, mx = 0;
-    if (k < k1 && j < j1) {
-        for (int64_t i = ia; i < ib; i++) {
-            const int64_t x = i * P + j * K + k;
-            const float v = __ldcs(wrk2 + x);
-            __stcs(p + x, v);
-            if (i == i0 && push_top) push_top[x] = v;
-            if (i == i1 - 1 && push_bot) push_bot[x] = v;
-            mn = (u64)x < mn ? (u64)x : mn;
-            mx = (u64)x > mx ? (u64)x : mx;
+    for (int64_t r = wg; r < rows; r += nw) {
+        const int64_t i = i0 + r / nj, j = j0 + r % nj;
+        const int64_t base = i * P + j * K + k0;
+        float *tp = (i == i0) ? push_top : nullptr;
+        float *bp = (i == i1 - 1) ? push_bot : nullptr;
+        for (int64_t kk = lane; kk < len; kk += 128) {
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (kk + 32 * u < len) v[u] = __ldcs(wrk2 + base + kk + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (kk + 32 * u < len) {
+                    const int64_t x = base + kk + 32 * u;
+                    __stcs(p + x, v[u]);
+                    if (tp) tp[x] = v[u];
+                    if (bp) bp[x] = v[u];
+                }
+        }
+        if (len > 0) {
+            mn = (u64)base < mn ? (u64)base : mn;
+            mx = (u64)(base + len - 1) > mx ? (u64)(base + len - 1) : mx;
         }
     }
-    // publish (reset of the other slot keyed on the flattened block id)
-    __shared__ u64 smn[HX * HY / 32], smx[HX * HY / 32];
-    const int tid = ty * HX + tx;
-    const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    mn = warp_min_u64(mn);
-    mx = warp_max_u64(mx);
-    if ((tid & 31) == 0) {
-        smn[tid >> 5] = mn;
-        smx[tid >> 5] = mx;
-    }
-    if (bid == 0 && tid == 0) {
-        u64 *nx = reinterpret_cast<u64 *>(reinterpret_cast<uintptr_t>(dirty) ^ 16u);
-        nx[0] = kU64Max;
-        nx[1] = kU64Max;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        u64 lo = smn[0], hi = smx[0];
-        for (int w = 1; w < HX * HY / 32; w++) {
-            lo = smn[w] < lo ? smn[w] : lo;
-            hi = smx[w] > hi ? smx[w] : hi;
-        }
-        if (lo != kU64Max) {
-            atomicMin(&dirty[0], lo);
-            atomicMin(&dirty[1], ~hi);
-        }
-    }
+    publish_dirty_flat(mn, mx, dirty);
 }
-
 // ---------------------------------------------------------------------------
 // BK5  merges over peer memory (NVLink P2P stores; plain stores for virtual
 // devices that share one GPU)
@@ -1124,26 +1099,14 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
 }
 
 
-static dim3 himeno_grid(int64_t ni, int64_t nj, int64_t nk, int64_t max_blocks) {
-    const int64_t gx = (nk + HX - 1) / HX, gy = (nj + HY - 1) / HY;
-    int64_t gz = (ni + 7) / 8;  // ~8 planes per block
-    const int64_t cap = max_blocks / (gx * gy) > 0 ? max_blocks / (gx * gy) : 1;
-    if (gz > cap) gz = cap;
-    if (gz > 65535) gz = 65535;
-    if (gz < 1) gz = 1;
-    return dim3((unsigned)gx, (unsigned)gy, (unsigned)gz);
-}
-
 cudaError_t himeno_stencil(cudaStream_t s, const float *p, const float *a, const float *b,
                            const float *c, const float *wrk1, const float *bnd, float *wrk2,
                            int64_t I, int64_t J, int64_t K, int64_t i0, int64_t i1, int64_t j0,
                            int64_t j1, int64_t k0, int64_t k1, float omega, double *partials,
                            unsigned *ticket, double *out, u64 *dirty) {
     if (i1 <= i0 || j1 <= j0 || k1 <= k0) return cudaErrorInvalidValue;
-    if (((j1 - j0 + HY - 1) / HY) * ((k1 - k0 + HX - 1) / HX) > kHimenoPartials)
-        return cudaErrorInvalidValue;  // plane too large for the partials buffer
-    const dim3 g = himeno_grid(i1 - i0, j1 - j0, k1 - k0, kHimenoPartials);
-    himeno_stencil_kernel<<<g, dim3(HX, HY), 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0, i1,
+    static_assert(kHimenoGrid <= kHimenoPartials, "partials buffer");
+    himeno_stencil_kernel<<<kHimenoGrid, HT, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0, i1,
                                                      j0, j1, k0, k1, omega, partials, ticket, out,
                                                      dirty);
     return cudaGetLastError();
@@ -1154,8 +1117,7 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
                         int64_t k1, u64 *dirty, float *push_top, float *push_bot) {
     (void)I;
     if (i1 <= i0 || j1 <= j0 || k1 <= k0) return cudaErrorInvalidValue;
-    const dim3 g = himeno_grid(i1 - i0, j1 - j0, k1 - k0, 1 << 20);
-    himeno_copy_kernel<<<g, dim3(HX, HY), 0, s>>>(wrk2, p, J, K, i0, i1, j0, j1, k0, k1, dirty,
+    himeno_copy_kernel<<<kHimenoGrid, HT, 0, s>>>(wrk2, p, J, K, i0, i1, j0, j1, k0, k1, dirty,
                                                   push_top, push_bot);
     return cudaGetLastError();
 }

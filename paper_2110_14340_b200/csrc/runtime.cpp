@@ -932,9 +932,12 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         Device &dv = R.dev[d];
         const DevPlan &p = L.plan[d];
         set_dev(d);
-        for (int q = 0; q < n; q++)
-            if (q != d && (comm[d][q] || R.comm_prev[d][q]))
-                CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
+        // (the first launch of a capture skips them: every earlier launch is
+        // complete and its events live outside the graph)
+        if (!(R.capturing && R.cap.launches == 0))
+            for (int q = 0; q < n; q++)
+                if (q != d && (comm[d][q] || R.comm_prev[d][q]))
+                    CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
         for (const Pull &pl : pulls) {
             if (pl.dst != d) continue;
             const size_t e = pl.reg->elem;

@@ -63,6 +63,21 @@ def main():
         for _ in range(reps):
             J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, J.make_range(0, S),
                           [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)], 0)
+    elif which == "himeno":
+        I, Jd, K = 1025, 513, 513
+        arrs = synth.himeno_init(I, Jd, K)
+        w2 = np.zeros_like(arrs[0])
+        for arr in list(arrs) + [w2]:
+            J.jacc_data_create(arr)
+            J.jacc_update_device(arr)
+        hp, ha, hb, hc, hw1, hbd = arrs
+        g = np.zeros(1)
+        for _ in range(reps):
+            J.jacc_launch(J.JACC_LOOP_HIMENO_F32, None,
+                          [J.arg(IN, hp), J.arg(IN, ha), J.arg(IN, hb), J.arg(IN, hc), J.arg(IN, hw1),
+                           J.arg(IN, hbd), J.arg(OUT, w2), J.arg(J.JACC_ARG_REDUCE_SUM_F64, g),
+                           J.arg(J.JACC_ARG_SCALAR_F64, f64=0.8)])
+            J.jacc_launch(J.JACC_LOOP_HIMENO_COPY_F32, None, [J.arg(IN, w2), J.arg(OUT, hp)], 0)
     J.jacc_wait()
     J.jacc_finalize()
 
