@@ -107,6 +107,28 @@ jacc_status jacc_set_mode(int mode);
  * E < 0, n < 1, d outside [0, n) or NULL outputs. */
 jacc_status jacc_partition(int64_t E, int n, int d, int64_t *lo, int64_t *hi);
 
+/* A18 parallel-dimension selection: n_parallel[k] /
+ * n_sequential[k] = number of parallel / sequential loop iterators in the
+ * index expression of dimension k of an updated array.  *dim = the
+ * dimension with the most parallel iterators, among those the fewest
+ * sequential ones, ties to the leftmost (C, fortran_order = 0) or rightmost
+ * (Fortran); -1 when no dimension holds a parallel iterator (the array is
+ * computed in duplicate).  Pure host logic.  Errors: JACC_ERR_INVALID. */
+jacc_status jacc_select_split_dim(int ndims, const int *n_parallel, const int *n_sequential,
+                                  int fortran_order, int *dim);
+
+/* A19 exchange plan ("GPU-to-GPU communication through
+ * cudaMemcpy2DAsync"): device d's owned block along split_dim of a
+ * row-major array (extents[0..ndims), elem bytes) as `count` pitched 2-D
+ * copies; copy c, row r (r < height) covers the bytes
+ * [first + c*outer + r*pitch, + width).  split_dim 0 gives one contiguous
+ * copy; an empty block gives count 0.  Pure host logic. */
+typedef struct {
+    int64_t count, height, width_bytes, pitch_bytes, first_offset_bytes, outer_stride_bytes;
+} jacc_copy2d_plan;
+jacc_status jacc_exchange_plan(int ndims, const int64_t *extents, size_t elem, int split_dim, int n,
+                               int d, jacc_copy2d_plan *out);
+
 /* ---------------------------------------------------------------------- */
 /* Present table ("managed in a red-black tree ... to accept any */
 /* address of declared data")                       */

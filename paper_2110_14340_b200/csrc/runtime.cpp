@@ -432,6 +432,33 @@ void partition(int64_t E, int n, int d, int64_t &lo, int64_t &hi) {
     hi = (int64_t)(d + 1) * q + std::min<int64_t>(d + 1, r);
 }
 
+// A19: device d's block [lo, hi) along split dimension s of a
+// row-major array decomposes into `count` 2-D copies (cudaMemcpy2D-shaped):
+// copy c, row r covers bytes [first + c*outer + r*pitch, ... + width).
+struct Copy2D {
+    int64_t count = 0, height = 0, width = 0, pitch = 0, first = 0, outer = 0;
+};
+
+Copy2D copy2d_plan(int ndims, const int64_t *ext, int64_t elem, int s, int64_t lo, int64_t hi) {
+    Copy2D c;
+    if (hi <= lo) return c;
+    int64_t inner = 1;
+    for (int k = s + 1; k < ndims; k++) inner *= ext[k];
+    c.width = (hi - lo) * inner * elem;
+    c.first = lo * inner * elem;
+    if (s == 0) {
+        c.count = c.height = 1;
+        c.pitch = c.outer = c.width;
+        return c;
+    }
+    c.height = ext[s - 1];
+    c.pitch = ext[s] * inner * elem;
+    c.outer = c.height * c.pitch;
+    c.count = 1;
+    for (int k = 0; k < s - 1; k++) c.count *= ext[k];
+    return c;
+}
+
 // ---------------------------------------------------------------------------
 // loop descriptors (D12) and per-device plans
 // ---------------------------------------------------------------------------
@@ -1324,6 +1351,48 @@ jacc_status jacc_finalize(void) {
 }
 
 int jacc_num_devices(void) { return R.init ? R.n : 0; }
+
+jacc_status jacc_select_split_dim(int ndims, const int *n_parallel, const int *n_sequential,
+                                  int fortran_order, int *dim) {
+    if (ndims < 1 || !n_parallel || !n_sequential || !dim) return JACC_ERR_INVALID;
+    int best = 0;
+    for (int k = 0; k < ndims; k++) best = std::max(best, n_parallel[k]);
+    if (best == 0) {
+        *dim = -1;  // no parallel dimension: duplicate
+        return JACC_OK;
+    }
+    int pick = -1, fewest = 0;
+    for (int k = 0; k < ndims; k++) {
+        if (n_parallel[k] != best) continue;
+        // strictly fewer sequential iterators wins; ties keep the leftmost
+        // (C) or take the later one (Fortran: rightmost)
+        if (pick < 0 || n_sequential[k] < fewest || (fortran_order && n_sequential[k] == fewest)) {
+            pick = k;
+            fewest = n_sequential[k];
+        }
+    }
+    *dim = pick;
+    return JACC_OK;
+}
+
+jacc_status jacc_exchange_plan(int ndims, const int64_t *extents, size_t elem, int split_dim, int n,
+                               int d, jacc_copy2d_plan *out) {
+    if (ndims < 1 || ndims > 8 || !extents || elem == 0 || split_dim < 0 || split_dim >= ndims ||
+        n < 1 || d < 0 || d >= n || !out)
+        return JACC_ERR_INVALID;
+    for (int k = 0; k < ndims; k++)
+        if (extents[k] < 1) return JACC_ERR_INVALID;
+    int64_t lo, hi;
+    partition(extents[split_dim], n, d, lo, hi);
+    const Copy2D c = copy2d_plan(ndims, extents, (int64_t)elem, split_dim, lo, hi);
+    out->count = c.count;
+    out->height = c.height;
+    out->width_bytes = c.width;
+    out->pitch_bytes = c.pitch;
+    out->first_offset_bytes = c.first;
+    out->outer_stride_bytes = c.outer;
+    return JACC_OK;
+}
 
 jacc_status jacc_partition(int64_t E, int n, int d, int64_t *lo, int64_t *hi) {
     if (E < 0 || n < 1 || d < 0 || d >= n || !lo || !hi) return JACC_ERR_INVALID;

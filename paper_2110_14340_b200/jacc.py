@@ -56,6 +56,7 @@ EXPORTS = [
     "jacc_export_region", "jacc_import_region", "jacc_rank",
     "jacc_adaptive_replay", "jacc_adaptive_history",
     "jacc_graph_begin", "jacc_graph_end", "jacc_graph_replay", "jacc_graph_destroy",
+    "jacc_select_split_dim", "jacc_exchange_plan",
 ]
 JACC_MODE_ADAPTIVE = 2
 JACC_UNIQUE_ID_BYTES = 128
@@ -65,6 +66,11 @@ JACC_REGION_HANDLE_BYTES = 64
 
 class jacc_range(ctypes.Structure):
     _fields_ = [("ndims", ctypes.c_int), ("lo", ctypes.c_int64 * 3), ("hi", ctypes.c_int64 * 3)]
+
+
+class jacc_copy2d_plan(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in ("count", "height", "width_bytes", "pitch_bytes",
+                                              "first_offset_bytes", "outer_stride_bytes")]
 
 
 class jacc_arg(ctypes.Structure):
@@ -106,6 +112,9 @@ for _name, _args in {
     "jacc_import_region": [_P, _I, _P, _SZ],
     "jacc_adaptive_replay": [_I, ctypes.c_double, _I, _P, _P, _P, _P],
     "jacc_graph_begin": [],
+    "jacc_select_split_dim": [_I, ctypes.POINTER(_I), ctypes.POINTER(_I), _I, ctypes.POINTER(_I)],
+    "jacc_exchange_plan": [_I, ctypes.POINTER(ctypes.c_int64), _SZ, _I, _I, _I,
+                           ctypes.POINTER(jacc_copy2d_plan)],
     "jacc_graph_end": [ctypes.POINTER(_I)],
     "jacc_graph_replay": [_I, _I],
     "jacc_graph_destroy": [_I],
@@ -368,3 +377,22 @@ def jacc_graph_replay(graph_id, count=1):
 
 def jacc_graph_destroy(graph_id):
     return _ck(lib.jacc_graph_destroy(graph_id), "jacc_graph_destroy")
+
+
+# ---- A18 / A19 division of multidimensional arrays ---------------------------
+def jacc_select_split_dim(n_parallel, n_sequential, fortran=False):
+    nd = len(n_parallel)
+    par = (ctypes.c_int * nd)(*n_parallel)
+    seq = (ctypes.c_int * nd)(*n_sequential)
+    d = ctypes.c_int()
+    _ck(lib.jacc_select_split_dim(nd, par, seq, 1 if fortran else 0, ctypes.byref(d)),
+        "jacc_select_split_dim")
+    return d.value
+
+
+def jacc_exchange_plan(extents, elem, split_dim, n, d):
+    ext = (ctypes.c_int64 * len(extents))(*extents)
+    out = jacc_copy2d_plan()
+    _ck(lib.jacc_exchange_plan(len(extents), ext, elem, split_dim, n, d, ctypes.byref(out)),
+        "jacc_exchange_plan")
+    return {k: getattr(out, k) for k, _ in jacc_copy2d_plan._fields_}
