@@ -100,6 +100,17 @@ jacc_status jacc_set_merge_policy(int policy);
 enum { JACC_MODE_MULTI = 0, JACC_MODE_DUP = 1, JACC_MODE_ADAPTIVE = 2 };
 jacc_status jacc_set_mode(int mode);
 
+/* Split dimension of the written array for the multidimensional loops
+ * (Jacobi-2D, GEMM, Himeno): -1 (default) applies the P:524-525 rule, which
+ * for these loop bodies selects dim 0 (contiguous row / plane blocks, fused
+ * boundary pushes); dim 1 or 2 divides columns / the innermost dimension
+ * instead: every device's block is then strided, write sets
+ * are boxes, and merges are pitched box copies over peer memory
+ * (EAGER: the dirty box; HALO: the boundary slabs).  Other loops are 1-D
+ * and always split dim 0.  Errors: JACC_ERR_INVALID outside [-1, 2]; a
+ * launch whose written array has no such dimension: JACC_ERR_INVALID. */
+jacc_status jacc_set_split_dim(int dim);
+
 /* Owned block [lo, hi) of logical device d when an extent E is split over
  * n devices: "equally dividing parallel dimensions among GPUs",
  * the first E mod n blocks one element larger (R-2).  Pure host

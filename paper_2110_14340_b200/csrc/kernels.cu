@@ -931,6 +931,33 @@ __global__ void __launch_bounds__(256) merge_range_kernel(const char *__restrict
     }
 }
 
+
+template <typename T>
+__global__ void __launch_bounds__(256) merge_box_kernel(const char *__restrict__ src, PeerPtrs dsts,
+                                                        Box2D b, const u64 *dirty) {
+    int64_t ds = 0, de = INT64_MAX;
+    if (dirty) {
+        const u64 dmin = dirty[0], dmax = ~dirty[1];
+        if (dmin > dmax) return;
+        ds = (int64_t)dmin * (int64_t)sizeof(T);
+        de = ((int64_t)dmax + 1) * (int64_t)sizeof(T);
+    }
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = b.count * b.height;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < rows; r += nw) {
+        const int64_t off = b.first + (r / b.height) * b.outer + (r % b.height) * b.pitch;
+        const int64_t a = off > ds ? off : ds;
+        const int64_t e = off + b.width < de ? off + b.width : de;
+        for (int64_t x = a + lane * (int64_t)sizeof(T); x < e; x += 32 * (int64_t)sizeof(T)) {
+            const T v = *reinterpret_cast<const T *>(src + x);
+            for (int d = 0; d < dsts.n; d++)
+                *reinterpret_cast<T *>(static_cast<char *>(dsts.p[d]) + x) = v;
+        }
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) merge_bitmap_kernel(const T *__restrict__ src, PeerPtrs dsts,
                                                            const uint32_t *__restrict__ bitmap,
@@ -1183,6 +1210,19 @@ cudaError_t merge_range(cudaStream_t s, const void *src, PeerPtrs dsts, const u6
     if (hi <= lo || dsts.n == 0) return cudaSuccess;
     merge_range_kernel<<<grid_for((hi - lo) * elem, 256 * 16 * 4, 148 * 8), 256, 0, s>>>(
         static_cast<const char *>(src), dsts, dirty, elem, lo, hi);
+    return cudaGetLastError();
+}
+
+cudaError_t merge_box(cudaStream_t s, const void *src, PeerPtrs dsts, Box2D b, const u64 *dirty,
+                      int64_t elem) {
+    if (b.count <= 0 || b.height <= 0 || b.width <= 0 || dsts.n == 0) return cudaSuccess;
+    const int g = grid_for(b.count * b.height, 8, 148 * 8);  // 8 warps per block, warp per row
+    if (elem == 8)
+        merge_box_kernel<double><<<g, 256, 0, s>>>(static_cast<const char *>(src), dsts, b, dirty);
+    else if (elem == 4)
+        merge_box_kernel<float><<<g, 256, 0, s>>>(static_cast<const char *>(src), dsts, b, dirty);
+    else
+        return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 

@@ -98,6 +98,16 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
 // every peer replica; `max_elems` bounds the grid (host-known write bound).
 cudaError_t merge_range(cudaStream_t s, const void *src, PeerPtrs dsts, const u64 *dirty,
                         int64_t elem, int64_t lo, int64_t hi);
+// merge_box copies a strided box (2-D or 3-D sub-box of a row-major array,
+// described as `count` pitched 2-D copies, all in bytes) from src to every
+// peer, restricted to the device-recorded dirty span when dirty != nullptr
+// (split dimensions > 0: the paper's cudaMemcpy2DAsync exchange
+// done with peer stores).
+struct Box2D {
+    int64_t count, height, width, pitch, first, outer;
+};
+cudaError_t merge_box(cudaStream_t s, const void *src, PeerPtrs dsts, Box2D b, const u64 *dirty,
+                      int64_t elem);
 // merge_bitmap copies exactly the elements whose dirty bit is set within
 // [lo, hi) into every peer replica (elem = 4 or 8 bytes).
 cudaError_t merge_bitmap(cudaStream_t s, const void *src, PeerPtrs dsts, const uint32_t *bitmap,

@@ -216,6 +216,7 @@ struct Runtime {
     std::map<uintptr_t, std::unique_ptr<Region>> table;
     int policy = JACC_MERGE_EAGER;
     int mode = JACC_MODE_MULTI;
+    int split_dim = -1;  // -1: A18 rule (dim 0 for the built-in loops)
     int gen = 0;
     bool distinct = true;
     bool use_nccl = false;
@@ -476,6 +477,9 @@ struct Foot {  // read footprint: region, element interval
 struct DevPlan {
     bool active = false;
     int64_t i0 = 0, i1 = 0, j0 = 0, j1 = 0;  // iteration sub-range
+    int64_t k0 = 0, k1 = 0;                  // (3-D loops)
+    int64_t blo[3] = {0, 0, 0}, bhi[3] = {0, 0, 0};  // write box (box loops)
+    std::vector<std::pair<int64_t, int64_t>> wbox;   // exact write intervals (split dim > 0)
     int64_t wlo = 0, whi = 0;                // write bound (elements of written region), [wlo,whi)
     int64_t own_lo = 0, own_hi = 0;          // owned block of the split extent
     std::vector<Foot> reads;
@@ -532,8 +536,162 @@ struct Launch {
     int64_t N = 0;             // jacobi grid
     int64_t M = 0, Nn = 0, K = 0;  // gemm
     int64_t HI = 0, HJ = 0, HK = 0;  // himeno grid
+    int split = 0;                   // split dimension of the written array (A18)
     double scalar = 0;               // SCALAR_F64 argument (himeno omega)
 };
+
+// Element intervals of the box [lo, hi) (per dim) of a row-major array with
+// extents ext[0..nd); dims fully covered at the tail collapse into one
+// contiguous run, so a box of whole rows / planes is a single interval.
+void box_intervals(int nd, const int64_t *ext, const int64_t *lo, const int64_t *hi, int64_t base,
+                   std::vector<std::pair<int64_t, int64_t>> &out) {
+    for (int k = 0; k < nd; k++)
+        if (hi[k] <= lo[k]) return;
+    // t = first dim from which the box is contiguous
+    int t = nd - 1;
+    while (t > 0 && lo[t] == 0 && hi[t] == ext[t]) t--;
+    int64_t inner = 1;
+    for (int k = t + 1; k < nd; k++) inner *= ext[k];
+    int64_t idx[8];
+    for (int k = 0; k < t; k++) idx[k] = lo[k];
+    for (;;) {
+        int64_t f = 0;
+        for (int k = 0; k < t; k++) f = f * ext[k] + idx[k];
+        f = f * ext[t];
+        const int64_t a = base + (f + lo[t]) * inner, b = base + (f + hi[t]) * inner;
+        if (!out.empty() && out.back().second == a) out.back().second = b;
+        else out.push_back({a, b});
+        int k = t - 1;
+        for (; k >= 0; k--) {
+            if (++idx[k] < hi[k]) break;
+            idx[k] = lo[k];
+        }
+        if (k < 0) break;
+    }
+}
+
+void push_box(std::vector<Foot> &reads, Region *r, int nd, const int64_t *lo, const int64_t *hi,
+              int64_t base = 0) {
+    std::vector<std::pair<int64_t, int64_t>> iv;
+    int64_t l[4], h[4];
+    for (int k = 0; k < nd; k++) {  // clamp to the array
+        l[k] = std::max<int64_t>(lo[k], 0);
+        h[k] = std::min<int64_t>(hi[k], r->ext[r->ndims - nd + k]);
+    }
+    box_intervals(nd, r->ext + (r->ndims - nd), l, h, base, iv);
+    for (auto &x : iv) reads.push_back({r, x.first, x.second});
+}
+
+// Box loops (Jacobi, GEMM, Himeno): the written array's split dimension
+// L.split is divided equally; the iteration box is clipped to the
+// owned block along it.  Write set = the clipped box; read footprints are
+// boxes of the inputs (stencil halos included).
+void plan_box(Launch &L, int d, int nd, int dd, DevPlan &p) {
+    (void)d;
+    const int id = L.D->id;
+    Region *Wr = L.a[L.D->out_arg].reg;
+    const int s = L.split;
+    const int nb = (id == JACC_LOOP_JACOBI2D_F64 || id == JACC_LOOP_GEMM_F64) ? 2 : 3;
+    int64_t lo[3], hi[3];
+    for (int k = 0; k < nb; k++) {
+        lo[k] = L.rg.lo[k];
+        hi[k] = L.rg.hi[k];
+    }
+    partition(Wr->ext[s], nd, dd, p.own_lo, p.own_hi);
+    lo[s] = std::max(lo[s], p.own_lo);
+    hi[s] = std::min(hi[s], p.own_hi);
+    p.active = true;
+    for (int k = 0; k < nb; k++) {
+        p.blo[k] = lo[k];
+        p.bhi[k] = hi[k];
+        if (hi[k] <= lo[k]) p.active = false;
+    }
+    p.i0 = lo[0];
+    p.i1 = hi[0];
+    p.j0 = lo[1];
+    p.j1 = hi[1];
+    if (nb == 3) {
+        p.k0 = lo[2];
+        p.k1 = hi[2];
+    }
+    if (!p.active) return;
+    const int64_t *ext = Wr->ext;
+    if (s == 0) {  // contiguous block: one span (its unwritten elements are owner-valid)
+        int64_t f0 = 0, f1 = 0;
+        for (int k = 0; k < nb; k++) {
+            f0 = f0 * ext[k] + lo[k];
+            f1 = f1 * ext[k] + (hi[k] - 1);
+        }
+        p.wlo = f0;
+        p.whi = f1 + 1;
+    } else {
+        box_intervals(nb, ext, lo, hi, 0, p.wbox);
+        p.wlo = p.wbox.front().first;
+        p.whi = p.wbox.back().second;
+    }
+    if (id == JACC_LOOP_JACOBI2D_F64) {
+        const int64_t rl[2] = {lo[0] - 1, lo[1] - 1}, rh[2] = {hi[0] + 1, hi[1] + 1};
+        push_box(p.reads, L.a[0].reg, 2, rl, rh);
+    } else if (id == JACC_LOOP_GEMM_F64) {
+        const int64_t al[2] = {lo[0], 0}, ah[2] = {hi[0], L.K};
+        const int64_t bl[2] = {0, lo[1]}, bh[2] = {L.K, hi[1]};
+        push_box(p.reads, L.a[0].reg, 2, al, ah);
+        push_box(p.reads, L.a[1].reg, 2, bl, bh);
+    } else if (id == JACC_LOOP_HIMENO_F32) {
+        const int64_t pl[3] = {lo[0] - 1, lo[1] - 1, lo[2] - 1}, ph[3] = {hi[0] + 1, hi[1] + 1, hi[2] + 1};
+        push_box(p.reads, L.a[0].reg, 3, pl, ph);
+        const int stacks[6] = {1, 4, 3, 3, 1, 1};
+        const int64_t V = L.HI * L.HJ * L.HK;
+        for (int k = 1; k < 6; k++)
+            for (int m = 0; m < stacks[k]; m++)
+                push_box(p.reads, L.a[k].reg, 3, lo, hi, m * V);
+    } else {  // himeno copy
+        push_box(p.reads, L.a[0].reg, 3, lo, hi);
+    }
+}
+
+bool is_box_loop(int id) {
+    return id == JACC_LOOP_JACOBI2D_F64 || id == JACC_LOOP_GEMM_F64 || id == JACC_LOOP_HIMENO_F32 ||
+           id == JACC_LOOP_HIMENO_COPY_F32;
+}
+
+// exact write intervals of a device plan
+std::vector<std::pair<int64_t, int64_t>> write_intervals(const DevPlan &p) {
+    if (!p.wbox.empty()) return p.wbox;
+    return {{p.wlo, p.whi}};
+}
+
+// the boundary slab of d's write box at index x along split dim s
+void slab_box(const Launch &L, const DevPlan &p, int64_t x, int64_t *lo, int64_t *hi) {
+    for (int k = 0; k < 3; k++) {
+        lo[k] = p.blo[k];
+        hi[k] = p.bhi[k];
+    }
+    lo[L.split] = x;
+    hi[L.split] = x + 1;
+}
+
+jk::Box2D make_box2d(const Region *r, int nb, const int64_t *lo, const int64_t *hi) {
+    const int64_t *e = r->ext + (r->ndims - nb);
+    const int64_t el = (int64_t)r->elem;
+    jk::Box2D b{};
+    if (nb == 2) {
+        b.count = 1;
+        b.height = hi[0] - lo[0];
+        b.width = (hi[1] - lo[1]) * el;
+        b.pitch = e[1] * el;
+        b.first = (lo[0] * e[1] + lo[1]) * el;
+        b.outer = 0;
+    } else {
+        b.count = hi[0] - lo[0];
+        b.height = hi[1] - lo[1];
+        b.width = (hi[2] - lo[2]) * el;
+        b.pitch = e[2] * el;
+        b.first = ((lo[0] * e[1] + lo[1]) * e[2] + lo[2]) * el;
+        b.outer = e[1] * e[2] * el;
+    }
+    return b;
+}
 
 void plan_launch(Launch &L) {
     const int n = R.n;
@@ -556,18 +714,7 @@ void plan_launch(Launch &L) {
                 p.reads.push_back({L.a[0].reg, L.a[0].off + p.i0, L.a[0].off + p.i1});
             }
         } else if (id == JACC_LOOP_JACOBI2D_F64) {
-            const int64_t N = L.N;
-            partition(N, nd, dd, p.own_lo, p.own_hi);  // rows of dst
-            p.i0 = std::max(L.rg.lo[0], p.own_lo);
-            p.i1 = std::min(L.rg.hi[0], p.own_hi);
-            p.j0 = L.rg.lo[1];
-            p.j1 = L.rg.hi[1];
-            p.active = p.i1 > p.i0 && p.j1 > p.j0;
-            if (p.active) {
-                p.wlo = p.i0 * N + p.j0;
-                p.whi = (p.i1 - 1) * N + p.j1;
-                p.reads.push_back({L.a[0].reg, (p.i0 - 1) * N, (p.i1 + 1) * N});
-            }
+            plan_box(L, d, nd, dd, p);
         } else if (id == JACC_LOOP_DOT_F64 || id == JACC_LOOP_SUM_F64) {
             // reductions: filter by the outermost parallel iterator
             int64_t lo, hi;
@@ -579,40 +726,9 @@ void plan_launch(Launch &L) {
             if (p.active)
                 for (int k = 0; k < narr; k++)
                     p.reads.push_back({L.a[k].reg, L.a[k].off + p.i0, L.a[k].off + p.i1});
-        } else if (id == JACC_LOOP_GEMM_F64) {
-            partition(L.M, nd, dd, p.own_lo, p.own_hi);  // rows of C
-            p.i0 = std::max(L.rg.lo[0], p.own_lo);
-            p.i1 = std::min(L.rg.hi[0], p.own_hi);
-            p.j0 = L.rg.lo[1];
-            p.j1 = L.rg.hi[1];
-            p.active = p.i1 > p.i0 && p.j1 > p.j0;
-            if (p.active) {
-                p.wlo = p.i0 * L.Nn + p.j0;
-                p.whi = (p.i1 - 1) * L.Nn + p.j1;
-                p.reads.push_back({L.a[0].reg, p.i0 * L.K, p.i1 * L.K});
-                p.reads.push_back({L.a[1].reg, 0, L.K * L.Nn});
-            }
-        } else if (id == JACC_LOOP_HIMENO_F32 || id == JACC_LOOP_HIMENO_COPY_F32) {
-            const int64_t P = L.HJ * L.HK, V = L.HI * P;
-            partition(L.HI, nd, dd, p.own_lo, p.own_hi);  // planes of the written array
-            p.i0 = std::max(L.rg.lo[0], p.own_lo);
-            p.i1 = std::min(L.rg.hi[0], p.own_hi);
-            p.j0 = L.rg.lo[1];
-            p.j1 = L.rg.hi[1];
-            p.active = p.i1 > p.i0 && p.j1 > p.j0 && L.rg.hi[2] > L.rg.lo[2];
-            if (p.active) {
-                p.wlo = p.i0 * P + p.j0 * L.HK + L.rg.lo[2];
-                p.whi = (p.i1 - 1) * P + (p.j1 - 1) * L.HK + L.rg.hi[2];
-                if (id == JACC_LOOP_HIMENO_F32) {
-                    p.reads.push_back({L.a[0].reg, (p.i0 - 1) * P, (p.i1 + 1) * P});  // p +- 1 plane
-                    const int stacks[6] = {1, 4, 3, 3, 1, 1};
-                    for (int k = 1; k < 6; k++)
-                        for (int m = 0; m < stacks[k]; m++)
-                            p.reads.push_back({L.a[k].reg, m * V + p.i0 * P, m * V + p.i1 * P});
-                } else {
-                    p.reads.push_back({L.a[0].reg, p.i0 * P, p.i1 * P});  // wrk2 planes
-                }
-            }
+        } else if (id == JACC_LOOP_GEMM_F64 || id == JACC_LOOP_HIMENO_F32 ||
+                   id == JACC_LOOP_HIMENO_COPY_F32) {
+            plan_box(L, d, nd, dd, p);
         } else {  // scatter: owned slice of a; every device scans all i
             Region *ar = L.a[2].reg;
             partition(ar->nelem, nd, dd, p.own_lo, p.own_hi);
@@ -637,11 +753,12 @@ void halo_targets(const Launch &L, int d, int &top, int &bot) {
     top = bot = -1;
     const DevPlan &me = L.plan[d];
     if (!me.active) return;
+    const int s = L.split;
     for (int p = 0; p < R.n; p++) {
         if (p == d || !L.plan[p].active) continue;
-        const int64_t flo = L.plan[p].i0 - L.D->halo_rows, fhi = L.plan[p].i1 + L.D->halo_rows;
-        if (me.i0 >= flo && me.i0 < fhi) top = p;
-        if (me.i1 - 1 >= flo && me.i1 - 1 < fhi) bot = p;
+        const int64_t flo = L.plan[p].blo[s] - L.D->halo_rows, fhi = L.plan[p].bhi[s] + L.D->halo_rows;
+        if (me.blo[s] >= flo && me.blo[s] < fhi) top = p;
+        if (me.bhi[s] - 1 >= flo && me.bhi[s] - 1 < fhi) bot = p;
     }
 }
 
@@ -833,6 +950,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         }
     }
     L.rg = rg;
+    if (is_box_loop(id)) {
+        L.split = R.split_dim < 0 ? 0 : R.split_dim;  // A18: built-in loops -> leftmost (dim 0)
+        invalid_if(L.split >= L.a[D->out_arg].reg->ndims);
+    }
     if (R.mode == JACC_MODE_DUP) L.dup = true;
     // ---- NEXT-1 adaptive utilization (single process, n > 1) ---------------
     const bool adaptive =
@@ -884,7 +1005,9 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     // no-op: an owner is the only writer of its block)
     if (W && id != JACC_LOOP_SCATTER_ADD_F64 && id != JACC_LOOP_SCATTER_ADD_I32)
         for (int d = 0; d < n; d++)
-            if (L.plan[d].active) L.plan[d].reads.push_back({W, L.plan[d].wlo, L.plan[d].whi});
+            if (L.plan[d].active)
+                for (auto &iv : write_intervals(L.plan[d]))
+                    L.plan[d].reads.push_back({W, iv.first, iv.second});
 
     // ---- pulls: stale input intervals (validity tracker) -------------------
     std::vector<Pull> pulls;
@@ -1002,8 +1125,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 break;
             }
             case JACC_LOOP_JACOBI2D_F64: {
-                double *pt = top[d] >= 0 ? reinterpret_cast<double *>(W->rep[top[d]]) : nullptr;
-                double *pb = bot[d] >= 0 ? reinterpret_cast<double *>(W->rep[bot[d]]) : nullptr;
+                // split dim 0: the boundary rows are pushed by the stencil kernel
+                // itself; other split dims push boundary slabs after it
+                double *pt = (L.split == 0 && top[d] >= 0) ? reinterpret_cast<double *>(W->rep[top[d]]) : nullptr;
+                double *pb = (L.split == 0 && bot[d] >= 0) ? reinterpret_cast<double *>(W->rep[bot[d]]) : nullptr;
                 CK(jk::jacobi2d(dv.s, reinterpret_cast<const double *>(L.a[0].reg->rep[d]),
                                 reinterpret_cast<double *>(W->rep[d]), L.N, p.i0, p.i1, p.j0, p.j1,
                                 drec, pt, pb));
@@ -1032,17 +1157,17 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 auto F = [&](int k) { return reinterpret_cast<const float *>(L.a[k].reg->rep[d]); };
                 CK(jk::himeno_stencil(dv.s, F(0), F(1), F(2), F(3), F(4), F(5),
                                       reinterpret_cast<float *>(W->rep[d]), L.HI, L.HJ, L.HK, p.i0,
-                                      p.i1, p.j0, p.j1, L.rg.lo[2], L.rg.hi[2], (float)L.scalar,
+                                      p.i1, p.j0, p.j1, p.k0, p.k1, (float)L.scalar,
                                       dv.partials, dv.ticket, dv.part, drec));
                 break;
             }
             case JACC_LOOP_HIMENO_COPY_F32: {
-                float *pt = top[d] >= 0 ? reinterpret_cast<float *>(W->rep[top[d]]) : nullptr;
-                float *pb = bot[d] >= 0 ? reinterpret_cast<float *>(W->rep[bot[d]]) : nullptr;
+                float *pt = (L.split == 0 && top[d] >= 0) ? reinterpret_cast<float *>(W->rep[top[d]]) : nullptr;
+                float *pb = (L.split == 0 && bot[d] >= 0) ? reinterpret_cast<float *>(W->rep[bot[d]]) : nullptr;
                 CK(jk::himeno_copy(dv.s, reinterpret_cast<const float *>(L.a[0].reg->rep[d]),
                                    reinterpret_cast<float *>(W->rep[d]), L.HI, L.HJ, L.HK, p.i0, p.i1,
-                                   p.j0, p.j1, L.rg.lo[2], L.rg.hi[2], drec, pt, pb));
-                const int64_t planeb = (p.j1 - p.j0) * (L.rg.hi[2] - L.rg.lo[2]) * 4;
+                                   p.j0, p.j1, p.k0, p.k1, drec, pt, pb));
+                const int64_t planeb = (p.j1 - p.j0) * (p.k1 - p.k0) * 4;
                 if (pt) merged_bytes += planeb;
                 if (pb) merged_bytes += planeb;
                 break;
@@ -1105,12 +1230,30 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         }
         if (prof) CK(cudaEventRecord(pr.k1, dv.s));
         if (adaptive) CK(cudaEventRecord(ap.k1, dv.s));
+        const int nbox = (id == JACC_LOOP_JACOBI2D_F64 || id == JACC_LOOP_GEMM_F64) ? 2 : 3;
+        // ---- HALO with a split dim > 0: push the boundary slabs (strided) --
+        if (writes && p.active && R.policy == JACC_MERGE_HALO && L.split > 0 && D->halo_rows > 0) {
+            for (int side = 0; side < 2; side++) {
+                const int tgt = side == 0 ? top[d] : bot[d];
+                if (tgt < 0) continue;
+                int64_t lo[3], hi[3];
+                slab_box(L, p, side == 0 ? p.blo[L.split] : p.bhi[L.split] - 1, lo, hi);
+                jk::PeerPtrs pp{};
+                pp.p[pp.n++] = W->rep[tgt];
+                const jk::Box2D bx = make_box2d(W, nbox, lo, hi);
+                CK(jk::merge_box(dv.s, W->rep[d], pp, bx, drec, (int64_t)W->elem));
+                merged_bytes += (uint64_t)(bx.count * bx.height * bx.width);
+            }
+        }
         // ---- EAGER merge: push the recorded dirty region to every peer ----
         if (writes && p.active && R.policy == JACC_MERGE_EAGER && n > 1) {
             jk::PeerPtrs pp{};
             for (int q = 0; q < n; q++)
                 if (q != d) pp.p[pp.n++] = W->rep[q];
-            if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
+            if (is_box_loop(id) && L.split > 0) {
+                const jk::Box2D bx = make_box2d(W, nbox, p.blo, p.bhi);
+                CK(jk::merge_box(dv.s, W->rep[d], pp, bx, drec, (int64_t)W->elem));
+            } else if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
                 CK(jk::merge_bitmap(dv.s, W->rep[d], pp, W->bitmap[d], (int64_t)W->elem, p.wlo, p.whi));
             } else {
                 CK(jk::merge_range(dv.s, W->rep[d], pp, drec, (int64_t)W->elem, p.wlo, p.whi));
@@ -1136,22 +1279,32 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     if (W && L.dup) {
         // duplicated: every device computed (after pulling) the whole block
         for (int d = 0; d < n; d++)
-            if (L.plan[d].active) W->valid[d].add(L.plan[d].wlo, L.plan[d].whi);
+            if (L.plan[d].active)
+                for (auto &iv : write_intervals(L.plan[d])) W->valid[d].add(iv.first, iv.second);
     }
     if (writes) {
         for (int d = 0; d < n; d++) {
             const DevPlan &p = L.plan[d];
             if (!p.active) continue;
-            W->valid[d].add(p.wlo, p.whi);
+            const auto wiv = write_intervals(p);
+            for (auto &iv : wiv) W->valid[d].add(iv.first, iv.second);
             if (R.policy == JACC_MERGE_EAGER) continue;  // every peer received the dirty set
             for (int q = 0; q < n; q++) {
                 if (q == d) continue;
-                // q keeps validity only on the rows pushed to it (HALO)
+                // q keeps validity only on the rows / slabs pushed to it (HALO)
                 std::vector<std::pair<int64_t, int64_t>> keep;
-                if (D->halo_rows > 0) {
+                if (D->halo_rows > 0 && L.split == 0) {
                     const int64_t unit = W->nelem / W->ext[0];  // elements per split index
                     if (top[d] == q) keep.push_back({p.i0 * unit, (p.i0 + 1) * unit});
                     if (bot[d] == q) keep.push_back({(p.i1 - 1) * unit, p.i1 * unit});
+                } else if (D->halo_rows > 0) {
+                    const int nb = (id == JACC_LOOP_JACOBI2D_F64) ? 2 : 3;
+                    for (int side = 0; side < 2; side++) {
+                        if ((side == 0 ? top[d] : bot[d]) != q) continue;
+                        int64_t lo[3], hi[3];
+                        slab_box(L, p, side == 0 ? p.blo[L.split] : p.bhi[L.split] - 1, lo, hi);
+                        box_intervals(nb, W->ext + (W->ndims - nb), lo, hi, 0, keep);
+                    }
                 }
                 std::vector<std::pair<int64_t, int64_t>> had;
                 for (auto &k : keep) {
@@ -1161,7 +1314,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                     for (auto &m : W->valid[q].missing(k.first, k.second)) tmp.remove(m.first, m.second);
                     for (auto &iv : tmp.iv) had.push_back(iv);
                 }
-                W->valid[q].remove(p.wlo, p.whi);
+                for (auto &iv : wiv) W->valid[q].remove(iv.first, iv.second);
                 for (auto &h : had) W->valid[q].add(h.first, h.second);
             }
         }
@@ -1404,6 +1557,13 @@ jacc_status jacc_set_merge_policy(int policy) {
     if (!R.init || R.poisoned) return JACC_ERR_STATE;
     if (policy != JACC_MERGE_EAGER && policy != JACC_MERGE_HALO) return JACC_ERR_INVALID;
     R.policy = policy;
+    return JACC_OK;
+}
+
+jacc_status jacc_set_split_dim(int dim) {
+    if (!R.init || R.poisoned) return JACC_ERR_STATE;
+    if (dim < -1 || dim > 2) return JACC_ERR_INVALID;
+    R.split_dim = dim;
     return JACC_OK;
 }
 

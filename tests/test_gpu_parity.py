@@ -741,3 +741,112 @@ def test_graph_rules(J):
         # replica validity: replay refused
         J.jacc_update_device(B)
         assert J.lib.jacc_graph_replay(gid, 1) == J.JACC_ERR_STATE
+
+
+# --------------------------------------------------------------------------
+# NEXT-2 multidimensional division: split dims > 0 (strided blocks)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("N", [17, 64, 301])
+@pytest.mark.parametrize("n", [2, 3, 8])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_jacobi_column_split(J, N, n, policy):
+    T = 2
+    A0 = synth.uniform_f64(N * N, 99 + N, 1).reshape(N, N)
+    B0 = synth.uniform_f64(N * N, 99 + N, 2).reshape(N, N)
+    Ar, Br = A0.copy(), B0.copy()
+    orc.jacobi2d(T, Ar, Br)
+    A, B = A0.copy(), B0.copy()
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    with runtime(J, n, policy):
+        J.jacc_set_split_dim(1)
+        _create(J, A, B)
+        dirt = None
+        for t in range(T):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, A), J.arg(OUT, B)], 0)
+            if t == 0:
+                dirt = [J.jacc_get_dirty_range(B, d) for d in range(n)]
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, B), J.arg(OUT, A)], 0)
+        if policy == 0:
+            for d in range(n):
+                assert np.array_equal(J.jacc_get_replica(A, d), Ar)
+        J.jacc_update_host(A)
+        J.jacc_update_host(B)
+    assert np.array_equal(A, Ar) and np.array_equal(B, Br)
+    for d in range(n):
+        lo, hi = orc.partition(N, n, d)     # column block
+        a, b = max(lo, 1), min(hi, N - 1)
+        exp = (2**64 - 1, 0) if a >= b else (1 * N + a, (N - 2) * N + b - 1)
+        assert dirt[d] == exp
+
+
+@pytest.mark.parametrize("split", [1, 2])
+@pytest.mark.parametrize("n", [2, 3])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_himeno_split_dims(J, split, n, policy):
+    I, Jd, K = 13, 11, 17
+    arrs = synth.himeno_random(I, Jd, K, 100)
+    nn = 2
+    p, a, b, c, w1, bd = (x.copy() for x in arrs)
+    wrk2 = np.zeros_like(p)
+    refs = []
+    for _ in range(nn):
+        refs.append(orc.himeno_stencil(p, a, b, c, w1, bd, wrk2)[1])
+        orc.himeno_copy(wrk2, p)
+    gp, gw, gosas, _ = _himeno_gpu_split(J, arrs, nn, n, policy, split)
+    assert np.array_equal(gp, p) and np.array_equal(gw, wrk2)
+    for g, r in zip(gosas, refs):
+        assert abs(g - r) <= 1e-12 * abs(r)
+
+
+def _himeno_gpu_split(J, arrs, nn, n, policy, split):
+    p, a, b, c, w1, bd = (x.copy() for x in arrs)
+    wrk2 = np.zeros_like(p)
+    gosas = []
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    with runtime(J, n, policy):
+        J.jacc_set_split_dim(split)
+        _create(J, p, a, b, c, w1, bd, wrk2)
+        for _ in range(nn):
+            g = np.zeros(1)
+            J.jacc_launch(J.JACC_LOOP_HIMENO_F32, None,
+                          [J.arg(IN, p), J.arg(IN, a), J.arg(IN, b), J.arg(IN, c), J.arg(IN, w1),
+                           J.arg(IN, bd), J.arg(OUT, wrk2), J.arg(J.JACC_ARG_REDUCE_SUM_F64, g),
+                           J.arg(J.JACC_ARG_SCALAR_F64, f64=0.8)])
+            gosas.append(g[0])
+            J.jacc_launch(J.JACC_LOOP_HIMENO_COPY_F32, None, [J.arg(IN, wrk2), J.arg(OUT, p)], 0)
+        J.jacc_update_host(p)
+        J.jacc_update_host(wrk2)
+    return p, wrk2, gosas, None
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_gemm_column_split(J, n):
+    M, N, K = 70, 90, 33
+    A = synth.uniform_f64(M * K, 101, 1).reshape(M, K)
+    B = synth.uniform_f64(K * N, 101, 2).reshape(K, N)
+    ref = orc.gemm_f64(A, B)
+    C = np.zeros((M, N))
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    with runtime(J, n):
+        J.jacc_set_split_dim(1)
+        _create(J, A, B, C)
+        J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, [J.arg(IN, A), J.arg(IN, B), J.arg(OUT, C)])
+        reps = [J.jacc_get_replica(C, d) for d in range(n)]
+        J.jacc_update_host(C)
+    assert (np.abs(C - ref) <= 1e-12 * (np.abs(A) @ np.abs(B))).all()
+    for r in reps:
+        assert np.array_equal(r, C)
+
+
+def test_split_dim_validation(J):
+    x = np.zeros(10, dtype=np.float32)
+    y = np.zeros(10, dtype=np.float32)
+    A = np.zeros((8, 8)); B = np.zeros((8, 8))
+    with runtime(J, 2):
+        with pytest.raises(J.JaccError):
+            J.jacc_set_split_dim(3)
+        J.jacc_set_split_dim(2)
+        _create(J, A, B, x, y)
+        st = J.jacc_launch_status(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)])
+        assert st == J.JACC_ERR_INVALID          # a 2-D array has no dim 2
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(0, 10), [_in(J, y), _out(J, x)])  # 1-D: dim 0
