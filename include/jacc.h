@@ -111,6 +111,18 @@ jacc_status jacc_set_mode(int mode);
  * launch whose written array has no such dimension: JACC_ERR_INVALID. */
 jacc_status jacc_set_split_dim(int dim);
 
+/* NEXT-3 scatter distribution.  0 (default): the paper's owner filter
+ * (R-6): every device scans all iterations and applies
+ * the updates whose index falls in its slice of `a`.  1: iteration split
+ * with an additive merge: each device scatters its block of iterations
+ * into a private zero-kept delta array (+ delta bitmap); then the owner of
+ * each word-aligned slice of `a` adds every device's delta for the words
+ * dirty anywhere, in device order, reading them over peer memory, and the
+ * merge policy distributes the result (its dirty bitmap = the union).
+ * Single-process mode only.  Errors: JACC_ERR_INVALID in multi-process
+ * mode. */
+jacc_status jacc_set_scatter_split(int iteration_split);
+
 /* Owned block [lo, hi) of logical device d when an extent E is split over
  * n devices: "equally dividing parallel dimensions among GPUs",
  * the first E mod n blocks one element larger (R-2).  Pure host

@@ -768,6 +768,86 @@ __device__ __forceinline__ void publish_dirty_flat(u64 mn, u64 mx, u64 *dirty) {
     publish_dirty<HT / 32>(mn, mx, dirty);
 }
 
+// one interior point, exactly as written (scalar path: row heads / tails)
+__device__ __forceinline__ float himeno_point(const float *__restrict__ p,
+                                              const float *const *__restrict__ co, int64_t P,
+                                              int64_t K, int64_t x, float omega, float *w2) {
+    const float *q = p + x;
+    float s0 = __fmul_rn(__ldcs(co[0] + x), __ldg(q + P));
+    s0 = __fadd_rn(s0, __fmul_rn(__ldcs(co[1] + x), __ldg(q + K)));
+    s0 = __fadd_rn(s0, __fmul_rn(__ldcs(co[2] + x), __ldg(q + 1)));
+    s0 = __fadd_rn(s0, __fmul_rn(__ldcs(co[4] + x),
+                                 __fadd_rn(__fsub_rn(__fsub_rn(__ldg(q + P + K), __ldg(q + P - K)),
+                                                     __ldg(q - P + K)),
+                                           __ldg(q - P - K))));
+    s0 = __fadd_rn(s0, __fmul_rn(__ldcs(co[5] + x),
+                                 __fadd_rn(__fsub_rn(__fsub_rn(__ldg(q + K + 1), __ldg(q - K + 1)),
+                                                     __ldg(q + K - 1)),
+                                           __ldg(q - K - 1))));
+    s0 = __fadd_rn(s0, __fmul_rn(__ldcs(co[6] + x),
+                                 __fadd_rn(__fsub_rn(__fsub_rn(__ldg(q + P + 1), __ldg(q - P + 1)),
+                                                     __ldg(q + P - 1)),
+                                           __ldg(q - P - 1))));
+    s0 = __fadd_rn(s0, __fmul_rn(__ldcs(co[7] + x), __ldg(q - P)));
+    s0 = __fadd_rn(s0, __fmul_rn(__ldcs(co[8] + x), __ldg(q - K)));
+    s0 = __fadd_rn(s0, __fmul_rn(__ldcs(co[9] + x), __ldg(q - 1)));
+    s0 = __fadd_rn(s0, __ldcs(co[10] + x));
+    const float p0 = __ldg(q);
+    const float ss = __fmul_rn(__fsub_rn(__fmul_rn(s0, __ldcs(co[3] + x)), p0), __ldcs(co[11] + x));
+    *w2 = __fadd_rn(p0, __fmul_rn(omega, ss));
+    return __fmul_rn(ss, ss);
+}
+
+__device__ __forceinline__ float4 ld4cs(const float *p) { return __ldcs(reinterpret_cast<const float4 *>(p)); }
+__device__ __forceinline__ float4 ld4g(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+__device__ __forceinline__ float f4(const float4 &v, int e) {
+    return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+
+// A p row of the chunk with its k-1 / k+4 neighbours (shuffled from the
+// adjacent lanes, loaded by the lanes at a warp or body edge).  Only the
+// centre row is 16-byte aligned (x = row base + aligned k); rows at +-K,
+// +-P have the residue of K, P mod 4, so they are loaded as 4 scalars.
+struct PRow {
+    float4 v;
+    float l, r;
+};
+template <bool ALIGNED>
+__device__ __forceinline__ PRow prow(const float *p, int64_t at, bool valid, bool own_l, bool own_r) {
+    PRow o;
+    if (valid) {
+        if constexpr (ALIGNED) {
+            o.v = ld4g(p + at);
+        } else {
+            o.v = make_float4(__ldg(p + at), __ldg(p + at + 1), __ldg(p + at + 2), __ldg(p + at + 3));
+        }
+    } else {
+        o.v = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float fl = __shfl_up_sync(0xffffffffu, o.v.w, 1);
+    const float fr = __shfl_down_sync(0xffffffffu, o.v.x, 1);
+    o.l = (valid && own_l) ? __ldg(p + at - 1) : fl;
+    o.r = (valid && own_r) ? __ldg(p + at + 4) : fr;
+    return o;
+}
+__device__ __forceinline__ float4 ld4s(const float *p) {
+    return make_float4(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3));
+}
+// streamed array: 128-bit load when its base keeps x 16-byte aligned (the
+// stacked a/b/c arrays start at m*V, which need not be), else 4 scalars
+__device__ __forceinline__ float4 ld4cs_any(const float *p, bool aligned) {
+    if (aligned) return __ldcs(reinterpret_cast<const float4 *>(p));
+    return make_float4(__ldcs(p), __ldcs(p + 1), __ldcs(p + 2), __ldcs(p + 3));
+}
+__device__ __forceinline__ float km(const PRow &R, int e) { return e == 0 ? R.l : f4(R.v, e - 1); }
+__device__ __forceinline__ float kp(const PRow &R, int e) { return e == 3 ? R.r : f4(R.v, e + 1); }
+
+// Warp per (i, j) row; the 16-byte-aligned body of the row is processed as
+// float4 chunks (one per lane): the 12 streamed arrays and the centre p row
+// as 128-bit loads, the 8 neighbour p rows as scalars, k +- 1 neighbours by
+// shuffle -- ~45 load instructions per 4 points instead of 124.  The
+// unaligned head/tail (<= 3 + 3 points) take the scalar path.  Arithmetic
+// per point exactly as written.
 __global__ void __launch_bounds__(HT) himeno_stencil_kernel(
     const float *__restrict__ p, const float *__restrict__ a, const float *__restrict__ b,
     const float *__restrict__ c, const float *__restrict__ wrk1, const float *__restrict__ bnd,
@@ -776,48 +856,89 @@ __global__ void __launch_bounds__(HT) himeno_stencil_kernel(
     double *out, u64 *dirty) {
     __shared__ double sh[HT / 32];
     __shared__ bool last;
-    const int tid = threadIdx.x;
-    const int tx = tid % HX, ty = tid / HX;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int64_t P = J * K, V = I * J * K;
-    const float *a0 = a, *a1 = a + V, *a2 = a + 2 * V, *a3 = a + 3 * V;
-    const float *b0 = b, *b1 = b + V, *b2 = b + 2 * V;
-    const float *c0 = c, *c1 = c + V, *c2 = c + 2 * V;
-    const int64_t nkt = (k1 - k0 + HX - 1) / HX, njt = (j1 - j0 + HY - 1) / HY;
-    const int64_t ntiles = nkt * njt * (i1 - i0);
+    const float *co[12] = {a, a + V, a + 2 * V, a + 3 * V, b, b + V, b + 2 * V,
+                           c, c + V, c + 2 * V, wrk1, bnd};
+    bool al[12];  // x is aligned relative to p; is it relative to co[m]?
+    for (int m = 0; m < 12; m++)
+        al[m] = ((reinterpret_cast<uintptr_t>(co[m]) - reinterpret_cast<uintptr_t>(p)) & 15) == 0 &&
+                (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+    const int64_t nj = j1 - j0, rows = (i1 - i0) * nj;
+    const int64_t wg = ((int64_t)blockIdx.x * HT + tid) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * HT) >> 5;
     double g = 0.0;
     u64 mn = kU64Max, mx = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t kt = t % nkt, r = t / nkt;
-        const int64_t jt = r % njt, i = i0 + r / njt;
-        const int64_t k = k0 + kt * HX + tx, j = j0 + jt * HY + ty;
-        if (k >= k1 || j >= j1) continue;
-        const int64_t x = i * P + j * K + k;
-        const float *q = p + x;
-        // all loads independent; arithmetic exactly as written, no contraction
-        const float pip = __ldg(q + P), pjp = __ldg(q + K), pkp = __ldg(q + 1);
-        const float pim = __ldg(q - P), pjm = __ldg(q - K), pkm = __ldg(q - 1), p0 = __ldg(q);
-        const float q1 = __ldg(q + P + K), q2 = __ldg(q + P - K), q3 = __ldg(q - P + K), q4 = __ldg(q - P - K);
-        const float q5 = __ldg(q + K + 1), q6 = __ldg(q - K + 1), q7 = __ldg(q + K - 1), q8 = __ldg(q - K - 1);
-        const float q9 = __ldg(q + P + 1), q10 = __ldg(q - P + 1), q11 = __ldg(q + P - 1), q12 = __ldg(q - P - 1);
-        const float va0 = __ldcs(a0 + x), va1 = __ldcs(a1 + x), va2 = __ldcs(a2 + x), va3 = __ldcs(a3 + x);
-        const float vb0 = __ldcs(b0 + x), vb1 = __ldcs(b1 + x), vb2 = __ldcs(b2 + x);
-        const float vc0 = __ldcs(c0 + x), vc1 = __ldcs(c1 + x), vc2 = __ldcs(c2 + x);
-        const float vw = __ldcs(wrk1 + x), vbnd = __ldcs(bnd + x);
-        float s0 = __fmul_rn(va0, pip);
-        s0 = __fadd_rn(s0, __fmul_rn(va1, pjp));
-        s0 = __fadd_rn(s0, __fmul_rn(va2, pkp));
-        s0 = __fadd_rn(s0, __fmul_rn(vb0, __fadd_rn(__fsub_rn(__fsub_rn(q1, q2), q3), q4)));
-        s0 = __fadd_rn(s0, __fmul_rn(vb1, __fadd_rn(__fsub_rn(__fsub_rn(q5, q6), q7), q8)));
-        s0 = __fadd_rn(s0, __fmul_rn(vb2, __fadd_rn(__fsub_rn(__fsub_rn(q9, q10), q11), q12)));
-        s0 = __fadd_rn(s0, __fmul_rn(vc0, pim));
-        s0 = __fadd_rn(s0, __fmul_rn(vc1, pjm));
-        s0 = __fadd_rn(s0, __fmul_rn(vc2, pkm));
-        s0 = __fadd_rn(s0, vw);
-        const float ss = __fmul_rn(__fsub_rn(__fmul_rn(s0, va3), p0), vbnd);
-        g += (double)__fmul_rn(ss, ss);
-        __stcs(wrk2 + x, __fadd_rn(p0, __fmul_rn(omega, ss)));
-        mn = (u64)x < mn ? (u64)x : mn;
-        mx = (u64)x > mx ? (u64)x : mx;
+    for (int64_t r = wg; r < rows; r += nw) {
+        const int64_t i = i0 + r / nj, j = j0 + r % nj;
+        const int64_t rb = i * P + j * K;
+        int64_t ka = k0 + ((4 - ((rb + k0) & 3)) & 3);  // first 16-byte aligned k
+        if (ka > k1) ka = k1;
+        const int64_t nch = (k1 - ka) >> 2;             // float4 chunks
+        const int64_t kt = ka + 4 * nch;                // tail start
+        // head [k0, ka) and tail [kt, k1): at most 3 + 3 scalar points
+        {
+            const int64_t nh = ka - k0;
+            int64_t k = -1;
+            if (lane < nh) k = k0 + lane;
+            else if (lane >= 8 && lane - 8 < k1 - kt) k = kt + (lane - 8);
+            if (k >= 0) {
+                float w2;
+                g += (double)himeno_point(p, co, P, K, rb + k, omega, &w2);
+                __stcs(wrk2 + rb + k, w2);
+            }
+        }
+        for (int64_t c0 = 0; c0 < nch; c0 += 32) {
+            const int64_t ch = c0 + lane;
+            const bool valid = ch < nch;
+            const bool own_l = lane == 0;
+            const bool own_r = lane == 31 || ch + 1 >= nch;
+            const int64_t x = rb + ka + 4 * ch;
+            const PRow C = prow<true>(p, x, valid, own_l, own_r);
+            const PRow JP = prow<false>(p, x + K, valid, own_l, own_r);
+            const PRow JM = prow<false>(p, x - K, valid, own_l, own_r);
+            const PRow IP = prow<false>(p, x + P, valid, own_l, own_r);
+            const PRow IM = prow<false>(p, x - P, valid, own_l, own_r);
+            if (!valid) continue;  // no shuffles below
+            const float4 pp = ld4s(p + x + P + K), pm = ld4s(p + x + P - K);
+            const float4 mp = ld4s(p + x - P + K), mm = ld4s(p + x - P - K);
+            const float4 A0 = ld4cs_any(co[0] + x, al[0]), A1 = ld4cs_any(co[1] + x, al[1]),
+                         A2 = ld4cs_any(co[2] + x, al[2]), A3 = ld4cs_any(co[3] + x, al[3]);
+            const float4 B0 = ld4cs_any(co[4] + x, al[4]), B1 = ld4cs_any(co[5] + x, al[5]),
+                         B2 = ld4cs_any(co[6] + x, al[6]);
+            const float4 C0 = ld4cs_any(co[7] + x, al[7]), C1 = ld4cs_any(co[8] + x, al[8]),
+                         C2 = ld4cs_any(co[9] + x, al[9]);
+            const float4 W1 = ld4cs_any(co[10] + x, al[10]), BD = ld4cs_any(co[11] + x, al[11]);
+            float res[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                float s0 = __fmul_rn(f4(A0, e), f4(IP.v, e));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(A1, e), f4(JP.v, e)));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(A2, e), kp(C, e)));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(B0, e),
+                                             __fadd_rn(__fsub_rn(__fsub_rn(f4(pp, e), f4(pm, e)), f4(mp, e)),
+                                                       f4(mm, e))));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(B1, e),
+                                             __fadd_rn(__fsub_rn(__fsub_rn(kp(JP, e), kp(JM, e)), km(JP, e)),
+                                                       km(JM, e))));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(B2, e),
+                                             __fadd_rn(__fsub_rn(__fsub_rn(kp(IP, e), kp(IM, e)), km(IP, e)),
+                                                       km(IM, e))));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(C0, e), f4(IM.v, e)));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(C1, e), f4(JM.v, e)));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(C2, e), km(C, e)));
+                s0 = __fadd_rn(s0, f4(W1, e));
+                const float p0 = f4(C.v, e);
+                const float ss = __fmul_rn(__fsub_rn(__fmul_rn(s0, f4(A3, e)), p0), f4(BD, e));
+                g += (double)__fmul_rn(ss, ss);
+                res[e] = __fadd_rn(p0, __fmul_rn(omega, ss));
+            }
+            __stcs(reinterpret_cast<float4 *>(wrk2 + x), make_float4(res[0], res[1], res[2], res[3]));
+        }
+        if (lane == 0 && k1 > k0) {
+            mn = (u64)(rb + k0) < mn ? (u64)(rb + k0) : mn;
+            mx = (u64)(rb + k1 - 1) > mx ? (u64)(rb + k1 - 1) : mx;
+        }
     }
     // fixed-order reduction: warp, block, then the last block over the grid
 #pragma unroll
@@ -835,7 +956,7 @@ __global__ void __launch_bounds__(HT) himeno_stencil_kernel(
     if (last) {
         __threadfence();
         double v = 0.0;
-        for (unsigned i = tid; i < gridDim.x; i += HT) v += __ldcg(partials + i);
+        for (unsigned q = tid; q < gridDim.x; q += HT) v += __ldcg(partials + q);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
         __syncthreads();
@@ -889,6 +1010,62 @@ __global__ void __launch_bounds__(HT) himeno_copy_kernel(
     }
     publish_dirty_flat(mn, mx, dirty);
 }
+// ---------------------------------------------------------------------------
+// NEXT-3  additive merge of the iteration-split scatter (see kernels.cuh)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) scatter_combine_kernel(T *a, uint32_t *bm_out, PeerPtrs deltas,
+                                                              PeerPtrs dbms, int64_t w0, int64_t w1,
+                                                              int64_t M, u64 *dirty) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    u64 mn = kU64Max, mx = 0;
+    for (int64_t base = w0 + gw * 32; base < w1; base += nw * 32) {
+        const int64_t w = base + lane;
+        uint32_t u = 0;
+        if (w < w1) {
+            for (int q = 0; q < dbms.n; q++) {
+                uint32_t *bq = static_cast<uint32_t *>(dbms.p[q]) + w;
+                const uint32_t v = *bq;
+                if (v) {
+                    u |= v;
+                    *bq = 0u;  // consumed: keep the delta bitmaps zero
+                }
+            }
+            bm_out[w] = u;
+        }
+        unsigned any = __ballot_sync(0xffffffffu, u != 0u);
+        while (any) {
+            const int jj = __ffs(any) - 1;
+            any &= any - 1;
+            const uint32_t bits = __shfl_sync(0xffffffffu, u, jj);
+            if ((bits >> lane) & 1u) {
+                const int64_t e = ((base + jj) << 5) + lane;
+                if (e < M) {
+                    T sum = T(0);
+                    for (int q = 0; q < deltas.n; q++) {  // device order
+                        T *dq = static_cast<T *>(deltas.p[q]) + e;
+                        const T v = *dq;
+                        if constexpr (sizeof(T) == 4)
+                            sum = (T)((uint32_t)sum + (uint32_t)v);
+                        else
+                            sum = sum + v;
+                        *dq = T(0);
+                    }
+                    if constexpr (sizeof(T) == 4)
+                        a[e] = (T)((uint32_t)a[e] + (uint32_t)sum);
+                    else
+                        a[e] = a[e] + sum;
+                    mn = (u64)e < mn ? (u64)e : mn;
+                    mx = (u64)e > mx ? (u64)e : mx;
+                }
+            }
+        }
+    }
+    publish_dirty<8>(mn, mx, dirty);
+}
+
 // ---------------------------------------------------------------------------
 // BK5  merges over peer memory (NVLink P2P stores; plain stores for virtual
 // devices that share one GPU)
@@ -1223,6 +1400,19 @@ cudaError_t merge_box(cudaStream_t s, const void *src, PeerPtrs dsts, Box2D b, c
         merge_box_kernel<float><<<g, 256, 0, s>>>(static_cast<const char *>(src), dsts, b, dirty);
     else
         return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+cudaError_t scatter_combine(cudaStream_t s, bool is_f64, void *a, uint32_t *bm_out,
+                            PeerPtrs deltas, PeerPtrs dbms, int64_t w0, int64_t w1, int64_t M,
+                            u64 *dirty) {
+    const int g = grid_for(w1 - w0, 8 * 32, 148 * 8);
+    if (is_f64)
+        scatter_combine_kernel<double><<<g, 256, 0, s>>>(static_cast<double *>(a), bm_out, deltas,
+                                                         dbms, w0, w1, M, dirty);
+    else
+        scatter_combine_kernel<int32_t><<<g, 256, 0, s>>>(static_cast<int32_t *>(a), bm_out, deltas,
+                                                          dbms, w0, w1, M, dirty);
     return cudaGetLastError();
 }
 

@@ -93,6 +93,18 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
                         int64_t K, int64_t i0, int64_t i1, int64_t j0, int64_t j1, int64_t k0,
                         int64_t k1, u64 *dirty, float *push_top, float *push_bot);
 
+// NEXT-3  Iteration-split scatter with an additive merge.  Phase 1 (every
+// device, its block of iterations): the scatter kernels above with
+// lo = 0, hi = M into a zero-kept delta array + delta bitmap.  Phase 2
+// (owner of the word-aligned slice [32*w0, 32*w1) of a): for every word
+// dirty in any device's delta bitmap, a[e] += sum_q delta_q[e] in device
+// order, read over peer memory; the consumed deltas and delta-bitmap words
+// are zeroed (so they stay zero for the next launch); the union bitmap is
+// the owner's dirty bitmap, min/max its dirty range.
+cudaError_t scatter_combine(cudaStream_t s, bool is_f64, void *a, uint32_t *bm_out,
+                            PeerPtrs deltas, PeerPtrs dbms, int64_t w0, int64_t w1, int64_t M,
+                            u64 *dirty);
+
 // BK5  Dirty-region merge over peer memory.  merge_range copies the
 // recorded span [dirty min, dirty max] (clamped to [lo, hi)) of src into
 // every peer replica; `max_elems` bounds the grid (host-known write bound).

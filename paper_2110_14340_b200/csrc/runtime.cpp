@@ -161,6 +161,8 @@ struct Device {
     double *hscal = nullptr;     // pinned host scalar
     ncclComm_t comm = nullptr;
     void *scratch = nullptr;     // binned-scatter pairs (grown on demand)
+    cudaEvent_t pe = nullptr;    // phase event (iteration-split scatter)
+    u64 *scr_dirty = nullptr;    // scratch dirty record (phase-1 kernels)
     size_t scratch_bytes = 0;
     // profiling
     double kernel_s = 0, merge_s = 0;
@@ -179,6 +181,8 @@ struct Region {
     std::vector<int> dslot;            // per device: slot of the most recent launch
     std::vector<uint32_t *> bitmap;    // per device, lazily allocated
     std::vector<uint8_t *> bytemap;    // per device epoch byte-map (binned scatter)
+    std::vector<char *> delta;         // per device delta array (iteration-split scatter)
+    std::vector<uint32_t *> dbm;       // per device delta bitmap
     std::vector<uint8_t> epoch;
     std::vector<IntervalSet> valid;    // per device
 };
@@ -217,6 +221,7 @@ struct Runtime {
     int policy = JACC_MERGE_EAGER;
     int mode = JACC_MODE_MULTI;
     int split_dim = -1;  // -1: A18 rule (dim 0 for the built-in loops)
+    bool scatter_itersplit = false;
     int gen = 0;
     bool distinct = true;
     bool use_nccl = false;
@@ -416,6 +421,8 @@ void free_region(Region *r) {
         if (r->dirty[d]) cudaFree(r->dirty[d]);
         if (r->bitmap[d]) cudaFree(r->bitmap[d]);
         if (r->bytemap[d]) cudaFree(r->bytemap[d]);
+        if (r->delta[d]) cudaFree(r->delta[d]);
+        if (r->dbm[d]) cudaFree(r->dbm[d]);
     }
     if (r->pinned) cudaHostUnregister((void *)r->base);
 }
@@ -478,6 +485,7 @@ struct DevPlan {
     bool active = false;
     int64_t i0 = 0, i1 = 0, j0 = 0, j1 = 0;  // iteration sub-range
     int64_t k0 = 0, k1 = 0;                  // (3-D loops)
+    int64_t it0 = 0, it1 = 0;                // iteration block (iteration-split scatter)
     int64_t blo[3] = {0, 0, 0}, bhi[3] = {0, 0, 0};  // write box (box loops)
     std::vector<std::pair<int64_t, int64_t>> wbox;   // exact write intervals (split dim > 0)
     int64_t wlo = 0, whi = 0;                // write bound (elements of written region), [wlo,whi)
@@ -537,6 +545,7 @@ struct Launch {
     int64_t M = 0, Nn = 0, K = 0;  // gemm
     int64_t HI = 0, HJ = 0, HK = 0;  // himeno grid
     int split = 0;                   // split dimension of the written array (A18)
+    bool itersplit = false;          // NEXT-3 iteration-split scatter
     double scalar = 0;               // SCALAR_F64 argument (himeno omega)
 };
 
@@ -570,13 +579,19 @@ void box_intervals(int nd, const int64_t *ext, const int64_t *lo, const int64_t 
     }
 }
 
+// Footprint of a box on array r (its last nd dims), widened to the full
+// extent in every dimension after the split dimension: a conservative
+// superset (pulls of stale-but-unread elements are harmless) that keeps the
+// interval count at one per split-dimension row instead of one per row of
+// the box (a 1025x513x513 interior box would otherwise be 5e5 intervals).
 void push_box(std::vector<Foot> &reads, Region *r, int nd, const int64_t *lo, const int64_t *hi,
-              int64_t base = 0) {
+              int64_t base = 0, int split = 0) {
     std::vector<std::pair<int64_t, int64_t>> iv;
     int64_t l[4], h[4];
-    for (int k = 0; k < nd; k++) {  // clamp to the array
-        l[k] = std::max<int64_t>(lo[k], 0);
-        h[k] = std::min<int64_t>(hi[k], r->ext[r->ndims - nd + k]);
+    for (int k = 0; k < nd; k++) {  // clamp to the array, widen after the split dim
+        const int64_t e = r->ext[r->ndims - nd + k];
+        l[k] = k > split ? 0 : std::max<int64_t>(lo[k], 0);
+        h[k] = k > split ? e : std::min<int64_t>(hi[k], e);
     }
     box_intervals(nd, r->ext + (r->ndims - nd), l, h, base, iv);
     for (auto &x : iv) reads.push_back({r, x.first, x.second});
@@ -625,28 +640,35 @@ void plan_box(Launch &L, int d, int nd, int dd, DevPlan &p) {
         p.wlo = f0;
         p.whi = f1 + 1;
     } else {
-        box_intervals(nb, ext, lo, hi, 0, p.wbox);
+        // superset write set for the tracker: full extent after the split
+        // dim (those elements are unchanged, so owner-valid; see push_box)
+        int64_t wl[3], wh[3];
+        for (int k = 0; k < nb; k++) {
+            wl[k] = k > s ? 0 : lo[k];
+            wh[k] = k > s ? ext[k] : hi[k];
+        }
+        box_intervals(nb, ext, wl, wh, 0, p.wbox);
         p.wlo = p.wbox.front().first;
         p.whi = p.wbox.back().second;
     }
     if (id == JACC_LOOP_JACOBI2D_F64) {
         const int64_t rl[2] = {lo[0] - 1, lo[1] - 1}, rh[2] = {hi[0] + 1, hi[1] + 1};
-        push_box(p.reads, L.a[0].reg, 2, rl, rh);
+        push_box(p.reads, L.a[0].reg, 2, rl, rh, 0, s);
     } else if (id == JACC_LOOP_GEMM_F64) {
         const int64_t al[2] = {lo[0], 0}, ah[2] = {hi[0], L.K};
         const int64_t bl[2] = {0, lo[1]}, bh[2] = {L.K, hi[1]};
-        push_box(p.reads, L.a[0].reg, 2, al, ah);
-        push_box(p.reads, L.a[1].reg, 2, bl, bh);
+        push_box(p.reads, L.a[0].reg, 2, al, ah, 0, s);
+        push_box(p.reads, L.a[1].reg, 2, bl, bh, 0, s);
     } else if (id == JACC_LOOP_HIMENO_F32) {
         const int64_t pl[3] = {lo[0] - 1, lo[1] - 1, lo[2] - 1}, ph[3] = {hi[0] + 1, hi[1] + 1, hi[2] + 1};
-        push_box(p.reads, L.a[0].reg, 3, pl, ph);
+        push_box(p.reads, L.a[0].reg, 3, pl, ph, 0, s);
         const int stacks[6] = {1, 4, 3, 3, 1, 1};
         const int64_t V = L.HI * L.HJ * L.HK;
         for (int k = 1; k < 6; k++)
             for (int m = 0; m < stacks[k]; m++)
-                push_box(p.reads, L.a[k].reg, 3, lo, hi, m * V);
+                push_box(p.reads, L.a[k].reg, 3, lo, hi, m * V, s);
     } else {  // himeno copy
-        push_box(p.reads, L.a[0].reg, 3, lo, hi);
+        push_box(p.reads, L.a[0].reg, 3, lo, hi, 0, s);
     }
 }
 
@@ -729,6 +751,27 @@ void plan_launch(Launch &L) {
         } else if (id == JACC_LOOP_GEMM_F64 || id == JACC_LOOP_HIMENO_F32 ||
                    id == JACC_LOOP_HIMENO_COPY_F32) {
             plan_box(L, d, nd, dd, p);
+        } else if (L.itersplit) {
+            // NEXT-3: iterations split in blocks; a divided in word-aligned
+            // owner slices, each owner adds every device's delta
+            Region *ar = L.a[2].reg;
+            int64_t w0, w1, b0, b1;
+            partition((ar->nelem + 31) / 32, nd, dd, w0, w1);
+            p.own_lo = std::min<int64_t>(32 * w0, ar->nelem);
+            p.own_hi = std::min<int64_t>(32 * w1, ar->nelem);
+            partition(L.rg.hi[0] - L.rg.lo[0], nd, dd, b0, b1);
+            p.it0 = L.rg.lo[0] + b0;
+            p.it1 = L.rg.lo[0] + b1;
+            p.i0 = p.it0;
+            p.i1 = p.it1;
+            p.active = p.own_hi > p.own_lo || p.it1 > p.it0;
+            p.wlo = p.own_lo;
+            p.whi = p.own_hi;
+            if (p.it1 > p.it0) {
+                p.reads.push_back({L.a[0].reg, L.a[0].off + p.it0, L.a[0].off + p.it1});
+                p.reads.push_back({L.a[1].reg, L.a[1].off + p.it0, L.a[1].off + p.it1});
+            }
+            if (p.own_hi > p.own_lo) p.reads.push_back({ar, p.own_lo, p.own_hi});
         } else {  // scatter: owned slice of a; every device scans all i
             Region *ar = L.a[2].reg;
             partition(ar->nelem, nd, dd, p.own_lo, p.own_hi);
@@ -955,6 +998,9 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         invalid_if(L.split >= L.a[D->out_arg].reg->ndims);
     }
     if (R.mode == JACC_MODE_DUP) L.dup = true;
+    L.itersplit = R.scatter_itersplit && R.n > 1 &&
+                  (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32);
+    if (L.itersplit && (R.mp || L.dup)) return JACC_ERR_INVALID;
     // ---- NEXT-1 adaptive utilization (single process, n > 1) ---------------
     const bool adaptive =
         R.mode == JACC_MODE_ADAPTIVE && R.n > 1 && !R.mp && !L.dup && !R.capturing;
@@ -1077,6 +1123,47 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 CK(cudaMemsetAsync(W->bitmap[d], 0, words * 4, R.dev[d].s));
             }
     }
+    // ---- NEXT-3 phase 1: every device scatters its iteration block into its
+    // delta array (after the usual waits and pulls) ---------------------------
+    std::vector<char> waited(n, 0);
+    if (L.itersplit) {
+        const size_t words = (size_t)((W->nelem + 31) / 32);
+        for (int d = 0; d < n; d++) {
+            Device &dv = R.dev[d];
+            const DevPlan &p = L.plan[d];
+            set_dev(d);
+            if (!W->delta[d]) {
+                CK(cudaMalloc(&W->delta[d], W->bytes));
+                CK(cudaMalloc(&W->dbm[d], words * 4));
+                CK(cudaMemsetAsync(W->delta[d], 0, W->bytes, dv.s));
+                CK(cudaMemsetAsync(W->dbm[d], 0, words * 4, dv.s));
+            }
+            for (int q = 0; q < n; q++)
+                if (q != d && (comm[d][q] || R.comm_prev[d][q]))
+                    CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
+            for (const Pull &pl : pulls) {
+                if (pl.dst != d) continue;
+                const size_t e = pl.reg->elem;
+                CK(cudaMemcpyAsync(pl.reg->rep[d] + pl.lo * e, pl.reg->rep[pl.src] + pl.lo * e,
+                                   (size_t)(pl.hi - pl.lo) * e, cudaMemcpyDefault, dv.s));
+                merged_bytes += (uint64_t)(pl.hi - pl.lo) * e;
+            }
+            waited[d] = 1;
+            if (p.it1 > p.it0) {
+                const int32_t *ix = reinterpret_cast<const int32_t *>(L.a[0].reg->rep[d]) + L.a[0].off + p.it0;
+                const char *bsrc = L.a[1].reg->rep[d] + (L.a[1].off + p.it0) * (int64_t)W->elem;
+                if (id == JACC_LOOP_SCATTER_ADD_F64)
+                    CK(jk::scatter_add_f64(dv.s, ix, reinterpret_cast<const double *>(bsrc),
+                                           reinterpret_cast<double *>(W->delta[d]), p.it1 - p.it0, 0,
+                                           W->nelem, W->dbm[d], dv.scr_dirty));
+                else
+                    CK(jk::scatter_add_i32(dv.s, ix, reinterpret_cast<const int32_t *>(bsrc),
+                                           reinterpret_cast<int32_t *>(W->delta[d]), p.it1 - p.it0, 0,
+                                           W->nelem, W->dbm[d], dv.scr_dirty));
+            }
+            CK(cudaEventRecord(dv.pe, dv.s));
+        }
+    }
     for (int d = 0; d < n; d++) {
         if (!local(d)) continue;
         Device &dv = R.dev[d];
@@ -1084,12 +1171,12 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         set_dev(d);
         // (the first launch of a capture skips them: every earlier launch is
         // complete and its events live outside the graph)
-        if (!(R.capturing && R.cap.launches == 0))
+        if (!(R.capturing && R.cap.launches == 0) && !waited[d])
             for (int q = 0; q < n; q++)
                 if (q != d && (comm[d][q] || R.comm_prev[d][q]))
                     CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
         for (const Pull &pl : pulls) {
-            if (pl.dst != d) continue;
+            if (pl.dst != d || waited[d]) continue;
             const size_t e = pl.reg->elem;
             // UVA: peer device pointer or CUDA-IPC mapped peer replica
             CK(cudaMemcpyAsync(pl.reg->rep[d] + pl.lo * e, pl.reg->rep[pl.src] + pl.lo * e,
@@ -1174,6 +1261,24 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             }
             case JACC_LOOP_SCATTER_ADD_F64:
             case JACC_LOOP_SCATTER_ADD_I32: {
+                if (L.itersplit) {
+                    // phase 2: owner of the word-aligned slice adds every delta
+                    for (int q = 0; q < n; q++)
+                        if (q != d) CK(cudaStreamWaitEvent(dv.s, R.dev[q].pe, 0));
+                    jk::PeerPtrs dl{}, db{};
+                    for (int q = 0; q < n; q++) {
+                        dl.p[dl.n++] = W->delta[q];
+                        db.p[db.n++] = W->dbm[q];
+                    }
+                    const int64_t w0 = p.own_lo >> 5, w1 = (p.own_hi + 31) >> 5;
+                    if (p.own_hi > p.own_lo)
+                        CK(jk::scatter_combine(dv.s, id == JACC_LOOP_SCATTER_ADD_F64, W->rep[d],
+                                               W->bitmap[d], dl, db, w0, w1, W->nelem, drec));
+                    else
+                        CK(cudaMemsetAsync(drec, 0xff, 16, dv.s));
+                    merged_bytes += (uint64_t)(p.own_hi - p.own_lo) * W->elem * (n - 1);
+                    break;
+                }
                 const int32_t *ix = reinterpret_cast<const int32_t *>(L.a[0].reg->rep[d]) + L.a[0].off + p.i0;
                 uint32_t *bm = W->bitmap[d];
                 {
@@ -1410,6 +1515,9 @@ jacc_status jacc_init(int n_devices, const int *device_ids) {
                 CK(cudaMalloc(&dv.res, 8));
                 CK(cudaMemset(dv.part, 0, 8));
                 CK(cudaMallocHost(&dv.hscal, 8));
+                CK(cudaEventCreateWithFlags(&dv.pe, cudaEventDisableTiming));
+                CK(cudaMalloc(&dv.scr_dirty, 32));
+                CK(cudaMemset(dv.scr_dirty, 0xff, 32));
             }
             // peer access between distinct GPUs (NVLink / NVSwitch P2P)
             for (int d = 0; d < n_devices; d++)
@@ -1485,6 +1593,8 @@ jacc_status jacc_finalize(void) {
         cudaSetDevice(dv.ord);
         if (dv.comm) ncclCommDestroy(dv.comm);
         if (dv.scratch) cudaFree(dv.scratch);
+        if (dv.pe) cudaEventDestroy(dv.pe);
+        if (dv.scr_dirty) cudaFree(dv.scr_dirty);
         cudaFree(dv.partials);
         cudaFree(dv.ticket);
         cudaFree(dv.part);
@@ -1560,6 +1670,13 @@ jacc_status jacc_set_merge_policy(int policy) {
     return JACC_OK;
 }
 
+jacc_status jacc_set_scatter_split(int iteration_split) {
+    if (!R.init || R.poisoned) return JACC_ERR_STATE;
+    if (iteration_split && R.mp) return JACC_ERR_INVALID;
+    R.scatter_itersplit = iteration_split != 0;
+    return JACC_OK;
+}
+
 jacc_status jacc_set_split_dim(int dim) {
     if (!R.init || R.poisoned) return JACC_ERR_STATE;
     if (dim < -1 || dim > 2) return JACC_ERR_INVALID;
@@ -1608,6 +1725,8 @@ jacc_status jacc_data_create(void *host, size_t bytes, size_t elem_size, int ndi
         r->bitmap.assign(R.n, nullptr);
         r->dslot.assign(R.n, 0);
         r->bytemap.assign(R.n, nullptr);
+        r->delta.assign(R.n, nullptr);
+        r->dbm.assign(R.n, nullptr);
         r->epoch.assign(R.n, 0);
         r->valid.assign(R.n, IntervalSet{});
         for (int d = 0; d < R.n; d++) {

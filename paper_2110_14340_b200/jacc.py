@@ -57,6 +57,7 @@ EXPORTS = [
     "jacc_adaptive_replay", "jacc_adaptive_history",
     "jacc_graph_begin", "jacc_graph_end", "jacc_graph_replay", "jacc_graph_destroy",
     "jacc_select_split_dim", "jacc_exchange_plan", "jacc_set_split_dim",
+    "jacc_set_scatter_split",
 ]
 JACC_MODE_ADAPTIVE = 2
 JACC_UNIQUE_ID_BYTES = 128
@@ -89,6 +90,7 @@ for _name, _args in {
     "jacc_set_merge_policy": [_I],
     "jacc_set_mode": [_I],
     "jacc_set_split_dim": [_I],
+    "jacc_set_scatter_split": [_I],
     "jacc_data_create": [_P, _SZ, _SZ, _I, ctypes.POINTER(ctypes.c_int64)],
     "jacc_data_delete": [_P],
     "jacc_update_device": [_P, _SZ, _SZ],
@@ -175,6 +177,10 @@ def jacc_partition(E, n, d):
 
 def jacc_set_merge_policy(policy):
     return _ck(lib.jacc_set_merge_policy(policy), "jacc_set_merge_policy")
+
+
+def jacc_set_scatter_split(iteration_split):
+    return _ck(lib.jacc_set_scatter_split(1 if iteration_split else 0), "jacc_set_scatter_split")
 
 
 def jacc_set_split_dim(dim):

@@ -850,3 +850,42 @@ def test_split_dim_validation(J):
         st = J.jacc_launch_status(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)])
         assert st == J.JACC_ERR_INVALID          # a 2-D array has no dim 2
         J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(0, 10), [_in(J, y), _out(J, x)])  # 1-D: dim 0
+
+
+# --------------------------------------------------------------------------
+# NEXT-3 iteration-split scatter with an additive merge
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [2, 3, 8])
+@pytest.mark.parametrize("sizes", [(100_003, 5000), (1_000_000, 1_000_003)])
+@pytest.mark.parametrize("dtype", ["f64", "i32"])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_scatter_iteration_split(J, n, sizes, dtype, policy):
+    N, M = sizes
+    idx = synth.index_i32(N, M, 102, 5)
+    if dtype == "f64":
+        b, a0 = synth.dyadic_f64(N, 102, 6), synth.dyadic_f64(M, 102, 7)
+        loop = J.JACC_LOOP_SCATTER_ADD_F64
+    else:
+        b, a0 = synth.int_i32(N, -1000, 1000, 102, 6), synth.int_i32(M, -10**6, 10**6, 102, 7)
+        loop = J.JACC_LOOP_SCATTER_ADD_I32
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    orc.scatter_add(idx, b, ref)             # two launches
+    a = a0.copy()
+    with runtime(J, n, policy):
+        J.jacc_set_scatter_split(1)
+        _create(J, idx, b, a)
+        args = [_in(J, idx), _in(J, b), _inout(J, a)]
+        J.jacc_launch(loop, J.make_range(0, N), args)
+        J.jacc_launch(loop, J.make_range(0, N), args)   # deltas must have been re-zeroed
+        words = (M + 31) // 32
+        for d in range(n):
+            w0, w1 = orc.partition(words, n, d)
+            lo, hi = min(32 * w0, M), min(32 * w1, M)
+            bm, mn, mx = orc.scatter_add_filtered(idx, b, a0.copy(), lo, hi - 1)
+            assert np.array_equal(J.jacc_get_dirty_bitmap(a, d, M), bm)
+            assert J.jacc_get_dirty_range(a, d) == (mn, mx)
+            if policy == 0:
+                assert np.array_equal(J.jacc_get_replica(a, d), ref)
+        J.jacc_update_host(a)
+    assert np.array_equal(a, ref)
