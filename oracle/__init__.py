@@ -51,6 +51,8 @@ def _load():
                                     ctypes.c_float, ctypes.POINTER(ctypes.c_double), PU, PU],
                                    ctypes.c_float),
             "orc_himeno_copy": ([I, I, I, P, P, I, I, PU, PU], None),
+            "orc_fig4": ([I, P, P, P, D, P, P], None),
+            "orc_fig4_filtered": ([I, P, P, P, D, P, P, I, I, I, I, PU, PU, PU, PU], None),
             "orc_exchange_bitmap": ([ctypes.c_int, P, ctypes.c_size_t, I, P], None),
         }
         for name, (args, res) in sig.items():
@@ -223,3 +225,19 @@ def himeno_iterations(nn, p, a, b, c, wrk1, bnd, wrk2, omega=0.8):
         g = himeno_stencil(p, a, b, c, wrk1, bnd, wrk2, omega)
         himeno_copy(wrk2, p)
     return g
+
+
+# ---- NEXT-3 Fig. 4 statement chain -----------------------------
+def fig4(jx, kx, c, x_in, a, b):
+    """Sequential loop of Fig. 4 (top), in place on a and b."""
+    _load().orc_fig4(jx.size, _p(jx), _p(kx), _p(c), x_in, _p(a), _p(b))
+
+
+def fig4_filtered(jx, kx, c, x_in, a, b, a_bounds, b_bounds):
+    """Fig. 4 (bottom) for one device; bounds inclusive; returns the write
+    logs ((amin, amax), (bmin, bmax))."""
+    v = [ctypes.c_uint64() for _ in range(4)]
+    _load().orc_fig4_filtered(jx.size, _p(jx), _p(kx), _p(c), x_in, _p(a), _p(b),
+                              a_bounds[0], a_bounds[1], b_bounds[0], b_bounds[1],
+                              *[ctypes.byref(t) for t in v])
+    return (v[0].value, v[1].value), (v[2].value, v[3].value)

@@ -453,3 +453,53 @@ void orc_himeno_copy(int64_t I, int64_t J, int64_t K, const float *wrk2, float *
     if (wmax) *wmax = mx;
 }
 #undef HI
+
+/* ------------------------------------------------------------------ */
+/* NEXT-3  Fig. 4 predicate-filtered statement chain.       */
+/* Loop body (x is firstprivate, initialised to x_in every iteration):  */
+/*   a[i]=x; b[i]=a[i]; x=c[j]; a[k]=x; b[k]=a[k];                      */
+/* with j = jx[i], k = kx[i] (index arrays).  Sequential oracle:        */
+/* ------------------------------------------------------------------ */
+void orc_fig4(int64_t n, const int32_t *jx, const int32_t *kx, const double *c, double x_in,
+              double *a, double *b)
+{
+    for (int64_t i = 0; i < n; i++) {
+        double x = x_in;
+        int64_t j = jx[i], k = kx[i];
+        a[i] = x;
+        b[i] = a[i];
+        x = c[j];
+        a[k] = x;
+        b[k] = a[k];
+    }
+}
+
+/* The filtered code of Fig. 4 (bottom) for one device, guards verbatim:
+ *   ((a_lb<=i && a_ub>=i)||(b_lb<=i && b_ub>=i)) ? a[i]=x : a[i];
+ *   ((b_lb<=i && b_ub>=i)) ? b[i]=a[i] : b[i];
+ *   x = ((a_lb<=k && a_ub>=k)||(b_lb<=k && b_ub>=k)) ? c[j] : 0;
+ *   ((a_lb<=k && a_ub>=k)||(b_lb<=k && b_ub>=k)) ? a[k]=x : a[k];
+ *   ((b_lb<=k && b_ub>=k)) ? b[k]=a[k] : b[k];
+ * Bounds inclusive.  Records the write logs of a and b (min/max
+ * of every executed store, including the duplicated stores to a outside
+ * a's own bounds that the guards of b require). */
+void orc_fig4_filtered(int64_t n, const int32_t *jx, const int32_t *kx, const double *c,
+                       double x_in, double *a, double *b, int64_t a_lb, int64_t a_ub,
+                       int64_t b_lb, int64_t b_ub, uint64_t *amin, uint64_t *amax,
+                       uint64_t *bmin, uint64_t *bmax)
+{
+    uint64_t an = UINT64_MAX, ax = 0, bn = UINT64_MAX, bx = 0;
+#define LOGW(mn, mx, f) do { if ((uint64_t)(f) < mn) mn = (uint64_t)(f); \
+                             if ((uint64_t)(f) > mx) mx = (uint64_t)(f); } while (0)
+    for (int64_t i = 0; i < n; i++) {
+        double x = x_in;
+        int64_t j = jx[i], k = kx[i];
+        if ((a_lb <= i && a_ub >= i) || (b_lb <= i && b_ub >= i)) { a[i] = x; LOGW(an, ax, i); }
+        if (b_lb <= i && b_ub >= i) { b[i] = a[i]; LOGW(bn, bx, i); }
+        x = ((a_lb <= k && a_ub >= k) || (b_lb <= k && b_ub >= k)) ? c[j] : 0;
+        if ((a_lb <= k && a_ub >= k) || (b_lb <= k && b_ub >= k)) { a[k] = x; LOGW(an, ax, k); }
+        if (b_lb <= k && b_ub >= k) { b[k] = a[k]; LOGW(bn, bx, k); }
+    }
+#undef LOGW
+    *amin = an; *amax = ax; *bmin = bn; *bmax = bx;
+}

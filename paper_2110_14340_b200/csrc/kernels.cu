@@ -848,7 +848,7 @@ __device__ __forceinline__ float kp(const PRow &R, int e) { return e == 3 ? R.r 
 // shuffle -- ~45 load instructions per 4 points instead of 124.  The
 // unaligned head/tail (<= 3 + 3 points) take the scalar path.  Arithmetic
 // per point exactly as written.
-__global__ void __launch_bounds__(HT) himeno_stencil_kernel(
+__global__ void __launch_bounds__(HT, 2) himeno_stencil_kernel(
     const float *__restrict__ p, const float *__restrict__ a, const float *__restrict__ b,
     const float *__restrict__ c, const float *__restrict__ wrk1, const float *__restrict__ bnd,
     float *__restrict__ wrk2, int64_t I, int64_t J, int64_t K, int64_t i0, int64_t i1, int64_t j0,
@@ -972,40 +972,60 @@ __global__ void __launch_bounds__(HT) himeno_stencil_kernel(
     publish_dirty_flat(mn, mx, dirty);
 }
 
-// copy loop: one warp per (i, j) row of the box, 4 independent loads in
-// flight per lane
+// copy loop: one warp per (i, j) row of the box; the 16-byte-aligned body
+// as float4 (p and wrk2 share the layout), head / tail as scalars
 __global__ void __launch_bounds__(HT) himeno_copy_kernel(
     const float *__restrict__ wrk2, float *__restrict__ p, int64_t J, int64_t K, int64_t i0,
     int64_t i1, int64_t j0, int64_t j1, int64_t k0, int64_t k1, u64 *dirty, float *push_top,
     float *push_bot) {
     const int lane = threadIdx.x & 31;
     const int64_t P = J * K;
-    const int64_t nj = j1 - j0, rows = (i1 - i0) * nj, len = k1 - k0;
+    const int64_t nj = j1 - j0, rows = (i1 - i0) * nj;
     const int64_t wg = ((int64_t)blockIdx.x * HT + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * HT) >> 5;
+    const bool vec = ((reinterpret_cast<uintptr_t>(wrk2) | reinterpret_cast<uintptr_t>(p) |
+                       reinterpret_cast<uintptr_t>(push_top) | reinterpret_cast<uintptr_t>(push_bot)) &
+                      15) == 0;
     u64 mn = kU64Max, mx = 0;
     for (int64_t r = wg; r < rows; r += nw) {
         const int64_t i = i0 + r / nj, j = j0 + r % nj;
-        const int64_t base = i * P + j * K + k0;
+        const int64_t rb = i * P + j * K;
         float *tp = (i == i0) ? push_top : nullptr;
         float *bp = (i == i1 - 1) ? push_bot : nullptr;
-        for (int64_t kk = lane; kk < len; kk += 128) {
-            float v[4];
+        int64_t ka = vec ? k0 + ((4 - ((rb + k0) & 3)) & 3) : k1;
+        if (ka > k1) ka = k1;
+        const int64_t nch = (k1 - ka) >> 2, kt = ka + 4 * nch;
+        // scalar head [k0, ka) and tail [kt, k1)
+        for (int64_t k = k0 + lane; k < ka; k += 32) {
+            const float v = __ldcs(wrk2 + rb + k);
+            __stcs(p + rb + k, v);
+            if (tp) tp[rb + k] = v;
+            if (bp) bp[rb + k] = v;
+        }
+        for (int64_t k = kt + lane; k < k1; k += 32) {
+            const float v = __ldcs(wrk2 + rb + k);
+            __stcs(p + rb + k, v);
+            if (tp) tp[rb + k] = v;
+            if (bp) bp[rb + k] = v;
+        }
+        for (int64_t ch = lane; ch < nch; ch += 64) {
+            float4 v[2];
 #pragma unroll
-            for (int u = 0; u < 4; u++)
-                if (kk + 32 * u < len) v[u] = __ldcs(wrk2 + base + kk + 32 * u);
+            for (int u = 0; u < 2; u++)
+                if (ch + 32 * u < nch)
+                    v[u] = __ldcs(reinterpret_cast<const float4 *>(wrk2 + rb + ka) + ch + 32 * u);
 #pragma unroll
-            for (int u = 0; u < 4; u++)
-                if (kk + 32 * u < len) {
-                    const int64_t x = base + kk + 32 * u;
-                    __stcs(p + x, v[u]);
-                    if (tp) tp[x] = v[u];
-                    if (bp) bp[x] = v[u];
+            for (int u = 0; u < 2; u++)
+                if (ch + 32 * u < nch) {
+                    const int64_t x = rb + ka + 4 * (ch + 32 * u);
+                    __stcs(reinterpret_cast<float4 *>(p + x), v[u]);
+                    if (tp) *reinterpret_cast<float4 *>(tp + x) = v[u];
+                    if (bp) *reinterpret_cast<float4 *>(bp + x) = v[u];
                 }
         }
-        if (len > 0) {
-            mn = (u64)base < mn ? (u64)base : mn;
-            mx = (u64)(base + len - 1) > mx ? (u64)(base + len - 1) : mx;
+        if (k1 > k0) {
+            mn = (u64)(rb + k0) < mn ? (u64)(rb + k0) : mn;
+            mx = (u64)(rb + k1 - 1) > mx ? (u64)(rb + k1 - 1) : mx;
         }
     }
     publish_dirty_flat(mn, mx, dirty);
