@@ -211,6 +211,13 @@ jacc_status jacc_update_host(void *host, size_t offset_bytes, size_t bytes);
  *       ss = (s0*a3 - p)*bnd; gosa += ss*ss; wrk2 = p + omega*ss (fp32 as
  *       written; gosa accumulated in fp64).
  *   JACC_LOOP_HIMENO_COPY_F32 : wrk2 IN, p OUT; p = wrk2 over the range.
+ *   JACC_LOOP_FIG4_F64        (NEXT-3, Fig. 4): jx IN i32[n],
+ *       kx IN i32[n], c IN f64, a OUT f64, b OUT f64, x SCALAR_F64; for i in
+ *       range: x = x_in; a[i]=x; b[i]=a[i]; x=c[jx[i]]; a[kx[i]]=x;
+ *       b[kx[i]]=a[kx[i]] -- two written arrays divided separately, every
+ *       store guarded as in Fig. 4 (a's stores by a's and b's blocks, b's
+ *       by b's, the read of c by the guard of the stores it feeds).  The
+ *       loop must be race-free (kx injective, disjoint from the range).
  * 1-D array arguments may point inside a region (the loop's array starts
  * there); multi-dimensional arguments must point at the region base. */
 enum {
@@ -222,7 +229,8 @@ enum {
     JACC_LOOP_SCATTER_ADD_F64 = 6,
     JACC_LOOP_SCATTER_ADD_I32 = 7,
     JACC_LOOP_HIMENO_F32 = 8,
-    JACC_LOOP_HIMENO_COPY_F32 = 9
+    JACC_LOOP_HIMENO_COPY_F32 = 9,
+    JACC_LOOP_FIG4_F64 = 10
 };
 
 /* Iteration range, half-open per dimension (R-3). */

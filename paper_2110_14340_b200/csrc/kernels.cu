@@ -1087,6 +1087,50 @@ __global__ void __launch_bounds__(256) scatter_combine_kernel(T *a, uint32_t *bm
 }
 
 // ---------------------------------------------------------------------------
+// NEXT-3  Fig. 4 filtered statement chain
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) fig4_kernel(const int32_t *__restrict__ jx,
+                                                   const int32_t *__restrict__ kx,
+                                                   const double *__restrict__ c, int64_t nc,
+                                                   double x_in, double *a, double *b, int64_t na,
+                                                   int64_t i0, int64_t i1, int64_t alo, int64_t ahi,
+                                                   int64_t blo, int64_t bhi, u64 *adirty,
+                                                   u64 *bdirty) {
+    u64 an = kU64Max, ax = 0, bn = kU64Max, bx = 0;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < i1; i += nth) {
+        double x = x_in;
+        const int64_t j = __ldg(jx + i), k = __ldg(kx + i);
+        const bool ia = i >= alo && i < ahi, ib = i >= blo && i < bhi;
+        if (ia || ib) {
+            a[i] = x;
+            an = (u64)i < an ? (u64)i : an;
+            ax = (u64)i > ax ? (u64)i : ax;
+        }
+        if (ib) {
+            b[i] = x;  // = a[i], just stored by this thread
+            bn = (u64)i < bn ? (u64)i : bn;
+            bx = (u64)i > bx ? (u64)i : bx;
+        }
+        const bool ka = k >= alo && k < ahi, kb = k >= blo && k < bhi;
+        const bool gk = (ka || kb) && k < na && j >= 0 && j < nc;
+        x = gk ? __ldg(c + j) : 0.0;  // the read of c carries the guard of the writes it feeds
+        if (gk) {
+            a[k] = x;
+            an = (u64)k < an ? (u64)k : an;
+            ax = (u64)k > ax ? (u64)k : ax;
+            if (kb) {
+                b[k] = x;  // = a[k]
+                bn = (u64)k < bn ? (u64)k : bn;
+                bx = (u64)k > bx ? (u64)k : bx;
+            }
+        }
+    }
+    publish_dirty<8>(an, ax, adirty);
+    publish_dirty<8>(bn, bx, bdirty);
+}
+
+// ---------------------------------------------------------------------------
 // BK5  merges over peer memory (NVLink P2P stores; plain stores for virtual
 // devices that share one GPU)
 // ---------------------------------------------------------------------------
@@ -1433,6 +1477,15 @@ cudaError_t scatter_combine(cudaStream_t s, bool is_f64, void *a, uint32_t *bm_o
     else
         scatter_combine_kernel<int32_t><<<g, 256, 0, s>>>(static_cast<int32_t *>(a), bm_out, deltas,
                                                           dbms, w0, w1, M, dirty);
+    return cudaGetLastError();
+}
+
+cudaError_t fig4(cudaStream_t s, const int32_t *jx, const int32_t *kx, const double *c, int64_t nc,
+                 double x_in, double *a, double *b, int64_t na, int64_t i0, int64_t i1, int64_t alo,
+                 int64_t ahi, int64_t blo, int64_t bhi, u64 *adirty, u64 *bdirty) {
+    if (i1 <= i0) return cudaSuccess;
+    fig4_kernel<<<grid_for(i1 - i0, 256 * 4, 148 * 8), 256, 0, s>>>(
+        jx, kx, c, nc, x_in, a, b, na, i0, i1, alo, ahi, blo, bhi, adirty, bdirty);
     return cudaGetLastError();
 }
 

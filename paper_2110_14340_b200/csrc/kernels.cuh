@@ -105,6 +105,16 @@ cudaError_t scatter_combine(cudaStream_t s, bool is_f64, void *a, uint32_t *bm_o
                             PeerPtrs deltas, PeerPtrs dbms, int64_t w0, int64_t w1, int64_t M,
                             u64 *dirty);
 
+// NEXT-3  Fig. 4 statement chain, filtered for one device:
+// for i in [i0,i1): x = x_in; j = jx[i]; k = kx[i];
+//   (i in A|B) ? a[i] = x;  (i in B) ? b[i] = a[i];
+//   x = (k in A|B) ? c[j] : 0;  (k in A|B) ? a[k] = x;  (k in B) ? b[k] = a[k];
+// A = [alo,ahi), B = [blo,bhi) (half-open owned blocks of a and b); every
+// executed store is logged (dirty a / dirty b), duplicated a stores included.
+cudaError_t fig4(cudaStream_t s, const int32_t *jx, const int32_t *kx, const double *c, int64_t nc,
+                 double x_in, double *a, double *b, int64_t na, int64_t i0, int64_t i1, int64_t alo,
+                 int64_t ahi, int64_t blo, int64_t bhi, u64 *adirty, u64 *bdirty);
+
 // BK5  Dirty-region merge over peer memory.  merge_range copies the
 // recorded span [dirty min, dirty max] (clamped to [lo, hi)) of src into
 // every peer replica; `max_elems` bounds the grid (host-known write bound).

@@ -486,6 +486,7 @@ struct DevPlan {
     int64_t i0 = 0, i1 = 0, j0 = 0, j1 = 0;  // iteration sub-range
     int64_t k0 = 0, k1 = 0;                  // (3-D loops)
     int64_t it0 = 0, it1 = 0;                // iteration block (iteration-split scatter)
+    int64_t w2lo = 0, w2hi = 0;              // owned block of the second written array
     int64_t blo[3] = {0, 0, 0}, bhi[3] = {0, 0, 0};  // write box (box loops)
     std::vector<std::pair<int64_t, int64_t>> wbox;   // exact write intervals (split dim > 0)
     int64_t wlo = 0, whi = 0;                // write bound (elements of written region), [wlo,whi)
@@ -502,6 +503,7 @@ struct Desc {
     int out_arg;       // index of written array (-1 none)
     bool reduction;
     int halo_rows;     // stencil radius along the split dim (HALO prediction)
+    int out2 = -1;     // second written array (Fig. 4 chain), -1 none
 };
 
 const Desc kDescs[] = {
@@ -517,6 +519,10 @@ const Desc kDescs[] = {
       JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT, JACC_ARG_REDUCE_SUM_F64, JACC_ARG_SCALAR_F64},
      {4, 4, 4, 4, 4, 4, 4, 0, 0}, 6, true, 0},
     {JACC_LOOP_HIMENO_COPY_F32, "himeno_copy_f32", 2, {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT}, {4, 4}, 1, false, 1},
+    {JACC_LOOP_FIG4_F64, "fig4_f64", 6,
+     {JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_IN, JACC_ARG_ARRAY_OUT, JACC_ARG_ARRAY_OUT,
+      JACC_ARG_SCALAR_F64},
+     {4, 4, 8, 8, 8, 0}, 3, false, 0, 4},
 };
 
 const Desc *find_desc(int id) {
@@ -751,6 +757,22 @@ void plan_launch(Launch &L) {
         } else if (id == JACC_LOOP_GEMM_F64 || id == JACC_LOOP_HIMENO_F32 ||
                    id == JACC_LOOP_HIMENO_COPY_F32) {
             plan_box(L, d, nd, dd, p);
+        } else if (id == JACC_LOOP_FIG4_F64) {
+            // NEXT-3 Fig. 4: every device runs all iterations; stores are
+            // guarded by the owned blocks of a and of b
+            Region *ar = L.a[3].reg, *br = L.a[4].reg;
+            partition(ar->nelem, nd, dd, p.own_lo, p.own_hi);
+            partition(br->nelem, nd, dd, p.w2lo, p.w2hi);
+            p.i0 = L.rg.lo[0];
+            p.i1 = L.rg.hi[0];
+            p.wlo = p.own_lo;
+            p.whi = p.own_hi;
+            p.active = p.i1 > p.i0;
+            if (p.active) {
+                for (int k = 0; k < 2; k++)
+                    p.reads.push_back({L.a[k].reg, L.a[k].off + p.i0, L.a[k].off + p.i1});
+                p.reads.push_back({L.a[2].reg, 0, L.a[2].reg->nelem});  // c[j]: any j
+            }
         } else if (L.itersplit) {
             // NEXT-3: iterations split in blocks; a divided in word-aligned
             // owner slices, each owner adds every device's delta
@@ -980,11 +1002,19 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
                 if (k == 2) continue;  // a is indexed by idx values
             }
+            if (id == JACC_LOOP_FIG4_F64 && k >= 2) continue;  // c[j], a[i|k], b[i|k]
             invalid_if(L.a[k].off + rg.hi[0] > L.a[k].reg->nelem);
         }
         if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
             invalid_if(L.a[2].off != 0);
             invalid_if(L.a[2].reg == L.a[0].reg || L.a[2].reg == L.a[1].reg);  // race (R-12)
+        }
+        if (id == JACC_LOOP_FIG4_F64) {
+            invalid_if(L.a[3].off != 0 || L.a[4].off != 0 || L.a[2].off != 0);
+            invalid_if(rg.hi[0] > std::min(L.a[3].reg->nelem, L.a[4].reg->nelem));
+            invalid_if(L.a[3].reg == L.a[4].reg);  // a and b distinct (R-12)
+            for (int k = 0; k < 3; k++)
+                invalid_if(L.a[k].reg == L.a[3].reg || L.a[k].reg == L.a[4].reg);
         }
         if (id == JACC_LOOP_SQUARE_F32 && L.a[0].reg == L.a[1].reg) {
             // two pointers to one array, one read and one written:
@@ -1046,14 +1076,17 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     const int n = R.n;
     const int out = D->out_arg;
     Region *W = out >= 0 ? L.a[out].reg : nullptr;
+    Region *W2 = D->out2 >= 0 ? L.a[D->out2].reg : nullptr;  // second written array
     // elements of the write block the kernel may leave untouched must be
     // current on the owner before it is declared valid there (normally a
     // no-op: an owner is the only writer of its block)
     if (W && id != JACC_LOOP_SCATTER_ADD_F64 && id != JACC_LOOP_SCATTER_ADD_I32)
         for (int d = 0; d < n; d++)
-            if (L.plan[d].active)
+            if (L.plan[d].active) {
                 for (auto &iv : write_intervals(L.plan[d]))
                     L.plan[d].reads.push_back({W, iv.first, iv.second});
+                if (W2) L.plan[d].reads.push_back({W2, L.plan[d].w2lo, L.plan[d].w2hi});
+            }
 
     // ---- pulls: stale input intervals (validity tracker) -------------------
     std::vector<Pull> pulls;
@@ -1203,6 +1236,12 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             drec = W->dirty[d] + 2 * W->dslot[d];
             if (!p.active) CK(cudaMemsetAsync(drec, 0xff, 16, dv.s));  // nothing will write it
         }
+        u64 *drec2 = nullptr;
+        if (W2) {
+            W2->dslot[d] ^= 1;
+            drec2 = W2->dirty[d] + 2 * W2->dslot[d];
+            if (!p.active) CK(cudaMemsetAsync(drec2, 0xff, 16, dv.s));
+        }
         if (p.active) {
             switch (id) {
             case JACC_LOOP_SQUARE_F32: {
@@ -1240,6 +1279,15 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                                 reinterpret_cast<double *>(W->rep[d]), L.M, L.Nn, L.K, p.i0, p.i1,
                                 p.j0, p.j1, drec));
                 break;
+            case JACC_LOOP_FIG4_F64: {
+                const int32_t *jx = reinterpret_cast<const int32_t *>(L.a[0].reg->rep[d]) + L.a[0].off;
+                const int32_t *kx = reinterpret_cast<const int32_t *>(L.a[1].reg->rep[d]) + L.a[1].off;
+                CK(jk::fig4(dv.s, jx, kx, reinterpret_cast<const double *>(L.a[2].reg->rep[d]),
+                            L.a[2].reg->nelem, L.scalar, reinterpret_cast<double *>(W->rep[d]),
+                            reinterpret_cast<double *>(W2->rep[d]), W->nelem, p.i0, p.i1, p.own_lo,
+                            p.own_hi, p.w2lo, p.w2hi, drec, drec2));
+                break;
+            }
             case JACC_LOOP_HIMENO_F32: {
                 auto F = [&](int k) { return reinterpret_cast<const float *>(L.a[k].reg->rep[d]); };
                 CK(jk::himeno_stencil(dv.s, F(0), F(1), F(2), F(3), F(4), F(5),
@@ -1364,6 +1412,13 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 CK(jk::merge_range(dv.s, W->rep[d], pp, drec, (int64_t)W->elem, p.wlo, p.whi));
             }
             merged_bytes += (uint64_t)(p.whi - p.wlo) * W->elem * (n - 1);  // upper bound (host view)
+            if (W2) {  // second written array: its own block, its own dirty record
+                jk::PeerPtrs p2{};
+                for (int q = 0; q < n; q++)
+                    if (q != d) p2.p[p2.n++] = W2->rep[q];
+                CK(jk::merge_range(dv.s, W2->rep[d], p2, drec2, (int64_t)W2->elem, p.w2lo, p.w2hi));
+                merged_bytes += (uint64_t)(p.w2hi - p.w2lo) * W2->elem * (n - 1);
+            }
         }
         if (prof) {
             CK(cudaEventRecord(pr.m1, dv.s));
@@ -1387,6 +1442,19 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             if (L.plan[d].active)
                 for (auto &iv : write_intervals(L.plan[d])) W->valid[d].add(iv.first, iv.second);
     }
+    if (writes && W2) {
+        for (int d = 0; d < n; d++) {
+            const DevPlan &p = L.plan[d];
+            if (!p.active) continue;
+            W2->valid[d].add(p.w2lo, p.w2hi);
+            if (R.policy == JACC_MERGE_EAGER) continue;
+            for (int q = 0; q < n; q++)
+                if (q != d) W2->valid[q].remove(p.w2lo, p.w2hi);
+        }
+    }
+    if (W2 && L.dup)
+        for (int d = 0; d < n; d++)
+            if (L.plan[d].active) W2->valid[d].add(L.plan[d].w2lo, L.plan[d].w2hi);
     if (writes) {
         for (int d = 0; d < n; d++) {
             const DevPlan &p = L.plan[d];

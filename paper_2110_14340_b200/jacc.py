@@ -38,6 +38,7 @@ JACC_LOOP_SCATTER_ADD_F64 = 6
 JACC_LOOP_SCATTER_ADD_I32 = 7
 JACC_LOOP_HIMENO_F32 = 8
 JACC_LOOP_HIMENO_COPY_F32 = 9
+JACC_LOOP_FIG4_F64 = 10
 JACC_ARG_ARRAY_IN = 0
 JACC_ARG_ARRAY_OUT = 1
 JACC_ARG_ARRAY_INOUT = 2

@@ -10,7 +10,7 @@ from contextlib import contextmanager
 import numpy as np
 import pytest
 
-import oracle as orc
+import oracle as orc  # noqa: E402
 import synth
 
 pytestmark = pytest.mark.gpu
@@ -889,3 +889,36 @@ def test_scatter_iteration_split(J, n, sizes, dtype, policy):
                 assert np.array_equal(J.jacc_get_replica(a, d), ref)
         J.jacc_update_host(a)
     assert np.array_equal(a, ref)
+
+
+# --------------------------------------------------------------------------
+# NEXT-3 Fig. 4 filtered statement chain (two written arrays)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n_it", [1, 257, 100_003])
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_fig4_chain(J, n_it, n, policy):
+    from test_oracle_fig4 import _inputs
+    x_in = 0.375
+    jx, kx, c, a0, b0 = _inputs(n_it, 3)
+    a_ref, b_ref = a0.copy(), b0.copy()
+    orc.fig4(jx, kx, c, x_in, a_ref, b_ref)
+    a, b = a0.copy(), b0.copy()
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    with runtime(J, n, policy):
+        _create(J, jx, kx, c, a, b)
+        J.jacc_launch(J.JACC_LOOP_FIG4_F64, J.make_range(0, n_it),
+                      [J.arg(IN, jx), J.arg(IN, kx), J.arg(IN, c), J.arg(OUT, a), J.arg(OUT, b),
+                       J.arg(J.JACC_ARG_SCALAR_F64, f64=x_in)])
+        for d in range(n):
+            alo, ahi = orc.partition(a0.size, n, d)
+            blo, bhi = orc.partition(b0.size, n, d)
+            da, db = a0.copy(), b0.copy()
+            la, lb = orc.fig4_filtered(jx, kx, c, x_in, da, db, (alo, ahi - 1), (blo, bhi - 1))
+            assert J.jacc_get_dirty_range(a, d) == la and J.jacc_get_dirty_range(b, d) == lb
+            if policy == 0:
+                assert np.array_equal(J.jacc_get_replica(a, d), a_ref)
+                assert np.array_equal(J.jacc_get_replica(b, d), b_ref)
+        J.jacc_update_host(a)
+        J.jacc_update_host(b)
+    assert np.array_equal(a, a_ref) and np.array_equal(b, b_ref)
