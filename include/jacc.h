@@ -276,8 +276,31 @@ typedef struct {
 jacc_status jacc_launch(int loop_id, const jacc_range *range,
                         const jacc_arg *args, int nargs, int async_id);
 
-/* Wait for outstanding work (async_id -1 = all queues). */
+/* Wait for outstanding work (async_id -1 = all queues; with several async
+ * queues, async_id >= 0 waits for that queue on every device). */
 jacc_status jacc_wait(int async_id);
+
+/* NEXT-4 automated asynchronous execution (Fig. 2).  With
+ * nq > 1 queues (CUDA streams per device; the paper uses 16) every
+ * launch is scheduled by its array dependencies: RAW/WAW on the last
+ * writer of an array it touches, WAR on the last readers of an array it
+ * writes.  async_id = JACC_ASYNC_AUTO (or -1): the queue of the most recent
+ * dependency, or the least recently used queue when there is none;
+ * async_id >= 0: that queue.  The launch waits only for the other queues
+ * whose dependencies are not already ordered before it (a matrix of the
+ * latest synchronisation between queues, transitive).  Single-process mode,
+ * not during a graph capture.  nq = 1 restores the single stream. */
+#define JACC_MAX_QUEUES 32
+#define JACC_ASYNC_AUTO (-2)
+jacc_status jacc_set_queues(int nq);
+
+/* Pure host logic of the scheduler (no GPU): replay `nlaunch` launches with
+ * nreads[l] / nwrites[l] array ids (concatenated in reads / writes) and
+ * requested[l] (queue, or -1 = automatic); queue_out[l] = chosen queue,
+ * waits_out[l*nq + q] = 1 if launch l waits for queue q. */
+jacc_status jacc_queue_replay(int nq, int nlaunch, const int *nreads, const int64_t *reads,
+                              const int *nwrites, const int64_t *writes, const int *requested,
+                              int *queue_out, int *waits_out);
 
 /* ---------------------------------------------------------------------- */
 /* Introspection (parity tests and measurement)                            */

@@ -150,6 +150,84 @@ struct AdaptiveCtl {
 };
 
 // ---------------------------------------------------------------------------
+// NEXT-4: automated asynchronous execution (Fig. 2; DESIGN R-20).
+// Arrays' last writer (queue, time) and last readers (per queue) give the
+// RAW / WAW / WAR dependencies of a launch; it joins the queue of its most
+// recent dependency (none: the least recently used queue) and waits only on
+// other queues whose dependency is not already ordered before it, tracked
+// in a matrix of the latest synchronisation between queues (transitive).
+// ---------------------------------------------------------------------------
+struct QueueSched {
+    int nq = 1;
+    int64_t T = 0;
+    std::vector<int64_t> last_use;
+    std::map<int64_t, std::pair<int, int64_t>> writer;
+    std::map<int64_t, std::map<int, int64_t>> readers;
+    std::vector<std::vector<int64_t>> sync;
+    void reset(int q) {
+        nq = q;
+        T = 0;
+        last_use.assign(q, -1);
+        writer.clear();
+        readers.clear();
+        sync.assign(q, std::vector<int64_t>(q, -1));
+    }
+    int schedule(const std::vector<int64_t> &reads, const std::vector<int64_t> &writes, int req,
+                 std::vector<int> &waits) {
+        T++;
+        std::vector<int64_t> touched(reads);
+        touched.insert(touched.end(), writes.begin(), writes.end());
+        std::sort(touched.begin(), touched.end());
+        touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+        std::vector<std::pair<int, int64_t>> deps;
+        for (int64_t r : touched) {
+            auto it = writer.find(r);
+            if (it != writer.end()) deps.push_back(it->second);
+        }
+        std::vector<int64_t> ws(writes);
+        std::sort(ws.begin(), ws.end());
+        ws.erase(std::unique(ws.begin(), ws.end()), ws.end());
+        for (int64_t w : ws) {
+            auto it = readers.find(w);
+            if (it != readers.end())
+                for (auto &kv : it->second) deps.push_back({kv.first, kv.second});
+        }
+        int q;
+        if (req >= 0) {
+            q = req;
+        } else if (!deps.empty()) {
+            int64_t tmax = -1;
+            for (auto &d : deps) tmax = std::max(tmax, d.second);
+            q = nq;
+            for (auto &d : deps)
+                if (d.second == tmax) q = std::min(q, d.first);
+        } else {
+            q = 0;
+            for (int k = 1; k < nq; k++)
+                if (last_use[k] < last_use[q]) q = k;
+        }
+        std::vector<char> w(nq, 0);
+        for (auto &d : deps) {
+            const int p = d.first;
+            if (p == q || sync[q][p] >= d.second) continue;  // same queue / already solved
+            w[p] = 1;
+            sync[q][p] = last_use[p];
+            for (int x = 0; x < nq; x++) sync[q][x] = std::max(sync[q][x], sync[p][x]);
+        }
+        waits.clear();
+        for (int p = 0; p < nq; p++)
+            if (w[p]) waits.push_back(p);
+        for (int64_t r : reads) readers[r][q] = T;
+        for (int64_t x : ws) {
+            writer[x] = {q, T};
+            readers[x].clear();
+        }
+        last_use[q] = T;
+        return q;
+    }
+};
+
+// ---------------------------------------------------------------------------
 struct Device {
     int ord = 0;
     cudaStream_t s = nullptr;
@@ -161,6 +239,8 @@ struct Device {
     double *hscal = nullptr;     // pinned host scalar
     ncclComm_t comm = nullptr;
     void *scratch = nullptr;     // binned-scatter pairs (grown on demand)
+    std::vector<cudaStream_t> qs;   // async queues (qs[0] = s), NEXT-4
+    std::vector<cudaEvent_t> qev;   // last launch's completion per queue
     cudaEvent_t pe = nullptr;    // phase event (iteration-split scatter)
     u64 *scr_dirty = nullptr;    // scratch dirty record (phase-1 kernels)
     size_t scratch_bytes = 0;
@@ -222,6 +302,8 @@ struct Runtime {
     int mode = JACC_MODE_MULTI;
     int split_dim = -1;  // -1: A18 rule (dim 0 for the built-in loops)
     bool scatter_itersplit = false;
+    int nq = 1;          // async queues per device (NEXT-4); 1 = single stream
+    QueueSched sched;
     int gen = 0;
     bool distinct = true;
     bool use_nccl = false;
@@ -359,6 +441,7 @@ void local_sync() {
         if (!local(d)) continue;
         set_dev(d);
         CK(cudaStreamSynchronize(R.dev[d].s));
+        for (size_t q = 1; q < R.dev[d].qs.size(); q++) CK(cudaStreamSynchronize(R.dev[d].qs[q]));
     }
 }
 
@@ -1139,6 +1222,41 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     }
     if (R.comm_prev.empty()) R.comm_prev.assign(n, std::vector<char>(n, 0));
 
+    // ---- NEXT-4 automated async queues ---------------------------
+    // The launch joins a queue chosen from its array dependencies and waits
+    // (on every device) only for the other queues it depends on; the
+    // per-generation comm waits are then subsumed by the array tracker.
+    struct StreamSwap {
+        std::vector<cudaStream_t> saved;
+        ~StreamSwap() {
+            for (size_t d = 0; d < saved.size(); d++)
+                if (saved[d]) R.dev[d].s = saved[d];
+        }
+    } swap;
+    int qsel = 0;
+    const bool multiq = R.nq > 1;
+    if (multiq) {
+        std::vector<int64_t> rd, wr;
+        for (int k = 0; k < nargs; k++) {
+            if (!L.a[k].reg) continue;
+            const int64_t key = (int64_t)(uintptr_t)L.a[k].reg;
+            if (L.a[k].kind == JACC_ARG_ARRAY_IN || L.a[k].kind == JACC_ARG_ARRAY_INOUT) rd.push_back(key);
+            if (L.a[k].kind == JACC_ARG_ARRAY_OUT || L.a[k].kind == JACC_ARG_ARRAY_INOUT) wr.push_back(key);
+        }
+        std::vector<int> waits;
+        qsel = R.sched.schedule(rd, wr, async_id >= 0 ? async_id % R.nq : -1, waits);
+        swap.saved.assign(n, nullptr);
+        for (int d = 0; d < n; d++) {
+            swap.saved[d] = R.dev[d].s;
+            R.dev[d].s = R.dev[d].qs[qsel];
+        }
+        for (int pq : waits)
+            for (int d = 0; d < n; d++) {
+                set_dev(d);
+                for (int d2 = 0; d2 < n; d2++) CK(cudaStreamWaitEvent(R.dev[d].s, R.dev[d2].qev[pq], 0));
+            }
+    }
+
     // ---- enqueue per device -------------------------------------------------
     if (R.prof.size() > 30000) flush_prof();
     R.last_start = R.prof.size();
@@ -1171,9 +1289,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 CK(cudaMemsetAsync(W->delta[d], 0, W->bytes, dv.s));
                 CK(cudaMemsetAsync(W->dbm[d], 0, words * 4, dv.s));
             }
-            for (int q = 0; q < n; q++)
-                if (q != d && (comm[d][q] || R.comm_prev[d][q]))
-                    CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
+            if (!multiq)
+                for (int q = 0; q < n; q++)
+                    if (q != d && (comm[d][q] || R.comm_prev[d][q]))
+                        CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
             for (const Pull &pl : pulls) {
                 if (pl.dst != d) continue;
                 const size_t e = pl.reg->elem;
@@ -1204,7 +1323,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         set_dev(d);
         // (the first launch of a capture skips them: every earlier launch is
         // complete and its events live outside the graph)
-        if (!(R.capturing && R.cap.launches == 0) && !waited[d])
+        if (!(R.capturing && R.cap.launches == 0) && !waited[d] && !multiq)
             for (int q = 0; q < n; q++)
                 if (q != d && (comm[d][q] || R.comm_prev[d][q]))
                     CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
@@ -1432,6 +1551,11 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         dv.launches++;
     }
     if (R.mp) shm_store(&R.shm[R.me].launches, R.gen + 1);
+    if (multiq)
+        for (int d = 0; d < n; d++) {
+            set_dev(d);
+            CK(cudaEventRecord(R.dev[d].qev[qsel], R.dev[d].s));
+        }
     if (adaptive) R.adapt_pending.push_back({akey, n, L.dup, adapt_ws, adapt_evs});
 
     // ---- validity bookkeeping ---------------------------------------------
@@ -1534,7 +1658,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         // combines are done
         if (R.mp && !R.use_nccl) rank_barrier();
     }
-    if (async_id < 0) sync_all();
+    if (async_id == -1) sync_all();  // JACC_ASYNC_AUTO (-2) and queues >= 0 stay async
     return JACC_OK;
 }
 
@@ -1662,6 +1786,8 @@ jacc_status jacc_finalize(void) {
         if (dv.comm) ncclCommDestroy(dv.comm);
         if (dv.scratch) cudaFree(dv.scratch);
         if (dv.pe) cudaEventDestroy(dv.pe);
+        for (size_t q = 1; q < dv.qs.size(); q++) cudaStreamDestroy(dv.qs[q]);
+        for (auto e : dv.qev) cudaEventDestroy(e);
         if (dv.scr_dirty) cudaFree(dv.scr_dirty);
         cudaFree(dv.partials);
         cudaFree(dv.ticket);
@@ -1742,6 +1868,55 @@ jacc_status jacc_set_scatter_split(int iteration_split) {
     if (!R.init || R.poisoned) return JACC_ERR_STATE;
     if (iteration_split && R.mp) return JACC_ERR_INVALID;
     R.scatter_itersplit = iteration_split != 0;
+    return JACC_OK;
+}
+
+jacc_status jacc_set_queues(int nq) {
+    return guard([&]() -> jacc_status {
+        if (R.mp || R.capturing || nq < 1 || nq > JACC_MAX_QUEUES) return JACC_ERR_INVALID;
+        sync_all();
+        for (int d = 0; d < R.n; d++) {
+            Device &dv = R.dev[d];
+            set_dev(d);
+            if (dv.qs.empty()) dv.qs.push_back(dv.s);
+            while ((int)dv.qs.size() < nq) {
+                cudaStream_t st;
+                CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+                dv.qs.push_back(st);
+            }
+            while ((int)dv.qev.size() < (int)dv.qs.size()) {
+                cudaEvent_t e;
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                dv.qev.push_back(e);
+            }
+            for (size_t q = 0; q < dv.qs.size(); q++) CK(cudaEventRecord(dv.qev[q], dv.qs[q]));
+        }
+        R.nq = nq;
+        R.sched.reset(nq);
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_queue_replay(int nq, int nlaunch, const int *nreads, const int64_t *reads,
+                              const int *nwrites, const int64_t *writes, const int *requested,
+                              int *queue_out, int *waits_out) {
+    if (nq < 1 || nq > JACC_MAX_QUEUES || nlaunch < 0 || (nlaunch > 0 && (!nreads || !nwrites ||
+        !requested || !queue_out || !waits_out)))
+        return JACC_ERR_INVALID;
+    QueueSched qs;
+    qs.reset(nq);
+    int64_t ri = 0, wi = 0;
+    for (int l = 0; l < nlaunch; l++) {
+        std::vector<int64_t> rd(reads + ri, reads + ri + nreads[l]);
+        std::vector<int64_t> wr(writes + wi, writes + wi + nwrites[l]);
+        ri += nreads[l];
+        wi += nwrites[l];
+        if (requested[l] >= nq) return JACC_ERR_INVALID;
+        std::vector<int> waits;
+        queue_out[l] = qs.schedule(rd, wr, requested[l], waits);
+        for (int q = 0; q < nq; q++) waits_out[l * nq + q] = 0;
+        for (int q : waits) waits_out[l * nq + q] = 1;
+    }
     return JACC_OK;
 }
 
@@ -1920,9 +2095,15 @@ jacc_status jacc_launch(int loop_id, const jacc_range *range, const jacc_arg *ar
 }
 
 jacc_status jacc_wait(int async_id) {
-    (void)async_id;
     return guard([&]() -> jacc_status {
         if (R.capturing) return JACC_ERR_STATE;
+        if (R.nq > 1 && async_id >= 0) {  // one queue, on every device
+            for (int d = 0; d < R.n; d++) {
+                set_dev(d);
+                CK(cudaStreamSynchronize(R.dev[d].qs[async_id % R.nq]));
+            }
+            return JACC_OK;
+        }
         sync_all();
         return JACC_OK;
     });
@@ -2219,7 +2400,7 @@ void join_into(int h) {
 
 jacc_status jacc_graph_begin(void) {
     return guard([&]() -> jacc_status {
-        if (R.mp || R.capturing || R.mode == JACC_MODE_ADAPTIVE) return JACC_ERR_INVALID;
+        if (R.mp || R.capturing || R.mode == JACC_MODE_ADAPTIVE || R.nq > 1) return JACC_ERR_INVALID;
         sync_all();
         flush_prof();
         R.cap = GraphRec{};

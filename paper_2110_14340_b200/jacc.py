@@ -58,8 +58,10 @@ EXPORTS = [
     "jacc_adaptive_replay", "jacc_adaptive_history",
     "jacc_graph_begin", "jacc_graph_end", "jacc_graph_replay", "jacc_graph_destroy",
     "jacc_select_split_dim", "jacc_exchange_plan", "jacc_set_split_dim",
-    "jacc_set_scatter_split",
+    "jacc_set_scatter_split", "jacc_set_queues", "jacc_queue_replay",
 ]
+JACC_MAX_QUEUES = 32
+JACC_ASYNC_AUTO = -2
 JACC_MODE_ADAPTIVE = 2
 JACC_UNIQUE_ID_BYTES = 128
 JACC_RUNTIME_HANDLE_BYTES = 192
@@ -92,6 +94,8 @@ for _name, _args in {
     "jacc_set_mode": [_I],
     "jacc_set_split_dim": [_I],
     "jacc_set_scatter_split": [_I],
+    "jacc_set_queues": [_I],
+    "jacc_queue_replay": [_I, _I, _P, _P, _P, _P, _P, _P, _P],
     "jacc_data_create": [_P, _SZ, _SZ, _I, ctypes.POINTER(ctypes.c_int64)],
     "jacc_data_delete": [_P],
     "jacc_update_device": [_P, _SZ, _SZ],
@@ -408,3 +412,23 @@ def jacc_exchange_plan(extents, elem, split_dim, n, d):
     _ck(lib.jacc_exchange_plan(len(extents), ext, elem, split_dim, n, d, ctypes.byref(out)),
         "jacc_exchange_plan")
     return {k: getattr(out, k) for k, _ in jacc_copy2d_plan._fields_}
+
+
+# ---- NEXT-4 automated async queues -------------------------------------------
+def jacc_set_queues(nq):
+    return _ck(lib.jacc_set_queues(nq), "jacc_set_queues")
+
+
+def jacc_queue_replay(nq, trace):
+    """trace: list of (reads, writes, requested or None) -> [(queue, waits)]"""
+    m = len(trace)
+    nr = np.array([len(t[0]) for t in trace] or [0], dtype=np.int32)
+    nw = np.array([len(t[1]) for t in trace] or [0], dtype=np.int32)
+    rd = np.array([x for t in trace for x in t[0]] or [0], dtype=np.int64)
+    wr = np.array([x for t in trace for x in t[1]] or [0], dtype=np.int64)
+    rq = np.array([(-1 if t[2] is None else t[2]) for t in trace] or [0], dtype=np.int32)
+    qo = np.zeros(max(m, 1), dtype=np.int32)
+    wo = np.zeros(max(m, 1) * nq, dtype=np.int32)
+    _ck(lib.jacc_queue_replay(nq, m, nr.ctypes.data, rd.ctypes.data, nw.ctypes.data, wr.ctypes.data,
+                              rq.ctypes.data, qo.ctypes.data, wo.ctypes.data), "jacc_queue_replay")
+    return [(int(qo[l]), [q for q in range(nq) if wo[l * nq + q]]) for l in range(m)]

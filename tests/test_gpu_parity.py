@@ -922,3 +922,48 @@ def test_fig4_chain(J, n_it, n, policy):
         J.jacc_update_host(a)
         J.jacc_update_host(b)
     assert np.array_equal(a, a_ref) and np.array_equal(b, b_ref)
+
+
+# --------------------------------------------------------------------------
+# NEXT-4 automated async queues
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [1, 3])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_async_queues_independent_and_dependent_loops(J, n, policy):
+    """Two independent Jacobi problems and a dependent dot/scatter chain,
+    launched JACC_ASYNC_AUTO over 16 queues: every result equals the
+    oracle (the scheduler's waits make the cross-queue dependencies safe)."""
+    N = 130
+    A1 = synth.uniform_f64(N * N, 110, 1).reshape(N, N); B1 = synth.uniform_f64(N * N, 110, 2).reshape(N, N)
+    A2 = synth.uniform_f64(N * N, 111, 1).reshape(N, N); B2 = synth.uniform_f64(N * N, 111, 2).reshape(N, N)
+    refs = []
+    for A, B in ((A1, B1), (A2, B2)):
+        Ar, Br = A.copy(), B.copy()
+        orc.jacobi2d(3, Ar, Br)
+        refs += [Ar, Br]
+    idx = synth.index_i32(5000, N * N, 112, 5)
+    bb = synth.dyadic_f64(5000, 112, 6)
+    IN, OUT, INOUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT, J.JACC_ARG_ARRAY_INOUT
+    AUTO = J.JACC_ASYNC_AUTO
+    with runtime(J, n, policy):
+        J.jacc_set_queues(16)
+        _create(J, A1, B1, A2, B2, idx, bb)
+        for _ in range(3):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, A1), J.arg(OUT, B1)], AUTO)
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, A2), J.arg(OUT, B2)], AUTO)
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, B1), J.arg(OUT, A1)], AUTO)
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, B2), J.arg(OUT, A2)], AUTO)
+        # dependent chain on A1: scatter into it (reads A1's final state), then a dot
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, J.make_range(0, 5000),
+                      [J.arg(IN, idx), J.arg(IN, bb), J.arg(INOUT, A1.reshape(-1))], AUTO)
+        s = np.zeros(1)
+        J.jacc_launch(J.JACC_LOOP_SUM_F64, J.make_range(0, N * N),
+                      [J.arg(IN, A1.reshape(-1)), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s)], AUTO)
+        J.jacc_wait(-1)
+        for x in (A1, B1, A2, B2):
+            J.jacc_update_host(x)
+    Ar1 = refs[0].copy()
+    orc.scatter_add(idx, bb, Ar1.reshape(-1))
+    assert np.array_equal(A1, Ar1) and np.array_equal(B1, refs[1])
+    assert np.array_equal(A2, refs[2]) and np.array_equal(B2, refs[3])
+    assert s[0] == pytest.approx(orc.sum_neumaier(Ar1.reshape(-1)), rel=1e-12)
