@@ -326,7 +326,11 @@ def run_jacc(args):
         t = C.timed(timed_step, args.steps)
     bytes_step = 2 * TSTEPS * algo_bytes_per_sweep(N, n)
     value = bytes_step * args.steps / t / 1e9
-    launches = C.reduce(sum(k[2] for k in kern.values()), "sum")
+    # kernels per timed step: one loop kernel per device per launch (HALO
+    # boundary pushes are fused into it), plus one merge kernel per device
+    # per launch under EAGER with n > 1
+    per_launch = 1 + (1 if (args.merge == "eager" and n > 1) else 0)
+    launches = C.reduce(sum(k[2] for k in kern.values()), "sum") * per_launch * args.steps
     # dominant kernel: jacobi2d; average launch duration on the slowest device
     k_avg = C.reduce(max(k[0] / max(k[2], 1) for k in kern.values()), "max")
     per_dev_bytes = algo_bytes_per_sweep_dev(N, n, 0)

@@ -13,6 +13,7 @@
 #include "kernels.cuh"
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 
 namespace jk {
@@ -628,30 +629,32 @@ __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off,
     if (lane == 31) *total = inc;
 }
 
-template <typename T>
+template <typename T, int E>
 __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restrict__ idx,
                                                          const T *__restrict__ b, int64_t n,
                                                          int64_t lo, int64_t hi, int shift, int nb,
                                                          u64 *cursor, int32_t *__restrict__ pidx,
                                                          T *__restrict__ pval) {
+    constexpr int TILE = SB_T * E;
     __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB];
     __shared__ u64 gbase[SB_MAXB];
-    __shared__ int32_t sk[SB_TILE];
-    __shared__ T sv[SB_TILE];
-    __shared__ uint16_t sbk[SB_TILE];
     __shared__ unsigned total;
+    extern __shared__ __align__(16) unsigned char sdyn[];  // [TILE] T, [TILE] i32, [TILE] u16
+    T *sv = reinterpret_cast<T *>(sdyn);
+    int32_t *sk = reinterpret_cast<int32_t *>(sdyn + TILE * sizeof(T));
+    uint16_t *sbk = reinterpret_cast<uint16_t *>(sdyn + TILE * (sizeof(T) + 4));
     const int tid = threadIdx.x;
-    const int64_t ntiles = (n + SB_TILE - 1) / SB_TILE;
+    const int64_t ntiles = (n + TILE - 1) / TILE;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int i = tid; i < nb; i += SB_T) hist[i] = 0;
         __syncthreads();
-        int32_t k[SB_E];
-        T v[SB_E];
-        int bk[SB_E];
-        unsigned rk[SB_E];
+        int32_t k[E];
+        T v[E];
+        int bk[E];
+        unsigned rk[E];
 #pragma unroll
-        for (int j = 0; j < SB_E; j++) {
-            const int64_t i = t * SB_TILE + j * SB_T + tid;
+        for (int j = 0; j < E; j++) {
+            const int64_t i = t * TILE + j * SB_T + tid;
             bk[j] = -1;
             if (i < n) {
                 k[j] = __ldcs(idx + i);
@@ -662,7 +665,7 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restri
             }
         }
 #pragma unroll
-        for (int j = 0; j < SB_E; j++)
+        for (int j = 0; j < E; j++)
             if (bk[j] >= 0) rk[j] = atomicAdd(&hist[bk[j]], 1u);
         __syncthreads();
         if (tid < 32) warp_exscan(hist, loff, nb, &total);
@@ -670,7 +673,7 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restri
             gbase[i] = hist[i] ? atomicAdd(&cursor[i], (u64)hist[i]) : 0;
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < SB_E; j++)
+        for (int j = 0; j < E; j++)
             if (bk[j] >= 0) {
                 const unsigned pos = loff[bk[j]] + rk[j];
                 sk[pos] = k[j];
@@ -848,7 +851,8 @@ __device__ __forceinline__ float kp(const PRow &R, int e) { return e == 3 ? R.r 
 // shuffle -- ~45 load instructions per 4 points instead of 124.  The
 // unaligned head/tail (<= 3 + 3 points) take the scalar path.  Arithmetic
 // per point exactly as written.
-__global__ void __launch_bounds__(HT, 2) himeno_stencil_kernel(
+template <int MINB>
+__global__ void __launch_bounds__(HT, MINB) himeno_stencil_kernel(
     const float *__restrict__ p, const float *__restrict__ a, const float *__restrict__ b,
     const float *__restrict__ c, const float *__restrict__ wrk1, const float *__restrict__ bnd,
     float *__restrict__ wrk2, int64_t I, int64_t J, int64_t K, int64_t i0, int64_t i1, int64_t j0,
@@ -1374,9 +1378,19 @@ cudaError_t himeno_stencil(cudaStream_t s, const float *p, const float *a, const
                            unsigned *ticket, double *out, u64 *dirty) {
     if (i1 <= i0 || j1 <= j0 || k1 <= k0) return cudaErrorInvalidValue;
     static_assert(kHimenoGrid <= kHimenoPartials, "partials buffer");
-    himeno_stencil_kernel<<<kHimenoGrid, HT, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0, i1,
-                                                     j0, j1, k0, k1, omega, partials, ticket, out,
-                                                     dirty);
+    static int variant = -1;  // JACC_HIMENO_VARIANT: 1 = one CTA/SM (more registers)
+    if (variant < 0) {
+        const char *e = getenv("JACC_HIMENO_VARIANT");
+        variant = e ? atoi(e) : 0;
+    }
+    if (variant == 1)
+        himeno_stencil_kernel<1><<<kHimenoGrid, HT, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0,
+                                                            i1, j0, j1, k0, k1, omega, partials,
+                                                            ticket, out, dirty);
+    else
+        himeno_stencil_kernel<2><<<kHimenoGrid, HT, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0,
+                                                            i1, j0, j1, k0, k1, omega, partials,
+                                                            ticket, out, dirty);
     return cudaGetLastError();
 }
 
@@ -1398,7 +1412,12 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
     if (!(force && force[0] == '1') && (n < (1 << 22) || span * elem <= (int64_t)96 << 20))
         return p;  // a fits in L2: the direct kernel is already L2-resident
     int shift = 0;
-    while (((int64_t)elem << shift) < ((int64_t)16 << 20)) shift++;  // 16 MiB buckets
+    static int64_t bucket_mb = -1;  // JACC_SCATTER_BUCKET_MB (default 16)
+    if (bucket_mb < 0) {
+        const char *e = getenv("JACC_SCATTER_BUCKET_MB");
+        bucket_mb = e ? std::max(1, atoi(e)) : 16;
+    }
+    while (((int64_t)elem << shift) < (bucket_mb << 20)) shift++;
     while (((span + ((int64_t)1 << shift) - 1) >> shift) > SB_MAXB) shift++;
     p.binned = true;
     p.shift = shift;
@@ -1425,19 +1444,40 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     if (e != cudaSuccess) return e;
     scat_hist_kernel<<<148 * 8, 256, 0, s>>>(idx, n, lo, hi, pl.shift, pl.nb, counts);
     scat_scan_kernel<<<1, 32, 0, s>>>(counts, pl.nb, base, cursor, work);
-    const int64_t tiles = (n + SB_TILE - 1) / SB_TILE;
+    static int pe = -1;  // partition elements per thread (JACC_SCATTER_PART_E: 8 or 16)
+    if (pe < 0) {
+        const char *e = getenv("JACC_SCATTER_PART_E");
+        pe = (e && atoi(e) == 16) ? 16 : 8;
+    }
+    const int64_t tile = (int64_t)SB_T * pe;
+    const int64_t tiles = (n + tile - 1) / tile;
+    const size_t dsm = (size_t)tile * ((is_f64 ? 8 : 4) + 4 + 2);
     const int pg = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
     if (is_f64) {
-        scat_part_kernel<double><<<pg, SB_T, 0, s>>>(idx, static_cast<const double *>(b), n, lo, hi,
-                                                     pl.shift, pl.nb, cursor, pidx,
-                                                     reinterpret_cast<double *>(pv));
+        if (pe == 16) {
+            cudaFuncSetAttribute(scat_part_kernel<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+            scat_part_kernel<double, 16><<<pg, SB_T, dsm, s>>>(idx, static_cast<const double *>(b), n, lo,
+                                                                hi, pl.shift, pl.nb, cursor, pidx,
+                                                                reinterpret_cast<double *>(pv));
+        } else {
+            scat_part_kernel<double, 8><<<pg, SB_T, dsm, s>>>(idx, static_cast<const double *>(b), n, lo,
+                                                               hi, pl.shift, pl.nb, cursor, pidx,
+                                                               reinterpret_cast<double *>(pv));
+        }
         scat_apply_kernel<double><<<148 * 8, 256, 0, s>>>(
             pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
             static_cast<double *>(a), bytemap, epoch, dirty);
     } else {
-        scat_part_kernel<int32_t><<<pg, SB_T, 0, s>>>(idx, static_cast<const int32_t *>(b), n, lo,
-                                                      hi, pl.shift, pl.nb, cursor, pidx,
-                                                      reinterpret_cast<int32_t *>(pv));
+        if (pe == 16) {
+            cudaFuncSetAttribute(scat_part_kernel<int32_t, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+            scat_part_kernel<int32_t, 16><<<pg, SB_T, dsm, s>>>(idx, static_cast<const int32_t *>(b), n,
+                                                                 lo, hi, pl.shift, pl.nb, cursor, pidx,
+                                                                 reinterpret_cast<int32_t *>(pv));
+        } else {
+            scat_part_kernel<int32_t, 8><<<pg, SB_T, dsm, s>>>(idx, static_cast<const int32_t *>(b), n,
+                                                                lo, hi, pl.shift, pl.nb, cursor, pidx,
+                                                                reinterpret_cast<int32_t *>(pv));
+        }
         scat_apply_kernel<int32_t><<<148 * 8, 256, 0, s>>>(
             pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
             static_cast<int32_t *>(a), bytemap, epoch, dirty);
