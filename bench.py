@@ -304,6 +304,13 @@ def run_jacc(args):
 
     for _ in range(args.warmup):
         step()
+    # host cost of issuing one launch (plan + enqueue on every device), timed
+    # while the GPU is still busy with earlier work (asynchronous launches)
+    C.sync()
+    h0 = time.perf_counter()
+    step()
+    host_us = (time.perf_counter() - h0) / (2 * TSTEPS) * 1e6
+    J.jacc_wait()
     # kernel-level timing (CUDA events around every launch on its stream)
     J.jacc_set_profiling(1)
     J.jacc_profile_reset()
@@ -376,6 +383,7 @@ def run_jacc(args):
                    "merge": args.merge, "launch": "one process per GPU" if C.mp else "single process",
                    "issue": "CUDA graph replay of the captured step" if use_graph else "jacc_launch x200",
                    "ms_per_step_plain_launches": t_plain * 1e3,
+                   "host_us_per_launch": host_us,
                    "virtual_devices": C.virtual,
                    "l2": "no flush: inputs 2x2 GiB >> 126 MB L2",
                    "parallelism": f"row-block owner partition over {n} device(s)"},

@@ -130,7 +130,9 @@ __device__ __forceinline__ void jload(JRow<V> &o, const double *__restrict__ src
 #pragma unroll
         for (int k = 0; k < V; k++) o.v[k] = 0.0;
     }
-    o.l = (ok && lane == 0 && cs >= 1) ? __ldg(p + cs - 1) : 0.0;
+    // slab edges: only for slabs that hold columns (cs < N), else the left
+    // edge of the last row would read past the end of the array
+    o.l = (ok && lane == 0 && cs >= 1 && cs < N) ? __ldg(p + cs - 1) : 0.0;
     o.r = (ok && lane == 31 && cs + 32 * V < N) ? __ldg(p + cs + 32 * V) : 0.0;
 }
 
