@@ -366,6 +366,8 @@ def run_jacc(args):
     if args.extra and not C.mp:
         extra = run_extra_loops(J, C, n, peak)
     C.finalize()
+    if args.extra and not C.mp and n == 1:
+        extra["eager_merge_2virtual"] = eager_merge_probe(J, torch, A, B)
 
     cpu = None
     if args.cpu_baseline and n == 1 and C.rank == 0:
@@ -508,6 +510,37 @@ def run_extra_loops(J, C, n, peak):
     for arr in (hp, ha, hb, hc, hw1, hbd, hw2):
         J.jacc_data_delete(arr)
     return out
+
+
+def eager_merge_probe(J, torch, A, B):
+    """BK5 merge kernel bandwidth: J16K with two virtual devices on this GPU
+    under EAGER, so after every launch each device pushes its ~1 GiB dirty
+    half into the other replica.  On one GPU the push is a local HBM copy
+    (read + write), a proxy for the kernel's efficiency, not NVLink."""
+    J.jacc_init(2, [0, 0])
+    J.jacc_set_merge_policy(J.JACC_MERGE_EAGER)
+    for arr in (A, B):
+        J.jacc_data_create(arr)
+        J.jacc_update_device(arr)
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    args_ab = [J.arg(IN, A), J.arg(OUT, B)]
+    J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ab, 0)
+    J.jacc_wait()
+    J.jacc_set_profiling(1)
+    J.jacc_profile_reset()
+    reps = 6
+    for _ in range(reps):
+        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ab, 0)
+    J.jacc_wait()
+    k, m, nl, _ = J.jacc_profile_totals(0)
+    J.jacc_set_profiling(0)
+    lo, hi = J.jacc_partition(N_GRID, 2, 0)
+    dirty_bytes = (min(hi, N_GRID - 1) - max(lo, 1)) * N_GRID * 8   # span rows x full width
+    J.jacc_finalize()
+    mt = m / max(nl, 1)
+    return {"merge_us": mt * 1e6, "bytes_pushed": dirty_bytes,
+            "copy_gbs": 2 * dirty_bytes / mt / 1e9,
+            "note": "one peer, virtual devices: local HBM read+write, not NVLink"}
 
 
 def main():

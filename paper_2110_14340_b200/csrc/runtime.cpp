@@ -1274,6 +1274,39 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 CK(cudaMemsetAsync(W->bitmap[d], 0, words * 4, R.dev[d].s));
             }
     }
+    // binned-scatter scratch is reserved before anything is enqueued, so an
+    // allocation failure cannot leave a launch half-issued (the loop then
+    // falls back to the direct kernel on that device)
+    if (W && !R.capturing && !L.itersplit &&
+        (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32)) {
+        for (int d = 0; d < n; d++) {
+            if (!local(d) || !L.plan[d].active) continue;
+            const DevPlan &p = L.plan[d];
+            const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
+            const jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
+            if (!sp.binned) continue;
+            Device &dv = R.dev[d];
+            set_dev(d);
+            if (dv.scratch_bytes < sp.scratch) {
+                CK(cudaStreamSynchronize(dv.s));
+                if (dv.scratch) CK(cudaFree(dv.scratch));
+                dv.scratch = nullptr;
+                dv.scratch_bytes = 0;
+                if (cudaMalloc(&dv.scratch, sp.scratch) == cudaSuccess) dv.scratch_bytes = sp.scratch;
+                else cudaGetLastError();
+            }
+            const size_t bmap = (size_t)((W->nelem + 31) / 32) * 32;  // whole region
+            if (!W->bytemap[d]) {
+                if (cudaMalloc(&W->bytemap[d], bmap) == cudaSuccess) {
+                    CK(cudaMemsetAsync(W->bytemap[d], 0, bmap, dv.s));
+                    W->epoch[d] = 0;
+                } else {
+                    W->bytemap[d] = nullptr;
+                    cudaGetLastError();
+                }
+            }
+        }
+    }
     // ---- NEXT-3 phase 1: every device scatters its iteration block into its
     // delta array (after the usual waits and pulls) ---------------------------
     std::vector<char> waited(n, 0);
@@ -1457,28 +1490,11 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
                 jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
                 if (R.capturing) sp.binned = false;  // epoch byte-map state is host-side
+                if (sp.binned && (dv.scratch_bytes < sp.scratch || !W->bytemap[d]))
+                    sp.binned = false;  // scratch could not be reserved up front: direct kernel
                 if (sp.binned) {
-                    if (dv.scratch_bytes < sp.scratch) {
-                        CK(cudaStreamSynchronize(dv.s));
-                        if (dv.scratch) CK(cudaFree(dv.scratch));
-                        dv.scratch = nullptr;
-                        dv.scratch_bytes = 0;
-                        if (cudaMalloc(&dv.scratch, sp.scratch) != cudaSuccess) {
-                            cudaGetLastError();
-                            throw Fail{JACC_ERR_OOM};
-                        }
-                        dv.scratch_bytes = sp.scratch;
-                    }
-                    if (!W->bytemap[d]) {
-                        if (cudaMalloc(&W->bytemap[d], sp.bytemap) != cudaSuccess) {
-                            cudaGetLastError();
-                            throw Fail{JACC_ERR_OOM};
-                        }
-                        CK(cudaMemsetAsync(W->bytemap[d], 0, sp.bytemap, dv.s));
-                        W->epoch[d] = 0;
-                    }
                     if (W->epoch[d] == 255) {  // wrap: clear stale epochs
-                        CK(cudaMemsetAsync(W->bytemap[d], 0, sp.bytemap, dv.s));
+                        CK(cudaMemsetAsync(W->bytemap[d], 0, (size_t)((W->nelem + 31) / 32) * 32, dv.s));
                         W->epoch[d] = 0;
                     }
                     W->epoch[d]++;
