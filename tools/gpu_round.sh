@@ -15,3 +15,10 @@ cap scat_apply scatter scat_apply
 cap himeno_stencil himeno himeno_stencil
 cap himeno_copy himeno himeno_copy
 ls gpurun_out/*.ncu-rep
+# summarise on the box (ncu -i), keep the dominant kernel's report only
+python tools/summarize_ncu.py ${ROUND_TAG:-r01} > gpurun_out/summary_print.txt 2>&1
+mkdir -p gpurun_out/profiles_new && cp profiles/ncu_summary_${ROUND_TAG:-r01}.json profiles/launches_${ROUND_TAG:-r01}.md gpurun_out/profiles_new/ 2>/dev/null
+for f in gpurun_out/prof_*.ncu-rep; do
+  case "$f" in *prof_jacobi.ncu-rep) ;; *) rm -f "$f" ;; esac
+done
+du -sh gpurun_out

@@ -34,6 +34,8 @@ METRICS = {
     "lts__t_bytes.sum": "l2_bytes",
     "launch__occupancy_limit_registers": "occ_limit_regs",
     "sm__maximum_warps_per_active_cycle_pct": "theoretical_occupancy_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "smsp__inst_executed.sum": "warp_instructions",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "nsecond": 1e-9,
