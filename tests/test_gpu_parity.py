@@ -967,3 +967,30 @@ def test_async_queues_independent_and_dependent_loops(J, n, policy):
     assert np.array_equal(A1, Ar1) and np.array_equal(B1, refs[1])
     assert np.array_equal(A2, refs[2]) and np.array_equal(B2, refs[3])
     assert s[0] == pytest.approx(orc.sum_neumaier(Ar1.reshape(-1)), rel=1e-12)
+
+
+# --------------------------------------------------------------------------
+# merge traffic accounting (per-link bytes non-increasing in n)
+# --------------------------------------------------------------------------
+def test_merge_bytes_scale_with_n(J):
+    N = 514
+    A = synth.uniform_f64(N * N, 120, 1).reshape(N, N)
+    B = synth.uniform_f64(N * N, 120, 2).reshape(N, N)
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    eager, halo = {}, {}
+    for n in (2, 4, 8):
+        for policy, store in ((0, eager), (1, halo)):
+            with runtime(J, n, policy):
+                _create(J, A, B)
+                J.jacc_set_profiling(1)
+                J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, A), J.arg(OUT, B)])
+                _, _, nb = J.jacc_last_timing()
+                store[n] = nb
+    # EAGER: every device sends its block to n-1 peers: total (n-1) x block
+    # sum = (n-1)/n x the written region; per link (one peer) = block, which
+    # shrinks with n
+    per_link = {n: eager[n] / (n * (n - 1)) for n in eager}
+    assert per_link[2] > per_link[4] > per_link[8]
+    # HALO: two boundary rows per interior device, independent of the block
+    assert halo[2] == 2 * (N - 2) * 8
+    assert halo[8] == 2 * (8 - 1) * (N - 2) * 8
