@@ -289,7 +289,10 @@ jacc_status jacc_wait(int async_id);
  * async_id >= 0: that queue.  The launch waits only for the other queues
  * whose dependencies are not already ordered before it (a matrix of the
  * latest synchronisation between queues, transitive).  Single-process mode,
- * not during a graph capture.  nq = 1 restores the single stream. */
+ * not during a graph capture.  nq = 1 restores the single stream.  With
+ * several queues each queue has its own reduction scratch, scatters use the
+ * direct kernel (the binned pipeline's scratch is per device) and the
+ * iteration-split scatter is refused (JACC_ERR_INVALID). */
 #define JACC_MAX_QUEUES 32
 #define JACC_ASYNC_AUTO (-2)
 jacc_status jacc_set_queues(int nq);

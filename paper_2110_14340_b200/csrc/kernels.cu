@@ -407,7 +407,7 @@ __device__ __forceinline__ void gemm_load_tile(double *As, double *Bs, const dou
     }
 }
 
-template <int BM, int BN, int BK, int ST, int WM, int WN, bool V16>
+template <int BM, int BN, int BK, int ST, int WM, int WN, bool V16, int GROUP = 0>
 __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, ST, WM, WN>::NT)
     gemm_f64_kernel(const double *__restrict__ A, const double *__restrict__ B,
                     double *__restrict__ C, int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1,
@@ -419,8 +419,19 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, ST, WM, WN>::NT)
     double *Bs = gsm + ST * BM * G::AP;     // [ST][BK][BP]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp / WCOLS, wn = warp % WCOLS;
-    const int64_t m0 = r0 + (int64_t)blockIdx.y * BM;
-    const int64_t n0 = c0 + (int64_t)blockIdx.x * BN;
+    int64_t tm = blockIdx.y, tn = blockIdx.x;
+    if constexpr (GROUP > 0) {
+        // grouped rasterisation: GROUP row tiles sweep the column tiles
+        // together, so concurrently resident CTAs share A and B panels in L2
+        const int64_t nt = gridDim.x, mt = gridDim.y;
+        const int64_t t = (int64_t)blockIdx.y * nt + blockIdx.x;
+        const int64_t per = (int64_t)GROUP * nt, g = t / per;
+        const int64_t gm = mt - g * GROUP < GROUP ? mt - g * GROUP : GROUP;
+        tm = g * GROUP + (t % per) % gm;
+        tn = (t % per) / gm;
+    }
+    const int64_t m0 = r0 + tm * BM;
+    const int64_t n0 = c0 + tn * BN;
 
     double acc[MI][NJ][2];
 #pragma unroll
@@ -875,7 +886,17 @@ __global__ void __launch_bounds__(HT, MINB) himeno_stencil_kernel(
     const int64_t nw = ((int64_t)gridDim.x * HT) >> 5;
     double g = 0.0;
     u64 mn = kU64Max, mx = 0;
-    for (int64_t r = wg; r < rows; r += nw) {
+    // rows are handed out in global order by an atomic counter, so the
+    // rows in flight stay within a few planes and the p neighbour planes
+    // stay L2-resident (a static stride lets warps drift apart)
+    u64 *rowctr = reinterpret_cast<u64 *>(ticket + 8);
+    (void)wg;
+    (void)nw;
+    for (;;) {
+        int64_t r = 0;
+        if (lane == 0) r = (int64_t)atomicAdd(rowctr, 1ull);
+        r = __shfl_sync(0xffffffffu, r, 0);
+        if (r >= rows) break;
         const int64_t i = i0 + r / nj, j = j0 + r % nj;
         const int64_t rb = i * P + j * K;
         int64_t ka = k0 + ((4 - ((rb + k0) & 3)) & 3);  // first 16-byte aligned k
@@ -973,6 +994,7 @@ __global__ void __launch_bounds__(HT, MINB) himeno_stencil_kernel(
             for (int w = 0; w < HT / 32; w++) tot += sh[w];
             *out = tot;
             *ticket = 0u;
+            *rowctr = 0ull;  // every CTA has left the row loop
         }
     }
     publish_dirty_flat(mn, mx, dirty);
@@ -983,7 +1005,7 @@ __global__ void __launch_bounds__(HT, MINB) himeno_stencil_kernel(
 __global__ void __launch_bounds__(HT) himeno_copy_kernel(
     const float *__restrict__ wrk2, float *__restrict__ p, int64_t J, int64_t K, int64_t i0,
     int64_t i1, int64_t j0, int64_t j1, int64_t k0, int64_t k1, u64 *dirty, float *push_top,
-    float *push_bot) {
+    float *push_bot, unsigned *ticket) {
     const int lane = threadIdx.x & 31;
     const int64_t P = J * K;
     const int64_t nj = j1 - j0, rows = (i1 - i0) * nj;
@@ -993,7 +1015,14 @@ __global__ void __launch_bounds__(HT) himeno_copy_kernel(
                        reinterpret_cast<uintptr_t>(push_top) | reinterpret_cast<uintptr_t>(push_bot)) &
                       15) == 0;
     u64 mn = kU64Max, mx = 0;
-    for (int64_t r = wg; r < rows; r += nw) {
+    u64 *rowctr = reinterpret_cast<u64 *>(ticket + 8);  // dynamic row order, as the stencil
+    (void)wg;
+    (void)nw;
+    for (;;) {
+        int64_t r = 0;
+        if (lane == 0) r = (int64_t)atomicAdd(rowctr, 1ull);
+        r = __shfl_sync(0xffffffffu, r, 0);
+        if (r >= rows) break;
         const int64_t i = i0 + r / nj, j = j0 + r % nj;
         const int64_t rb = i * P + j * K;
         float *tp = (i == i0) ? push_top : nullptr;
@@ -1032,6 +1061,17 @@ __global__ void __launch_bounds__(HT) himeno_copy_kernel(
         if (k1 > k0) {
             mn = (u64)(rb + k0) < mn ? (u64)(rb + k0) : mn;
             mx = (u64)(rb + k1 - 1) > mx ? (u64)(rb + k1 - 1) : mx;
+        }
+    }
+    // the last CTA to finish resets the row counter for the next launch
+    __shared__ bool lastc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        lastc = atomicAdd(ticket + 2, 1u) == gridDim.x - 1;
+        if (lastc) {
+            *rowctr = 0ull;
+            ticket[2] = 0u;
         }
     }
     publish_dirty_flat(mn, mx, dirty);
@@ -1313,13 +1353,13 @@ cudaError_t combine(cudaStream_t s, PeerPtrs parts, double s_in, double *out) {
     return cudaGetLastError();
 }
 
-template <int BM, int BN, int BK, int ST, int WM, int WN>
+template <int BM, int BN, int BK, int ST, int WM, int WN, int GROUP = 0>
 static cudaError_t gemm_launch(cudaStream_t s, bool v16, const double *A, const double *B,
                                double *C, int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1,
                                int64_t c0, int64_t c1, u64 *dirty) {
     using G = GemmCfg<BM, BN, BK, ST, WM, WN>;
-    auto kt = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, true>;
-    auto kf = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, false>;
+    auto kt = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, true, GROUP>;
+    auto kf = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, false, GROUP>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
@@ -1352,6 +1392,9 @@ cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C
     case 4: return gemm_launch<64, 128, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
     case 5: return gemm_launch<64, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
     case 6: return gemm_launch<128, 128, 32, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 7: return gemm_launch<64, 64, 16, 3, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 8: return gemm_launch<64, 64, 16, 3, 32, 32, 16>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 9: return gemm_launch<64, 64, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
     default: return gemm_launch<64, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
     }
 }
@@ -1398,11 +1441,12 @@ cudaError_t himeno_stencil(cudaStream_t s, const float *p, const float *a, const
 
 cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, int64_t J,
                         int64_t K, int64_t i0, int64_t i1, int64_t j0, int64_t j1, int64_t k0,
-                        int64_t k1, u64 *dirty, float *push_top, float *push_bot) {
+                        int64_t k1, u64 *dirty, float *push_top, float *push_bot,
+                        unsigned *ticket) {
     (void)I;
     if (i1 <= i0 || j1 <= j0 || k1 <= k0) return cudaErrorInvalidValue;
     himeno_copy_kernel<<<kHimenoGrid, HT, 0, s>>>(wrk2, p, J, K, i0, i1, j0, j1, k0, k1, dirty,
-                                                  push_top, push_bot);
+                                                  push_top, push_bot, ticket);
     return cudaGetLastError();
 }
 

@@ -91,7 +91,8 @@ cudaError_t himeno_stencil(cudaStream_t s, const float *p, const float *a, const
                            unsigned *ticket, double *out, u64 *dirty);
 cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, int64_t J,
                         int64_t K, int64_t i0, int64_t i1, int64_t j0, int64_t j1, int64_t k0,
-                        int64_t k1, u64 *dirty, float *push_top, float *push_bot);
+                        int64_t k1, u64 *dirty, float *push_top, float *push_bot,
+                        unsigned *ticket);  // ticket: the device's zeroed counter block
 
 // NEXT-3  Iteration-split scatter with an additive merge.  Phase 1 (every
 // device, its block of iterations): the scatter kernels above with

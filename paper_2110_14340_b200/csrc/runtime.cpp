@@ -241,6 +241,9 @@ struct Device {
     void *scratch = nullptr;     // binned-scatter pairs (grown on demand)
     std::vector<cudaStream_t> qs;   // async queues (qs[0] = s), NEXT-4
     std::vector<cudaEvent_t> qev;   // last launch's completion per queue
+    // per-queue reduction scratch (concurrent queues must not share it)
+    std::vector<double *> qpartials, qpart, qres;
+    std::vector<unsigned *> qticket;
     cudaEvent_t pe = nullptr;    // phase event (iteration-split scatter)
     u64 *scr_dirty = nullptr;    // scratch dirty record (phase-1 kernels)
     size_t scratch_bytes = 0;
@@ -1113,7 +1116,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     if (R.mode == JACC_MODE_DUP) L.dup = true;
     L.itersplit = R.scatter_itersplit && R.n > 1 &&
                   (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32);
-    if (L.itersplit && (R.mp || L.dup)) return JACC_ERR_INVALID;
+    if (L.itersplit && (R.mp || L.dup || R.nq > 1)) return JACC_ERR_INVALID;
     // ---- NEXT-1 adaptive utilization (single process, n > 1) ---------------
     const bool adaptive =
         R.mode == JACC_MODE_ADAPTIVE && R.n > 1 && !R.mp && !L.dup && !R.capturing;
@@ -1228,9 +1231,17 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     // per-generation comm waits are then subsumed by the array tracker.
     struct StreamSwap {
         std::vector<cudaStream_t> saved;
+        std::vector<double *> partials, part, res;
+        std::vector<unsigned *> ticket;
         ~StreamSwap() {
             for (size_t d = 0; d < saved.size(); d++)
-                if (saved[d]) R.dev[d].s = saved[d];
+                if (saved[d]) {
+                    R.dev[d].s = saved[d];
+                    R.dev[d].partials = partials[d];
+                    R.dev[d].part = part[d];
+                    R.dev[d].res = res[d];
+                    R.dev[d].ticket = ticket[d];
+                }
         }
     } swap;
     int qsel = 0;
@@ -1246,9 +1257,24 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         std::vector<int> waits;
         qsel = R.sched.schedule(rd, wr, async_id >= 0 ? async_id % R.nq : -1, waits);
         swap.saved.assign(n, nullptr);
+        swap.partials.assign(n, nullptr);
+        swap.part.assign(n, nullptr);
+        swap.res.assign(n, nullptr);
+        swap.ticket.assign(n, nullptr);
         for (int d = 0; d < n; d++) {
-            swap.saved[d] = R.dev[d].s;
-            R.dev[d].s = R.dev[d].qs[qsel];
+            Device &dv = R.dev[d];
+            swap.saved[d] = dv.s;
+            swap.partials[d] = dv.partials;
+            swap.part[d] = dv.part;
+            swap.res[d] = dv.res;
+            swap.ticket[d] = dv.ticket;
+            dv.s = dv.qs[qsel];
+            if (qsel > 0) {  // queue 0 keeps the device's own scratch
+                dv.partials = dv.qpartials[qsel];
+                dv.part = dv.qpart[qsel];
+                dv.res = dv.qres[qsel];
+                dv.ticket = dv.qticket[qsel];
+            }
         }
         for (int pq : waits)
             for (int d = 0; d < n; d++) {
@@ -1277,7 +1303,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     // binned-scatter scratch is reserved before anything is enqueued, so an
     // allocation failure cannot leave a launch half-issued (the loop then
     // falls back to the direct kernel on that device)
-    if (W && !R.capturing && !L.itersplit &&
+    if (W && !R.capturing && !L.itersplit && R.nq == 1 &&
         (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32)) {
         for (int d = 0; d < n; d++) {
             if (!local(d) || !L.plan[d].active) continue;
@@ -1453,7 +1479,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 float *pb = (L.split == 0 && bot[d] >= 0) ? reinterpret_cast<float *>(W->rep[bot[d]]) : nullptr;
                 CK(jk::himeno_copy(dv.s, reinterpret_cast<const float *>(L.a[0].reg->rep[d]),
                                    reinterpret_cast<float *>(W->rep[d]), L.HI, L.HJ, L.HK, p.i0, p.i1,
-                                   p.j0, p.j1, p.k0, p.k1, drec, pt, pb));
+                                   p.j0, p.j1, p.k0, p.k1, drec, pt, pb, dv.ticket));
                 const int64_t planeb = (p.j1 - p.j0) * (p.k1 - p.k0) * 4;
                 if (pt) merged_bytes += planeb;
                 if (pb) merged_bytes += planeb;
@@ -1490,6 +1516,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
                 jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
                 if (R.capturing) sp.binned = false;  // epoch byte-map state is host-side
+                if (R.nq > 1) sp.binned = false;     // per-device scratch is not per queue
                 if (sp.binned && (dv.scratch_bytes < sp.scratch || !W->bytemap[d]))
                     sp.binned = false;  // scratch could not be reserved up front: direct kernel
                 if (sp.binned) {
@@ -1803,6 +1830,12 @@ jacc_status jacc_finalize(void) {
         if (dv.scratch) cudaFree(dv.scratch);
         if (dv.pe) cudaEventDestroy(dv.pe);
         for (size_t q = 1; q < dv.qs.size(); q++) cudaStreamDestroy(dv.qs[q]);
+        for (size_t q = 1; q < dv.qpartials.size(); q++) {
+            cudaFree(dv.qpartials[q]);
+            cudaFree(dv.qpart[q]);
+            cudaFree(dv.qres[q]);
+            cudaFree(dv.qticket[q]);
+        }
         for (auto e : dv.qev) cudaEventDestroy(e);
         if (dv.scr_dirty) cudaFree(dv.scr_dirty);
         cudaFree(dv.partials);
@@ -1904,6 +1937,26 @@ jacc_status jacc_set_queues(int nq) {
                 cudaEvent_t e;
                 CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
                 dv.qev.push_back(e);
+            }
+            if (dv.qpartials.empty()) {  // slot 0 = the device's own scratch
+                dv.qpartials.push_back(dv.partials);
+                dv.qpart.push_back(dv.part);
+                dv.qres.push_back(dv.res);
+                dv.qticket.push_back(dv.ticket);
+            }
+            while (dv.qpartials.size() < dv.qs.size()) {
+                double *pa, *pt, *rs;
+                unsigned *tk;
+                CK(cudaMalloc(&pa, jk::kHimenoPartials * sizeof(double)));
+                CK(cudaMalloc(&pt, 8));
+                CK(cudaMalloc(&rs, 8));
+                CK(cudaMalloc(&tk, 64));
+                CK(cudaMemset(pt, 0, 8));
+                CK(cudaMemset(tk, 0, 64));
+                dv.qpartials.push_back(pa);
+                dv.qpart.push_back(pt);
+                dv.qres.push_back(rs);
+                dv.qticket.push_back(tk);
             }
             for (size_t q = 0; q < dv.qs.size(); q++) CK(cudaEventRecord(dv.qev[q], dv.qs[q]));
         }
