@@ -1769,11 +1769,19 @@ jacc_status jacc_init(int n_devices, const int *device_ids) {
                     if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
                     else CK(e);
                 }
-            if (n_devices > 1 && R.distinct) {
+            if (n_devices > 1 && R.distinct && !getenv("JACC_NO_NCCL")) {
+                // NCCL allreduce for the reduction combine; if the communicator
+                // cannot be built the fixed-order peer-memory combine (P2P
+                // loads of every device's partial) is used instead
                 std::vector<ncclComm_t> comms(n_devices);
-                NK(ncclCommInitAll(comms.data(), n_devices, ords.data()));
-                for (int d = 0; d < n_devices; d++) R.dev[d].comm = comms[d];
-                R.use_nccl = true;
+                const ncclResult_t nr = ncclCommInitAll(comms.data(), n_devices, ords.data());
+                if (nr == ncclSuccess) {
+                    for (int d = 0; d < n_devices; d++) R.dev[d].comm = comms[d];
+                    R.use_nccl = true;
+                } else if (getenv("JACC_DEBUG")) {
+                    fprintf(stderr, "[jacc] ncclCommInitAll: %s; peer-memory combine\n",
+                            ncclGetErrorString(nr));
+                }
             }
             R.comm_prev.assign(n_devices, std::vector<char>(n_devices, 0));
             return JACC_OK;
