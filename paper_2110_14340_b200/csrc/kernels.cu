@@ -411,7 +411,7 @@ template <int BM, int BN, int BK, int ST, int WM, int WN, bool V16, int GROUP = 
 __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, ST, WM, WN>::NT)
     gemm_f64_kernel(const double *__restrict__ A, const double *__restrict__ B,
                     double *__restrict__ C, int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1,
-                    int64_t c0, int64_t c1, u64 *dirty) {
+                    int64_t c0, int64_t c1, u64 *dirty, PeerPtrs push) {
     using G = GemmCfg<BM, BN, BK, ST, WM, WN>;
     constexpr int MI = WM / 8, NJ = WN / 8, WCOLS = BN / WN;
     extern __shared__ __align__(16) double gsm[];
@@ -486,18 +486,25 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, ST, WM, WN>::NT)
         for (int j = 0; j < NJ; j++) {
             const int64_t n = n0 + wn * WN + j * 8 + ac * 2;
             const int64_t f = m * N + n;
+            // EAGER merge fused into the epilogue: finished C tiles are also
+            // stored into every peer replica (NVLink peer stores), so the
+            // exchange overlaps the remaining tiles' DMMA work
             if (V16 && n + 1 < c1) {
-                *reinterpret_cast<double2 *>(C + f) = make_double2(acc[i][j][0], acc[i][j][1]);
+                const double2 v2 = make_double2(acc[i][j][0], acc[i][j][1]);
+                *reinterpret_cast<double2 *>(C + f) = v2;
+                for (int q = 0; q < push.n; q++) *reinterpret_cast<double2 *>(static_cast<double *>(push.p[q]) + f) = v2;
                 mn = (u64)f < mn ? (u64)f : mn;
                 mx = (u64)(f + 1) > mx ? (u64)(f + 1) : mx;
             } else {
                 if (n < c1) {
                     C[f] = acc[i][j][0];
+                    for (int q = 0; q < push.n; q++) static_cast<double *>(push.p[q])[f] = acc[i][j][0];
                     mn = (u64)f < mn ? (u64)f : mn;
                     mx = (u64)f > mx ? (u64)f : mx;
                 }
                 if (n + 1 < c1) {
                     C[f + 1] = acc[i][j][1];
+                    for (int q = 0; q < push.n; q++) static_cast<double *>(push.p[q])[f + 1] = acc[i][j][1];
                     mx = (u64)(f + 1) > mx ? (u64)(f + 1) : mx;
                 }
             }
@@ -1356,7 +1363,7 @@ cudaError_t combine(cudaStream_t s, PeerPtrs parts, double s_in, double *out) {
 template <int BM, int BN, int BK, int ST, int WM, int WN, int GROUP = 0>
 static cudaError_t gemm_launch(cudaStream_t s, bool v16, const double *A, const double *B,
                                double *C, int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1,
-                               int64_t c0, int64_t c1, u64 *dirty) {
+                               int64_t c0, int64_t c1, u64 *dirty, PeerPtrs push) {
     using G = GemmCfg<BM, BN, BK, ST, WM, WN>;
     auto kt = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, true, GROUP>;
     auto kf = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, false, GROUP>;
@@ -1368,15 +1375,15 @@ static cudaError_t gemm_launch(cudaStream_t s, bool v16, const double *A, const 
     }
     dim3 grid((unsigned)((c1 - c0 + BN - 1) / BN), (unsigned)((r1 - r0 + BM - 1) / BM));
     if (v16)
-        kt<<<grid, G::NT, G::SMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+        kt<<<grid, G::NT, G::SMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     else
-        kf<<<grid, G::NT, G::SMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+        kf<<<grid, G::NT, G::SMEM, s>>>(A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     return cudaGetLastError();
 }
 
 cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C, int64_t M,
                      int64_t N, int64_t K, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
-                     u64 *dirty) {
+                     u64 *dirty, PeerPtrs push) {
     if (r1 <= r0 || c1 <= c0 || K <= 0) return cudaSuccess;
     const bool v16 = (K % 2 == 0) && (N % 2 == 0) && (c0 % 2 == 0) && ((uintptr_t)A % 16 == 0) &&
                      ((uintptr_t)B % 16 == 0) && ((uintptr_t)C % 16 == 0);
@@ -1386,16 +1393,16 @@ cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C
         variant = e ? atoi(e) : 0;
     }
     switch (variant) {
-    case 1: return gemm_launch<64, 64, 32, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    case 2: return gemm_launch<128, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    case 3: return gemm_launch<128, 128, 16, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    case 4: return gemm_launch<64, 128, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    case 5: return gemm_launch<64, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    case 6: return gemm_launch<128, 128, 32, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    case 7: return gemm_launch<64, 64, 16, 3, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    case 8: return gemm_launch<64, 64, 16, 3, 32, 32, 16>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    case 9: return gemm_launch<64, 64, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
-    default: return gemm_launch<64, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty);
+    case 1: return gemm_launch<64, 64, 32, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 2: return gemm_launch<128, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 3: return gemm_launch<128, 128, 16, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 4: return gemm_launch<64, 128, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 5: return gemm_launch<64, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 6: return gemm_launch<128, 128, 32, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 7: return gemm_launch<64, 64, 16, 3, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 8: return gemm_launch<64, 64, 16, 3, 32, 32, 16>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 9: return gemm_launch<64, 64, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    default: return gemm_launch<64, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     }
 }
 

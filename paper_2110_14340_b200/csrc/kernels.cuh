@@ -44,9 +44,11 @@ cudaError_t combine(cudaStream_t s, PeerPtrs parts, double s_in, double *out);
 
 // BK3  C[r0:r1, c0:c1] = A[r0:r1, :] * B[:, c0:c1] on the fp64 tensor pipe
 // (DMMA via mma.sync m8n8k4 f64), dirty-range tracking fused.
+// push: peer replicas of C that receive every finished tile in the
+// epilogue (the EAGER merge fused with the GEMM; n = 0: none).
 cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C,
                      int64_t M, int64_t N, int64_t K, int64_t r0, int64_t r1,
-                     int64_t c0, int64_t c1, u64 *dirty);
+                     int64_t c0, int64_t c1, u64 *dirty, PeerPtrs push);
 
 // BK4  Owner-filtered scatter: for i in [0,n):
 // k = idx[i]; if lo <= k < hi: a[k] += b[i] (atomic); bitmap bit k set

@@ -1300,6 +1300,9 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 CK(cudaMemsetAsync(W->bitmap[d], 0, words * 4, R.dev[d].s));
             }
     }
+    // GEMM under EAGER: the merge is fused into the kernel's epilogue
+    const bool gemm_fused_push = id == JACC_LOOP_GEMM_F64 && writes &&
+                                 R.policy == JACC_MERGE_EAGER && n > 1 && L.split == 0;
     // binned-scatter scratch is reserved before anything is enqueued, so an
     // allocation failure cannot leave a launch half-issued (the loop then
     // falls back to the direct kernel on that device)
@@ -1451,12 +1454,18 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                                   dv.ticket, dv.part));
                 break;
             }
-            case JACC_LOOP_GEMM_F64:
+            case JACC_LOOP_GEMM_F64: {
+                jk::PeerPtrs push{};
+                if (gemm_fused_push)
+                    for (int q = 0; q < n; q++)
+                        if (q != d) push.p[push.n++] = W->rep[q];
                 CK(jk::gemm_f64(dv.s, reinterpret_cast<const double *>(L.a[0].reg->rep[d]),
                                 reinterpret_cast<const double *>(L.a[1].reg->rep[d]),
                                 reinterpret_cast<double *>(W->rep[d]), L.M, L.Nn, L.K, p.i0, p.i1,
-                                p.j0, p.j1, drec));
+                                p.j0, p.j1, drec, push));
+                if (gemm_fused_push) merged_bytes += (uint64_t)(p.whi - p.wlo) * 8 * (n - 1);
                 break;
+            }
             case JACC_LOOP_FIG4_F64: {
                 const int32_t *jx = reinterpret_cast<const int32_t *>(L.a[0].reg->rep[d]) + L.a[0].off;
                 const int32_t *kx = reinterpret_cast<const int32_t *>(L.a[1].reg->rep[d]) + L.a[1].off;
@@ -1561,7 +1570,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             }
         }
         // ---- EAGER merge: push the recorded dirty region to every peer ----
-        if (writes && p.active && R.policy == JACC_MERGE_EAGER && n > 1) {
+        if (writes && p.active && R.policy == JACC_MERGE_EAGER && n > 1 && !gemm_fused_push) {
             jk::PeerPtrs pp{};
             for (int q = 0; q < n; q++)
                 if (q != d) pp.p[pp.n++] = W->rep[q];
