@@ -1022,14 +1022,10 @@ __global__ void __launch_bounds__(HT) himeno_copy_kernel(
                        reinterpret_cast<uintptr_t>(push_top) | reinterpret_cast<uintptr_t>(push_bot)) &
                       15) == 0;
     u64 mn = kU64Max, mx = 0;
-    u64 *rowctr = reinterpret_cast<u64 *>(ticket + 8);  // dynamic row order, as the stencil
-    (void)wg;
-    (void)nw;
-    for (;;) {
-        int64_t r = 0;
-        if (lane == 0) r = (int64_t)atomicAdd(rowctr, 1ull);
-        r = __shfl_sync(0xffffffffu, r, 0);
-        if (r >= rows) break;
+    // a pure stream (no neighbour reuse): static row stride; a shared row
+    // counter would serialise on its atomics (rows are only 2 KB of work)
+    (void)ticket;
+    for (int64_t r = wg; r < rows; r += nw) {
         const int64_t i = i0 + r / nj, j = j0 + r % nj;
         const int64_t rb = i * P + j * K;
         float *tp = (i == i0) ? push_top : nullptr;
@@ -1068,17 +1064,6 @@ __global__ void __launch_bounds__(HT) himeno_copy_kernel(
         if (k1 > k0) {
             mn = (u64)(rb + k0) < mn ? (u64)(rb + k0) : mn;
             mx = (u64)(rb + k1 - 1) > mx ? (u64)(rb + k1 - 1) : mx;
-        }
-    }
-    // the last CTA to finish resets the row counter for the next launch
-    __shared__ bool lastc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        lastc = atomicAdd(ticket + 2, 1u) == gridDim.x - 1;
-        if (lastc) {
-            *rowctr = 0ull;
-            ticket[2] = 0u;
         }
     }
     publish_dirty_flat(mn, mx, dirty);
