@@ -136,7 +136,7 @@ __device__ __forceinline__ void jload(JRow<V> &o, const double *__restrict__ src
     o.r = (ok && lane == 31 && cs + 32 * V < N) ? __ldg(p + cs + 32 * V) : 0.0;
 }
 
-template <int V, int JW, int JR, int JPF, int MINB>
+template <int V, int JW, int JR, int JPF, int MINB, bool CS = true>
 __global__ void __launch_bounds__(JW * 32, MINB)
     jacobi2d_kernel(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t r0,
                     int64_t r1, int64_t c0, int64_t c1, int64_t cs_base, int64_t ntiles_y,
@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(JW * 32, MINB)
             if (full) {
                 if constexpr (V == 2) {
                     const double2 o2 = make_double2(out[0], out[1]);
-                    __stcs(reinterpret_cast<double2 *>(dst + base + j0), o2);
+                    if constexpr (CS) __stcs(reinterpret_cast<double2 *>(dst + base + j0), o2);
+                    else *reinterpret_cast<double2 *>(dst + base + j0) = o2;
                     if (tp) *reinterpret_cast<double2 *>(tp + base + j0) = o2;
                     if (bp) *reinterpret_cast<double2 *>(bp + base + j0) = o2;
                 } else {
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
 // ---------------------------------------------------------------------------
 // BK4b destination-binned scatter (see kernels.cuh)
 // ---------------------------------------------------------------------------
-constexpr int SB_T = 256, SB_E = 8, SB_TILE = SB_T * SB_E;
+constexpr int SB_T = 256;  // partition tile = SB_T x E elements (E = 8 default, 16)
 constexpr int SB_MAXB = 1024;
 
 __global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restrict__ idx, int64_t n,
@@ -821,7 +822,6 @@ __device__ __forceinline__ float himeno_point(const float *__restrict__ p,
     return __fmul_rn(ss, ss);
 }
 
-__device__ __forceinline__ float4 ld4cs(const float *p) { return __ldcs(reinterpret_cast<const float4 *>(p)); }
 __device__ __forceinline__ float4 ld4g(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
 __device__ __forceinline__ float f4(const float4 &v, int e) {
     return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
@@ -1284,7 +1284,7 @@ cudaError_t square_f32(cudaStream_t s, const float *y, float *x, int64_t i0, int
     return cudaGetLastError();
 }
 
-template <int JW, int JR, int JPF, int MINB>
+template <int JW, int JR, int JPF, int MINB, bool CS = true>
 static cudaError_t jacobi2d_launch(cudaStream_t s, bool v2, const double *src, double *dst,
                                    int64_t N, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
                                    u64 *dirty, double *push_top, double *push_bot) {
@@ -1295,10 +1295,10 @@ static cudaError_t jacobi2d_launch(cudaStream_t s, bool v2, const double *src, d
     const int64_t ty = (r1 - r0 + JR - 1) / JR;
     dim3 grid((unsigned)gx, (unsigned)(ty < 65535 ? ty : 65535));
     if (v2)
-        jacobi2d_kernel<2, JW, JR, JPF, MINB><<<grid, JW * 32, 0, s>>>(
+        jacobi2d_kernel<2, JW, JR, JPF, MINB, CS><<<grid, JW * 32, 0, s>>>(
             src, dst, N, r0, r1, c0, c1, cs_base, ty, dirty, push_top, push_bot);
     else
-        jacobi2d_kernel<1, JW, JR, JPF, MINB><<<grid, JW * 32, 0, s>>>(
+        jacobi2d_kernel<1, JW, JR, JPF, MINB, CS><<<grid, JW * 32, 0, s>>>(
             src, dst, N, r0, r1, c0, c1, cs_base, ty, dirty, push_top, push_bot);
     return cudaGetLastError();
 }
@@ -1323,7 +1323,14 @@ cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N, 
     case 5: return jacobi2d_launch<8, 32, 3, 3>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
     case 6: return jacobi2d_launch<2, 32, 3, 12>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
     case 7: return jacobi2d_launch<4, 32, 6, 4>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    default: return jacobi2d_launch<4, 32, 3, 7>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 8: return jacobi2d_launch<4, 32, 3, 7, false>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 9: return jacobi2d_launch<4, 16, 3, 8>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 10: return jacobi2d_launch<4, 24, 3, 7>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 11: return jacobi2d_launch<8, 32, 3, 3, false>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    case 12: return jacobi2d_launch<4, 32, 3, 7, true>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    // default: measured best (tools/tune_jacobi.py): 4 warps x 32 rows,
+    // 3 rows of prefetch, 7 CTAs/SM, plain (write-back) stores
+    default: return jacobi2d_launch<4, 32, 3, 7, false>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
     }
 }
 

@@ -41,7 +41,6 @@
 namespace {
 
 using u64 = unsigned long long;
-constexpr u64 kEmptyMin = ~0ull;
 
 // ---------------------------------------------------------------------------
 // Interval set over element indices (half-open), used for replica validity.
