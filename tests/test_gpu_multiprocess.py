@@ -48,6 +48,24 @@ def test_multiprocess_parity(tmp_path, world, policy):
     av = synth.int_i32(M, -10**6, 10**6, 83, 7)
     a0 = av.copy()
     orc.scatter_add(idx, b, av)
+    GA = synth.uniform_f64(67 * 29, 84, 1).reshape(67, 29)
+    GB = synth.uniform_f64(29 * 45, 84, 2).reshape(29, 45)
+    gref = orc.gemm_f64(GA, GB)
+    gbound = np.abs(GA) @ np.abs(GB)
+    hp, ha, hb, hc, hw1, hbd = synth.himeno_random(11, 9, 13, 85)
+    hw2 = np.zeros_like(hp)
+    hg_ref = []
+    for _ in range(2):
+        hg_ref.append(orc.himeno_stencil(hp, ha, hb, hc, hw1, hbd, hw2)[1])
+        orc.himeno_copy(hw2, hp)
+    hp_ref = hp
+    fn = 301
+    kx = (synth.permutation_i32(fn, 86, 30) + fn).astype(np.int32)
+    jx = synth.index_i32(fn, 5 * fn + 7, 86, 31)
+    fc = synth.uniform_f64(5 * fn + 7, 86, 32)
+    fa_ref = synth.uniform_f64(2 * fn + 3, 86, 33)
+    fb_ref = synth.uniform_f64(3 * fn + 1, 86, 34)
+    orc.fig4(jx, kx, fc, 0.25, fa_ref, fb_ref)
     for rank in range(world):
         z = np.load(tmp_path / f"rank{rank}.npz")
         assert int(z["world"]) == world
@@ -63,3 +81,7 @@ def test_multiprocess_parity(tmp_path, world, policy):
         slo, shi = orc.partition(M, world, rank)
         bm, _, _ = orc.scatter_add_filtered(idx, b, a0.copy(), slo, shi - 1)
         assert np.array_equal(z["bitmap"], bm)
+        assert (np.abs(z["gemm"] - gref) <= 1e-12 * gbound).all()
+        assert np.array_equal(z["himeno_p"], hp_ref)
+        assert np.allclose(z["himeno_gosa"], hg_ref, rtol=1e-12, atol=0)
+        assert np.array_equal(z["fig4_a"], fa_ref) and np.array_equal(z["fig4_b"], fb_ref)

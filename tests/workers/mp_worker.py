@@ -73,6 +73,51 @@ def main():
     res["bitmap"] = J.jacc_get_dirty_bitmap(av, rank, M)
     J.jacc_update_host(av)
     res["scatter"] = av
+    # GEMM (EAGER: merge fused into the epilogue, IPC-mapped peer stores)
+    M, Nn, Kk = 67, 45, 29
+    GA = synth.uniform_f64(M * Kk, 84, 1).reshape(M, Kk)
+    GB = synth.uniform_f64(Kk * Nn, 84, 2).reshape(Kk, Nn)
+    GC = np.zeros((M, Nn))
+    for arr in (GA, GB, GC):
+        jd.data_create(arr)
+        J.jacc_update_device(arr)
+    J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, [J.arg(IN, GA), J.arg(IN, GB), J.arg(OUT, GC)])
+    J.jacc_update_host(GC)
+    res["gemm"] = GC
+    # Himeno (stencil + gosa reduction over ranks, copy with plane pushes)
+    hp, ha, hb, hc, hw1, hbd = synth.himeno_random(11, 9, 13, 85)
+    hw2 = np.zeros_like(hp)
+    for arr in (hp, ha, hb, hc, hw1, hbd, hw2):
+        jd.data_create(arr)
+        J.jacc_update_device(arr)
+    gos = []
+    for _ in range(2):
+        g = np.zeros(1)
+        J.jacc_launch(J.JACC_LOOP_HIMENO_F32, None,
+                      [J.arg(IN, hp), J.arg(IN, ha), J.arg(IN, hb), J.arg(IN, hc), J.arg(IN, hw1),
+                       J.arg(IN, hbd), J.arg(OUT, hw2), J.arg(J.JACC_ARG_REDUCE_SUM_F64, g),
+                       J.arg(J.JACC_ARG_SCALAR_F64, f64=0.8)])
+        gos.append(g[0])
+        J.jacc_launch(J.JACC_LOOP_HIMENO_COPY_F32, None, [J.arg(IN, hw2), J.arg(OUT, hp)], 0)
+    J.jacc_update_host(hp)
+    res["himeno_p"] = hp
+    res["himeno_gosa"] = np.array(gos)
+    # Fig. 4 chain (two written arrays, separately divided)
+    fn = 301
+    kx = (synth.permutation_i32(fn, 86, 30) + fn).astype(np.int32)
+    jx = synth.index_i32(fn, 5 * fn + 7, 86, 31)
+    fc = synth.uniform_f64(5 * fn + 7, 86, 32)
+    fa = synth.uniform_f64(2 * fn + 3, 86, 33)
+    fb = synth.uniform_f64(3 * fn + 1, 86, 34)
+    for arr in (jx, kx, fc, fa, fb):
+        jd.data_create(arr)
+        J.jacc_update_device(arr)
+    J.jacc_launch(J.JACC_LOOP_FIG4_F64, J.make_range(0, fn),
+                  [J.arg(IN, jx), J.arg(IN, kx), J.arg(IN, fc), J.arg(OUT, fa), J.arg(OUT, fb),
+                   J.arg(J.JACC_ARG_SCALAR_F64, f64=0.25)])
+    J.jacc_update_host(fa)
+    J.jacc_update_host(fb)
+    res["fig4_a"], res["fig4_b"] = fa, fb
     jd.finalize()
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), world=world, **res)
     dist.destroy_process_group()
