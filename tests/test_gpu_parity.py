@@ -526,6 +526,28 @@ def test_scatter_full_size(J):
     assert drs[0] == (int(idx.min()), int(idx.max()))
 
 
+def test_scatter_sparse_full_size(J):
+    """SURVEY 8(d) SCAT sparse variant: 2^20 updates into 2^28 elements on
+    two devices under EAGER -- the dirty bitmaps are 0.4 % dense, the merge
+    pushes only the set bits, and every replica equals the oracle."""
+    N, M = 2**20, 2**28
+    idx = synth.index_i32(N, M, 75, 5)
+    b = synth.dyadic_f64(N, 75, 6)
+    a0 = synth.dyadic_f64(M, 75, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, bms, drs, reps = _scatter(J, idx, b, a0, 2)
+    assert np.array_equal(a, ref)
+    for r in reps:
+        assert np.array_equal(r, ref)
+    u = np.unique(idx)
+    for d in range(2):
+        lo, hi = orc.partition(M, 2, d)
+        own = u[(u >= lo) & (u < hi)]
+        assert int(np.unpackbits(bms[d].view(np.uint8)).sum()) == own.size
+        assert drs[d] == (int(own.min()), int(own.max()))
+
+
 # --------------------------------------------------------------------------
 # runtime behaviour
 # --------------------------------------------------------------------------
