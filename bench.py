@@ -57,6 +57,22 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+HBM_SPEC_GBS = 8000.0      # B200 datasheet HBM3e
+FP64_SPEC_TFLOPS = 40.0    # B200 datasheet fp64 (tensor), SURVEY 8(d)
+
+
+def load_dgemm_peak():
+    """cuBLAS DGEMM 8192^3 measured on this pool (tools/probe_box.py ->
+    profiles/probe_box_r*.json): the fp64 tensor-pipe reference."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "probe_box_r*.json")), reverse=True):
+        with open(p) as f:
+            j = json.load(f)
+        if j.get("dgemm_tflops"):
+            return float(j["dgemm_tflops"]), os.path.basename(p)
+    return None, None
+
+
 def load_traffic(kernel="jacobi2d"):
     """dram bytes per launch of the dominant kernel from the committed ncu
     --set full summary (profiles/), or None."""
@@ -391,7 +407,8 @@ def run_jacc(args):
                    "parallelism": f"row-block owner partition over {n} device(s)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "jacobi2d_kernel<2>", "kernel_avg_us": k_avg * 1e6,
+                     "frac_of_spec": achieved / HBM_SPEC_GBS, "spec_peak": HBM_SPEC_GBS,
+                     "kernel": "jacobi2d_kernel", "kernel_avg_us": k_avg * 1e6,
                      "algo_bytes_per_launch": per_dev_bytes, "peak_source": peak_src,
                      "traffic_source": tsrc},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * A.nbytes,
@@ -447,6 +464,7 @@ def run_extra_loops(J, C, n, peak):
     byts = 16 * L
     out["dot_2^30"] = {"loop_gbs": byts / t / 1e9, "kernel_us": k * 1e6,
                        "kernel_gbs": byts / n / k / 1e9, "frac_of_peak": byts / n / k / 1e9 / peak,
+                       "frac_of_spec": byts / n / k / 1e9 / HBM_SPEC_GBS,
                        "launch_ms": t * 1e3}
     J.jacc_data_delete(x)
     J.jacc_data_delete(y)
@@ -462,8 +480,12 @@ def run_extra_loops(J, C, n, peak):
     gargs = [J.arg(IN, Ag), J.arg(IN, Bg), J.arg(OUT, Cg)]
     t, k, m = _time_loop(J, C, lambda: J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, gargs, 0), 3)
     fl = 2 * G**3
+    dg, dsrc = load_dgemm_peak()
     out["gemm_8192"] = {"loop_tflops": fl / t / 1e12, "kernel_ms": k * 1e3,
                         "kernel_tflops": fl / n / k / 1e12, "merge_ms": m * 1e3,
+                        "frac_of_cublas_dgemm": fl / n / k / 1e12 / dg if dg else None,
+                        "cublas_dgemm_tflops": dg, "cublas_source": dsrc,
+                        "frac_of_spec": fl / n / k / 1e12 / FP64_SPEC_TFLOPS,
                         "launch_ms": t * 1e3}
     for a in (Ag, Bg, Cg):
         J.jacc_data_delete(a)
@@ -483,6 +505,10 @@ def run_extra_loops(J, C, n, peak):
     byts = S * (4 + 8 + 16)
     out["scatter_f64_2^28"] = {"loop_gbs": byts / t / 1e9, "kernel_us": k * 1e6,
                                "kernel_alg_gbs": byts / k / 1e9 if n == 1 else None,
+                               "frac_of_peak": byts / k / 1e9 / peak if n == 1 else None,
+                               "frac_of_spec": byts / k / 1e9 / HBM_SPEC_GBS if n == 1 else None,
+                               # sector-level floor: 32 B read + 32 B write of a per update
+                               "frac_of_sector_roofline": S * (4 + 8 + 64) / k / 1e9 / peak if n == 1 else None,
                                "merge_us": m * 1e6, "launch_ms": t * 1e3}
     for arr in (idx, b, a):
         J.jacc_data_delete(arr)
@@ -505,6 +531,7 @@ def run_extra_loops(J, C, n, peak):
     sb, cb = 56 * pts, 8 * pts   # 12 coefficient/aux arrays + p read, wrk2 written | copy
     out["himeno_XL_fp32"] = {"stencil_us": ks * 1e6, "stencil_gbs": sb / n / ks / 1e9,
                              "stencil_frac": sb / n / ks / 1e9 / peak,
+                             "stencil_frac_of_spec": sb / n / ks / 1e9 / HBM_SPEC_GBS,
                              "copy_us": kc * 1e6, "copy_gbs": cb / n / kc / 1e9,
                              "iteration_ms": (ts + tc) * 1e3, "gosa": float(g[0])}
     for arr in (hp, ha, hb, hc, hw1, hbd, hw2):

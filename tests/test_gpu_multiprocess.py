@@ -24,7 +24,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("policy", ["halo", "eager"])
 def test_multiprocess_parity(tmp_path, world, policy):
     import __graft_entry__ as ge
