@@ -95,12 +95,26 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap,utilization.gpu")
 
-    def __init__(self, gpu_index):
-        self.idx = gpu_index
+    def __init__(self, cuda_ords):
+        # nvidia-smi indices of every GPU the job uses (through
+        # CUDA_VISIBLE_DEVICES when it remaps ordinals)
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        vis = [v.strip() for v in vis.split(",")] if vis else []
+        idx = [vis[o] if o < len(vis) and vis[o].isdigit() else str(o) for o in cuda_ords]
+        self.idx = ",".join(idx)
         self.samples = []
         self.proc = None
+        self.window = None
+
+    def mark(self, t0, t1):
+        """restrict the summary to samples taken in [t0, t1] (time.monotonic);
+        the sampler is started before the warm-up so nvidia-smi's own start-up
+        (seconds with several ranks on the box) never leaves it unsampled"""
+        self.window = (t0, t1)
 
     def __enter__(self):
+        if not self.idx:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
@@ -116,7 +130,7 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
-                self.samples.append(parts)
+                self.samples.append((time.monotonic(), parts))
 
     def __exit__(self, *a):
         if self.proc:
@@ -127,11 +141,20 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        samples = [p for _, p in self.samples]
+        where = "timed region"
+        if self.window:
+            t0, t1 = self.window
+            inside = [p for t, p in self.samples if t0 <= t <= t1]
+            if not inside:  # region shorter than the 100 ms period: nearest samples
+                inside = [p for t, p in self.samples if t0 - 0.25 <= t <= t1 + 0.25]
+                where = "timed region +-250 ms"
+            samples = inside
+        if not samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         sm, mx, reasons = [], None, set()
-        for s in self.samples:
+        for s in samples:
             try:
                 util = float(s[6])
                 if util > 50:
@@ -143,9 +166,9 @@ class ClockSampler:
                 if s[2 + k].lower().startswith("active"):
                     reasons.add(name)
         if not sm:
-            sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+            sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(samples), "window": where}
 
 
 # ----------------------------------------------------------------------------
@@ -231,11 +254,13 @@ class Ctx:
             self.virtual = not distinct
             self.local = [self.rank]
             self.ords = [ordv]
+            self.all_ords = sorted({r % ngpu for r in range(self.world)})
         else:
             self.virtual = ngpu < n
             self.ords = list(range(n)) if not self.virtual else [0] * n
             J.jacc_init(n, self.ords)
             self.local = list(range(n))
+            self.all_ords = sorted(set(self.ords))
         self.streams = {}
         for d in self.local:
             sp, o = J.jacc_get_stream(d)
@@ -318,6 +343,7 @@ def run_jacc(args):
             J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ab, 0)
             J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ba, 0)
 
+    clk = ClockSampler(C.all_ords if C.rank == 0 else []).__enter__()  # rank 0 samples all GPUs
     for _ in range(args.warmup):
         step()
     # host cost of issuing one launch (plan + enqueue on every device), timed
@@ -345,8 +371,10 @@ def run_jacc(args):
         timed_step = lambda: J.jacc_graph_replay(gid, 1)
     else:
         timed_step = step
-    with ClockSampler(C.ords[0]) as clk:
-        t = C.timed(timed_step, args.steps)
+    w0 = time.monotonic()
+    t = C.timed(timed_step, args.steps)
+    clk.mark(w0, time.monotonic())
+    clk.__exit__()
     bytes_step = 2 * TSTEPS * algo_bytes_per_sweep(N, n)
     value = bytes_step * args.steps / t / 1e9
     # kernels per timed step: one loop kernel per device per launch (HALO
