@@ -119,8 +119,10 @@ jacc_status jacc_set_split_dim(int dim);
  * each word-aligned slice of `a` adds every device's delta for the words
  * dirty anywhere, in device order, reading them over peer memory, and the
  * merge policy distributes the result (its dirty bitmap = the union).
- * Single-process mode only.  Errors: JACC_ERR_INVALID in multi-process
- * mode. */
+ * Single-process mode only; a duplicated launch (JACC_MODE_DUP, or DUP
+ * chosen by JACC_MODE_ADAPTIVE) runs every iteration on every device and
+ * ignores the setting.  Errors: JACC_ERR_INVALID in multi-process mode, or
+ * at launch with several async queues. */
 jacc_status jacc_set_scatter_split(int iteration_split);
 
 /* Owned block [lo, hi) of logical device d when an extent E is split over

@@ -1115,7 +1115,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     if (R.mode == JACC_MODE_DUP) L.dup = true;
     L.itersplit = R.scatter_itersplit && R.n > 1 &&
                   (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32);
-    if (L.itersplit && (R.mp || L.dup || R.nq > 1)) return JACC_ERR_INVALID;
+    if (L.itersplit && (R.mp || R.nq > 1)) return JACC_ERR_INVALID;
     // ---- NEXT-1 adaptive utilization (single process, n > 1) ---------------
     const bool adaptive =
         R.mode == JACC_MODE_ADAPTIVE && R.n > 1 && !R.mp && !L.dup && !R.capturing;
@@ -1152,6 +1152,8 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         }
         L.dup = R.adapt[akey].dup();
     }
+    // duplicated execution runs every iteration on every device: nothing to split
+    if (L.dup) L.itersplit = false;
     for (auto &ai : L.a)
         if (ai.reg)
             for (int d = 0; d < R.n; d++)
@@ -1679,7 +1681,14 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         const int h = R.mp ? R.me : 0;
         Device &d0 = R.dev[h];
         const double s_in = *L.red_ptr;
-        if (R.use_nccl) {
+        if (L.dup) {
+            // duplicated execution: every device reduced the whole range, so
+            // the result is this device's own total (no cross-device sum)
+            set_dev(h);
+            jk::PeerPtrs pp{};
+            pp.p[pp.n++] = d0.part;
+            CK(jk::combine(d0.s, pp, s_in, d0.res));
+        } else if (R.use_nccl) {
             NK(ncclGroupStart());
             for (int d = 0; d < n; d++)
                 if (local(d))

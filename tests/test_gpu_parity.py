@@ -510,6 +510,26 @@ def test_scatter_dup_mode(J):
     assert np.array_equal(a, ref)
 
 
+@pytest.mark.parametrize("n", [2, 3])
+def test_reductions_dup_mode(J, n):
+    """JACC_MODE_DUP: every device reduces the whole range; the result is one
+    device's total plus s_in, not the sum over devices (found by the
+    randomised programs)."""
+    L = 10_007
+    x = synth.dyadic_f64(L, 78, 1)
+    y = synth.dyadic_f64(L, 78, 2)
+    with runtime(J, n, mode=1):
+        _create(J, x, y)
+        s = np.array([1.5])
+        J.jacc_launch(J.JACC_LOOP_DOT_F64, J.make_range(0, L),
+                      [_in(J, x), _in(J, y), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s)])
+        assert s[0] == orc.dot_f64(x, y, 1.5)
+        s = np.array([-2.0])
+        J.jacc_launch(J.JACC_LOOP_SUM_F64, J.make_range(0, L),
+                      [_in(J, x), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s)])
+        assert s[0] == orc.sum_f64(x, -2.0)
+
+
 def test_scatter_full_size(J):
     """BASELINE config 5 at full size: 2^28 updates into 2^28 elements,
     random idx, dyadic b (exact in any order), n=1."""
