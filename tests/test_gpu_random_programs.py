@@ -1,5 +1,6 @@
 """Randomised programs through the C-ABI (-m gpu): seeded sequences of
-launches (Jacobi both directions, square, scatter-add, sum reduction),
+launches (Jacobi both directions, square, scatter-add, sum reduction,
+GEMM, the Fig. 4 chain, Himeno stencil + copy),
 partial update_host / update_device calls with host-side edits in between,
 and waits, under random runtime configurations (device count, merge
 policy, execution mode, split dimension, async queues, iteration-split
@@ -12,6 +13,8 @@ This exercises the validity tracker, the pulls, both merge policies and the
 dirty-record slots across arbitrary interleavings, beyond the fixed
 sequences of test_gpu_parity.py.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -47,6 +50,9 @@ class Program:
         N = int(r.integers(3, 70))
         L = int(r.integers(1, 3000))
         S, M = int(r.integers(1, 5000)), int(r.integers(1, 4000))
+        gm, gk, gn = (int(v) for v in r.integers(1, 40, 3))
+        fn = int(r.integers(1, 300))
+        hI, hJ, hK = (int(v) for v in r.integers(3, 14, 3))
         # host arrays (the user's) and the model's device state
         self.host = {
             "A": synth.uniform_f64(N * N, seed, 1).reshape(N, N),
@@ -56,7 +62,20 @@ class Program:
             "idx": synth.index_i32(S, M, seed, 4),
             "bs": synth.dyadic_f64(S, seed, 5),
             "a": synth.dyadic_f64(M, seed, 6),
+            # GEMM on small integers: exact in any summation order
+            "GA": synth.int_i32(gm * gk, -8, 8, seed, 7).astype(np.float64).reshape(gm, gk),
+            "GB": synth.int_i32(gk * gn, -8, 8, seed, 8).astype(np.float64).reshape(gk, gn),
+            "GC": np.zeros((gm, gn)),
+            # Fig. 4 chain: k = kx[i] injective into [n, 2n)
+            "jx": synth.index_i32(fn, 5 * fn + 7, seed, 9),
+            "kx": (synth.permutation_i32(fn, seed, 10) + fn).astype(np.int32),
+            "fc": synth.uniform_f64(5 * fn + 7, seed, 11),
+            "fa": synth.uniform_f64(2 * fn + 3, seed, 12),
+            "fb": synth.uniform_f64(3 * fn + 1, seed, 13),
         }
+        hp, ha, hb, hc, hw1, hbd = synth.himeno_random(hI, hJ, hK, seed)
+        self.host.update({"hp": hp, "ha": ha, "hb": hb, "hc": hc, "hw1": hw1, "hbd": hbd,
+                          "hw2": np.zeros_like(hp)})
         self.dev = {k: v.copy() for k, v in self.host.items()}
         self.model_host = {k: v.copy() for k, v in self.host.items()}
 
@@ -81,8 +100,9 @@ class Program:
     def step(self, log):
         J, r, h, dev = self.J, self.rng, self.host, self.dev
         IN, OUT, INOUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT, J.JACC_ARG_ARRAY_INOUT
-        op = r.choice(["jacAB", "jacBA", "square", "scatter", "sum", "uh", "ud", "wait"],
-                      p=[0.2, 0.2, 0.12, 0.15, 0.08, 0.12, 0.08, 0.05])
+        op = r.choice(["jacAB", "jacBA", "square", "scatter", "sum", "gemm", "fig4", "himeno",
+                       "uh", "ud", "wait"],
+                      p=[0.14, 0.14, 0.09, 0.1, 0.06, 0.08, 0.08, 0.1, 0.11, 0.06, 0.04])
         log.append(str(op))
         if op in ("jacAB", "jacBA"):
             s, d = ("A", "B") if op == "jacAB" else ("B", "A")
@@ -109,19 +129,45 @@ class Program:
                           [J.arg(IN, h["a"]), J.arg(J.JACC_ARG_REDUCE_SUM_F64, out)], self.aid())
             ref = orc.sum_f64(dev["a"], s_in)     # dyadic: exact in any order
             assert out[0] == ref, (self.desc(), log)
+        elif op == "gemm":
+            J.jacc_launch(J.JACC_LOOP_GEMM_F64, None,
+                          [J.arg(IN, h["GA"]), J.arg(IN, h["GB"]), J.arg(OUT, h["GC"])], self.aid())
+            dev["GC"][...] = orc.gemm_f64(dev["GA"], dev["GB"])
+        elif op == "fig4":
+            x_in = float(r.integers(-8, 8)) / 4
+            fn = h["jx"].size
+            J.jacc_launch(J.JACC_LOOP_FIG4_F64, J.make_range(0, fn),
+                          [J.arg(IN, h["jx"]), J.arg(IN, h["kx"]), J.arg(IN, h["fc"]),
+                           J.arg(OUT, h["fa"]), J.arg(OUT, h["fb"]),
+                           J.arg(J.JACC_ARG_SCALAR_F64, f64=x_in)], self.aid())
+            orc.fig4(dev["jx"], dev["kx"], dev["fc"], x_in, dev["fa"], dev["fb"])
+        elif op == "himeno":
+            g = np.zeros(1)
+            names = ("hp", "ha", "hb", "hc", "hw1", "hbd")
+            J.jacc_launch(J.JACC_LOOP_HIMENO_F32, None,
+                          [J.arg(IN, h[k]) for k in names] +
+                          [J.arg(OUT, h["hw2"]), J.arg(J.JACC_ARG_REDUCE_SUM_F64, g),
+                           J.arg(J.JACC_ARG_SCALAR_F64, f64=0.8)], self.aid())
+            _, gref, _ = orc.himeno_stencil(*(dev[k] for k in names), dev["hw2"])
+            assert abs(g[0] - gref) <= 1e-12 * abs(gref) + 1e-300, (self.desc(), log)
+            J.jacc_launch(J.JACC_LOOP_HIMENO_COPY_F32, None,
+                          [J.arg(IN, h["hw2"]), J.arg(OUT, h["hp"])], self.aid())
+            orc.himeno_copy(dev["hw2"], dev["hp"])
         elif op == "uh":
-            k = str(r.choice(["A", "B", "x", "a"]))
+            k = str(r.choice(["A", "B", "x", "a", "GC", "fa", "fb", "hp", "hw2"]))
             e0, e1 = self._subrange(h[k].size)
             J.jacc_update_host(h[k], e0 * h[k].itemsize, (e1 - e0) * h[k].itemsize)
             mh = self.model_host[k].reshape(-1)
             mh[e0:e1] = dev[k].reshape(-1)[e0:e1]
             assert np.array_equal(h[k], self.model_host[k]), (k, e0, e1, self.desc(), log)
         elif op == "ud":
-            k = str(r.choice(["A", "B", "y", "a"]))
+            k = str(r.choice(["A", "B", "y", "a", "GA", "fc", "fa", "hp", "ha"]))
             e0, e1 = self._subrange(h[k].size)
             flat = h[k].reshape(-1)
             if k == "a":
                 flat[e0:e1] = _dyadic(r, e1 - e0)
+            elif k == "GA":
+                flat[e0:e1] = r.integers(-8, 8, e1 - e0).astype(np.float64)
             else:
                 flat[e0:e1] = r.random(e1 - e0).astype(flat.dtype)
             self.model_host[k].reshape(-1)[e0:e1] = flat[e0:e1]
@@ -140,27 +186,28 @@ class Program:
         if self.policy != J.JACC_MERGE_EAGER:
             return
         J.jacc_wait()
-        for k in ("A", "B", "x", "a"):
+        for k in ("A", "B", "x", "a", "GC", "fa", "fb", "hp", "hw2"):
             for d in range(self.n):
                 assert np.array_equal(J.jacc_get_replica(self.host[k], d), self.dev[k]), \
                     (k, d, self.desc(), log)
 
 
-@pytest.mark.parametrize("seed", range(160))
+# JACC_RANDOM_PROGRAMS=<count> widens the sweep (bug hunting)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("JACC_RANDOM_PROGRAMS", "160"))))
 def test_random_program(J, seed):
     prog = Program(J, 1000 + seed)
     J.jacc_init(prog.n, [0] * prog.n)
     log = []
     try:
         prog.config()
-        for k in ("A", "B", "y", "x", "idx", "bs", "a"):
+        for k in prog.host:
             J.jacc_data_create(prog.host[k])
             J.jacc_update_device(prog.host[k])
         for i in range(60):
             prog.step(log)
             if i % 10 == 9:
                 prog.check_replicas(log)
-        for k in ("A", "B", "x", "a"):
+        for k in ("A", "B", "x", "a", "GC", "fa", "fb", "hp", "hw2"):
             J.jacc_update_host(prog.host[k])
             assert np.array_equal(prog.host[k], prog.dev[k]), (k, prog.desc(), log)
     finally:
