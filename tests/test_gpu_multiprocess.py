@@ -85,3 +85,19 @@ def test_multiprocess_parity(tmp_path, world, policy):
         assert np.array_equal(z["himeno_p"], hp_ref)
         assert np.allclose(z["himeno_gosa"], hg_ref, rtol=1e-12, atol=0)
         assert np.array_equal(z["fig4_a"], fa_ref) and np.array_equal(z["fig4_b"], fb_ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multiprocess_random_programs(world):
+    """Randomised programs (test_gpu_random_programs.Program) run SPMD in
+    one-process-per-GPU mode: every rank checks its own replicas and host
+    arrays against the oracle model."""
+    import __graft_entry__ as ge
+    ge.build_jacc()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+           str(world), "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "workers", "mp_random.py"), "--seeds", "24",
+           "--first", str(5000 + 100 * world)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("ok 24") == world

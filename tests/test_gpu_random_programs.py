@@ -37,7 +37,11 @@ def _dyadic(rng, n):
 
 
 class Program:
-    def __init__(self, J, seed):
+    """world=None: single process, random device count; world=W: one rank
+    of a W-process job (same seed on every rank: SPMD), where adaptive
+    mode, async queues and the iteration-split scatter do not apply."""
+
+    def __init__(self, J, seed, world=None):
         self.J = J
         self.rng = np.random.default_rng(seed)
         r = self.rng
@@ -47,6 +51,11 @@ class Program:
         self.split = int(r.choice([-1, -1, 1]))
         self.nq = int(r.choice([1, 1, 3]))
         self.itersplit = int(self.n > 1 and self.nq == 1 and r.random() < 0.3)
+        self.local = list(range(self.n))
+        if world is not None:
+            self.n, self.nq, self.itersplit = world, 1, 0
+            self.mode = int(r.choice([0, 0, 1]))
+            self.local = [J.jacc_rank()]
         N = int(r.integers(3, 70))
         L = int(r.integers(1, 3000))
         S, M = int(r.integers(1, 5000)), int(r.integers(1, 4000))
@@ -84,8 +93,25 @@ class Program:
         J.jacc_set_merge_policy(self.policy)
         J.jacc_set_mode(self.mode)
         J.jacc_set_split_dim(self.split)
-        J.jacc_set_queues(self.nq)
-        J.jacc_set_scatter_split(self.itersplit)
+        if self.nq > 1:
+            J.jacc_set_queues(self.nq)
+        if self.itersplit:
+            J.jacc_set_scatter_split(self.itersplit)
+
+    def run(self, steps, create):
+        J = self.J
+        log = []
+        self.config()
+        for k in self.host:
+            create(self.host[k])
+            J.jacc_update_device(self.host[k])
+        for i in range(steps):
+            self.step(log)
+            if i % 10 == 9:
+                self.check_replicas(log)
+        for k in ("A", "B", "x", "a", "GC", "fa", "fb", "hp", "hw2"):
+            J.jacc_update_host(self.host[k])
+            assert np.array_equal(self.host[k], self.dev[k]), (k, self.desc(), log)
 
     def desc(self):
         return (f"n={self.n} policy={self.policy} mode={self.mode} split={self.split} "
@@ -187,7 +213,7 @@ class Program:
             return
         J.jacc_wait()
         for k in ("A", "B", "x", "a", "GC", "fa", "fb", "hp", "hw2"):
-            for d in range(self.n):
+            for d in self.local:
                 assert np.array_equal(J.jacc_get_replica(self.host[k], d), self.dev[k]), \
                     (k, d, self.desc(), log)
 
@@ -197,18 +223,7 @@ class Program:
 def test_random_program(J, seed):
     prog = Program(J, 1000 + seed)
     J.jacc_init(prog.n, [0] * prog.n)
-    log = []
     try:
-        prog.config()
-        for k in prog.host:
-            J.jacc_data_create(prog.host[k])
-            J.jacc_update_device(prog.host[k])
-        for i in range(60):
-            prog.step(log)
-            if i % 10 == 9:
-                prog.check_replicas(log)
-        for k in ("A", "B", "x", "a", "GC", "fa", "fb", "hp", "hw2"):
-            J.jacc_update_host(prog.host[k])
-            assert np.array_equal(prog.host[k], prog.dev[k]), (k, prog.desc(), log)
+        prog.run(60, J.jacc_data_create)
     finally:
         J.jacc_finalize()
