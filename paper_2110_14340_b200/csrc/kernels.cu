@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
 // ---------------------------------------------------------------------------
 // BK4b destination-binned scatter (see kernels.cuh)
 // ---------------------------------------------------------------------------
-constexpr int SB_T = 256;  // partition tile = SB_T x E elements (E = 8 default, 16)
+constexpr int SB_T = 256;  // partition tile = SB_T x E elements (E = 16 default, 8, 12)
 constexpr int SB_MAXB = 1024;
 
 __global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restrict__ idx, int64_t n,
@@ -650,6 +650,10 @@ __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off,
     if (lane == 31) *total = inc;
 }
 
+// Per tile: all E keys of a thread are loaded first, then the values of the
+// in-range ones (two independent batches of loads in flight, not E
+// key->value dependency chains), then histogram, scan, staging in shared
+// memory and bucket-contiguous write-out.
 template <typename T, int E>
 __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restrict__ idx,
                                                          const T *__restrict__ b, int64_t n,
@@ -666,25 +670,31 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restri
     uint16_t *sbk = reinterpret_cast<uint16_t *>(sdyn + TILE * (sizeof(T) + 4));
     const int tid = threadIdx.x;
     const int64_t ntiles = (n + TILE - 1) / TILE;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        for (int i = tid; i < nb; i += SB_T) hist[i] = 0;
-        __syncthreads();
-        int32_t k[E];
-        T v[E];
-        int bk[E];
-        unsigned rk[E];
+    auto load_keys = [&](int64_t t, int32_t *k) {
 #pragma unroll
         for (int j = 0; j < E; j++) {
             const int64_t i = t * TILE + j * SB_T + tid;
-            bk[j] = -1;
-            if (i < n) {
-                k[j] = __ldcs(idx + i);
-                if (k[j] >= lo && k[j] < hi) {
-                    bk[j] = (int)((k[j] - lo) >> shift);
-                    v[j] = __ldcs(b + i);
-                }
-            }
+            k[j] = (t < ntiles && i < n) ? __ldcs(idx + i) : (int32_t)lo - 1;  // lo-1: out of range
         }
+    };
+    auto load_vals = [&](int64_t t, const int32_t *k, T *v) {
+#pragma unroll
+        for (int j = 0; j < E; j++) {
+            const int64_t i = t * TILE + j * SB_T + tid;
+            if (k[j] >= lo && k[j] < hi) v[j] = __ldcs(b + i);
+        }
+    };
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int32_t k[E];
+        T v[E];
+        load_keys(t, k);
+        load_vals(t, k, v);
+        for (int i = tid; i < nb; i += SB_T) hist[i] = 0;
+        __syncthreads();
+        int bk[E];
+        unsigned rk[E];
+#pragma unroll
+        for (int j = 0; j < E; j++) bk[j] = (k[j] >= lo && k[j] < hi) ? (int)((k[j] - lo) >> shift) : -1;
 #pragma unroll
         for (int j = 0; j < E; j++)
             if (bk[j] >= 0) rk[j] = atomicAdd(&hist[bk[j]], 1u);
@@ -1489,44 +1499,46 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     if (e != cudaSuccess) return e;
     scat_hist_kernel<<<148 * 8, 256, 0, s>>>(idx, n, lo, hi, pl.shift, pl.nb, counts);
     scat_scan_kernel<<<1, 32, 0, s>>>(counts, pl.nb, base, cursor, work);
-    static int pe = -1;  // partition elements per thread (JACC_SCATTER_PART_E: 8 or 16)
+    // partition elements per thread (JACC_SCATTER_PART_E: 8, 12 or 16);
+    // 16 measured best (tools/tune_scatter.py: 5.51 ms vs 5.76 ms for 8)
+    static int pe = -1;
     if (pe < 0) {
         const char *e = getenv("JACC_SCATTER_PART_E");
-        pe = (e && atoi(e) == 16) ? 16 : 8;
+        pe = e ? atoi(e) : 16;
+        if (pe != 8 && pe != 12) pe = 16;
     }
     const int64_t tile = (int64_t)SB_T * pe;
     const int64_t tiles = (n + tile - 1) / tile;
     const size_t dsm = (size_t)tile * ((is_f64 ? 8 : 4) + 4 + 2);
     const int pg = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
+#define PART_LAUNCH(T, E)                                                                          \
+    do {                                                                                           \
+        if (dsm > 32 * 1024) /* + 16 KB static: beyond the 48 KB default */                       \
+            cudaFuncSetAttribute(scat_part_kernel<T, E>,                                           \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);           \
+        scat_part_kernel<T, E><<<pg, SB_T, dsm, s>>>(idx, static_cast<const T *>(b), n, lo, hi,    \
+                                                     pl.shift, pl.nb, cursor, pidx,                \
+                                                     reinterpret_cast<T *>(pv));                   \
+    } while (0)
+#define PART_E(T)                                                                                  \
+    do {                                                                                           \
+        if (pe == 12) PART_LAUNCH(T, 12);                                                          \
+        else if (pe == 16) PART_LAUNCH(T, 16);                                                     \
+        else PART_LAUNCH(T, 8);                                                                    \
+    } while (0)
     if (is_f64) {
-        if (pe == 16) {
-            cudaFuncSetAttribute(scat_part_kernel<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-            scat_part_kernel<double, 16><<<pg, SB_T, dsm, s>>>(idx, static_cast<const double *>(b), n, lo,
-                                                                hi, pl.shift, pl.nb, cursor, pidx,
-                                                                reinterpret_cast<double *>(pv));
-        } else {
-            scat_part_kernel<double, 8><<<pg, SB_T, dsm, s>>>(idx, static_cast<const double *>(b), n, lo,
-                                                               hi, pl.shift, pl.nb, cursor, pidx,
-                                                               reinterpret_cast<double *>(pv));
-        }
+        PART_E(double);
         scat_apply_kernel<double><<<148 * 8, 256, 0, s>>>(
             pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
             static_cast<double *>(a), bytemap, epoch, dirty);
     } else {
-        if (pe == 16) {
-            cudaFuncSetAttribute(scat_part_kernel<int32_t, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-            scat_part_kernel<int32_t, 16><<<pg, SB_T, dsm, s>>>(idx, static_cast<const int32_t *>(b), n,
-                                                                 lo, hi, pl.shift, pl.nb, cursor, pidx,
-                                                                 reinterpret_cast<int32_t *>(pv));
-        } else {
-            scat_part_kernel<int32_t, 8><<<pg, SB_T, dsm, s>>>(idx, static_cast<const int32_t *>(b), n,
-                                                                lo, hi, pl.shift, pl.nb, cursor, pidx,
-                                                                reinterpret_cast<int32_t *>(pv));
-        }
+        PART_E(int32_t);
         scat_apply_kernel<int32_t><<<148 * 8, 256, 0, s>>>(
             pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
             static_cast<int32_t *>(a), bytemap, epoch, dirty);
     }
+#undef PART_E
+#undef PART_LAUNCH
     scat_pack_kernel<<<148 * 8, 256, 0, s>>>(bytemap, epoch, lo, hi, bitmap);
     return cudaGetLastError();
 }

@@ -47,7 +47,8 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         one()
     else:
-        for pe, mb in [(8, 16), (16, 16), (8, 8), (8, 32), (16, 32), (16, 8), (8, 4)]:
+        grid = [(16, 16), (12, 16), (8, 16), (16, 8), (12, 8), (16, 32)]
+        for pe, mb in grid:
             env = dict(os.environ, JACC_SCATTER_PART_E=str(pe), JACC_SCATTER_BUCKET_MB=str(mb))
             r = subprocess.run([sys.executable, __file__, "one"], env=env, capture_output=True, text=True)
             print(r.stdout.strip() or r.stderr[-800:], flush=True)
