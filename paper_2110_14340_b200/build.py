@@ -15,8 +15,10 @@ LIB = os.path.join(PKG, "libjacc.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "runtime.cpp", "kernels.cuh")] + [
-    os.path.join(INCLUDE, "jacc.h")]
+# host runtime translation units (all share csrc/rt.hpp)
+HOST = ("abi.cpp", "plan.cpp", "launch.cpp", "mp.cpp", "graphs.cpp")
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "kernels.cuh", "rt.hpp") + HOST] + [
+    os.path.join(INCLUDE, "jacc.h"), os.path.join(CSRC, "exports.map")]
 
 
 def nccl_paths():
@@ -42,16 +44,21 @@ def build(force=False, verbose=False):
     bdir = os.path.join(PKG, "_build")
     os.makedirs(bdir, exist_ok=True)
     ko = os.path.join(bdir, "kernels.o")
-    ro = os.path.join(bdir, "runtime.o")
     _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
           "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-c",
           os.path.join(CSRC, "kernels.cu"), "-o", ko])
-    _run(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE,
-          "-I", os.path.join(CUDA_HOME, "include"), "-I", nccl_inc, "-c",
-          os.path.join(CSRC, "runtime.cpp"), "-o", ro])
+    objs = [ko]
+    for src in HOST:
+        o = os.path.join(bdir, src.replace(".cpp", ".o"))
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE,
+              "-I", os.path.join(CUDA_HOME, "include"), "-I", nccl_inc, "-c",
+              os.path.join(CSRC, src), "-o", o])
+        objs.append(o)
     tmp = LIB + ".tmp"
-    _run([NVCC, *ARCH, "-shared", "-o", tmp, ko, ro, "-cudart", "static",
-          "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}"])
+    # only the jacc_* C-ABI is exported (csrc/exports.map)
+    _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static",
+          "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}",
+          "-Xlinker", f"--version-script={os.path.join(CSRC, 'exports.map')}"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -93,3 +93,15 @@ def test_sass_is_sm100a_and_uses_dmma(J):
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", so], capture_output=True,
                           text=True).stdout
     assert "DMMA" in sass
+
+
+def test_library_exports_only_the_c_abi(J):
+    """csrc/exports.map: the C-ABI and nothing else (no C++ runtime, kernel
+    wrapper or std:: template symbols leak out of libjacc.so)."""
+    import subprocess
+    r = subprocess.run(["nm", "-D", "--defined-only", J.lib._name], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip("nm unavailable")
+    syms = [ln.split()[-1] for ln in r.stdout.splitlines() if ln.strip()]
+    assert syms and all(s.startswith("jacc_") for s in syms), [s for s in syms if not s.startswith("jacc_")][:5]
+    assert sorted(syms) == _declared()

@@ -785,6 +785,53 @@ def test_graph_rules(J):
         assert J.lib.jacc_graph_replay(gid, 1) == J.JACC_ERR_STATE
 
 
+@pytest.mark.parametrize("count", [1, 2, 3])
+def test_graph_replay_odd_writes_keep_dirty_records_exact(J, count):
+    """A graph writing x three times flips x's dirty-record slot parity on
+    every replay; each replay must still leave the exact record of its last
+    launch (no stale min/max from the previous replay)."""
+    M = 100
+    y = synth.uniform_f32(M, 99, 1)
+    x = np.zeros(M, dtype=np.float32)
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    args = [J.arg(IN, y), J.arg(OUT, x)]
+    with runtime(J, 2):
+        _create(J, y, x)
+        J.jacc_graph_begin()
+        for lo, hi in ((0, 10), (20, 30), (40, 50)):
+            J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(lo, hi), args)
+        gid = J.jacc_graph_end()
+        J.jacc_graph_replay(gid, count)
+        J.jacc_wait()
+        # device 0 owns [0, 50): its last write was [40, 50); device 1 none
+        assert J.jacc_get_dirty_range(x, 0) == (40, 49)
+        assert J.jacc_get_dirty_range(x, 1) == (U64MAX, 0)
+        # a plain launch after the replays records its own range only
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(5, 7), args)
+        assert J.jacc_get_dirty_range(x, 0) == (5, 6)
+        J.jacc_update_host(x)
+    ref = np.zeros(M, dtype=np.float32)
+    for lo, hi in ((0, 10), (20, 30), (40, 50)):
+        ref[lo:hi] = orc.square_f32(np.ascontiguousarray(y[lo:hi]))
+    assert np.array_equal(x, ref)
+
+
+def test_graph_replay_count_needs_a_fixed_point(J):
+    """count > 1 replays back to back only when the graph maps the captured
+    validity state onto itself (its pulls were planned for that state)."""
+    N = 40
+    A = synth.uniform_f64(N * N, 99, 2).reshape(N, N)
+    B = synth.uniform_f64(N * N, 99, 3).reshape(N, N)
+    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
+    with runtime(J, 2, 1):  # HALO: peers' copies go stale
+        _create(J, A, B)
+        J.jacc_graph_begin()
+        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [J.arg(IN, A), J.arg(OUT, B)])
+        gid = J.jacc_graph_end()
+        assert J.lib.jacc_graph_replay(gid, 2) == J.JACC_ERR_STATE
+        assert J.lib.jacc_graph_replay(gid, 1) == J.JACC_OK
+
+
 # --------------------------------------------------------------------------
 # NEXT-2 multidimensional division: split dims > 0 (strided blocks, P:517-527)
 # --------------------------------------------------------------------------
