@@ -784,6 +784,287 @@ __global__ void __launch_bounds__(256) scat_pack_kernel(const uint8_t *__restric
 
 
 // ---------------------------------------------------------------------------
+// BK4c owner-slice apply (see kernels.cuh).  Fine bin g of the owned span is
+// the element slice [lo + g*2^fs, lo + (g+1)*2^fs) -- 64 KB of `a`, held in
+// one CTA's shared memory while its updates are added there; SL_FPC fine
+// bins make one coarse bucket (the partition's bucket).
+// ---------------------------------------------------------------------------
+constexpr int SL_FPC = 128;       // fine slices per coarse bucket
+constexpr int SL_MAXF = 32768;    // fine bins the histogram holds (128 KB smem)
+constexpr int SL_T = 512;         // threads of the slice kernel (1 CTA / SM)
+constexpr int SL_E = 8;           // pairs per thread of an A tile
+constexpr int SL_TA = SL_T * SL_E;
+constexpr int SL_SLICE = 64 * 1024;  // bytes of `a` per slice (2 CTAs / SM)
+
+struct SliceHdr {  // device-side layout of the header inside the scratch
+    unsigned *fcnt;  // [nf]
+    u64 *fbase;      // [nf + 1] pair offset of fine bin g (nested in coarse order)
+    u64 *fcur;       // [nf]
+    u64 *ccur;       // [nb] coarse cursors of the partition kernel
+    unsigned *doneA; // [nb] A tiles finished per coarse bucket
+    int *stage;      // [2 nb] stage -> (type << 16 | coarse bucket)
+    u64 *sstart;     // [2 nb + 1] first work item of each stage
+    u64 *work;       // work counter
+};
+
+__global__ void __launch_bounds__(1024) scat_fhist_kernel(const int32_t *__restrict__ idx, int64_t n,
+                                                         int64_t lo, int64_t hi, int fs, int nf,
+                                                         unsigned *fcnt) {
+    extern __shared__ unsigned fh[];
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) fh[i] = 0;
+    __syncthreads();
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t hd = (int64_t)((16 - ((uintptr_t)idx & 15)) & 15) >> 2;
+    if (hd > n) hd = n;
+    const int64_t n4 = (n - hd) >> 2;
+    const int4 *idx4 = reinterpret_cast<const int4 *>(idx + hd);
+    auto put = [&](int32_t k) {
+        if (k >= lo && k < hi) atomicAdd(&fh[(k - lo) >> fs], 1u);
+    };
+    if (tid < hd) put(idx[tid]);
+    for (int64_t q = tid; q < n4; q += nth) {
+        const int4 k = __ldg(idx4 + q);
+        put(k.x);
+        put(k.y);
+        put(k.z);
+        put(k.w);
+    }
+    for (int64_t i = hd + 4 * n4 + tid; i < n; i += nth) put(idx[i]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nf; i += blockDim.x)
+        if (fh[i]) atomicAdd(&fcnt[i], fh[i]);
+}
+
+// one CTA of 1024 threads: fine offsets, cursors and the work-stage table
+// (A(0), A(1), B(0), A(2), B(1), ..., B(nb-1): every B stage waits
+// only on A tiles dequeued before it, so the work queue cannot deadlock whatever
+// the residency)
+__global__ void __launch_bounds__(1024) scat_fscan_kernel(SliceHdr h, int nf, int nb) {
+    __shared__ u64 wsum[32];
+    constexpr int PER = SL_MAXF / 1024;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    u64 s = 0;
+    for (int i = 0; i < PER; i++) {
+        const int g = t * PER + i;
+        s += g < nf ? h.fcnt[g] : 0;
+    }
+    u64 inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        u64 x = wsum[lane], y = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 v = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += v;
+        }
+        wsum[lane] = y - x;
+    }
+    __syncthreads();
+    u64 run = wsum[w] + inc - s;
+    for (int i = 0; i < PER; i++) {
+        const int g = t * PER + i;
+        if (g < nf) {
+            h.fbase[g] = run;
+            h.fcur[g] = run;
+            run += h.fcnt[g];
+        }
+        if (g == nf - 1) h.fbase[nf] = run;
+    }
+    __syncthreads();
+    for (int c = t; c < nb; c += 1024) {
+        h.ccur[c] = h.fbase[c * SL_FPC];
+        h.doneA[c] = 0;
+    }
+    if (t == 0) {
+        *h.work = 0;
+        auto na = [&](int c) {
+            const int g1 = (c + 1) * SL_FPC < nf ? (c + 1) * SL_FPC : nf;
+            return (h.fbase[g1] - h.fbase[c * SL_FPC] + SL_TA - 1) / SL_TA;
+        };
+        auto nbk = [&](int c) { return (u64)((nf - c * SL_FPC) < SL_FPC ? nf - c * SL_FPC : SL_FPC); };
+        int k = 0;
+        u64 acc = 0;
+        auto push = [&](int type, int c, u64 items) {
+            h.stage[k] = (type << 16) | c;
+            h.sstart[k] = acc;
+            acc += items;
+            k++;
+        };
+        constexpr int LAG = 1;  // B(c) follows A(c + LAG) (LAG 2 measured slower)
+        for (int c = 0; c < nb + LAG; c++) {
+            if (c < nb) push(0, c, na(c));
+            if (c >= LAG) push(1, c - LAG, nbk(c - LAG));
+        }
+        h.sstart[k] = acc;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SL_T, 2) scat_slice_kernel(SliceHdr h, int nb, int nf, int fs,
+                                                            int64_t lo, int64_t hi,
+                                                            const int32_t *__restrict__ ck,
+                                                            const T *__restrict__ cv, int32_t *fk,
+                                                            T *fv, T *a, uint32_t *bitmap,
+                                                            u64 *dirty) {
+    constexpr int SLN = SL_SLICE / sizeof(T);  // elements of one slice
+    extern __shared__ __align__(16) unsigned char sdyn[];
+    // B item: [SLN] T slice (+16 B so it can sit congruent to `a` mod 16 B)
+    // and [SLN/32 + 2] u32 dirty bits; A item (aliased): [SL_TA] T,
+    // [SL_TA] i32, [SL_TA] u8 staging
+    uint32_t *sbits = reinterpret_cast<uint32_t *>(sdyn + SL_SLICE + 16);
+    T *sv = reinterpret_cast<T *>(sdyn);
+    int32_t *sk = reinterpret_cast<int32_t *>(sdyn + SL_TA * sizeof(T));
+    uint8_t *sbk = reinterpret_cast<uint8_t *>(sdyn + SL_TA * (sizeof(T) + 4));
+    __shared__ unsigned hist[SL_FPC], loff[SL_FPC], total;
+    __shared__ u64 gbase[SL_FPC];
+    __shared__ u64 item;
+    __shared__ int ist, ic;
+    const int tid = threadIdx.x;
+    const int nst = 2 * nb;
+    u64 mn = kU64Max, mx = 0;
+    for (;;) {
+        if (tid == 0) {
+            item = atomicAdd(h.work, 1ull);
+            int s0 = 0, s1 = nst;  // stage: largest s with sstart[s] <= item
+            while (s1 - s0 > 1) {
+                const int m = (s0 + s1) >> 1;
+                if (h.sstart[m] <= item) s0 = m;
+                else s1 = m;
+            }
+            ist = s0;
+            ic = h.stage[s0];
+        }
+        __syncthreads();
+        const u64 it = item;
+        const int st = ist, code = ic;
+        __syncthreads();
+        if (it >= h.sstart[nst]) break;
+        const int c = code & 0xffff;
+        const u64 j = it - h.sstart[st];
+        const int g0 = c * SL_FPC;
+        if ((code >> 16) == 0) {
+            // ---- A: fine-partition tile j of coarse bucket c -------------------
+            const int g1 = g0 + SL_FPC < nf ? g0 + SL_FPC : nf;
+            const u64 p0 = h.fbase[g0] + j * SL_TA, pe = h.fbase[g1];
+            const int cnt = (int)(pe - p0 < (u64)SL_TA ? pe - p0 : (u64)SL_TA);
+            for (int i = tid; i < SL_FPC; i += SL_T) hist[i] = 0;
+            int32_t k[SL_E];
+            T v[SL_E];
+#pragma unroll
+            for (int e = 0; e < SL_E; e++) {
+                const int q = e * SL_T + tid;
+                k[e] = q < cnt ? __ldcs(ck + p0 + q) : 0;
+            }
+#pragma unroll
+            for (int e = 0; e < SL_E; e++) {
+                const int q = e * SL_T + tid;
+                if (q < cnt) v[e] = __ldcs(cv + p0 + q);
+            }
+            __syncthreads();
+            int bk[SL_E];
+            unsigned rk[SL_E];
+#pragma unroll
+            for (int e = 0; e < SL_E; e++) {
+                const int q = e * SL_T + tid;
+                bk[e] = q < cnt ? (int)(((int64_t)k[e] - lo) >> fs) - g0 : -1;
+                if (bk[e] >= 0) rk[e] = atomicAdd(&hist[bk[e]], 1u);
+            }
+            __syncthreads();
+            if (tid < 32) warp_exscan(hist, loff, SL_FPC, &total);
+            if (tid < SL_FPC) gbase[tid] = hist[tid] ? atomicAdd(&h.fcur[g0 + tid], (u64)hist[tid]) : 0;
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < SL_E; e++)
+                if (bk[e] >= 0) {
+                    const unsigned pos = loff[bk[e]] + rk[e];
+                    sk[pos] = k[e];
+                    sv[pos] = v[e];
+                    sbk[pos] = (uint8_t)bk[e];
+                }
+            __syncthreads();
+            for (int pos = tid; pos < cnt; pos += SL_T) {
+                const int bb = sbk[pos];
+                const u64 g = gbase[bb] + (pos - loff[bb]);
+                fk[g] = sk[pos];
+                fv[g] = sv[pos];
+            }
+            __syncthreads();  // then one cumulative fence + release by thread 0
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(&h.doneA[c], 1u);
+            }
+        } else {
+            // ---- B: apply fine slice g = g0 + j in shared memory ---------------
+            const int g = g0 + (int)j;
+            const int64_t e0 = lo + ((int64_t)g << fs);
+            const int64_t e1 = e0 + SLN < hi ? e0 + SLN : hi;
+            const int len = (int)(e1 - e0);
+            const u64 q0 = h.fbase[g], q1 = h.fbase[g + 1];
+            const int64_t w0 = e0 >> 5, w1 = (e1 + 31) >> 5;  // bitmap words covering the slice
+            const int nw = (int)(w1 - w0);
+            if (q1 > q0) {
+                // slice -> shared memory: 16-byte cp.async for the aligned
+                // body (no register staging, all in flight at once), scalar
+                // head and tail
+                const int pad = (int)(((uintptr_t)(a + e0) & 15) / sizeof(T));
+                T *sa = reinterpret_cast<T *>(sdyn) + pad;
+                constexpr int V = 16 / sizeof(T);
+                const int head = pad ? V - pad : 0;
+                const int h2 = head < len ? head : len;
+                const int nv = (len - h2) / V;
+                for (int i = tid; i < nv; i += SL_T)
+                    cp_async16(sa + h2 + i * V, a + e0 + h2 + i * V, 16);
+                cp_commit();
+                if (tid < h2) sa[tid] = a[e0 + tid];
+                for (int i = h2 + nv * V + tid; i < len; i += SL_T) sa[i] = a[e0 + i];
+                for (int i = tid; i < nw; i += SL_T) sbits[i] = 0;
+                if (tid == 0) {
+                    const int g1 = g0 + SL_FPC < nf ? g0 + SL_FPC : nf;
+                    const unsigned need =
+                        (unsigned)((h.fbase[g1] - h.fbase[g0] + SL_TA - 1) / SL_TA);
+                    volatile unsigned *d = h.doneA + c;
+                    while (*d < need) __nanosleep(256);
+                    __threadfence();
+                }
+                cp_wait<0>();
+                __syncthreads();
+                const int sh = (int)(e0 & 31);  // bit of element e0 within word w0
+#pragma unroll 8
+                for (u64 p = q0 + tid; p < q1; p += SL_T) {
+                    const int32_t kk = __ldcg(fk + p);
+                    const T vv = __ldcg(fv + p);
+                    const int o = (int)((int64_t)kk - e0);
+                    atomicAdd(&sa[o], vv);
+                    atomicOr(&sbits[(o + sh) >> 5], 1u << ((o + sh) & 31));
+                    mn = (u64)kk < mn ? (u64)kk : mn;
+                    mx = (u64)kk > mx ? (u64)kk : mx;
+                }
+                __syncthreads();
+                for (int i = tid; i < len; i += SL_T) a[e0 + i] = sa[i];
+                for (int i = tid; i < nw; i += SL_T) {
+                    const uint32_t bits = sbits[i];
+                    if (i == 0 || i == nw - 1) {  // words shared with a neighbour slice
+                        if (bits) atomicOr(bitmap + w0 + i, bits);
+                    } else {
+                        bitmap[w0 + i] = bits;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    publish_dirty<SL_T / 32>(mn, mx, dirty);
+}
+
+
+// ---------------------------------------------------------------------------
 // NEXT-2  Himeno (19-point stencil + gosa reduction, and the copy loop)
 //
 // Persistent fixed grid; a tile is 32 consecutive k x 8 j at one plane i,
@@ -1460,12 +1741,37 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
 }
 
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
-    ScatterPlan p{false, 0, 1, 0, 0};
+    ScatterPlan p{false, false, 0, 1, 0, 0, 0, 0, 0};
     const int64_t span = hi - lo;
     const char *force = getenv("JACC_SCATTER_BINNED");  // "0" never, "1" always (tests)
     if (span <= 0 || n <= 0 || (force && force[0] == '0')) return p;
     if (!(force && force[0] == '1') && (n < (1 << 22) || span * elem <= (int64_t)96 << 20))
         return p;  // a fits in L2: the direct kernel is already L2-resident
+    // owner-slice apply (BK4c), opt-in with JACC_SCATTER_SLICE=1: measured
+    // slower than the byte-map apply at 2^28, kept as
+    // the L2-atomic-free alternative; needs dense updates (at least one per
+    // 4 elements: the slices of `a` are read and written whole) and a fine
+    // histogram that fits
+    const char *fsl = getenv("JACC_SCATTER_SLICE");
+    int fs = 0;
+    while (((int64_t)elem << fs) < SL_SLICE) fs++;
+    const int64_t nf = (span + ((int64_t)1 << fs) - 1) >> fs;
+    const bool slice = nf <= SL_MAXF && fsl && fsl[0] == '1' && 4 * n >= span;
+    if (slice) {
+        p.binned = p.slice = true;
+        p.fs = fs;
+        p.nf = (int)nf;
+        p.shift = fs + 7;  // SL_FPC = 128 fine slices per coarse bucket
+        p.nb = (int)((nf + SL_FPC - 1) / SL_FPC);
+        const size_t nb = (size_t)p.nb, f = (size_t)nf;
+        p.hdr = ((f + 1) * 8 + f * 8 + nb * 8 + (2 * nb + 1) * 8 + 8 + f * 4 + nb * 4 + 2 * nb * 4 +
+                 255) & ~(size_t)255;
+        const size_t pk = ((size_t)n * 4 + 255) & ~(size_t)255;
+        const size_t pv = ((size_t)n * elem + 255) & ~(size_t)255;
+        p.scratch = p.hdr + 2 * (pk + pv);
+        p.bytemap = 0;
+        return p;
+    }
     int shift = 0;
     static int64_t bucket_mb = -1;  // JACC_SCATTER_BUCKET_MB (default 16)
     if (bucket_mb < 0) {
@@ -1483,10 +1789,77 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
     return p;
 }
 
+namespace {
+SliceHdr slice_hdr(void *scratch, const ScatterPlan &pl) {
+    char *c = static_cast<char *>(scratch);
+    const size_t f = (size_t)pl.nf, nb = (size_t)pl.nb;
+    SliceHdr h;
+    h.fbase = reinterpret_cast<u64 *>(c);
+    c += (f + 1) * 8;
+    h.fcur = reinterpret_cast<u64 *>(c);
+    c += f * 8;
+    h.ccur = reinterpret_cast<u64 *>(c);
+    c += nb * 8;
+    h.sstart = reinterpret_cast<u64 *>(c);
+    c += (2 * nb + 1) * 8;
+    h.work = reinterpret_cast<u64 *>(c);
+    c += 8;
+    h.fcnt = reinterpret_cast<unsigned *>(c);
+    c += f * 4;
+    h.doneA = reinterpret_cast<unsigned *>(c);
+    c += nb * 4;
+    h.stage = reinterpret_cast<int *>(c);
+    return h;
+}
+
+template <typename T>
+cudaError_t scatter_slice(cudaStream_t s, const int32_t *idx, const T *b, T *a, int64_t n,
+                          int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty,
+                          const ScatterPlan &pl, void *scratch) {
+    SliceHdr h = slice_hdr(scratch, pl);
+    char *sc = static_cast<char *>(scratch) + pl.hdr;
+    const size_t pk = ((size_t)n * 4 + 255) & ~(size_t)255;
+    const size_t pv = ((size_t)n * sizeof(T) + 255) & ~(size_t)255;
+    int32_t *ck = reinterpret_cast<int32_t *>(sc);
+    T *cv = reinterpret_cast<T *>(sc + pk);
+    int32_t *fk = reinterpret_cast<int32_t *>(sc + pk + pv);
+    T *fv = reinterpret_cast<T *>(sc + 2 * pk + pv);
+    cudaError_t e = cudaMemsetAsync(h.fcnt, 0, (size_t)pl.nf * 4, s);
+    if (e != cudaSuccess) return e;
+    // attributes are per device: set on every call (host-side, cheap)
+    cudaFuncSetAttribute(scat_fhist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SL_MAXF * 4);
+    const int pdsm = SB_T * 16 * (int)(sizeof(T) + 6);
+    cudaFuncSetAttribute(scat_part_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+    const int sdyn = SL_SLICE + 16 + (int)(SL_SLICE / sizeof(T) / 32 + 2) * 4;
+    e = cudaFuncSetAttribute(scat_slice_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sdyn);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+    scat_fhist_kernel<<<nsm, 1024, pl.nf * 4, s>>>(idx, n, lo, hi, pl.fs, pl.nf, h.fcnt);
+    scat_fscan_kernel<<<1, 1024, 0, s>>>(h, pl.nf, pl.nb);
+    const int64_t tile = (int64_t)SB_T * 16;
+    const int64_t tiles = (n + tile - 1) / tile;
+    const int pg = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
+    scat_part_kernel<T, 16><<<pg, SB_T, pdsm, s>>>(idx, b, n, lo, hi, pl.shift, pl.nb, h.ccur, ck, cv);
+    scat_slice_kernel<T><<<2 * nsm, SL_T, sdyn, s>>>(h, pl.nb, pl.nf, pl.fs, lo, hi, ck, cv, fk, fv, a,
+                                                 bitmap, dirty);
+    return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
                                u64 *dirty, const ScatterPlan &pl, void *scratch, uint8_t *bytemap,
                                uint8_t epoch) {
+    if (pl.slice)
+        return is_f64 ? scatter_slice<double>(s, idx, static_cast<const double *>(b),
+                                              static_cast<double *>(a), n, lo, hi, bitmap, dirty, pl,
+                                              scratch)
+                      : scatter_slice<int32_t>(s, idx, static_cast<const int32_t *>(b),
+                                               static_cast<int32_t *>(a), n, lo, hi, bitmap, dirty,
+                                               pl, scratch);
     char *sc = static_cast<char *>(scratch);
     u64 *counts = reinterpret_cast<u64 *>(sc);
     u64 *cursor = counts + pl.nb;

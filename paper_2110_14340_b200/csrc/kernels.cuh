@@ -66,11 +66,23 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
 // bucket by bucket, so the read-modify-writes of a hit L2 and every line of
 // a moves to/from HBM about once.  Write tracking (bitmap + range) is fused
 // into (4).  is_f64: T = double, else int32.
+//
+// BK4c Owner-slice apply (opt-in: JACC_SCATTER_SLICE=1, dense updates; measured
+// slower than BK4b at 2^28): the partition above
+// into 16 MiB coarse buckets, then one persistent kernel whose work queue
+// interleaves A items (fine-partition 4096 pairs of a coarse bucket into its
+// 128 slices of 128 KB) and B items (one CTA loads a slice of a into shared
+// memory, adds the slice's updates there -- shared-memory atomics instead of
+// L2 atomics -- sets the slice's dirty bits in shared memory and writes the
+// slice and its bitmap words back).  No byte-map.
 struct ScatterPlan {
     bool binned;
-    int shift, nb;
+    bool slice;       // BK4c owner-slice apply
+    int shift, nb;    // coarse bucket = 2^shift elements, nb buckets
     size_t scratch;   // bytes of pair scratch
-    size_t bytemap;   // bytes of the epoch byte-map (elements of a, rounded to 32)
+    size_t bytemap;   // bytes of the epoch byte-map (elements of a, rounded to 32; 0 = none)
+    int fs, nf;       // BK4c: slice = 2^fs elements, nf slices
+    size_t hdr;       // BK4c: header bytes at the start of the scratch
 };
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem);
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,

@@ -441,13 +441,15 @@ def test_scatter_permutation_exact(J):
     assert np.array_equal(a, ref)
 
 
-@pytest.mark.parametrize("binned", ["0", "1"])
+@pytest.mark.parametrize("binned,slice_", [("0", "0"), ("1", "0"), ("1", "1")])
 @pytest.mark.parametrize("n", [1, 3])
 @pytest.mark.parametrize("lo", [0, 1, 2, 3, 5])
-def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, n, lo):
-    """Direct and destination-binned scatter pipelines, iteration ranges
-    starting at any element (int4 head/tail handling)."""
+def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, slice_, n, lo):
+    """Direct, destination-binned (byte-map) and owner-slice scatter
+    pipelines, iteration ranges starting at any element (int4 head/tail
+    handling)."""
     monkeypatch.setenv("JACC_SCATTER_BINNED", binned)
+    monkeypatch.setenv("JACC_SCATTER_SLICE", slice_)
     N, M = 30_011, 4099
     idx = synth.index_i32(N, M, 75, 5)
     b = synth.dyadic_f64(N, 75, 6)
@@ -470,10 +472,13 @@ def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, n, lo):
     assert np.array_equal(a, ref)
 
 
+@pytest.mark.parametrize("slice_", ["0", "1"])
 @pytest.mark.parametrize("dtype", ["f64", "i32"])
 @pytest.mark.parametrize("n", [1, 2])
-def test_scatter_binned_large(J, dtype, n):
-    """Arrays larger than L2 take the binned pipeline by default."""
+def test_scatter_binned_large(J, monkeypatch, dtype, n, slice_):
+    """Arrays larger than L2 take the binned pipeline by default (byte-map
+    apply; the owner-slice apply with JACC_SCATTER_SLICE=1)."""
+    monkeypatch.setenv("JACC_SCATTER_SLICE", slice_)
     M = 2**25 if dtype == "f64" else 2**26
     N = 2**23
     idx = synth.index_i32(N, M, 76, 5)
@@ -481,6 +486,34 @@ def test_scatter_binned_large(J, dtype, n):
         b, a0 = synth.dyadic_f64(N, 76, 6), synth.dyadic_f64(M, 76, 7)
     else:
         b, a0 = synth.int_i32(N, -1000, 1000, 76, 6), synth.int_i32(M, -10**6, 10**6, 76, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, bms, drs, reps = _scatter(J, idx, b, a0, n)
+    assert np.array_equal(a, ref)
+    for d in range(n):
+        lo, hi = orc.partition(M, n, d)
+        bm, mn, mx = orc.scatter_add_filtered(idx, b, a0.copy(), lo, hi - 1)
+        assert np.array_equal(bms[d], bm) and drs[d] == (mn, mx)
+        assert np.array_equal(reps[d], ref)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "i32"])
+@pytest.mark.parametrize("n", [1, 3, 8])
+def test_scatter_slice_ragged(J, monkeypatch, dtype, n):
+    """Owner-slice pipeline over several coarse buckets with a ragged last
+    bucket and slice, owned spans starting off word boundaries (n=3, 8),
+    skewed index mix (a hot band plus uniform), exact inputs."""
+    monkeypatch.setenv("JACC_SCATTER_BINNED", "1")
+    monkeypatch.setenv("JACC_SCATTER_SLICE", "1")
+    M = 3 * 2**21 + 777 if dtype == "f64" else 3 * 2**22 + 777
+    N = 2**22 + 3
+    idx = synth.index_i32(N, M, 79, 5)
+    hot = synth.index_i32(N // 4, 2**16, 79, 8) + np.int32(M // 3)
+    idx[: N // 4] = hot
+    if dtype == "f64":
+        b, a0 = synth.dyadic_f64(N, 79, 6), synth.dyadic_f64(M, 79, 7)
+    else:
+        b, a0 = synth.int_i32(N, -1000, 1000, 79, 6), synth.int_i32(M, -10**6, 10**6, 79, 7)
     ref = a0.copy()
     orc.scatter_add(idx, b, ref)
     a, bms, drs, reps = _scatter(J, idx, b, a0, n)

@@ -39,7 +39,7 @@ def one():
     t = e0.elapsed_time(e1) / 1e3 / reps
     J.jacc_finalize()
     print(json.dumps({"part_e": os.environ.get("JACC_SCATTER_PART_E", "8"),
-                      "bucket_mb": os.environ.get("JACC_SCATTER_BUCKET_MB", "16"),
+                      "bucket_mb": os.environ.get("JACC_SCATTER_BUCKET_MB", "16"), "slice": os.environ.get("JACC_SCATTER_SLICE", "auto"),
                       "ms": t * 1e3, "alg_gbs": S * 28 / t / 1e9}))
 
 
@@ -47,7 +47,7 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         one()
     else:
-        grid = [(16, 16), (12, 16), (8, 16), (16, 8), (12, 8), (16, 32)]
+        grid = [tuple(map(int, g.split(":"))) for g in os.environ.get("GRID", "16:16,12:16,8:16,16:8,12:8,16:32").split(",")]
         for pe, mb in grid:
             env = dict(os.environ, JACC_SCATTER_PART_E=str(pe), JACC_SCATTER_BUCKET_MB=str(mb))
             r = subprocess.run([sys.executable, __file__, "one"], env=env, capture_output=True, text=True)
