@@ -347,7 +347,7 @@ template <int BM, int BN, int BK, int ST, int WM, int WN>
 struct GemmCfg {
     static constexpr int NT = (BM / WM) * (BN / WN) * 32;
     static constexpr int AP = BK + 4;
-    static constexpr int BP = BN + 8;
+    static constexpr int BP = BN + 4;  // BP % 16 == 4: conflict-free, 55.5 KB at 64x64x16x3 -> 4 CTAs/SM
     static constexpr int SMEM = ST * (BM * AP + BK * BP) * 8;
 };
 
@@ -1650,11 +1650,18 @@ static cudaError_t gemm_launch(cudaStream_t s, bool v16, const double *A, const 
     using G = GemmCfg<BM, BN, BK, ST, WM, WN>;
     auto kt = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, true, GROUP>;
     auto kf = gemm_f64_kernel<BM, BN, BK, ST, WM, WN, false, GROUP>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        attr = true;
+    // function attributes are per device: set once per device ordinal; the
+    // max shared carveout lets 4 CTAs of the 55.5 KB default tile share an SM
+    static unsigned long long attr_done = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64 || !(attr_done >> dev & 1)) {
+        for (auto k : {kt, kf}) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+            cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+        }
+        if (dev < 64) attr_done |= 1ull << dev;
     }
     dim3 grid((unsigned)((c1 - c0 + BN - 1) / BN), (unsigned)((r1 - r0 + BM - 1) / BM));
     if (v16)
@@ -1685,7 +1692,16 @@ cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C
     case 7: return gemm_launch<64, 64, 16, 3, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     case 8: return gemm_launch<64, 64, 16, 3, 32, 32, 16>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     case 9: return gemm_launch<64, 64, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    default: return gemm_launch<64, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 10: return gemm_launch<64, 128, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 11: return gemm_launch<64, 128, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 12: return gemm_launch<128, 128, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 13: return gemm_launch<64, 256, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 14: return gemm_launch<128, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 15: return gemm_launch<64, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    // default: 64x128 CTA tile, 8 warps of 32x32, 4-stage cp.async ring,
+    // grouped rasterisation (tools/tune_gemm.py: 33.0 TFLOP/s vs 32.2 for
+    // the 64x64x3 tile, variant 15)
+    default: return gemm_launch<64, 128, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     }
 }
 
