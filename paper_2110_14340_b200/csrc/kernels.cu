@@ -731,7 +731,7 @@ constexpr int SA_CH = 4096;
 // The write log is kept as an epoch byte-map (one plain byte store per
 // update, no L2 atomic) and packed into the dirty bitmap afterwards: the
 // bitmap atomics would otherwise double the L2 atomic traffic of the pass.
-template <typename T>
+template <typename T, bool BYTEMAP>
 __global__ void __launch_bounds__(256) scat_apply_kernel(const int32_t *__restrict__ pidx,
                                                          const T *__restrict__ pval, const u64 *base,
                                                          int nb, u64 *work, T *a, uint8_t *bytemap,
@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(256) scat_apply_kernel(const int32_t *__restri
             const int32_t k = __ldcs(pidx + p);
             const T v = __ldcs(pval + p);
             atomicAdd(a + k, v);
-            bytemap[k] = epoch;
+            if (BYTEMAP) bytemap[k] = epoch;
             mn = (u64)k < mn ? (u64)k : mn;
             mx = (u64)k > mx ? (u64)k : mx;
         }
@@ -782,6 +782,63 @@ __global__ void __launch_bounds__(256) scat_pack_kernel(const uint8_t *__restric
     }
 }
 
+
+// Dirty bitmap of the binned scatter from the bucket-ordered keys: CTA
+// (bucket, part) owns 2^20 elements of the bucket (a 128 KB bitmap in shared
+// memory), scans the bucket's keys (16-byte loads), sets its bits with
+// shared-memory atomicOr and writes its words (boundary words shared with a
+// neighbour part by atomicOr into the zeroed bitmap).  Replaces the byte-map
+// stores in the apply (random 1-byte L2 writes) and the pack pass.  (A
+// cluster version that reads every key once and sets remote bits over DSMEM
+// measured 3.4x slower: remote shared-memory atomics.)
+constexpr int SBITS_LB = 20;  // elements per part = 2^20 -> 32768 words
+__global__ void __launch_bounds__(1024) scat_bits_kernel(const int32_t *__restrict__ pidx,
+                                                         const u64 *__restrict__ base, int nb,
+                                                         int shift, int64_t lo, int64_t hi,
+                                                         uint32_t *bitmap) {
+    extern __shared__ uint32_t sw[];
+    const int lp = shift > SBITS_LB ? shift - SBITS_LB : 0;  // log2 parts per bucket
+    const int pb = shift > SBITS_LB ? SBITS_LB : shift;      // log2 elements per part
+    const int64_t items = (int64_t)nb << lp;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int bk = (int)(it >> lp), q = (int)(it & ((1 << lp) - 1));
+        const int64_t e0 = lo + ((int64_t)bk << shift) + ((int64_t)q << pb);
+        if (e0 >= hi) continue;  // uniform per CTA
+        const int64_t e1 = e0 + ((int64_t)1 << pb) < hi ? e0 + ((int64_t)1 << pb) : hi;
+        const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
+        for (int i = threadIdx.x; i < nw; i += 1024) sw[i] = 0;
+        __syncthreads();
+        const u64 p0 = base[bk], p1 = base[bk + 1];
+        auto put = [&](int64_t k) {
+            if (k >= e0 && k < e1) atomicOr(&sw[(k >> 5) - w0], 1u << (k & 31));
+        };
+        // 16-byte loads for the aligned body (pidx is 256-byte aligned)
+        u64 pa = (p0 + 3) & ~(u64)3;
+        if (pa > p1) pa = p1;
+        const u64 n4 = (p1 - pa) >> 2, pt = pa + 4 * n4;
+        if (threadIdx.x < pa - p0) put(pidx[p0 + threadIdx.x]);
+        if (threadIdx.x < p1 - pt) put(pidx[pt + threadIdx.x]);
+        const int4 *k4 = reinterpret_cast<const int4 *>(pidx + pa);
+#pragma unroll 4
+        for (u64 q4 = threadIdx.x; q4 < n4; q4 += 1024) {
+            const int4 k = __ldcs(k4 + q4);
+            put(k.x);
+            put(k.y);
+            put(k.z);
+            put(k.w);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nw; i += 1024) {
+            const uint32_t v = sw[i];
+            if (i == 0 || i == nw - 1) {
+                if (v) atomicOr(bitmap + w0 + i, v);
+            } else {
+                bitmap[w0 + i] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
 
 // ---------------------------------------------------------------------------
 // BK4c owner-slice apply (see kernels.cuh).  Fine bin g of the owned span is
@@ -1801,7 +1858,10 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
     p.nb = (int)((span + ((int64_t)1 << shift) - 1) >> shift);
     const size_t hdr = ((size_t)(3 * p.nb + 2) * 8 + 255) & ~(size_t)255;
     p.scratch = hdr + (((size_t)n * 4 + 255) & ~(size_t)255) + (size_t)n * elem;
-    p.bytemap = (size_t)(((hi + 31) >> 5) << 5);
+    // JACC_SCATTER_BYTEMAP=1: dirty bits through the epoch byte-map written
+    // by the apply (the previous default), else the bucket-parallel bits pass
+    const char *bm = getenv("JACC_SCATTER_BYTEMAP");
+    p.bytemap = (bm && bm[0] == '1') ? (size_t)(((hi + 31) >> 5) << 5) : 0;
     return p;
 }
 
@@ -1915,20 +1975,47 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
         else if (pe == 16) PART_LAUNCH(T, 16);                                                     \
         else PART_LAUNCH(T, 8);                                                                    \
     } while (0)
+    // dirty bits: a bucket-parallel pass over the partitioned keys
+    // (default), or the epoch byte-map written by the apply and packed
+    // (JACC_SCATTER_BYTEMAP=1, or when no byte-map exists)
+    const bool use_bytemap = pl.bytemap && bytemap;
     if (is_f64) {
         PART_E(double);
-        scat_apply_kernel<double><<<148 * 8, 256, 0, s>>>(
-            pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
-            static_cast<double *>(a), bytemap, epoch, dirty);
+        if (use_bytemap)
+            scat_apply_kernel<double, true><<<148 * 8, 256, 0, s>>>(
+                pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
+                static_cast<double *>(a), bytemap, epoch, dirty);
+        else
+            scat_apply_kernel<double, false><<<148 * 8, 256, 0, s>>>(
+                pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
+                static_cast<double *>(a), bytemap, epoch, dirty);
     } else {
         PART_E(int32_t);
-        scat_apply_kernel<int32_t><<<148 * 8, 256, 0, s>>>(
-            pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
-            static_cast<int32_t *>(a), bytemap, epoch, dirty);
+        if (use_bytemap)
+            scat_apply_kernel<int32_t, true><<<148 * 8, 256, 0, s>>>(
+                pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
+                static_cast<int32_t *>(a), bytemap, epoch, dirty);
+        else
+            scat_apply_kernel<int32_t, false><<<148 * 8, 256, 0, s>>>(
+                pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
+                static_cast<int32_t *>(a), bytemap, epoch, dirty);
     }
 #undef PART_E
 #undef PART_LAUNCH
-    scat_pack_kernel<<<148 * 8, 256, 0, s>>>(bytemap, epoch, lo, hi, bitmap);
+    if (use_bytemap) {
+        scat_pack_kernel<<<148 * 8, 256, 0, s>>>(bytemap, epoch, lo, hi, bitmap);
+    } else {
+        const int pb = pl.shift > SBITS_LB ? SBITS_LB : pl.shift;
+        const int smem = (int)((((int64_t)1 << pb) >> 5) + 2) * 4;
+        cudaFuncSetAttribute(scat_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        const int64_t items = (int64_t)pl.nb << (pl.shift - pb);
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nsm <= 0) nsm = 148;
+        const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
+        scat_bits_kernel<<<g, 1024, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap);
+    }
     return cudaGetLastError();
 }
 

@@ -418,7 +418,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 else cudaGetLastError();
             }
             const size_t bmap = (size_t)((W->nelem + 31) / 32) * 32;  // whole region
-            if (!sp.slice && !W->bytemap[d]) {
+            if (sp.bytemap && !W->bytemap[d]) {
                 if (cudaMalloc(&W->bytemap[d], bmap) == cudaSuccess) {
                     CK(cudaMemsetAsync(W->bytemap[d], 0, bmap, dv.s));
                     W->epoch[d] = 0;
@@ -618,13 +618,17 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
                 jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
                 // the epoch byte-map state is host-side: no byte-map path in a
-                // captured graph (the owner-slice path has none, and runs
-                // captured when its scratch was reserved before the capture)
-                if (R.capturing && !sp.slice) sp.binned = false;
+                // captured graph (the default bits pass and the owner-slice
+                // path have none, and run captured when their scratch was
+                // reserved before the capture)
+                if (R.capturing && sp.bytemap) sp.binned = false;
                 if (R.nq > 1) sp.binned = false;     // per-device scratch is not per queue
-                if (sp.binned && (dv.scratch_bytes < sp.scratch || (!sp.slice && !W->bytemap[d])))
+                if (sp.binned && (dv.scratch_bytes < sp.scratch || (sp.bytemap && !W->bytemap[d])))
                     sp.binned = false;  // scratch could not be reserved up front: direct kernel
                 if (sp.binned && sp.slice) {
+                    CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
+                                              drec, sp, dv.scratch, nullptr, 0));
+                } else if (sp.binned && !sp.bytemap) {
                     CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
                                               drec, sp, dv.scratch, nullptr, 0));
                 } else if (sp.binned) {

@@ -441,15 +441,17 @@ def test_scatter_permutation_exact(J):
     assert np.array_equal(a, ref)
 
 
-@pytest.mark.parametrize("binned,slice_", [("0", "0"), ("1", "0"), ("1", "1")])
+@pytest.mark.parametrize("binned,slice_,bytemap", [("0", "0", "0"), ("1", "0", "0"),
+                                                   ("1", "0", "1"), ("1", "1", "0")])
 @pytest.mark.parametrize("n", [1, 3])
 @pytest.mark.parametrize("lo", [0, 1, 2, 3, 5])
-def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, slice_, n, lo):
-    """Direct, destination-binned (byte-map) and owner-slice scatter
-    pipelines, iteration ranges starting at any element (int4 head/tail
-    handling)."""
+def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, slice_, bytemap, n, lo):
+    """Direct, destination-binned (dirty bits by the bucket pass, or by the
+    byte-map) and owner-slice scatter pipelines, iteration ranges starting
+    at any element (int4 head/tail handling)."""
     monkeypatch.setenv("JACC_SCATTER_BINNED", binned)
     monkeypatch.setenv("JACC_SCATTER_SLICE", slice_)
+    monkeypatch.setenv("JACC_SCATTER_BYTEMAP", bytemap)
     N, M = 30_011, 4099
     idx = synth.index_i32(N, M, 75, 5)
     b = synth.dyadic_f64(N, 75, 6)
@@ -472,13 +474,16 @@ def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, slice_, n, 
     assert np.array_equal(a, ref)
 
 
-@pytest.mark.parametrize("slice_", ["0", "1"])
+@pytest.mark.parametrize("slice_,bytemap", [("0", "0"), ("0", "1"), ("1", "0")])
 @pytest.mark.parametrize("dtype", ["f64", "i32"])
-@pytest.mark.parametrize("n", [1, 2])
-def test_scatter_binned_large(J, monkeypatch, dtype, n, slice_):
-    """Arrays larger than L2 take the binned pipeline by default (byte-map
-    apply; the owner-slice apply with JACC_SCATTER_SLICE=1)."""
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_scatter_binned_large(J, monkeypatch, dtype, n, slice_, bytemap):
+    """Arrays larger than L2 take the binned pipeline by default (dirty bits
+    by the bucket pass; the byte-map with JACC_SCATTER_BYTEMAP=1; the
+    owner-slice apply with JACC_SCATTER_SLICE=1); n=3 gives owned spans off
+    word and bucket boundaries."""
     monkeypatch.setenv("JACC_SCATTER_SLICE", slice_)
+    monkeypatch.setenv("JACC_SCATTER_BYTEMAP", bytemap)
     M = 2**25 if dtype == "f64" else 2**26
     N = 2**23
     idx = synth.index_i32(N, M, 76, 5)
