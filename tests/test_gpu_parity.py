@@ -800,6 +800,43 @@ def test_graph_capture_replay_jacobi(J, n, policy):
     assert np.array_equal(A, Ar) and np.array_equal(B, Br)
 
 
+@pytest.mark.parametrize("n", [1, 2])
+def test_graph_capture_replay_binned_scatter(J, monkeypatch, n):
+    """The binned scatter (dirty bits by the bucket pass, no host-side
+    byte-map state) runs inside a captured graph once its scratch was
+    reserved by a plain launch: 1 plain + 3 replays + 1 plain = 5 scatters
+    of the same updates, exact in int32; bitmap and range of the last."""
+    monkeypatch.setenv("JACC_SCATTER_BINNED", "1")
+    N, M = 200_003, 70_001
+    idx = synth.index_i32(N, M, 99, 5)
+    b = synth.int_i32(N, -50, 50, 99, 6)
+    a0 = synth.int_i32(M, -10**6, 10**6, 99, 7)
+    a = a0.copy()
+    args = [_in(J, idx), _in(J, b), _inout(J, a)]
+    rng = J.make_range(0, N)
+    with runtime(J, n):
+        _create(J, idx, b, a)
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_I32, rng, args, 0)
+        J.jacc_graph_begin()
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_I32, rng, args, 0)
+        gid = J.jacc_graph_end()
+        J.jacc_graph_replay(gid, 3)
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_I32, rng, args, 0)
+        J.jacc_wait()
+        bms = [J.jacc_get_dirty_bitmap(a, d, M) for d in range(n)]
+        drs = [J.jacc_get_dirty_range(a, d) for d in range(n)]
+        J.jacc_update_host(a)
+        J.jacc_graph_destroy(gid)
+    ref = a0.copy()
+    for _ in range(5):
+        orc.scatter_add(idx, b, ref)
+    assert np.array_equal(a, ref)
+    for d in range(n):
+        lo, hi = orc.partition(M, n, d)
+        bm, mn, mx = orc.scatter_add_filtered(idx, b, a0.copy(), lo, hi - 1)
+        assert np.array_equal(bms[d], bm) and drs[d] == (mn, mx)
+
+
 def test_graph_rules(J):
     N = 64
     A = synth.uniform_f64(N * N, 98, 1).reshape(N, N)
