@@ -60,7 +60,7 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
                             int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty);
 
 // BK4b Same loop, executed as a destination-binned pipeline for arrays far
-// larger than L2: (1) histogram of owned updates per 16 MiB bucket of a,
+// larger than L2: (1) histogram of owned updates per 8 MiB bucket of a,
 // (2) scan, (3) stable-per-CTA partition of (k, b[i]) pairs into bucket
 // order through shared memory (coalesced writes), (4) apply the pairs
 // bucket by bucket, so the read-modify-writes of a hit L2 and every line of

@@ -38,8 +38,8 @@ def one():
     J.jacc_wait()
     t = e0.elapsed_time(e1) / 1e3 / reps
     J.jacc_finalize()
-    print(json.dumps({"part_e": os.environ.get("JACC_SCATTER_PART_E", "8"),
-                      "bucket_mb": os.environ.get("JACC_SCATTER_BUCKET_MB", "16"), "slice": os.environ.get("JACC_SCATTER_SLICE", "auto"),
+    print(json.dumps({"part_e": os.environ.get("JACC_SCATTER_PART_E", "16"),
+                      "bucket_mb": os.environ.get("JACC_SCATTER_BUCKET_MB", "8"), "slice": os.environ.get("JACC_SCATTER_SLICE", "auto"),
                       "ms": t * 1e3, "alg_gbs": S * 28 / t / 1e9}))
 
 
