@@ -664,10 +664,9 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restri
     __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB];
     __shared__ u64 gbase[SB_MAXB];
     __shared__ unsigned total;
-    extern __shared__ __align__(16) unsigned char sdyn[];  // [TILE] T, [TILE] i32, [TILE] u16
+    extern __shared__ __align__(16) unsigned char sdyn[];  // [TILE] T, [TILE] i32
     T *sv = reinterpret_cast<T *>(sdyn);
     int32_t *sk = reinterpret_cast<int32_t *>(sdyn + TILE * sizeof(T));
-    uint16_t *sbk = reinterpret_cast<uint16_t *>(sdyn + TILE * (sizeof(T) + 4));
     const int tid = threadIdx.x;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     auto load_keys = [&](int64_t t, int32_t *k) {
@@ -709,14 +708,14 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restri
                 const unsigned pos = loff[bk[j]] + rk[j];
                 sk[pos] = k[j];
                 sv[pos] = v[j];
-                sbk[pos] = (uint16_t)bk[j];
             }
         __syncthreads();
         const unsigned cnt = total;
         for (unsigned pos = tid; pos < cnt; pos += SB_T) {
-            const int bb = sbk[pos];
+            const int32_t kk = sk[pos];
+            const int bb = (int)(((int64_t)kk - lo) >> shift);  // bucket from the key
             const u64 g = gbase[bb] + (pos - loff[bb]);
-            pidx[g] = sk[pos];
+            pidx[g] = kk;
             pval[g] = sv[pos];
         }
         __syncthreads();
@@ -1904,7 +1903,7 @@ cudaError_t scatter_slice(cudaStream_t s, const int32_t *idx, const T *b, T *a, 
     if (e != cudaSuccess) return e;
     // attributes are per device: set on every call (host-side, cheap)
     cudaFuncSetAttribute(scat_fhist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SL_MAXF * 4);
-    const int pdsm = SB_T * 16 * (int)(sizeof(T) + 6);
+    const int pdsm = SB_T * 16 * (int)(sizeof(T) + 4);
     cudaFuncSetAttribute(scat_part_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
     const int sdyn = SL_SLICE + 16 + (int)(SL_SLICE / sizeof(T) / 32 + 2) * 4;
     e = cudaFuncSetAttribute(scat_slice_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sdyn);
@@ -1958,11 +1957,11 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     }
     const int64_t tile = (int64_t)SB_T * pe;
     const int64_t tiles = (n + tile - 1) / tile;
-    const size_t dsm = (size_t)tile * ((is_f64 ? 8 : 4) + 4 + 2);
+    const size_t dsm = (size_t)tile * ((is_f64 ? 8 : 4) + 4);
     const int pg = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
 #define PART_LAUNCH(T, E)                                                                          \
     do {                                                                                           \
-        if (dsm > 32 * 1024) /* + 16 KB static: beyond the 48 KB default */                       \
+        /* always: dynamic + 16 KB static smem may pass the 48 KB default */                      \
             cudaFuncSetAttribute(scat_part_kernel<T, E>,                                           \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);           \
         scat_part_kernel<T, E><<<pg, SB_T, dsm, s>>>(idx, static_cast<const T *>(b), n, lo, hi,    \
