@@ -12,6 +12,7 @@ cap dot dot reduce_kernel
 cap gemm gemm gemm_f64
 cap scat_part scatter scat_part
 cap scat_apply scatter scat_apply
+cap scat_bits scatter scat_bits
 cap himeno_stencil himeno himeno_stencil
 cap himeno_copy himeno himeno_copy
 ls gpurun_out/*.ncu-rep
