@@ -1811,6 +1811,9 @@ cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C
     case 13: return gemm_launch<64, 256, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     case 14: return gemm_launch<128, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     case 15: return gemm_launch<64, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 16: return gemm_launch<64, 128, 16, 4, 32, 64, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 17: return gemm_launch<128, 128, 16, 3, 32, 64, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
+    case 18: return gemm_launch<64, 128, 16, 4, 32, 32, 16>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
     // default: 64x128 CTA tile, 8 warps of 32x32, 4-stage cp.async ring,
     // grouped rasterisation (tools/tune_gemm.py: 33.0 TFLOP/s vs 32.2 for
     // the 64x64x3 tile, variant 15)
