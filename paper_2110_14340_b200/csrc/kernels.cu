@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restri
 // Pairs are applied in global order through a dynamic chunk counter, so
 // the chunks in flight at any moment span ~one bucket of `a` (static
 // grid-stride lets CTAs drift apart and the working set spill out of L2).
-constexpr int SA_CH = 4096;
+constexpr int SA_CH = 4096;  // default chunk (JACC_SCATTER_APPLY_CH)
 
 // The write log is kept as an epoch byte-map (one plain byte store per
 // update, no L2 atomic) and packed into the dirty bitmap afterwards: the
@@ -755,10 +755,10 @@ template <typename T, bool BYTEMAP>
 __global__ void __launch_bounds__(256) scat_apply_kernel(const int32_t *__restrict__ pidx,
                                                          const T *__restrict__ pval, const u64 *base,
                                                          int nb, u64 *work, T *a, uint8_t *bytemap,
-                                                         uint8_t epoch, u64 *dirty) {
+                                                         uint8_t epoch, u64 *dirty, int ch) {
     __shared__ u64 chunk;
     const int64_t m = (int64_t)base[nb];
-    const int64_t nchunks = (m + SA_CH - 1) / SA_CH;
+    const int64_t nchunks = (m + ch - 1) / ch;
     u64 mn = kU64Max, mx = 0;
     for (;;) {
         if (threadIdx.x == 0) chunk = atomicAdd(work, 1ull);
@@ -766,8 +766,8 @@ __global__ void __launch_bounds__(256) scat_apply_kernel(const int32_t *__restri
         const int64_t c = (int64_t)chunk;
         __syncthreads();
         if (c >= nchunks) break;
-        const int64_t p0 = c * SA_CH;
-        const int64_t p1 = p0 + SA_CH < m ? p0 + SA_CH : m;
+        const int64_t p0 = c * ch;
+        const int64_t p1 = p0 + ch < m ? p0 + ch : m;
 #pragma unroll 4
         for (int64_t p = p0 + threadIdx.x; p < p1; p += 256) {
             const int32_t k = __ldcs(pidx + p);
@@ -2038,26 +2038,34 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     // (default), or the epoch byte-map written by the apply and packed
     // (JACC_SCATTER_BYTEMAP=1, or when no byte-map exists)
     const bool use_bytemap = pl.bytemap && bytemap;
+    // apply chunk and CTAs per SM (JACC_SCATTER_APPLY_CH, JACC_SCATTER_APPLY_BPS)
+    static int ach = -1, abps = -1;
+    if (ach < 0) {
+        const char *e1 = getenv("JACC_SCATTER_APPLY_CH"), *e2 = getenv("JACC_SCATTER_APPLY_BPS");
+        ach = e1 ? std::max(256, atoi(e1)) : SA_CH;
+        abps = e2 ? std::max(1, std::min(8, atoi(e2))) : 3;  // 3: 4.17 ms vs 5.1 ms at 8 (fewer chunks in flight)
+    }
+    const int ag = 148 * abps;
     if (is_f64) {
         PART_E(double);
         if (use_bytemap)
-            scat_apply_kernel<double, true><<<148 * 8, 256, 0, s>>>(
+            scat_apply_kernel<double, true><<<ag, 256, 0, s>>>(
                 pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
-                static_cast<double *>(a), bytemap, epoch, dirty);
+                static_cast<double *>(a), bytemap, epoch, dirty, ach);
         else
-            scat_apply_kernel<double, false><<<148 * 8, 256, 0, s>>>(
+            scat_apply_kernel<double, false><<<ag, 256, 0, s>>>(
                 pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
-                static_cast<double *>(a), bytemap, epoch, dirty);
+                static_cast<double *>(a), bytemap, epoch, dirty, ach);
     } else {
         PART_E(int32_t);
         if (use_bytemap)
-            scat_apply_kernel<int32_t, true><<<148 * 8, 256, 0, s>>>(
+            scat_apply_kernel<int32_t, true><<<ag, 256, 0, s>>>(
                 pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
-                static_cast<int32_t *>(a), bytemap, epoch, dirty);
+                static_cast<int32_t *>(a), bytemap, epoch, dirty, ach);
         else
-            scat_apply_kernel<int32_t, false><<<148 * 8, 256, 0, s>>>(
+            scat_apply_kernel<int32_t, false><<<ag, 256, 0, s>>>(
                 pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
-                static_cast<int32_t *>(a), bytemap, epoch, dirty);
+                static_cast<int32_t *>(a), bytemap, epoch, dirty, ach);
     }
 #undef PART_E
 #undef PART_LAUNCH
