@@ -2018,7 +2018,12 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     const int64_t tile = (int64_t)SB_T * pe;
     const int64_t tiles = (n + tile - 1) / tile;
     const size_t dsm = (size_t)tile * ((is_f64 ? 8 : 4) + 4);
-    const int pg = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
+    static int pbps = -1;  // partition CTAs per SM in the grid (JACC_SCATTER_PART_BPS)
+    if (pbps < 0) {
+        const char *e = getenv("JACC_SCATTER_PART_BPS");
+        pbps = e ? std::max(1, std::min(16, atoi(e))) : 8;
+    }
+    const int pg = (int)(tiles < 148 * pbps ? tiles : 148 * pbps);
 #define PART_LAUNCH(T, E)                                                                          \
     do {                                                                                           \
         /* always: dynamic + 16 KB static smem may pass the 48 KB default */                      \
