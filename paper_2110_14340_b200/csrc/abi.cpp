@@ -131,6 +131,8 @@ jacc_status jacc_finalize(void) {
         cudaSetDevice(dv.ord);
         if (dv.comm) ncclCommDestroy(dv.comm);
         if (dv.scratch) cudaFree(dv.scratch);
+        for (void *p : dv.retired) cudaFree(p);
+        dv.retired.clear();
         if (dv.pe) cudaEventDestroy(dv.pe);
         for (size_t q = 1; q < dv.qs.size(); q++) cudaStreamDestroy(dv.qs[q]);
         for (size_t q = 1; q < dv.qpartials.size(); q++) {

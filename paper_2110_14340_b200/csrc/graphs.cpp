@@ -181,6 +181,14 @@ jacc_status jacc_graph_destroy(int graph_id) {
         if (it == R.graphs.end()) return JACC_ERR_INVALID;
         destroy_graph(it->second);
         R.graphs.erase(it);
+        if (R.graphs.empty())  // scratch a graph might still have referenced
+            for (int d = 0; d < R.n; d++) {
+                if (R.dev[d].retired.empty()) continue;
+                set_dev(d);
+                CK(cudaStreamSynchronize(R.dev[d].s));
+                for (void *p : R.dev[d].retired) CK(cudaFree(p));
+                R.dev[d].retired.clear();
+            }
         return JACC_OK;
     });
 }

@@ -207,7 +207,9 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
     if (R.mode == JACC_MODE_DUP) L.dup = true;
     L.itersplit = R.scatter_itersplit && R.n > 1 &&
                   (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32);
-    if (L.itersplit && (R.mp || R.nq > 1)) return JACC_ERR_INVALID;
+    // iteration-split scatter allocates and zeroes its delta arrays on first
+    // use, which a capture would only record, not run
+    if (L.itersplit && (R.mp || R.nq > 1 || R.capturing)) return JACC_ERR_INVALID;
     // ---- NEXT-1 adaptive utilization (single process, n > 1) ---------------
     const bool adaptive =
         R.mode == JACC_MODE_ADAPTIVE && R.n > 1 && !R.mp && !L.dup && !R.capturing;
@@ -374,6 +376,16 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 set_dev(d);
                 for (int d2 = 0; d2 < n; d2++) CK(cudaStreamWaitEvent(R.dev[d].s, R.dev[d2].qev[pq], 0));
             }
+        // a same-queue dependency is stream order only on one device: queue
+        // qsel on device d must also follow the previous launch of queue qsel
+        // on every peer it may exchange with (pushes into, pulls from, or
+        // whose pushes it reads)
+        if (n > 1)
+            for (int d = 0; d < n; d++) {
+                set_dev(d);
+                for (int d2 = 0; d2 < n; d2++)
+                    if (d2 != d) CK(cudaStreamWaitEvent(R.dev[d].s, R.dev[d2].qev[qsel], 0));
+            }
     }
 
     // ---- enqueue per device -------------------------------------------------
@@ -411,7 +423,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             set_dev(d);
             if (dv.scratch_bytes < sp.scratch) {
                 CK(cudaStreamSynchronize(dv.s));
-                if (dv.scratch) CK(cudaFree(dv.scratch));
+                // a captured graph bakes in the scratch pointer: keep the old
+                // buffer alive until no graph exists (jacc_graph_destroy)
+                if (dv.scratch && !R.graphs.empty()) dv.retired.push_back(dv.scratch);
+                else if (dv.scratch) CK(cudaFree(dv.scratch));
                 dv.scratch = nullptr;
                 dv.scratch_bytes = 0;
                 if (cudaMalloc(&dv.scratch, sp.scratch) == cudaSuccess) dv.scratch_bytes = sp.scratch;
@@ -444,10 +459,11 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 CK(cudaMemsetAsync(W->delta[d], 0, W->bytes, dv.s));
                 CK(cudaMemsetAsync(W->dbm[d], 0, words * 4, dv.s));
             }
-            if (!multiq)
-                for (int q = 0; q < n; q++)
-                    if (q != d && (comm[d][q] || R.comm_prev[d][q]))
-                        CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
+            // every peer: the previous launch's phase 2 on peer q read and
+            // zeroed this device's delta over peer memory, and this phase 1
+            // writes it again (WAR across devices, whatever the merge policy)
+            for (int q = 0; q < n; q++)
+                if (q != d) CK(cudaStreamWaitEvent(dv.s, R.dev[q].ev[prev], 0));
             for (const Pull &pl : pulls) {
                 if (pl.dst != d) continue;
                 const size_t e = pl.reg->elem;
@@ -508,13 +524,15 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         if (W) {
             W->dslot[d] ^= 1;
             drec = W->dirty[d] + 2 * W->dslot[d];
-            if (!p.active) CK(cudaMemsetAsync(drec, 0xff, 16, dv.s));  // nothing will write it
+            // nothing will write it: clear both slots (the other one is the
+            // next launch's, normally cleared by this launch's kernel)
+            if (!p.active) CK(cudaMemsetAsync(W->dirty[d], 0xff, 32, dv.s));
         }
         u64 *drec2 = nullptr;
         if (W2) {
             W2->dslot[d] ^= 1;
             drec2 = W2->dirty[d] + 2 * W2->dslot[d];
-            if (!p.active) CK(cudaMemsetAsync(drec2, 0xff, 16, dv.s));
+            if (!p.active) CK(cudaMemsetAsync(W2->dirty[d], 0xff, 32, dv.s));
         }
         if (p.active) {
             switch (id) {

@@ -242,6 +242,9 @@ struct Device {
     double *hscal = nullptr;     // pinned host scalar
     ncclComm_t comm = nullptr;
     void *scratch = nullptr;     // binned-scatter pairs (grown on demand)
+    // scratch buffers replaced while a captured graph may still reference
+    // them (freed once no graph exists)
+    std::vector<void *> retired;
     std::vector<cudaStream_t> qs;   // async queues (qs[0] = s), NEXT-4
     std::vector<cudaEvent_t> qev;   // last launch's completion per queue
     // per-queue reduction scratch (concurrent queues must not share it)

@@ -1158,3 +1158,133 @@ def test_merge_bytes_scale_with_n(J):
     # HALO: two boundary rows per interior device, independent of the block
     assert halo[2] == 2 * (N - 2) * 8
     assert halo[8] == 2 * (8 - 1) * (N - 2) * 8
+
+
+# --------------------------------------------------------------------------
+# Regression tests for the round-1 advisor findings
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [1, 2])
+def test_graph_scratch_survives_regrowth(J, monkeypatch, n):
+    """A graph captured over a binned scatter keeps its scratch: a later,
+    larger uncaptured scatter must not free the buffer the graph baked in
+    (it is retired until jacc_graph_destroy)."""
+    monkeypatch.setenv("JACC_SCATTER_BINNED", "1")
+    N, M = 100_003, 70_001
+    idx = synth.index_i32(N, M, 111, 5)
+    b = synth.int_i32(N, -50, 50, 111, 6)
+    a0 = synth.int_i32(M, -10**6, 10**6, 111, 7)
+    N2 = 3_000_017
+    idx2 = synth.index_i32(N2, M, 111, 8)
+    b2 = synth.int_i32(N2, -50, 50, 111, 9)
+    a = a0.copy()
+    args = [_in(J, idx), _in(J, b), _inout(J, a)]
+    with runtime(J, n):
+        _create(J, idx, b, a, idx2, b2)
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_I32, J.make_range(0, N), args, 0)
+        J.jacc_graph_begin()
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_I32, J.make_range(0, N), args, 0)
+        gid = J.jacc_graph_end()
+        # needs a larger scratch: the old one is retired, not freed
+        J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_I32, J.make_range(0, N2),
+                      [_in(J, idx2), _in(J, b2), _inout(J, a)], 0)
+        J.jacc_wait()
+        # the captured state is S_start again only if the validity matches:
+        # under EAGER n=2 / n=1 every replica is valid, so replay is allowed
+        J.jacc_graph_replay(gid, 2)
+        J.jacc_wait()
+        J.jacc_update_host(a)
+        J.jacc_graph_destroy(gid)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    orc.scatter_add(idx2, b2, ref)
+    orc.scatter_add(idx, b, ref)
+    orc.scatter_add(idx, b, ref)
+    assert np.array_equal(a, ref)
+
+
+def test_iteration_split_rejected_in_capture(J):
+    N, M = 1000, 500
+    idx = synth.index_i32(N, M, 112, 5)
+    b = synth.int_i32(N, -5, 5, 112, 6)
+    a = synth.int_i32(M, -5, 5, 112, 7)
+    with runtime(J, 2):
+        J.jacc_set_scatter_split(1)
+        _create(J, idx, b, a)
+        J.jacc_graph_begin()
+        st = J.jacc_launch_status(J.JACC_LOOP_SCATTER_ADD_I32, J.make_range(0, N),
+                                  [_in(J, idx), _in(J, b), _inout(J, a)], 0)
+        J.jacc_graph_end()
+    assert st == J.JACC_ERR_INVALID
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+@pytest.mark.parametrize("dtype", ["f64", "i32"])
+def test_iteration_split_back_to_back_halo(J, policy, dtype):
+    """Iteration-split scatter launched back to back without host syncs:
+    phase 1 of launch k+1 must wait for every peer's phase 2 of launch k
+    (which read and zeroed this device's delta), under either policy."""
+    N, M = 2_000_003, 1_000_003
+    idx = synth.index_i32(N, M, 113, 5)
+    if dtype == "f64":
+        b, a0 = synth.dyadic_f64(N, 113, 6), synth.dyadic_f64(M, 113, 7)
+        loop = J.JACC_LOOP_SCATTER_ADD_F64
+    else:
+        b, a0 = synth.int_i32(N, -1000, 1000, 113, 6), synth.int_i32(M, -10**6, 10**6, 113, 7)
+        loop = J.JACC_LOOP_SCATTER_ADD_I32
+    K = 6
+    ref = a0.copy()
+    for _ in range(K):
+        orc.scatter_add(idx, b, ref)
+    a = a0.copy()
+    with runtime(J, 3, policy):
+        J.jacc_set_scatter_split(1)
+        _create(J, idx, b, a)
+        args = [_in(J, idx), _in(J, b), _inout(J, a)]
+        for _ in range(K):
+            J.jacc_launch(loop, J.make_range(0, N), args, 0)
+        J.jacc_wait()
+        J.jacc_update_host(a)
+    assert np.array_equal(a, ref)
+
+
+def test_inactive_device_dirty_slots_cleared(J):
+    """A device idle in one launch clears both dirty slots, so its next
+    active launch records only its own stores (not the union with the
+    range from two launches earlier)."""
+    y = synth.uniform_f32(3000, 114, 3)
+    x = np.zeros(3000, dtype=np.float32)
+    with runtime(J, 3):
+        _create(J, y, x)
+        args = [_in(J, y), _out(J, x)]
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(0, 3000), args)
+        assert J.jacc_get_dirty_range(x, 2) == (2000, 2999)
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(0, 1000), args)  # device 2 idle
+        assert J.jacc_get_dirty_range(x, 2) == J.EMPTY_RANGE
+        J.jacc_launch(J.JACC_LOOP_SQUARE_F32, J.make_range(2500, 2600), args)
+        assert J.jacc_get_dirty_range(x, 2) == (2500, 2599)
+        assert J.jacc_get_dirty_range(x, 0) == J.EMPTY_RANGE
+        J.jacc_update_host(x)
+    assert np.array_equal(x, y * y)
+
+
+@pytest.mark.parametrize("nq", [2, 3])
+def test_async_queues_cross_device_same_queue(J, nq):
+    """Jacobi ping-pong pinned to one explicit queue on 3 devices under HALO:
+    queue q on device d must follow queue q on its peers (their pushes into
+    d's replica, d's pushes into theirs)."""
+    N, T = 515, 6
+    A0 = synth.uniform_f64(N * N, 115, 1).reshape(N, N)
+    B0 = synth.uniform_f64(N * N, 115, 2).reshape(N, N)
+    Ar, Br = A0.copy(), B0.copy()
+    orc.jacobi2d(T, Ar, Br)
+    A, B = A0.copy(), B0.copy()
+    with runtime(J, 3, 1):
+        J.jacc_set_queues(nq)
+        _create(J, A, B)
+        for t in range(T):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)], 1)
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, B), _out(J, A)], 1)
+        J.jacc_wait()
+        J.jacc_update_host(A)
+        J.jacc_update_host(B)
+    assert np.array_equal(A, Ar) and np.array_equal(B, Br)

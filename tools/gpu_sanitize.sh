@@ -1,8 +1,33 @@
 #!/bin/bash
-# compute-sanitizer memcheck / racecheck over small parity cases
+# compute-sanitizer memcheck / racecheck / synccheck over small parity cases
+# that reach every shared-memory kernel:
+# Jacobi (BK1), reductions (BK2 + combine), GEMM (BK3), scatter direct /
+# binned (hist/part/apply/bits, byte-map) / owner-slice (BK4, BK4b, BK4c),
+# iteration-split scatter + combine, Himeno stencil/copy, Fig. 4, merges
+# (range/box/bitmap under EAGER), graphs and async queues.
 mkdir -p gpurun_out
+TAG=${ROUND_TAG:-r02}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-K='J256 or test_jacobi_multi_device and 17- or test_scatter_exact and 100- or test_square_multi and 1000- or test_dot_sum_dyadic_exact and 4096 or test_gemm_random_tolerance and 37 or himeno_multi_device and shape1 or fig4_chain and -257- or iteration_split and 100003 and f64 or test_graph_capture or async_queues'
-timeout 1500 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -m gpu -k "$K" > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/memcheck.log
-timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -m gpu -k "J256 or test_scatter_exact and 100-" > gpurun_out/racecheck.log 2>&1; echo "racecheck rc=$?" >> gpurun_out/racecheck.log
-tail -4 gpurun_out/memcheck.log; tail -4 gpurun_out/racecheck.log
+T=tests/test_gpu_parity.py
+K='J256 or test_jacobi_multi_device and 17- or test_scatter_exact and 100- or test_square_multi and 1000- or test_dot_sum_dyadic_exact and 4096 or test_gemm_random_tolerance or himeno_multi_device and shape1 or fig4_chain and -257- or iteration_split and 100003 or test_graph_capture or async_queues or test_scatter_paths_and_misaligned_ranges and -3- or test_jacobi_column_split'
+for tool in memcheck racecheck synccheck; do
+  extra=""
+  [ $tool = memcheck ] && extra="--leak-check no"
+  [ $tool = racecheck ] && extra="--racecheck-report hazard"
+  timeout 2400 compute-sanitizer --tool $tool $extra --error-exitcode 9 python -m pytest $T -q -m gpu -k "$K" \
+      > gpurun_out/san_${tool}_${TAG}.log 2>&1
+  echo "$tool rc=$?" >> gpurun_out/san_${tool}_${TAG}.log
+  tail -3 gpurun_out/san_${tool}_${TAG}.log
+done
+# kernels each test reached (names from the memcheck run's --print-level info would be verbose;
+# the launch list of the same subset gives them)
+timeout 900 ncu --metrics gpu__time_duration.sum --csv --log-file gpurun_out/san_kernels_${TAG}.csv \
+    python -m pytest $T -q -m gpu -k "$K" > /dev/null 2>&1
+python - <<EOF
+import csv, collections
+c = collections.Counter()
+for r in csv.DictReader(l for l in open("gpurun_out/san_kernels_${TAG}.csv") if l.startswith('"')):
+    c[r["Kernel Name"].split("(")[0].split("<")[0]] += 1
+open("gpurun_out/san_kernels_${TAG}.txt", "w").write("\n".join(f"{k} {v}" for k, v in sorted(c.items())) + "\n")
+print(len(c), "distinct kernels under the sanitizer subset")
+EOF
