@@ -7,10 +7,16 @@ loop GB/s (8 B read per src element + 8 B written per interior dst element
 per launch), whole job.  Inputs (2 x 2 GiB) are far larger than L2, so no
 explicit flush is needed between timed iterations.
 
+The other BASELINE configs (DOT 2^30, GEMM 8192^3, SCAT 2^28 f64 and i32)
+and the Himeno XL workload are measured in the same run under "loops", each
+with its own roofline block, CPU-oracle baseline and end-to-end number; the
+BK5 merge kernels are measured in isolation under "merge".
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl jacc|reference]
 
 Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (the
-only reference this tier has) on a bounded sample of the same workload.
+only reference this tier has) on a bounded sample of the same workload,
+pinned to one host core.
 """
 import argparse
 import json
@@ -30,22 +36,50 @@ N_GRID = 16384
 TSTEPS = 100
 METRIC = "loop GB/s (Jacobi-2D fp64 16384^2, 100 timesteps, HALO merge)"
 UNIT = "GB/s"
+WORKLOAD = "J16K: Jacobi-2D fp64 16384x16384, 100 timesteps (200 launches/step)"
+
+HBM_SPEC_GBS = 8000.0      # B200 datasheet HBM3e
+FP64_SPEC_TFLOPS = 40.0    # B200 datasheet fp64 (tensor), SURVEY 8(d)
+NVLINK_GBS = 770.0         # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+NVLINK_SPEC_GBS = 900.0
+FP64_PER_BF16 = 40.0 / 2250.0   # nominal fp64 tensor / dense bf16 ratio (guide)
+
+# workload sizes (BASELINE.json configs)
+DOT_L = 2**30
+GEMM_N = 8192
+SCAT_N = 2**28
+HIMENO = (1025, 513, 513)
+
+
+def algo_bytes_per_sweep_dev(N, n, d):
+    """Algorithmic HBM bytes of one Jacobi launch on device d: its owned rows
+    plus one halo row each side read (8 B/element), its interior elements
+    written (8 B/element)."""
+    q, r = divmod(N, n)
+    lo = d * q + min(d, r)
+    hi = (d + 1) * q + min(d + 1, r)
+    i0, i1 = max(lo, 1), min(hi, N - 1)
+    if i1 <= i0:
+        return 0
+    return 8 * N * (i1 - i0 + 2) + 8 * (i1 - i0) * (N - 2)
 
 
 def algo_bytes_per_sweep(N, n):
-    """Algorithmic HBM bytes of one Jacobi launch summed over devices: each
-    device reads its owned rows plus one halo row each side (8 B/element)
-    and writes its interior elements (8 B/element)."""
-    tot = 0
-    for d in range(n):
-        q, r = divmod(N, n)
-        lo = d * q + min(d, r)
-        hi = (d + 1) * q + min(d + 1, r)
-        i0, i1 = max(lo, 1), min(hi, N - 1)
-        if i1 <= i0:
-            continue
-        tot += 8 * N * (i1 - i0 + 2) + 8 * (i1 - i0) * (N - 2)
-    return tot
+    return sum(algo_bytes_per_sweep_dev(N, n, d) for d in range(n))
+
+
+def halo_bytes_dev(N, n, d):
+    """Bytes device d pushes per Jacobi launch under HALO: its first and last
+    interior rows (N-2 doubles each) to the neighbours that read them."""
+    if n == 1:
+        return 0
+    q, r = divmod(N, n)
+    lo = d * q + min(d, r)
+    hi = (d + 1) * q + min(d + 1, r)
+    if min(hi, N - 1) <= max(lo, 1):
+        return 0
+    rows = (1 if d > 0 else 0) + (1 if d < n - 1 else 0)
+    return rows * 8 * (N - 2)
 
 
 def load_peaks():
@@ -53,12 +87,9 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             j = json.load(f)
-        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
-
-
-HBM_SPEC_GBS = 8000.0      # B200 datasheet HBM3e
-FP64_SPEC_TFLOPS = 40.0    # B200 datasheet fp64 (tensor), SURVEY 8(d)
+        return j, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+        "fallback (B200_PROFILING.md)"
 
 
 def load_dgemm_peak():
@@ -73,20 +104,32 @@ def load_dgemm_peak():
     return None, None
 
 
-def load_traffic(kernel="jacobi2d"):
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    --set full summary (profiles/), or None."""
+def load_traffic(*kernels):
+    """DRAM bytes (read + write) per launch summed over the given kernels,
+    from the newest committed ncu --set full summary (profiles/), or None."""
     import glob
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")), reverse=True):
         try:
             with open(p) as f:
-                j = json.load(f)
-            k = j.get("kernels", {}).get(kernel)
-            if k and k.get("dram_bytes_per_launch"):
-                return float(k["dram_bytes_per_launch"]), os.path.basename(p)
+                j = json.load(f).get("kernels", {})
+            if all(j.get(k, {}).get("dram_bytes_per_launch") for k in kernels):
+                return sum(float(j[k]["dram_bytes_per_launch"]) for k in kernels), os.path.basename(p)
         except Exception:
             pass
     return None, None
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "model": model}
 
 
 class ClockSampler:
@@ -96,8 +139,6 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap,utilization.gpu")
 
     def __init__(self, cuda_ords):
-        # nvidia-smi indices of every GPU the job uses (through
-        # CUDA_VISIBLE_DEVICES when it remaps ordinals)
         vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
         vis = [v.strip() for v in vis.split(",")] if vis else []
         idx = [vis[o] if o < len(vis) and vis[o].isdigit() else str(o) for o in cuda_ords]
@@ -109,7 +150,7 @@ class ClockSampler:
     def mark(self, t0, t1):
         """restrict the summary to samples taken in [t0, t1] (time.monotonic);
         the sampler is started before the warm-up so nvidia-smi's own start-up
-        (seconds with several ranks on the box) never leaves it unsampled"""
+        never leaves the timed region unsampled"""
         self.window = (t0, t1)
 
     def __enter__(self):
@@ -146,7 +187,7 @@ class ClockSampler:
         if self.window:
             t0, t1 = self.window
             inside = [p for t, p in self.samples if t0 <= t <= t1]
-            if not inside:  # region shorter than the 100 ms period: nearest samples
+            if not inside:
                 inside = [p for t, p in self.samples if t0 - 0.25 <= t <= t1 + 0.25]
                 where = "timed region +-250 ms"
             samples = inside
@@ -172,55 +213,117 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------
-# reference arm / cpu baseline: the CPU oracle on a bounded sample
+# CPU oracle timing (cpu_baseline leg and the reference arm).  Runs in a child
+# process pinned to ONE host core (sched_setaffinity == taskset -c), on the
+# same seeded inputs as the GPU run (synth/), each a bounded sample.
 # ----------------------------------------------------------------------------
-_ORC_GRID = None
-
-
-def oracle_sample(sweeps):
-    """Time `sweeps` oracle launches of the J16K sweep on the full 16384^2
-    grid (single thread).  Returns (GB/s algorithmic, seconds, sample text)."""
-    global _ORC_GRID
+def _oracle_worker(name, arg):
+    core = sorted(os.sched_getaffinity(0))[-1]
+    os.sched_setaffinity(0, {core})
     import __graft_entry__ as ge
     ge.build_oracle()
     ge.build_synth()
     import oracle as orc
     import synth
-    if _ORC_GRID is None:
-        _ORC_GRID = synth.polybench_jacobi2d(N_GRID)
-    A, B = _ORC_GRID
-    t0 = time.perf_counter()
-    src, dst = A, B
-    for _ in range(sweeps):
-        orc.jacobi2d_sweep(src, dst)
-        src, dst = dst, src
-    dt = time.perf_counter() - t0
-    gbs = sweeps * algo_bytes_per_sweep(N_GRID, 1) / dt / 1e9
-    return gbs, dt, f"{sweeps} oracle sweeps of the 16384^2 grid (of 200 per step), 1 thread"
+    res = {"core": core}
+    if name == "j16k":
+        sweeps = int(arg)
+        A, B = synth.polybench_jacobi2d(N_GRID)
+        t0 = time.perf_counter()
+        src, dst = A, B
+        for _ in range(sweeps):
+            orc.jacobi2d_sweep(src, dst)
+            src, dst = dst, src
+        dt = time.perf_counter() - t0
+        res.update(seconds=dt, work=sweeps * algo_bytes_per_sweep(N_GRID, 1),
+                   sample=f"{sweeps} oracle sweeps of the 16384^2 grid (of 200 per step)")
+    elif name == "dot":
+        L = int(arg)
+        x = synth.uniform_f64(L, 1, synth.AID["x"])
+        y = synth.uniform_f64(L, 1, synth.AID["y"])
+        t0 = time.perf_counter()
+        orc.dot_f64(x, y, 0.0)
+        dt = time.perf_counter() - t0
+        res.update(seconds=dt, work=16 * L,
+                   sample=f"oracle dot over the first {L} of the 2^30 elements (same seeded x, y)")
+    elif name == "gemm":
+        rows = int(arg)
+        G = GEMM_N
+        A = synth.uniform_f64(G * G, 2, synth.AID["A"]).reshape(G, G)
+        B = synth.uniform_f64(G * G, 2, synth.AID["B"]).reshape(G, G)
+        Ar = np.ascontiguousarray(A[:rows])
+        t0 = time.perf_counter()
+        orc.gemm_f64(Ar, B, ikj=True)
+        dt = time.perf_counter() - t0
+        res.update(seconds=dt, work=2 * rows * G * G,
+                   sample=f"oracle GEMM (i-k-j form, bit-identical to i-j-k, DESIGN R-11) of C rows "
+                          f"[0, {rows}) of 8192 (same A, B); "
+                          f"rate scales linearly to the full product")
+    elif name in ("scat_f64", "scat_i32"):
+        n_upd = int(arg)
+        idx = synth.index_i32(SCAT_N, SCAT_N, 3, synth.AID["idx"])[:n_upd].copy()
+        if name == "scat_f64":
+            b = synth.dyadic_f64(SCAT_N, 3, synth.AID["b"])[:n_upd].copy()
+            a = synth.dyadic_f64(SCAT_N, 3, synth.AID["a0"])
+            per = 28
+        else:
+            b = synth.int_i32(SCAT_N, -1000, 1000, 3, synth.AID["b"])[:n_upd].copy()
+            a = synth.int_i32(SCAT_N, -10**6, 10**6, 3, synth.AID["a0"])
+            per = 16
+        t0 = time.perf_counter()
+        orc.scatter_add(idx, b, a)
+        dt = time.perf_counter() - t0
+        res.update(seconds=dt, work=per * n_upd,
+                   sample=f"oracle a[idx[i]] += b[i] for the first {n_upd} of the 2^28 updates "
+                          f"into the full 2^28-element a (same seeded idx, b, a)")
+    else:
+        raise SystemExit(f"unknown oracle worker {name}")
+    print(json.dumps(res), flush=True)
+
+
+def cpu_baseline(name, arg, unit, scale):
+    """Run the oracle worker in a child pinned to one core; value = work /
+    seconds * scale in `unit`."""
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-worker", name,
+                        "--oracle-arg", str(arg)], capture_output=True, text=True, cwd=ROOT)
+    if r.returncode != 0:
+        return {"value": None, "unit": unit, "error": r.stderr.strip()[-300:]}
+    j = json.loads(r.stdout.strip().splitlines()[-1])
+    hi = host_info()
+    return {"value": j["work"] / j["seconds"] * scale, "unit": unit, "cores": 1, "kind": "oracle",
+            "sample": j["sample"], "seconds": j["seconds"], "pinned_core": j["core"],
+            "host_nproc": hi["nproc"], "host_model": hi["model"],
+            "oracle": "oracle/oracle.c, gcc -O2 -ffp-contract=off, single thread"}
 
 
 def run_reference(args):
+    """The reference arm of this tier: the CPU oracle on a bounded sample of
+    the J16K step (2 of its 200 sweeps per timed step), pinned to one core.
+    ms_per_step and value are what was timed (no extrapolation)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     sweeps = 2
     for _ in range(args.warmup):
-        oracle_sample(1)
-    vals, times = [], []
+        cpu_baseline("j16k", 1, UNIT, 1e-9)
+    vals, times, last = [], [], None
     for _ in range(args.steps):
-        g, dt, sample = oracle_sample(sweeps)
-        vals.append(g)
-        times.append(dt)
+        last = cpu_baseline("j16k", sweeps, UNIT, 1e-9)
+        vals.append(last["value"])
+        times.append(last["seconds"])
     v = statistics.median(vals)
+    cb = dict(last)
+    cb["value"] = v
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.median(times) * 1e3 * (2 * TSTEPS / sweeps),
+        "ms_per_step": statistics.median(times) * 1e3, "extrapolated": False,
+        "step": f"one step = {sweeps} of the 200 oracle sweeps of a J16K step (bounded sample)",
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (PolyBench jacobi-2d init)",
-        "config": {"workload": "J16K: Jacobi-2D fp64 16384x16384, 100 timesteps",
-                   "sample": sample, "l2": "inputs 2x2 GiB >> 126 MB L2"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "config": {"workload": WORKLOAD, "sample": cb.get("sample"),
+                   "l2": "inputs 2x2 GiB >> 126 MB L2"},
+        "cpu_baseline": cb,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -328,6 +431,7 @@ def run_jacc(args):
 
     n = args.gpus
     C = Ctx(J, torch, n)
+    info = J.jacc_get_info()
     N = N_GRID
     A, B = synth.polybench_jacobi2d(N)
     J.jacc_set_merge_policy(J.JACC_MERGE_HALO if args.merge == "halo" else J.JACC_MERGE_EAGER)
@@ -368,7 +472,7 @@ def run_jacc(args):
         step()
         gid = J.jacc_graph_end()
         J.jacc_graph_replay(gid, 1)  # warm the graph
-        timed_step = lambda: J.jacc_graph_replay(gid, 1)
+        timed_step = lambda: J.jacc_graph_replay(gid, 1)  # noqa: E731
     else:
         timed_step = step
     w0 = time.monotonic()
@@ -386,10 +490,20 @@ def run_jacc(args):
     k_avg = C.reduce(max(k[0] / max(k[2], 1) for k in kern.values()), "max")
     per_dev_bytes = algo_bytes_per_sweep_dev(N, n, 0)
     achieved = per_dev_bytes / k_avg / 1e9
-    peak, peak_src = load_peaks()
+    peaks, peak_src = load_peaks()
+    peak = float(peaks["hbm_gbs"])
     traffic, tsrc = load_traffic("jacobi2d")
     if traffic is not None and n > 1:
         traffic = None  # the committed capture is of the n=1 launch
+    # two-term per-launch roofline: the
+    # slower of the busiest device's HBM bytes and its merged bytes over
+    # NVLink (HALO: two boundary rows per interior device per launch)
+    merged_dev = max(halo_bytes_dev(N, n, d) for d in range(n)) if args.merge == "halo" else \
+        max((algo_bytes_per_sweep_dev(N, n, d) // 2) * (n - 1) for d in range(n)) if n > 1 else 0
+    t_hbm = max(algo_bytes_per_sweep_dev(N, n, d) for d in range(n)) / (peak * 1e9)
+    t_nvl = merged_dev / (NVLINK_GBS * 1e9)
+    t_roof = max(t_hbm, t_nvl)
+    t_launch = t / args.steps / (2 * TSTEPS)
 
     # ---- e2e through the public API with host buffers ----
     e2e_times = []
@@ -405,19 +519,28 @@ def run_jacc(args):
         if it > 0:
             e2e_times.append(C.reduce(t1 - t0, "max"))
     e2e = bytes_step / statistics.median(e2e_times) / 1e9
+    e2e_h2d, e2e_d2h = A.nbytes + B.nbytes, A.nbytes
 
-    extra = {}
+    loops, merge = {}, {}
     if args.extra and not C.mp:
-        extra = run_extra_loops(J, C, n, peak)
+        J.jacc_data_delete(A)
+        J.jacc_data_delete(B)
+        loops = run_loops(J, C, n, peaks, args)
     C.finalize()
     if args.extra and not C.mp and n == 1:
-        extra["eager_merge_2virtual"] = eager_merge_probe(J, torch, A, B)
+        del A, B
+        merge = merge_probes(J)
 
     cpu = None
     if args.cpu_baseline and n == 1 and C.rank == 0:
-        g, dt, sample = oracle_sample(args.cpu_sweeps)
-        cpu = {"value": g, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
-               "seconds": dt}
+        cpu = cpu_baseline("j16k", args.cpu_sweeps, UNIT, 1e-9)
+        for name, (key, arg, unit, scale) in {
+                "dot_2^30": ("dot", 2**29, "GB/s", 1e-9),
+                "gemm_8192": ("gemm", 32, "TFLOP/s", 1e-12),
+                "scatter_f64_2^28": ("scat_f64", 2**26, "GB/s", 1e-9),
+                "scatter_i32_2^28": ("scat_i32", 2**26, "GB/s", 1e-9)}.items():
+            if name in loops:
+                loops[name]["cpu_baseline"] = cpu_baseline(key, arg, unit, scale)
     if C.rank != 0:
         return
     line = {
@@ -425,45 +548,47 @@ def run_jacc(args):
         "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (PolyBench jacobi-2d init, seeded generators in synth/)",
-        "config": {"workload": "J16K: Jacobi-2D fp64 16384x16384, 100 timesteps (200 launches/step)",
+        "config": {"workload": WORKLOAD,
                    "merge": args.merge, "launch": "one process per GPU" if C.mp else "single process",
                    "issue": "CUDA graph replay of the captured step" if use_graph else "jacc_launch x200",
                    "ms_per_step_plain_launches": t_plain * 1e3,
                    "host_us_per_launch": host_us,
                    "virtual_devices": C.virtual,
+                   "combine": info["combine"], "distinct_gpus": bool(info["distinct_gpus"]),
+                   "peer_pairs": info["peer_pairs"],
                    "l2": "no flush: inputs 2x2 GiB >> 126 MB L2",
                    "parallelism": f"row-block owner partition over {n} device(s)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "roofline": {"bound": "hbm" if t_hbm >= t_nvl else "nvlink", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "frac_of_spec": achieved / HBM_SPEC_GBS, "spec_peak": HBM_SPEC_GBS,
                      "kernel": "jacobi2d_kernel", "kernel_avg_us": k_avg * 1e6,
                      "algo_bytes_per_launch": per_dev_bytes, "peak_source": peak_src,
-                     "traffic_source": tsrc},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * A.nbytes,
-                "d2h_bytes_per_step": A.nbytes},
+                     "traffic_source": tsrc,
+                     "two_term": {"merged_bytes_per_device_per_launch": merged_dev,
+                                  "nvlink_gbs": NVLINK_GBS, "nvlink_spec_gbs": NVLINK_SPEC_GBS,
+                                  "t_hbm_us": t_hbm * 1e6, "t_nvlink_us": t_nvl * 1e6,
+                                  "t_roof_us": t_roof * 1e6, "t_launch_us": t_launch * 1e6,
+                                  "frac_of_t_roof": t_roof / t_launch if t_launch else None}},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d,
+                "d2h_bytes_per_step": e2e_d2h},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+        "host": host_info(),
     }
-    if extra:
-        line["loops"] = extra
+    if loops:
+        line["loops"] = loops
+    if merge:
+        line["merge"] = merge
     print(json.dumps(line), flush=True)
-
-
-def algo_bytes_per_sweep_dev(N, n, d):
-    q, r = divmod(N, n)
-    lo = d * q + min(d, r)
-    hi = (d + 1) * q + min(d + 1, r)
-    i0, i1 = max(lo, 1), min(hi, N - 1)
-    if i1 <= i0:
-        return 0
-    return 8 * N * (i1 - i0 + 2) + 8 * (i1 - i0) * (N - 2)
 
 
 def _time_loop(J, C, fn, reps):
     """Device time per call (max over devices/ranks) of fn, plus the
     profiled average kernel and merge time per launch on device 0."""
     fn()
+    J.jacc_wait()
     J.jacc_set_profiling(1)
     J.jacc_profile_reset()
     t = C.timed(fn, reps) / reps
@@ -472,14 +597,46 @@ def _time_loop(J, C, fn, reps):
     return t, k / max(nl, 1), m / max(nl, 1)
 
 
-def run_extra_loops(J, C, n, peak):
-    """The other BASELINE configs (DOT 2^30, GEMM 8192^3, SCAT 2^28) timed
-    through the same C-ABI: kernel-level roofline evidence, not bench lines."""
+def _e2e(J, C, upload, launch, download, reps=2):
+    """Seconds per end-to-end call through the public API: H2D of the
+    inputs from the (pinned) host arrays, the launch, D2H of the result."""
+    ts = []
+    for it in range(reps + 1):
+        C.sync()
+        t0 = time.perf_counter()
+        for a in upload:
+            J.jacc_update_device(a)
+        launch()
+        for a in download:
+            J.jacc_update_host(a)
+        J.jacc_wait()
+        if it:
+            ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def _hbm_roof(achieved, peak, peak_src, kernels, algo, k, traffic_keys):
+    traffic, tsrc = load_traffic(*traffic_keys)
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
+            "frac_of_spec": achieved / HBM_SPEC_GBS, "spec_peak": HBM_SPEC_GBS,
+            "kernel": kernels, "kernel_avg_us": k * 1e6, "algo_bytes_per_launch": algo,
+            "peak_source": peak_src}
+
+
+def run_loops(J, C, n, peaks, args):
+    """The other BASELINE configs (DOT 2^30, GEMM 8192^3, SCAT 2^28 f64 and
+    int32) and Himeno XL, timed through the same C-ABI.  Each entry carries
+    its metric, roofline block (algorithmic bytes or FLOPs / CUDA-event
+    kernel time vs the measured peak, ncu DRAM bytes), e2e through the
+    public API with declared bytes, and (n = 1) a CPU-oracle baseline."""
     import synth
+    peak = float(peaks["hbm_gbs"])
+    psrc = "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     out = {}
     IN, OUT, INOUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT, J.JACC_ARG_ARRAY_INOUT
-    # DOT 2^30
-    L = 2**30
+    # ---- DOT 2^30 (uniform [0,1), tolerance config) ----
+    L = DOT_L
     x = synth.uniform_f64(L, 1, synth.AID["x"])
     y = synth.uniform_f64(L, 1, synth.AID["y"])
     s = np.zeros(1)
@@ -488,17 +645,22 @@ def run_extra_loops(J, C, n, peak):
         J.jacc_update_device(a)
     dargs = [J.arg(IN, x), J.arg(IN, y), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s)]
     rng = J.make_range(0, L)
-    t, k, _ = _time_loop(J, C, lambda: J.jacc_launch(J.JACC_LOOP_DOT_F64, rng, dargs), 10)
+    launch = lambda: J.jacc_launch(J.JACC_LOOP_DOT_F64, rng, dargs)  # noqa: E731
+    t, k, _ = _time_loop(J, C, launch, 10)
     byts = 16 * L
-    out["dot_2^30"] = {"loop_gbs": byts / t / 1e9, "kernel_us": k * 1e6,
-                       "kernel_gbs": byts / n / k / 1e9, "frac_of_peak": byts / n / k / 1e9 / peak,
-                       "frac_of_spec": byts / n / k / 1e9 / HBM_SPEC_GBS,
-                       "launch_ms": t * 1e3}
+    te = _e2e(J, C, [x, y], launch, [])
+    out["dot_2^30"] = {
+        "workload": "DOT: s += x[i]*y[i], fp64, 2^30 elements, uniform [0,1)",
+        "metric": "loop GB/s", "value": byts / t / 1e9, "unit": "GB/s", "launch_ms": t * 1e3,
+        "roofline": _hbm_roof(byts / n / k / 1e9, peak, psrc, "reduce_kernel", byts // n, k, ["dot"]),
+        "e2e": {"value": byts / te / 1e9, "unit": "GB/s", "seconds": te,
+                "h2d_bytes_per_step": x.nbytes + y.nbytes, "d2h_bytes_per_step": 8},
+    }
     J.jacc_data_delete(x)
     J.jacc_data_delete(y)
     del x, y
-    # GEMM 8192^3
-    G = 8192
+    # ---- GEMM 8192^3 ----
+    G = GEMM_N
     Ag = synth.uniform_f64(G * G, 2, synth.AID["A"]).reshape(G, G)
     Bg = synth.uniform_f64(G * G, 2, synth.AID["B"]).reshape(G, G)
     Cg = np.zeros((G, G))
@@ -506,43 +668,73 @@ def run_extra_loops(J, C, n, peak):
         J.jacc_data_create(a)
         J.jacc_update_device(a)
     gargs = [J.arg(IN, Ag), J.arg(IN, Bg), J.arg(OUT, Cg)]
-    t, k, m = _time_loop(J, C, lambda: J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, gargs, 0), 3)
+    launch = lambda: J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, gargs, 0)  # noqa: E731
+    t, k, m = _time_loop(J, C, launch, 3)
     fl = 2 * G**3
     dg, dsrc = load_dgemm_peak()
-    out["gemm_8192"] = {"loop_tflops": fl / t / 1e12, "kernel_ms": k * 1e3,
-                        "kernel_tflops": fl / n / k / 1e12, "merge_ms": m * 1e3,
-                        "frac_of_cublas_dgemm": fl / n / k / 1e12 / dg if dg else None,
-                        "cublas_dgemm_tflops": dg, "cublas_source": dsrc,
-                        "frac_of_spec": fl / n / k / 1e12 / FP64_SPEC_TFLOPS,
-                        "launch_ms": t * 1e3}
+    scaled = float(peaks.get("bf16_tflops", 0)) * FP64_PER_BF16
+    te = _e2e(J, C, [Ag, Bg], launch, [Cg], reps=1)
+    traffic, tsrc = load_traffic("gemm")
+    ach = fl / n / k / 1e12
+    pk = dg if dg else scaled
+    out["gemm_8192"] = {
+        "workload": "GEMM: C = A B, fp64 8192^3, uniform [0,1), row blocks of C",
+        "metric": "loop TFLOP/s", "value": fl / t / 1e12, "unit": "TFLOP/s", "launch_ms": t * 1e3,
+        "merge_ms": m * 1e3,
+        "roofline": {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                     "frac": ach / pk, "traffic": traffic, "traffic_source": tsrc,
+                     "peak_source": (f"cuBLAS DGEMM 8192^3 measured on this pool ({dsrc})" if dg
+                                     else "MEASURED_PEAKS bf16 burst x nominal fp64/bf16 ratio"),
+                     "peak_bf16_scaled": scaled, "frac_of_bf16_scaled": ach / scaled if scaled else None,
+                     "spec_peak": FP64_SPEC_TFLOPS, "frac_of_spec": ach / FP64_SPEC_TFLOPS,
+                     "kernel": "gemm_f64_kernel (DMMA)", "kernel_avg_ms": k * 1e3,
+                     "algo_flops_per_launch": fl // n},
+        "e2e": {"value": fl / te / 1e12, "unit": "TFLOP/s", "seconds": te,
+                "h2d_bytes_per_step": Ag.nbytes + Bg.nbytes, "d2h_bytes_per_step": Cg.nbytes},
+    }
     for a in (Ag, Bg, Cg):
         J.jacc_data_delete(a)
     del Ag, Bg, Cg
-    # SCAT 2^28 f64
-    S = 2**28
+    # ---- SCAT 2^28 (f64 dyadic, int32) ----
+    S = SCAT_N
     idx = synth.index_i32(S, S, 3, synth.AID["idx"])
-    b = synth.dyadic_f64(S, 3, synth.AID["b"])
-    a = synth.dyadic_f64(S, 3, synth.AID["a0"])
-    for arr in (idx, b, a):
-        J.jacc_data_create(arr)
-        J.jacc_update_device(arr)
-    sargs = [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)]
-    srng = J.make_range(0, S)
-    t, k, m = _time_loop(J, C,
-                         lambda: J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, srng, sargs, 0), 5)
-    byts = S * (4 + 8 + 16)
-    out["scatter_f64_2^28"] = {"loop_gbs": byts / t / 1e9, "kernel_us": k * 1e6,
-                               "kernel_alg_gbs": byts / k / 1e9 if n == 1 else None,
-                               "frac_of_peak": byts / k / 1e9 / peak if n == 1 else None,
-                               "frac_of_spec": byts / k / 1e9 / HBM_SPEC_GBS if n == 1 else None,
-                               # sector-level floor: 32 B read + 32 B write of a per update
-                               "frac_of_sector_roofline": S * (4 + 8 + 64) / k / 1e9 / peak if n == 1 else None,
-                               "merge_us": m * 1e6, "launch_ms": t * 1e3}
-    for arr in (idx, b, a):
-        J.jacc_data_delete(arr)
-    del idx, b, a
-    # Himeno XL (NEXT-2 workload): stencil + gosa, then copy, fp32
-    I, Jd, K = 1025, 513, 513
+    for dt in ("f64", "i32"):
+        if dt == "f64":
+            b = synth.dyadic_f64(S, 3, synth.AID["b"])
+            a = synth.dyadic_f64(S, 3, synth.AID["a0"])
+            loop, per = J.JACC_LOOP_SCATTER_ADD_F64, 28
+        else:
+            b = synth.int_i32(S, -1000, 1000, 3, synth.AID["b"])
+            a = synth.int_i32(S, -10**6, 10**6, 3, synth.AID["a0"])
+            loop, per = J.JACC_LOOP_SCATTER_ADD_I32, 16
+        for arr in (idx, b, a):
+            J.jacc_data_create(arr)
+            J.jacc_update_device(arr)
+        sargs = [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)]
+        srng = J.make_range(0, S)
+        launch = lambda: J.jacc_launch(loop, srng, sargs, 0)  # noqa: E731
+        t, k, m = _time_loop(J, C, launch, 5)
+        byts = S * per
+        te = _e2e(J, C, [idx, b, a], launch, [a], reps=1)
+        tk = [f"scat_{p}" + ("" if dt == "f64" else "_i32") for p in ("part", "apply")]
+        ach = byts / k / 1e9 if n == 1 else None
+        out[f"scatter_{dt}_2^28"] = {
+            "workload": f"SCAT: a[idx[i]] += b[i], {dt}, 2^28 updates into 2^28 elements, "
+                        "idx uniform random (63% distinct targets)",
+            "metric": "loop GB/s", "value": byts / t / 1e9, "unit": "GB/s", "launch_ms": t * 1e3,
+            "merge_us": m * 1e6,
+            "roofline": _hbm_roof(ach, peak, psrc, "binned scatter pipeline (all kernels of the launch)",
+                                  byts, k, tk) if n == 1 else None,
+            "e2e": {"value": byts / te / 1e9, "unit": "GB/s", "seconds": te,
+                    "h2d_bytes_per_step": idx.nbytes + b.nbytes + a.nbytes,
+                    "d2h_bytes_per_step": a.nbytes},
+        }
+        for arr in (idx, b, a):
+            J.jacc_data_delete(arr)
+        del b, a
+    del idx
+    # ---- Himeno XL (NEXT-2 workload): stencil + gosa, then copy, fp32 ----
+    I, Jd, K = HIMENO
     hp, ha, hb, hc, hw1, hbd = synth.himeno_init(I, Jd, K)
     hw2 = np.zeros_like(hp)
     for arr in (hp, ha, hb, hc, hw1, hbd, hw2):
@@ -557,45 +749,96 @@ def run_extra_loops(J, C, n, peak):
     tc, kc, _ = _time_loop(J, C, lambda: J.jacc_launch(J.JACC_LOOP_HIMENO_COPY_F32, None, cargs, 0), 5)
     pts = (I - 2) * (Jd - 2) * (K - 2)
     sb, cb = 56 * pts, 8 * pts   # 12 coefficient/aux arrays + p read, wrk2 written | copy
-    out["himeno_XL_fp32"] = {"stencil_us": ks * 1e6, "stencil_gbs": sb / n / ks / 1e9,
-                             "stencil_frac": sb / n / ks / 1e9 / peak,
-                             "stencil_frac_of_spec": sb / n / ks / 1e9 / HBM_SPEC_GBS,
-                             "copy_us": kc * 1e6, "copy_gbs": cb / n / kc / 1e9,
-                             "iteration_ms": (ts + tc) * 1e3, "gosa": float(g[0])}
+    out["himeno_XL_fp32"] = {
+        "workload": f"Himeno {I}x{Jd}x{K} fp32: 19-point stencil + gosa, then copy",
+        "metric": "loop GB/s", "value": (sb + cb) / (ts + tc) / 1e9, "unit": "GB/s",
+        "iteration_ms": (ts + tc) * 1e3, "gosa": float(g[0]),
+        "roofline": _hbm_roof(sb / n / ks / 1e9, peak, psrc, "himeno_stencil_kernel", sb // n, ks,
+                              ["himeno_stencil"]),
+        "copy": {"us": kc * 1e6, "gbs": cb / n / kc / 1e9, "frac": cb / n / kc / 1e9 / peak},
+    }
     for arr in (hp, ha, hb, hc, hw1, hbd, hw2):
         J.jacc_data_delete(arr)
     return out
 
 
-def eager_merge_probe(J, torch, A, B):
-    """BK5 merge kernel bandwidth: J16K with two virtual devices on this GPU
-    under EAGER, so after every launch each device pushes its ~1 GiB dirty
-    half into the other replica.  On one GPU the push is a local HBM copy
-    (read + write), a proxy for the kernel's efficiency, not NVLink."""
+def merge_probes(J):
+    """BK5 merge kernels in isolation: two logical
+    devices on this GPU under EAGER, with the loop restricted to device 0's
+    block so device 1 runs no loop kernel and device 0's merge is the only
+    work in flight.  On one GPU the peer replica is local HBM, so the merge
+    is an HBM read + write: its fraction of the copy peak is the kernel's
+    efficiency; on distinct GPUs the same kernel's stores cross NVLink."""
+    import synth
+    peaks, _ = load_peaks()
+    peak = float(peaks["hbm_gbs"])
+    out = {}
+    IN, OUT, INOUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT, J.JACC_ARG_ARRAY_INOUT
+
+    def prof(fn, reps):
+        fn()
+        J.jacc_wait()
+        J.jacc_set_profiling(1)
+        J.jacc_profile_reset()
+        for _ in range(reps):
+            fn()
+        J.jacc_wait()
+        k, m, nl, _ = J.jacc_profile_totals(0)
+        J.jacc_set_profiling(0)
+        return m / max(nl, 1)
+
+    # merge_range: Jacobi rows [1, 8192) = device 0's block (device 1 idle)
     J.jacc_init(2, [0, 0])
-    J.jacc_set_merge_policy(J.JACC_MERGE_EAGER)
-    for arr in (A, B):
-        J.jacc_data_create(arr)
-        J.jacc_update_device(arr)
-    IN, OUT = J.JACC_ARG_ARRAY_IN, J.JACC_ARG_ARRAY_OUT
-    args_ab = [J.arg(IN, A), J.arg(OUT, B)]
-    J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ab, 0)
-    J.jacc_wait()
-    J.jacc_set_profiling(1)
-    J.jacc_profile_reset()
-    reps = 6
-    for _ in range(reps):
-        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, args_ab, 0)
-    J.jacc_wait()
-    k, m, nl, _ = J.jacc_profile_totals(0)
-    J.jacc_set_profiling(0)
-    lo, hi = J.jacc_partition(N_GRID, 2, 0)
-    dirty_bytes = (min(hi, N_GRID - 1) - max(lo, 1)) * N_GRID * 8   # span rows x full width
-    J.jacc_finalize()
-    mt = m / max(nl, 1)
-    return {"merge_us": mt * 1e6, "bytes_pushed": dirty_bytes,
-            "copy_gbs": 2 * dirty_bytes / mt / 1e9,
-            "note": "one peer, virtual devices: local HBM read+write, not NVLink"}
+    try:
+        J.jacc_set_merge_policy(J.JACC_MERGE_EAGER)
+        N = N_GRID
+        A, B = synth.polybench_jacobi2d(N)
+        for arr in (A, B):
+            J.jacc_data_create(arr)
+            J.jacc_update_device(arr)
+        lo, hi = J.jacc_partition(N, 2, 0)
+        rng = J.make_range((lo + 1, 1), (hi, N - 1))
+        args_ab = [J.arg(IN, A), J.arg(OUT, B)]
+        mt = prof(lambda: J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, rng, args_ab, 0), 6)
+        span = ((hi - 1) * N + N - 2) - ((lo + 1) * N + 1) + 1
+        byts = 8 * span
+        out["merge_range"] = {"kernel": "merge_range_kernel", "us": mt * 1e6,
+                              "dirty_bytes": byts, "copy_gbs": 2 * byts / mt / 1e9,
+                              "frac_of_hbm_copy": 2 * byts / mt / 1e9 / peak,
+                              "nvlink_time_at_770_us": byts / (NVLINK_GBS * 1e9) * 1e6}
+        del A, B
+    finally:
+        J.jacc_finalize()
+    # merge_bitmap: scatter whose targets all fall in device 0's slice
+    M = SCAT_N
+    for name, nupd in (("merge_bitmap_dense", 2**27), ("merge_bitmap_sparse", 2**20)):
+        J.jacc_init(2, [0, 0])
+        try:
+            J.jacc_set_merge_policy(J.JACC_MERGE_EAGER)
+            idx = synth.index_i32(nupd, M // 2, 4, synth.AID["idx"])
+            b = synth.dyadic_f64(nupd, 4, synth.AID["b"])
+            a = synth.dyadic_f64(M, 4, synth.AID["a0"])
+            for arr in (idx, b, a):
+                J.jacc_data_create(arr)
+                J.jacc_update_device(arr)
+            sargs = [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)]
+            mt = prof(lambda: J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, J.make_range(0, nupd),
+                                            sargs, 0), 4)
+            bm = J.jacc_get_dirty_bitmap(a, 0, M)
+            dirty = int(np.unpackbits(bm.view(np.uint8)).sum())
+            words = (M // 2 + 31) // 32
+            moved = 8 * dirty
+            out[name] = {"kernel": "merge_bitmap_kernel", "us": mt * 1e6, "updates": nupd,
+                         "dirty_elements": dirty, "bitmap_words_scanned": words,
+                         "bytes_pushed": moved,
+                         "hbm_bytes": 2 * moved + 4 * words,
+                         "gbs": (2 * moved + 4 * words) / mt / 1e9,
+                         "frac_of_hbm_copy": (2 * moved + 4 * words) / mt / 1e9 / peak,
+                         "nvlink_time_at_770_us": moved / (NVLINK_GBS * 1e9) * 1e6}
+            del idx, b, a
+        finally:
+            J.jacc_finalize()
+    return out
 
 
 def main():
@@ -607,10 +850,14 @@ def main():
     ap.add_argument("--merge", default="halo", choices=["halo", "eager"])
     ap.add_argument("--no-extra", dest="extra", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
-    ap.add_argument("--cpu-sweeps", type=int, default=10)
+    ap.add_argument("--cpu-sweeps", type=int, default=6)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--oracle-worker", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--oracle-arg", default="1", help=argparse.SUPPRESS)
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.oracle_worker:
+        _oracle_worker(args.oracle_worker, args.oracle_arg)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_jacc(args)

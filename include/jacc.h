@@ -341,6 +341,29 @@ jacc_status jacc_profile_reset(void);
  * CUDA ordinal, so callers can time the path with their own events. */
 jacc_status jacc_get_stream(int dev, void **stream, int *cuda_ordinal);
 
+/* What a measurement must state about the runtime: the
+ * logical devices, whether they are distinct GPUs, which reduction combine
+ * runs (NCCL allreduce across distinct GPUs; otherwise the
+ * fixed-order sum over peer memory), how many ordered pairs of distinct
+ * GPUs have peer access (NVLink P2P loads/stores of the merges) and
+ * the one-process-per-GPU mode.  With distinct GPUs an NCCL communicator
+ * that cannot be built makes jacc_init / jacc_init_rank fail with
+ * JACC_ERR_NCCL (never a silent switch of combine); JACC_NO_NCCL=1 asks
+ * for the peer-memory combine explicitly.
+ * Errors: JACC_ERR_STATE before init, JACC_ERR_INVALID for NULL. */
+enum { JACC_COMBINE_PEER = 0, JACC_COMBINE_NCCL = 1 };
+typedef struct {
+    int n_devices;
+    int distinct_gpus;   /* 1 if no two logical devices share a GPU */
+    int combine;         /* JACC_COMBINE_PEER or JACC_COMBINE_NCCL */
+    int peer_pairs;      /* ordered pairs (d, q), distinct GPUs, P2P enabled;
+                            -1 in one-process-per-GPU mode (CUDA-IPC mappings
+                            of the peers' memory carry the P2P there) */
+    int multiprocess;    /* 1 in one-process-per-GPU mode */
+    int rank;            /* this process's logical device (0: single process) */
+} jacc_info;
+jacc_status jacc_get_info(jacc_info *out);
+
 /* ---------------------------------------------------------------------- */
 /* One process per GPU (the launch model of bench.py under torchrun)       */
 /* ---------------------------------------------------------------------- */

@@ -63,20 +63,23 @@ jacc_status jacc_init(int n_devices, const int *device_ids) {
                     cudaError_t e = cudaDeviceEnablePeerAccess(ords[q], 0);
                     if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
                     else CK(e);
+                    R.peer_pairs++;
                 }
             if (n_devices > 1 && R.distinct && !getenv("JACC_NO_NCCL")) {
-                // NCCL allreduce for the reduction combine; if the communicator
-                // cannot be built the fixed-order peer-memory combine (P2P
-                // loads of every device's partial) is used instead
+                // NCCL allreduce for the reduction combine.  A
+                // communicator that cannot be built is an error, not a silent
+                // switch to the peer-memory combine (JACC_NO_NCCL=1 selects
+                // that one explicitly)
                 std::vector<ncclComm_t> comms(n_devices);
                 const ncclResult_t nr = ncclCommInitAll(comms.data(), n_devices, ords.data());
-                if (nr == ncclSuccess) {
-                    for (int d = 0; d < n_devices; d++) R.dev[d].comm = comms[d];
-                    R.use_nccl = true;
-                } else if (getenv("JACC_DEBUG")) {
-                    fprintf(stderr, "[jacc] ncclCommInitAll: %s; peer-memory combine\n",
-                            ncclGetErrorString(nr));
+                if (nr != ncclSuccess) {
+                    fprintf(stderr, "[jacc] ncclCommInitAll: %s (set JACC_NO_NCCL=1 for the "
+                            "peer-memory combine)\n", ncclGetErrorString(nr));
+                    jacc_finalize();
+                    return JACC_ERR_NCCL;
                 }
+                for (int d = 0; d < n_devices; d++) R.dev[d].comm = comms[d];
+                R.use_nccl = true;
             }
             R.comm_prev.assign(n_devices, std::vector<char>(n_devices, 0));
             return JACC_OK;
@@ -563,6 +566,19 @@ jacc_status jacc_get_stream(int dev, void **stream, int *ord) {
         if (dev < 0 || dev >= R.n || !local(dev)) return JACC_ERR_INVALID;
         if (stream) *stream = (void *)R.dev[dev].s;
         if (ord) *ord = R.dev[dev].ord;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_get_info(jacc_info *out) {
+    return guard([&]() -> jacc_status {
+        invalid_if(!out);
+        out->n_devices = R.n;
+        out->distinct_gpus = R.distinct ? 1 : 0;
+        out->combine = R.use_nccl ? JACC_COMBINE_NCCL : JACC_COMBINE_PEER;
+        out->peer_pairs = R.mp ? -1 : R.peer_pairs;
+        out->multiprocess = R.mp ? 1 : 0;
+        out->rank = R.mp ? R.me : 0;
         return JACC_OK;
     });
 }

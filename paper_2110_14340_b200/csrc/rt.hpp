@@ -316,6 +316,7 @@ struct Runtime {
     int gen = 0;
     bool distinct = true;
     bool use_nccl = false;
+    int peer_pairs = 0;  // ordered pairs of distinct GPUs with P2P enabled
     std::vector<std::vector<char>> comm_prev;  // [d][q]
     bool profiling = false;
     std::vector<ProfRec> prof;                 // unresolved event records

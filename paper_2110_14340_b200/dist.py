@@ -36,7 +36,8 @@ def init_rank(cuda_ordinal=None, use_nccl=None):
     uuids = _all_gather(uuid)
     distinct = len(set(uuids)) == world
     if use_nccl is None:
-        use_nccl = distinct and world > 1
+        # JACC_NO_NCCL=1: the fixed-order peer-memory combine, explicitly
+        use_nccl = distinct and world > 1 and not os.environ.get("JACC_NO_NCCL")
     if use_nccl and not distinct:
         raise ValueError("NCCL combine needs one distinct GPU per rank")
     box = [None]

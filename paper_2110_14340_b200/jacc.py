@@ -58,7 +58,7 @@ EXPORTS = [
     "jacc_adaptive_replay", "jacc_adaptive_history",
     "jacc_graph_begin", "jacc_graph_end", "jacc_graph_replay", "jacc_graph_destroy",
     "jacc_select_split_dim", "jacc_exchange_plan", "jacc_set_split_dim",
-    "jacc_set_scatter_split", "jacc_set_queues", "jacc_queue_replay",
+    "jacc_set_scatter_split", "jacc_set_queues", "jacc_queue_replay", "jacc_get_info",
 ]
 JACC_MAX_QUEUES = 32
 JACC_ASYNC_AUTO = -2
@@ -75,6 +75,15 @@ class jacc_range(ctypes.Structure):
 class jacc_copy2d_plan(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in ("count", "height", "width_bytes", "pitch_bytes",
                                               "first_offset_bytes", "outer_stride_bytes")]
+
+
+class jacc_info(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int) for k in ("n_devices", "distinct_gpus", "combine", "peer_pairs",
+                                            "multiprocess", "rank")]
+
+
+JACC_COMBINE_PEER = 0
+JACC_COMBINE_NCCL = 1
 
 
 class jacc_arg(ctypes.Structure):
@@ -303,6 +312,16 @@ def jacc_get_stream(dev):
     s, o = ctypes.c_void_p(), ctypes.c_int()
     _ck(lib.jacc_get_stream(dev, ctypes.byref(s), ctypes.byref(o)), "jacc_get_stream")
     return s.value, o.value
+
+
+def jacc_get_info():
+    """Runtime facts for measurements: devices, distinct GPUs, reduction
+    combine ("nccl" | "peer"), peer-access pairs, process mode."""
+    info = jacc_info()
+    _ck(lib.jacc_get_info(ctypes.byref(info)), "jacc_get_info")
+    d = {k: getattr(info, k) for k, _ in jacc_info._fields_}
+    d["combine"] = "nccl" if info.combine == JACC_COMBINE_NCCL else "peer"
+    return d
 
 
 def jacc_error_string(status):

@@ -237,6 +237,70 @@ def test_jacobi_full_size_sampled(J):
         assert np.array_equal(A, H)
 
 
+@pytest.mark.parametrize("n,policy", [(1, 0), (3, 1), (3, 0)])
+def test_jacobi_add_order_golden(J, n, policy):
+    """The hand-derived operand-order fixture (tests/golden/
+    jacobi_add_order.txt): the kernel's adds follow PolyBench's order and
+    it multiplies once by the binary64 0.2, on one device and across a
+    block boundary."""
+    from test_oracle import jacobi_add_order_case
+    A, exp = jacobi_add_order_case()
+    B = np.zeros_like(A)
+    ref = np.zeros_like(A)
+    orc.jacobi2d_sweep(A, ref)
+    with runtime(J, n, policy):
+        _create(J, A, B)
+        J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)])
+        J.jacc_update_host(B)
+    for (i, j), v in exp.items():
+        assert B[i, j].hex() == v.hex(), (i, j)
+    assert np.array_equal(B, ref)
+
+
+_J16K_CACHE = {}
+
+
+def _j16k_random_ref(sweeps):
+    """Random 16384^2 field (seeded) and the oracle after `sweeps` launches
+    (A->B, B->A, ...), computed once per module."""
+    N = 16384
+    if "A0" not in _J16K_CACHE:
+        _J16K_CACHE["A0"] = synth.uniform_f64(N * N, 45, 1).reshape(N, N)
+        _J16K_CACHE["B0"] = synth.uniform_f64(N * N, 45, 2).reshape(N, N)
+    if sweeps not in _J16K_CACHE:
+        A, B = _J16K_CACHE["A0"].copy(), _J16K_CACHE["B0"].copy()
+        src, dst = A, B
+        for _ in range(sweeps):
+            orc.jacobi2d_sweep(src, dst)
+            src, dst = dst, src
+        _J16K_CACHE[sweeps] = (A, B)
+    return _J16K_CACHE["A0"], _J16K_CACHE["B0"], _J16K_CACHE[sweeps]
+
+
+@pytest.mark.parametrize("n,policy", [(1, 1), (2, 1), (8, 1), (8, 0)])
+def test_jacobi_full_size_random_field_exact(J, n, policy):
+    """BASELINE config 2 at full size, whole field: a seeded random
+    16384^2 field (every operand order visible in the rounding) after two
+    launches (A->B, B->A), every element of A and B bit-exact against the
+    oracle, on 1 device and on 2 / 8 virtual devices under HALO and EAGER."""
+    A0, B0, (Ar, Br) = _j16k_random_ref(2)
+    A, B, _, _ = _jacobi_gpu(J, A0, B0, 1, n, policy, check_dirty=False)
+    assert np.array_equal(B, Br)
+    assert np.array_equal(A, Ar)
+
+
+@pytest.mark.parametrize("n", [1, 8])
+def test_jacobi_full_step_200_launches_exact(J, n):
+    """The whole timed J16K step (100 timesteps = 200 launches, HALO) on a
+    seeded random field, compared element by element with 200 oracle
+    sweeps: the exact configuration bench.py times (n = 1), and 8 virtual
+    devices."""
+    A0, B0, (Ar, Br) = _j16k_random_ref(200)
+    A, B, _, _ = _jacobi_gpu(J, A0, B0, 100, n, 1, check_dirty=False)
+    assert np.array_equal(A, Ar)
+    assert np.array_equal(B, Br)
+
+
 # --------------------------------------------------------------------------
 # c2 / c8 reductions
 # --------------------------------------------------------------------------
@@ -295,6 +359,19 @@ def test_dot_full_size(J):
     x = synth.dyadic_f64(size, 54, 3)
     y = synth.dyadic_f64(size, 54, 4)
     assert _reduce(J, x, y, 0.0, 1) == orc.dot_f64(x, y, 0.0)
+
+
+@pytest.mark.parametrize("n", [1, 8])
+def test_dot_full_size_uniform_tolerance(J, n):
+    """BASELINE config 3 at full size with the tolerance inputs: 2^30
+    uniform [0,1) pairs (the bench's data), GPU vs the oracle's Neumaier
+    reference within 1e-12 relative (north_star; DESIGN R-10)."""
+    size = 2**30
+    x = synth.uniform_f64(size, 1, synth.AID["x"])
+    y = synth.uniform_f64(size, 1, synth.AID["y"])
+    ref = orc.dot_neumaier(x, y, 0.0)
+    got = _reduce(J, x, y, 0.0, n)
+    assert abs(got - ref) <= 1e-12 * abs(ref)
 
 
 # --------------------------------------------------------------------------

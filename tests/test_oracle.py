@@ -440,3 +440,28 @@ def test_exchange_bitmap_coherence_scatter(n):
     orc.exchange_bitmap(R, bms)
     for d in range(n):
         assert np.array_equal(R[d], full)
+
+
+def jacobi_add_order_case():
+    """The hand-derived operand-order fixture (tests/golden/jacobi_add_order.txt):
+    (A grid, {(i, j): expected B value})."""
+    A = np.zeros((7, 7))
+    exp = {}
+    for r in _golden("jacobi_add_order.txt"):
+        i, j, v = int(r[1]), int(r[2]), float.fromhex(r[3])
+        if r[0] == "A":
+            A[i, j] = v
+        else:
+            exp[(i, j)] = v
+    return A, exp
+
+
+def test_jacobi_sweep_add_order_golden():
+    """Pins the PolyBench left-to-right add order and the single multiply by
+    the binary64 0.2 (DESIGN R-1): a dropped term, a different association
+    or a division by 5 changes at least one of the hand-derived values."""
+    A, exp = jacobi_add_order_case()
+    B = np.zeros_like(A)
+    orc.jacobi2d_sweep(A, B)
+    for (i, j), v in exp.items():
+        assert B[i, j].hex() == v.hex(), (i, j, B[i, j].hex(), v.hex())
