@@ -344,10 +344,8 @@ jacc_status jacc_data_create(void *host, size_t bytes, size_t elem_size, int ndi
         r->dirty.assign(R.n, nullptr);
         r->bitmap.assign(R.n, nullptr);
         r->dslot.assign(R.n, 0);
-        r->bytemap.assign(R.n, nullptr);
         r->delta.assign(R.n, nullptr);
         r->dbm.assign(R.n, nullptr);
-        r->epoch.assign(R.n, 0);
         r->valid.assign(R.n, IntervalSet{});
         for (int d = 0; d < R.n; d++) {
             if (!local(d)) continue;  // peers' replicas arrive via jacc_import_region

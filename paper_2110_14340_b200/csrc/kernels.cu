@@ -574,78 +574,21 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
 }
 
 // ---------------------------------------------------------------------------
-// BK4b destination-binned scatter (see kernels.cuh)
+// BK4b destination-binned scatter, single pass over the updates (see
+// kernels.cuh).  Owned pairs are partitioned into buckets of 2^shift
+// elements of `a`, written into pages of PG_P pairs that each bucket claims
+// from a pool as its stream grows; the apply walks the buckets in order so
+// the read-modify-writes of `a` are L2 hits, and after each bucket's pages a
+// bits item rebuilds that bucket's dirty-bitmap words in shared memory
+// while its keys are still L2-resident.
 // ---------------------------------------------------------------------------
-constexpr int SB_T = 256;  // partition tile = SB_T x E elements (E = 16 default, 8, 12)
-constexpr int SB_MAXB = 1024;
-
-__global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restrict__ idx, int64_t n,
-                                                        int64_t lo, int64_t hi, int shift, int nb,
-                                                        u64 *counts) {
-    __shared__ unsigned h[SB_MAXB];
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
-    __syncthreads();
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t hd = (int64_t)((16 - ((uintptr_t)idx & 15)) & 15) >> 2;
-    if (hd > n) hd = n;
-    const int64_t n4 = (n - hd) >> 2;
-    const int4 *idx4 = reinterpret_cast<const int4 *>(idx + hd);
-    if (tid < hd) {
-        const int32_t k = idx[tid];
-        if (k >= lo && k < hi) atomicAdd(&h[(k - lo) >> shift], 1u);
-    }
-    for (int64_t q = tid; q < n4; q += nth) {
-        const int4 k = __ldg(idx4 + q);
-        if (k.x >= lo && k.x < hi) atomicAdd(&h[(k.x - lo) >> shift], 1u);
-        if (k.y >= lo && k.y < hi) atomicAdd(&h[(k.y - lo) >> shift], 1u);
-        if (k.z >= lo && k.z < hi) atomicAdd(&h[(k.z - lo) >> shift], 1u);
-        if (k.w >= lo && k.w < hi) atomicAdd(&h[(k.w - lo) >> shift], 1u);
-    }
-    for (int64_t i = hd + 4 * n4 + tid; i < n; i += nth) {
-        const int32_t k = idx[i];
-        if (k >= lo && k < hi) atomicAdd(&h[(k - lo) >> shift], 1u);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < nb; i += blockDim.x)
-        if (h[i]) atomicAdd(&counts[i], (u64)h[i]);
-}
-
-// exclusive scan of counts[0..nb) -> base[0..nb] and cursor = base (1 block);
-// also zeroes the apply kernel's work counter
-__global__ void __launch_bounds__(1024) scat_scan_kernel(const u64 *counts, int nb, u64 *base,
-                                                         u64 *cursor, u64 *work) {
-    // nb <= SB_MAXB = 1024: one bucket per thread, block-wide exclusive scan
-    __shared__ u64 wsum[32];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const u64 c = t < nb ? counts[t] : 0;
-    u64 inc = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const u64 v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-    }
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        const u64 x = wsum[lane];
-        u64 y = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u64 v = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += v;
-        }
-        wsum[lane] = y - x;
-    }
-    __syncthreads();
-    const u64 ex = wsum[w] + inc - c;
-    if (t < nb) {
-        base[t] = ex;
-        cursor[t] = ex;
-    }
-    if (t == nb - 1) base[nb] = ex + c;
-    if (t == 0) *work = 0;
-}
+constexpr int SB_T = 256;        // partition CTA; tile = SB_T * SB_E updates
+constexpr int SB_E = 16;
+constexpr int SB_MAXB = 1024;    // max buckets
+constexpr int PG_LOG = 13;       // pairs per page = 8192 (>= a tile: a tile's
+constexpr int PG_P = 1 << PG_LOG;  //  bucket segment spans at most two pages)
+constexpr int SA_T = 1024;       // apply CTA (one per SM)
+static_assert(SB_T * SB_E <= PG_P, "a tile segment must fit in two pages");
 
 // warp 0 computes the exclusive scan of hist[0..nb) into off[]
 __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off, int nb,
@@ -671,62 +614,82 @@ __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off,
     if (lane == 31) *total = inc;
 }
 
-// Per tile: all E keys of a thread are loaded first, then the values of the
-// in-range ones (two independent batches of loads in flight, not E
-// key->value dependency chains), then histogram, scan, staging in shared
-// memory and bucket-contiguous write-out.
-template <typename T, int E>
-__global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restrict__ idx,
-                                                         const T *__restrict__ b, int64_t n,
-                                                         int64_t lo, int64_t hi, int shift, int nb,
-                                                         u64 *cursor, int32_t *__restrict__ pidx,
-                                                         T *__restrict__ pval) {
-    constexpr int TILE = SB_T * E;
-    __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB];
-    __shared__ u64 gbase[SB_MAXB];
+// Partition.  Per tile of SB_T*SB_E updates: keys (then the values of the
+// owned ones) into registers, per-bucket ranks by shared-memory atomics,
+// warp scan, then one thread per non-empty bucket reserves the tile's
+// segment of the bucket's stream (atomicAdd on fill[b]) and claims from the
+// pool every page whose first slot falls inside the segment, publishing it
+// in dir[b*kmax + k] (page id + 1).  The page holding the segment's first
+// slot, when it starts before the segment, was claimed by the CTA that
+// reserved that slot; its reservation precedes ours and it publishes right
+// after reserving (before any wait of its own), so the wait below always
+// ends.  The pairs are staged in bucket order in shared memory and written
+// out bucket-contiguously.
+template <typename T>
+__global__ void __launch_bounds__(SB_T) scat_part_kernel(
+    const int32_t *__restrict__ idx, const T *__restrict__ b, int64_t n, int64_t lo, int64_t hi,
+    int shift, int nb, int kmax, u64 *fill, unsigned *pool, unsigned *dir,
+    int32_t *__restrict__ pk, T *__restrict__ pv) {
+    constexpr int E = SB_E, TILE = SB_T * E;
+    __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB], gp0[SB_MAXB], gp1[SB_MAXB];
+    __shared__ u64 gv0[SB_MAXB];
     __shared__ unsigned total;
     extern __shared__ __align__(16) unsigned char sdyn[];  // [TILE] T, [TILE] i32
     T *sv = reinterpret_cast<T *>(sdyn);
     int32_t *sk = reinterpret_cast<int32_t *>(sdyn + TILE * sizeof(T));
     const int tid = threadIdx.x;
     const int64_t ntiles = (n + TILE - 1) / TILE;
-    auto load_keys = [&](int64_t t, int32_t *k) {
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int32_t k[E];
+        T v[E];
 #pragma unroll
         for (int j = 0; j < E; j++) {
             const int64_t i = t * TILE + j * SB_T + tid;
-            k[j] = (t < ntiles && i < n) ? __ldcs(idx + i) : (int32_t)lo - 1;  // lo-1: out of range
+            k[j] = i < n ? __ldcs(idx + i) : (int32_t)lo - 1;  // lo-1: not owned
         }
-    };
-    auto load_vals = [&](int64_t t, const int32_t *k, T *v) {
 #pragma unroll
         for (int j = 0; j < E; j++) {
             const int64_t i = t * TILE + j * SB_T + tid;
             if (k[j] >= lo && k[j] < hi) v[j] = __ldcs(b + i);
         }
-    };
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        int32_t k[E];
-        T v[E];
-        load_keys(t, k);
-        load_vals(t, k, v);
         for (int i = tid; i < nb; i += SB_T) hist[i] = 0;
         __syncthreads();
-        int bk[E];
         unsigned rk[E];
 #pragma unroll
-        for (int j = 0; j < E; j++) bk[j] = (k[j] >= lo && k[j] < hi) ? (int)((k[j] - lo) >> shift) : -1;
-#pragma unroll
         for (int j = 0; j < E; j++)
-            if (bk[j] >= 0) rk[j] = atomicAdd(&hist[bk[j]], 1u);
+            if (k[j] >= lo && k[j] < hi) rk[j] = atomicAdd(&hist[(int)(((int64_t)k[j] - lo) >> shift)], 1u);
         __syncthreads();
         if (tid < 32) warp_exscan(hist, loff, nb, &total);
-        for (int i = tid; i < nb; i += SB_T)
-            gbase[i] = hist[i] ? atomicAdd(&cursor[i], (u64)hist[i]) : 0;
+        // reserve + claim (no waiting), then resolve the first page (may wait)
+        for (int i = tid; i < nb; i += SB_T) {
+            const unsigned c = hist[i];
+            if (!c) continue;
+            const u64 v0 = atomicAdd(&fill[i], (u64)c);
+            const u64 k0 = v0 >> PG_LOG, k1 = (v0 + c - 1) >> PG_LOG;
+            unsigned p0 = 0, p1 = 0;
+            for (u64 kk = k0; kk <= k1; kk++)
+                if ((kk << PG_LOG) >= v0) {
+                    const unsigned pid = atomicAdd(pool, 1u) + 1u;
+                    atomicExch(&dir[(size_t)i * kmax + kk], pid);
+                    if (kk == k0) p0 = pid;
+                    else p1 = pid;
+                }
+            gv0[i] = v0;
+            gp0[i] = p0;
+            gp1[i] = p1;
+        }
+        for (int i = tid; i < nb; i += SB_T) {
+            if (!hist[i] || gp0[i]) continue;
+            unsigned *d = dir + (size_t)i * kmax + (gv0[i] >> PG_LOG);
+            unsigned p;
+            while ((p = atomicOr(d, 0u)) == 0) __nanosleep(64);  // read at L2
+            gp0[i] = p;
+        }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < E; j++)
-            if (bk[j] >= 0) {
-                const unsigned pos = loff[bk[j]] + rk[j];
+            if (k[j] >= lo && k[j] < hi) {
+                const unsigned pos = loff[(int)(((int64_t)k[j] - lo) >> shift)] + rk[j];
                 sk[pos] = k[j];
                 sv[pos] = v[j];
             }
@@ -734,121 +697,131 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(const int32_t *__restri
         const unsigned cnt = total;
         for (unsigned pos = tid; pos < cnt; pos += SB_T) {
             const int32_t kk = sk[pos];
-            const int bb = (int)(((int64_t)kk - lo) >> shift);  // bucket from the key
-            const u64 g = gbase[bb] + (pos - loff[bb]);
-            pidx[g] = kk;
-            pval[g] = sv[pos];
+            const int bb = (int)(((int64_t)kk - lo) >> shift);
+            const u64 vs = gv0[bb] + (pos - loff[bb]);
+            const unsigned pid = (vs >> PG_LOG) == (gv0[bb] >> PG_LOG) ? gp0[bb] : gp1[bb];
+            const size_t g = ((size_t)(pid - 1) << PG_LOG) | (size_t)(vs & (PG_P - 1));
+            pk[g] = kk;
+            pv[g] = sv[pos];
         }
         __syncthreads();
     }
 }
 
-// Pairs are applied in global order through a dynamic chunk counter, so
-// the chunks in flight at any moment span ~one bucket of `a` (static
-// grid-stride lets CTAs drift apart and the working set spill out of L2).
-constexpr int SA_CH = 4096;  // default chunk (JACC_SCATTER_APPLY_CH)
+// One block: the apply's work list.  For every non-empty bucket b, in
+// order, its pages (apply item = page id << 16 | pairs-1) then one bits item
+// (IT_BITS | b << 32 | page count).  Also clears the fill/pool/dir state for
+// the next launch and zeroes the apply's work counter; ctr[1] = item count.
+constexpr u64 IT_BITS = 1ull << 63;
+__global__ void __launch_bounds__(1024) scat_items_kernel(u64 *fill, unsigned *pool, unsigned *dir,
+                                                          int nb, int kmax, u64 *items,
+                                                          unsigned *ctr) {
+    __shared__ unsigned wsum[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    // buckets per thread: nb <= 1024
+    const u64 c = t < nb ? fill[t] : 0;
+    const unsigned np = (unsigned)((c + PG_P - 1) >> PG_LOG);
+    const unsigned own = np ? np + 1 : 0;  // pages + the bits item
+    unsigned inc = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const unsigned x = wsum[lane];
+        unsigned y = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += v;
+        }
+        wsum[lane] = y - x;
+    }
+    __syncthreads();
+    const unsigned base = wsum[w] + inc - own;
+    if (t < nb && np) {
+        for (unsigned k = 0; k < np; k++) {
+            unsigned *e = dir + (size_t)t * kmax + k;
+            const unsigned pid = *e - 1u;
+            *e = 0;
+            const u64 cnt = (k + 1 < np) ? (u64)PG_P : c - ((u64)k << PG_LOG);
+            items[base + k] = ((u64)pid << 16) | (cnt - 1);
+        }
+        items[base + np] = IT_BITS | ((u64)t << 32) | np;
+        fill[t] = 0;
+    }
+    if (t == nb - 1) ctr[1] = base + own;  // number of items
+    if (t == 0) {
+        *pool = 0;
+        ctr[0] = 0;  // work counter
+    }
+}
 
-// The write log is kept as an epoch byte-map (one plain byte store per
-// update, no L2 atomic) and packed into the dirty bitmap afterwards: the
-// bitmap atomics would otherwise double the L2 atomic traffic of the pass.
-template <typename T, bool BYTEMAP>
-__global__ void __launch_bounds__(256) scat_apply_kernel(const int32_t *__restrict__ pidx,
-                                                         const T *__restrict__ pval, const u64 *base,
-                                                         int nb, u64 *work, T *a, uint8_t *bytemap,
-                                                         uint8_t epoch, u64 *dirty, int ch) {
-    __shared__ u64 chunk;
-    const int64_t m = (int64_t)base[nb];
-    const int64_t nchunks = (m + ch - 1) / ch;
+// Apply (persistent, one CTA of SA_T threads per SM, items from a dynamic
+// counter in list order).  Apply item: a[k] += v for the page's pairs (L2
+// atomics; the buckets in flight are L2-resident).  Bits item of bucket b:
+// the bucket's keys (just applied, still in L2) set bits of a shared-memory
+// copy of the bucket's bitmap words, which are then written out once
+// (plain stores; the first/last word of a bucket may be shared with the
+// neighbour bucket when lo is not 32-aligned: atomicOr into the zeroed
+// bitmap).  Dirty range: min/max over the applied keys.
+template <typename T>
+__global__ void __launch_bounds__(SA_T, 1) scat_apply_kernel(
+    const u64 *__restrict__ items, unsigned *ctr, const int32_t *__restrict__ pk,
+    const T *__restrict__ pv, T *a, int64_t lo, int64_t hi, int shift, uint32_t *bitmap,
+    u64 *dirty) {
+    extern __shared__ uint32_t sw[];
+    __shared__ unsigned sj;
+    const unsigned nitems = ctr[1];
     u64 mn = kU64Max, mx = 0;
     for (;;) {
-        if (threadIdx.x == 0) chunk = atomicAdd(work, 1ull);
+        if (threadIdx.x == 0) sj = atomicAdd(&ctr[0], 1u);
         __syncthreads();
-        const int64_t c = (int64_t)chunk;
+        const unsigned j = sj;
         __syncthreads();
-        if (c >= nchunks) break;
-        const int64_t p0 = c * ch;
-        const int64_t p1 = p0 + ch < m ? p0 + ch : m;
+        if (j >= nitems) break;
+        const u64 it = items[j];
+        if (!(it & IT_BITS)) {
+            const size_t p0 = (size_t)(it >> 16) << PG_LOG;
+            const int cnt = (int)(it & 0xffff) + 1;
 #pragma unroll 4
-        for (int64_t p = p0 + threadIdx.x; p < p1; p += 256) {
-            const int32_t k = __ldcs(pidx + p);
-            const T v = __ldcs(pval + p);
-            atomicAdd(a + k, v);
-            if (BYTEMAP) bytemap[k] = epoch;
-            mn = (u64)k < mn ? (u64)k : mn;
-            mx = (u64)k > mx ? (u64)k : mx;
+            for (int p = threadIdx.x; p < cnt; p += SA_T) {
+                const int32_t k = __ldcs(pk + p0 + p);
+                atomicAdd(a + k, __ldcs(pv + p0 + p));
+                mn = (u64)k < mn ? (u64)k : mn;
+                mx = (u64)k > mx ? (u64)k : mx;
+            }
+            continue;
         }
-    }
-    publish_dirty<8>(mn, mx, dirty);
-}
-
-// bitmap word w <- bits of bytemap[32w .. 32w+31] == epoch, for words
-// covering [lo, hi) (elements outside [lo, hi) are never marked)
-__global__ void __launch_bounds__(256) scat_pack_kernel(const uint8_t *__restrict__ bytemap,
-                                                        uint8_t epoch, int64_t lo, int64_t hi,
-                                                        uint32_t *bitmap) {
-    const int64_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t w = w0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w1; w += nth) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(bytemap + (w << 5));
-        const uint4 q0 = __ldcs(p), q1 = __ldcs(p + 1);
-        const uint32_t wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        uint32_t bits = 0;
-#pragma unroll
-        for (int i = 0; i < 8; i++)
-#pragma unroll
-            for (int b = 0; b < 4; b++)
-                if (((wd[i] >> (8 * b)) & 0xffu) == epoch) bits |= 1u << (4 * i + b);
-        bitmap[w] = bits;
-    }
-}
-
-
-// Dirty bitmap of the binned scatter from the bucket-ordered keys: CTA
-// (bucket, part) owns 2^20 elements of the bucket (a 128 KB bitmap in shared
-// memory), scans the bucket's keys (16-byte loads), sets its bits with
-// shared-memory atomicOr and writes its words (boundary words shared with a
-// neighbour part by atomicOr into the zeroed bitmap).  Replaces the byte-map
-// stores in the apply (random 1-byte L2 writes) and the pack pass.  (A
-// cluster version that reads every key once and sets remote bits over DSMEM
-// measured 3.4x slower: remote shared-memory atomics.)
-constexpr int SBITS_LB = 20;  // elements per part = 2^20 -> 32768 words
-__global__ void __launch_bounds__(1024) scat_bits_kernel(const int32_t *__restrict__ pidx,
-                                                         const u64 *__restrict__ base, int nb,
-                                                         int shift, int64_t lo, int64_t hi,
-                                                         uint32_t *bitmap) {
-    extern __shared__ uint32_t sw[];
-    const int lp = shift > SBITS_LB ? shift - SBITS_LB : 0;  // log2 parts per bucket
-    const int pb = shift > SBITS_LB ? SBITS_LB : shift;      // log2 elements per part
-    const int64_t items = (int64_t)nb << lp;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int bk = (int)(it >> lp), q = (int)(it & ((1 << lp) - 1));
-        const int64_t e0 = lo + ((int64_t)bk << shift) + ((int64_t)q << pb);
-        if (e0 >= hi) continue;  // uniform per CTA
-        const int64_t e1 = e0 + ((int64_t)1 << pb) < hi ? e0 + ((int64_t)1 << pb) : hi;
+        const int bk = (int)((it >> 32) & 0xffff);
+        const unsigned np = (unsigned)(it & 0xffffffffu);
+        const int64_t e0 = lo + ((int64_t)bk << shift);
+        const int64_t e1 = e0 + ((int64_t)1 << shift) < hi ? e0 + ((int64_t)1 << shift) : hi;
         const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
-        for (int i = threadIdx.x; i < nw; i += 1024) sw[i] = 0;
+        for (int i = threadIdx.x; i < nw; i += SA_T) sw[i] = 0;
         __syncthreads();
-        const u64 p0 = base[bk], p1 = base[bk + 1];
-        auto put = [&](int64_t k) {
-            if (k >= e0 && k < e1) atomicOr(&sw[(k >> 5) - w0], 1u << (k & 31));
-        };
-        // 16-byte loads for the aligned body (pidx is 256-byte aligned)
-        u64 pa = (p0 + 3) & ~(u64)3;
-        if (pa > p1) pa = p1;
-        const u64 n4 = (p1 - pa) >> 2, pt = pa + 4 * n4;
-        if (threadIdx.x < pa - p0) put(pidx[p0 + threadIdx.x]);
-        if (threadIdx.x < p1 - pt) put(pidx[pt + threadIdx.x]);
-        const int4 *k4 = reinterpret_cast<const int4 *>(pidx + pa);
-#pragma unroll 4
-        for (u64 q4 = threadIdx.x; q4 < n4; q4 += 1024) {
-            const int4 k = __ldcs(k4 + q4);
-            put(k.x);
-            put(k.y);
-            put(k.z);
-            put(k.w);
+        for (unsigned q = 0; q < np; q++) {
+            const u64 ip = items[j - np + q];
+            const int4 *k4 = reinterpret_cast<const int4 *>(pk + ((size_t)(ip >> 16) << PG_LOG));
+            const int cnt = (int)(ip & 0xffff) + 1;
+            const int n4 = cnt >> 2;
+            for (int p = threadIdx.x; p < n4; p += SA_T) {
+                const int4 k = __ldcg(k4 + p);
+                atomicOr(&sw[(k.x >> 5) - w0], 1u << (k.x & 31));
+                atomicOr(&sw[(k.y >> 5) - w0], 1u << (k.y & 31));
+                atomicOr(&sw[(k.z >> 5) - w0], 1u << (k.z & 31));
+                atomicOr(&sw[(k.w >> 5) - w0], 1u << (k.w & 31));
+            }
+            if (threadIdx.x < (cnt & 3)) {
+                const int32_t k = __ldcg(reinterpret_cast<const int32_t *>(k4) + 4 * n4 + threadIdx.x);
+                atomicOr(&sw[(k >> 5) - w0], 1u << (k & 31));
+            }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < nw; i += 1024) {
+        for (int i = threadIdx.x; i < nw; i += SA_T) {
             const uint32_t v = sw[i];
             if (i == 0 || i == nw - 1) {
                 if (v) atomicOr(bitmap + w0 + i, v);
@@ -858,288 +831,8 @@ __global__ void __launch_bounds__(1024) scat_bits_kernel(const int32_t *__restri
         }
         __syncthreads();
     }
+    publish_dirty<SA_T / 32>(mn, mx, dirty);
 }
-
-// ---------------------------------------------------------------------------
-// BK4c owner-slice apply (see kernels.cuh).  Fine bin g of the owned span is
-// the element slice [lo + g*2^fs, lo + (g+1)*2^fs) -- 64 KB of `a`, held in
-// one CTA's shared memory while its updates are added there; SL_FPC fine
-// bins make one coarse bucket (the partition's bucket).
-// ---------------------------------------------------------------------------
-constexpr int SL_FPC = 128;       // fine slices per coarse bucket
-constexpr int SL_MAXF = 32768;    // fine bins the histogram holds (128 KB smem)
-constexpr int SL_T = 512;         // threads of the slice kernel (1 CTA / SM)
-constexpr int SL_E = 8;           // pairs per thread of an A tile
-constexpr int SL_TA = SL_T * SL_E;
-constexpr int SL_SLICE = 64 * 1024;  // bytes of `a` per slice (2 CTAs / SM)
-
-struct SliceHdr {  // device-side layout of the header inside the scratch
-    unsigned *fcnt;  // [nf]
-    u64 *fbase;      // [nf + 1] pair offset of fine bin g (nested in coarse order)
-    u64 *fcur;       // [nf]
-    u64 *ccur;       // [nb] coarse cursors of the partition kernel
-    unsigned *doneA; // [nb] A tiles finished per coarse bucket
-    int *stage;      // [2 nb] stage -> (type << 16 | coarse bucket)
-    u64 *sstart;     // [2 nb + 1] first work item of each stage
-    u64 *work;       // work counter
-};
-
-__global__ void __launch_bounds__(1024) scat_fhist_kernel(const int32_t *__restrict__ idx, int64_t n,
-                                                         int64_t lo, int64_t hi, int fs, int nf,
-                                                         unsigned *fcnt) {
-    extern __shared__ unsigned fh[];
-    for (int i = threadIdx.x; i < nf; i += blockDim.x) fh[i] = 0;
-    __syncthreads();
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t hd = (int64_t)((16 - ((uintptr_t)idx & 15)) & 15) >> 2;
-    if (hd > n) hd = n;
-    const int64_t n4 = (n - hd) >> 2;
-    const int4 *idx4 = reinterpret_cast<const int4 *>(idx + hd);
-    auto put = [&](int32_t k) {
-        if (k >= lo && k < hi) atomicAdd(&fh[(k - lo) >> fs], 1u);
-    };
-    if (tid < hd) put(idx[tid]);
-    for (int64_t q = tid; q < n4; q += nth) {
-        const int4 k = __ldg(idx4 + q);
-        put(k.x);
-        put(k.y);
-        put(k.z);
-        put(k.w);
-    }
-    for (int64_t i = hd + 4 * n4 + tid; i < n; i += nth) put(idx[i]);
-    __syncthreads();
-    for (int i = threadIdx.x; i < nf; i += blockDim.x)
-        if (fh[i]) atomicAdd(&fcnt[i], fh[i]);
-}
-
-// one CTA of 1024 threads: fine offsets, cursors and the work-stage table
-// (A(0), A(1), B(0), A(2), B(1), ..., B(nb-1): every B stage waits
-// only on A tiles dequeued before it, so the work queue cannot deadlock whatever
-// the residency)
-__global__ void __launch_bounds__(1024) scat_fscan_kernel(SliceHdr h, int nf, int nb) {
-    __shared__ u64 wsum[32];
-    constexpr int PER = SL_MAXF / 1024;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    u64 s = 0;
-    for (int i = 0; i < PER; i++) {
-        const int g = t * PER + i;
-        s += g < nf ? h.fcnt[g] : 0;
-    }
-    u64 inc = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const u64 v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-    }
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        u64 x = wsum[lane], y = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u64 v = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += v;
-        }
-        wsum[lane] = y - x;
-    }
-    __syncthreads();
-    u64 run = wsum[w] + inc - s;
-    for (int i = 0; i < PER; i++) {
-        const int g = t * PER + i;
-        if (g < nf) {
-            h.fbase[g] = run;
-            h.fcur[g] = run;
-            run += h.fcnt[g];
-        }
-        if (g == nf - 1) h.fbase[nf] = run;
-    }
-    __syncthreads();
-    for (int c = t; c < nb; c += 1024) {
-        h.ccur[c] = h.fbase[c * SL_FPC];
-        h.doneA[c] = 0;
-    }
-    if (t == 0) {
-        *h.work = 0;
-        auto na = [&](int c) {
-            const int g1 = (c + 1) * SL_FPC < nf ? (c + 1) * SL_FPC : nf;
-            return (h.fbase[g1] - h.fbase[c * SL_FPC] + SL_TA - 1) / SL_TA;
-        };
-        auto nbk = [&](int c) { return (u64)((nf - c * SL_FPC) < SL_FPC ? nf - c * SL_FPC : SL_FPC); };
-        int k = 0;
-        u64 acc = 0;
-        auto push = [&](int type, int c, u64 items) {
-            h.stage[k] = (type << 16) | c;
-            h.sstart[k] = acc;
-            acc += items;
-            k++;
-        };
-        constexpr int LAG = 1;  // B(c) follows A(c + LAG) (LAG 2 measured slower)
-        for (int c = 0; c < nb + LAG; c++) {
-            if (c < nb) push(0, c, na(c));
-            if (c >= LAG) push(1, c - LAG, nbk(c - LAG));
-        }
-        h.sstart[k] = acc;
-    }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(SL_T, 2) scat_slice_kernel(SliceHdr h, int nb, int nf, int fs,
-                                                            int64_t lo, int64_t hi,
-                                                            const int32_t *__restrict__ ck,
-                                                            const T *__restrict__ cv, int32_t *fk,
-                                                            T *fv, T *a, uint32_t *bitmap,
-                                                            u64 *dirty) {
-    constexpr int SLN = SL_SLICE / sizeof(T);  // elements of one slice
-    extern __shared__ __align__(16) unsigned char sdyn[];
-    // B item: [SLN] T slice (+16 B so it can sit congruent to `a` mod 16 B)
-    // and [SLN/32 + 2] u32 dirty bits; A item (aliased): [SL_TA] T,
-    // [SL_TA] i32, [SL_TA] u8 staging
-    uint32_t *sbits = reinterpret_cast<uint32_t *>(sdyn + SL_SLICE + 16);
-    T *sv = reinterpret_cast<T *>(sdyn);
-    int32_t *sk = reinterpret_cast<int32_t *>(sdyn + SL_TA * sizeof(T));
-    uint8_t *sbk = reinterpret_cast<uint8_t *>(sdyn + SL_TA * (sizeof(T) + 4));
-    __shared__ unsigned hist[SL_FPC], loff[SL_FPC], total;
-    __shared__ u64 gbase[SL_FPC];
-    __shared__ u64 item;
-    __shared__ int ist, ic;
-    const int tid = threadIdx.x;
-    const int nst = 2 * nb;
-    u64 mn = kU64Max, mx = 0;
-    for (;;) {
-        if (tid == 0) {
-            item = atomicAdd(h.work, 1ull);
-            int s0 = 0, s1 = nst;  // stage: largest s with sstart[s] <= item
-            while (s1 - s0 > 1) {
-                const int m = (s0 + s1) >> 1;
-                if (h.sstart[m] <= item) s0 = m;
-                else s1 = m;
-            }
-            ist = s0;
-            ic = h.stage[s0];
-        }
-        __syncthreads();
-        const u64 it = item;
-        const int st = ist, code = ic;
-        __syncthreads();
-        if (it >= h.sstart[nst]) break;
-        const int c = code & 0xffff;
-        const u64 j = it - h.sstart[st];
-        const int g0 = c * SL_FPC;
-        if ((code >> 16) == 0) {
-            // ---- A: fine-partition tile j of coarse bucket c -------------------
-            const int g1 = g0 + SL_FPC < nf ? g0 + SL_FPC : nf;
-            const u64 p0 = h.fbase[g0] + j * SL_TA, pe = h.fbase[g1];
-            const int cnt = (int)(pe - p0 < (u64)SL_TA ? pe - p0 : (u64)SL_TA);
-            for (int i = tid; i < SL_FPC; i += SL_T) hist[i] = 0;
-            int32_t k[SL_E];
-            T v[SL_E];
-#pragma unroll
-            for (int e = 0; e < SL_E; e++) {
-                const int q = e * SL_T + tid;
-                k[e] = q < cnt ? __ldcs(ck + p0 + q) : 0;
-            }
-#pragma unroll
-            for (int e = 0; e < SL_E; e++) {
-                const int q = e * SL_T + tid;
-                if (q < cnt) v[e] = __ldcs(cv + p0 + q);
-            }
-            __syncthreads();
-            int bk[SL_E];
-            unsigned rk[SL_E];
-#pragma unroll
-            for (int e = 0; e < SL_E; e++) {
-                const int q = e * SL_T + tid;
-                bk[e] = q < cnt ? (int)(((int64_t)k[e] - lo) >> fs) - g0 : -1;
-                if (bk[e] >= 0) rk[e] = atomicAdd(&hist[bk[e]], 1u);
-            }
-            __syncthreads();
-            if (tid < 32) warp_exscan(hist, loff, SL_FPC, &total);
-            if (tid < SL_FPC) gbase[tid] = hist[tid] ? atomicAdd(&h.fcur[g0 + tid], (u64)hist[tid]) : 0;
-            __syncthreads();
-#pragma unroll
-            for (int e = 0; e < SL_E; e++)
-                if (bk[e] >= 0) {
-                    const unsigned pos = loff[bk[e]] + rk[e];
-                    sk[pos] = k[e];
-                    sv[pos] = v[e];
-                    sbk[pos] = (uint8_t)bk[e];
-                }
-            __syncthreads();
-            for (int pos = tid; pos < cnt; pos += SL_T) {
-                const int bb = sbk[pos];
-                const u64 g = gbase[bb] + (pos - loff[bb]);
-                fk[g] = sk[pos];
-                fv[g] = sv[pos];
-            }
-            __syncthreads();  // then one cumulative fence + release by thread 0
-            if (tid == 0) {
-                __threadfence();
-                atomicAdd(&h.doneA[c], 1u);
-            }
-        } else {
-            // ---- B: apply fine slice g = g0 + j in shared memory ---------------
-            const int g = g0 + (int)j;
-            const int64_t e0 = lo + ((int64_t)g << fs);
-            const int64_t e1 = e0 + SLN < hi ? e0 + SLN : hi;
-            const int len = (int)(e1 - e0);
-            const u64 q0 = h.fbase[g], q1 = h.fbase[g + 1];
-            const int64_t w0 = e0 >> 5, w1 = (e1 + 31) >> 5;  // bitmap words covering the slice
-            const int nw = (int)(w1 - w0);
-            if (q1 > q0) {
-                // slice -> shared memory: 16-byte cp.async for the aligned
-                // body (no register staging, all in flight at once), scalar
-                // head and tail
-                const int pad = (int)(((uintptr_t)(a + e0) & 15) / sizeof(T));
-                T *sa = reinterpret_cast<T *>(sdyn) + pad;
-                constexpr int V = 16 / sizeof(T);
-                const int head = pad ? V - pad : 0;
-                const int h2 = head < len ? head : len;
-                const int nv = (len - h2) / V;
-                for (int i = tid; i < nv; i += SL_T)
-                    cp_async16(sa + h2 + i * V, a + e0 + h2 + i * V, 16);
-                cp_commit();
-                if (tid < h2) sa[tid] = a[e0 + tid];
-                for (int i = h2 + nv * V + tid; i < len; i += SL_T) sa[i] = a[e0 + i];
-                for (int i = tid; i < nw; i += SL_T) sbits[i] = 0;
-                if (tid == 0) {
-                    const int g1 = g0 + SL_FPC < nf ? g0 + SL_FPC : nf;
-                    const unsigned need =
-                        (unsigned)((h.fbase[g1] - h.fbase[g0] + SL_TA - 1) / SL_TA);
-                    volatile unsigned *d = h.doneA + c;
-                    while (*d < need) __nanosleep(256);
-                    __threadfence();
-                }
-                cp_wait<0>();
-                __syncthreads();
-                const int sh = (int)(e0 & 31);  // bit of element e0 within word w0
-#pragma unroll 8
-                for (u64 p = q0 + tid; p < q1; p += SL_T) {
-                    const int32_t kk = __ldcg(fk + p);
-                    const T vv = __ldcg(fv + p);
-                    const int o = (int)((int64_t)kk - e0);
-                    atomicAdd(&sa[o], vv);
-                    atomicOr(&sbits[(o + sh) >> 5], 1u << ((o + sh) & 31));
-                    mn = (u64)kk < mn ? (u64)kk : mn;
-                    mx = (u64)kk > mx ? (u64)kk : mx;
-                }
-                __syncthreads();
-                for (int i = tid; i < len; i += SL_T) a[e0 + i] = sa[i];
-                for (int i = tid; i < nw; i += SL_T) {
-                    const uint32_t bits = sbits[i];
-                    if (i == 0 || i == nw - 1) {  // words shared with a neighbour slice
-                        if (bits) atomicOr(bitmap + w0 + i, bits);
-                    } else {
-                        bitmap[w0 + i] = bits;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-    }
-    publish_dirty<SL_T / 32>(mn, mx, dirty);
-}
-
 
 // ---------------------------------------------------------------------------
 // NEXT-2  Himeno (19-point stencil + gosa reduction, and the copy loop)
@@ -1873,221 +1566,77 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
 }
 
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
-    ScatterPlan p{false, false, 0, 1, 0, 0, 0, 0, 0};
+    ScatterPlan p{false, 0, 0, 0, 0, 0, 0, 0};
     const int64_t span = hi - lo;
     const char *force = getenv("JACC_SCATTER_BINNED");  // "0" never, "1" always (tests)
     if (span <= 0 || n <= 0 || (force && force[0] == '0')) return p;
     if (!(force && force[0] == '1') && (n < (1 << 22) || span * elem <= (int64_t)96 << 20))
         return p;  // a fits in L2: the direct kernel is already L2-resident
-    // owner-slice apply (BK4c), opt-in with JACC_SCATTER_SLICE=1: measured
-    // slower than the byte-map apply at 2^28, kept as
-    // the L2-atomic-free alternative; needs dense updates (at least one per
-    // 4 elements: the slices of `a` are read and written whole) and a fine
-    // histogram that fits
-    const char *fsl = getenv("JACC_SCATTER_SLICE");
-    int fs = 0;
-    while (((int64_t)elem << fs) < SL_SLICE) fs++;
-    const int64_t nf = (span + ((int64_t)1 << fs) - 1) >> fs;
-    const bool slice = nf <= SL_MAXF && fsl && fsl[0] == '1' && 4 * n >= span;
-    if (slice) {
-        p.binned = p.slice = true;
-        p.fs = fs;
-        p.nf = (int)nf;
-        p.shift = fs + 7;  // SL_FPC = 128 fine slices per coarse bucket
-        p.nb = (int)((nf + SL_FPC - 1) / SL_FPC);
-        const size_t nb = (size_t)p.nb, f = (size_t)nf;
-        p.hdr = ((f + 1) * 8 + f * 8 + nb * 8 + (2 * nb + 1) * 8 + 8 + f * 4 + nb * 4 + 2 * nb * 4 +
-                 255) & ~(size_t)255;
-        const size_t pk = ((size_t)n * 4 + 255) & ~(size_t)255;
-        const size_t pv = ((size_t)n * elem + 255) & ~(size_t)255;
-        p.scratch = p.hdr + 2 * (pk + pv);
-        p.bytemap = 0;
-        return p;
-    }
-    int shift = 0;
-    static int64_t bucket_mb = -1;  // JACC_SCATTER_BUCKET_MB (default 8)
-    if (bucket_mb < 0) {
-        const char *e = getenv("JACC_SCATTER_BUCKET_MB");
-        bucket_mb = e ? std::max(1, atoi(e)) : 8;  // 8 MB: 5.16 ms vs 5.39 (16 MB) at 2^28
-    }
-    while (((int64_t)elem << shift) < (bucket_mb << 20)) shift++;
-    while (((span + ((int64_t)1 << shift) - 1) >> shift) > SB_MAXB) shift++;
+    // buckets of 2^20 elements (8 MiB of fp64, 4 MiB of int32): a bucket's
+    // dirty-bitmap words (128 KiB) fit one apply CTA's shared memory
+    const int shift = 20;
+    const int64_t nb = (span + ((int64_t)1 << shift) - 1) >> shift;
+    if (nb > SB_MAXB) return p;  // > 2^30 owned elements: the direct kernel
     p.binned = true;
     p.shift = shift;
-    p.nb = (int)((span + ((int64_t)1 << shift) - 1) >> shift);
-    const size_t hdr = ((size_t)(3 * p.nb + 2) * 8 + 255) & ~(size_t)255;
-    p.scratch = hdr + (((size_t)n * 4 + 255) & ~(size_t)255) + (size_t)n * elem;
-    // JACC_SCATTER_BYTEMAP=1: dirty bits through the epoch byte-map written
-    // by the apply (the previous default), else the bucket-parallel bits pass
-    const char *bm = getenv("JACC_SCATTER_BYTEMAP");
-    p.bytemap = (bm && bm[0] == '1') ? (size_t)(((hi + 31) >> 5) << 5) : 0;
+    p.nb = (int)nb;
+    p.kmax = (n + PG_P - 1) / PG_P + 1;      // pages one bucket can need
+    p.npool = (n + PG_P - 1) / PG_P + p.nb;  // every bucket: <= 1 partial page
+    // fill u64[nb] | ctr u32[4] | pool u32[4] | dir u32[nb*kmax] || items u64[npool+nb] || pages
+    p.state = ((size_t)p.nb * 8 + 32 + (size_t)p.nb * p.kmax * 4 + 255) & ~(size_t)255;
+    p.hdr = (p.state + (size_t)(p.npool + p.nb) * 8 + 255) & ~(size_t)255;
+    p.scratch = p.hdr + (size_t)p.npool * PG_P * (4 + (size_t)elem);
     return p;
 }
 
-namespace {
-SliceHdr slice_hdr(void *scratch, const ScatterPlan &pl) {
-    char *c = static_cast<char *>(scratch);
-    const size_t f = (size_t)pl.nf, nb = (size_t)pl.nb;
-    SliceHdr h;
-    h.fbase = reinterpret_cast<u64 *>(c);
-    c += (f + 1) * 8;
-    h.fcur = reinterpret_cast<u64 *>(c);
-    c += f * 8;
-    h.ccur = reinterpret_cast<u64 *>(c);
-    c += nb * 8;
-    h.sstart = reinterpret_cast<u64 *>(c);
-    c += (2 * nb + 1) * 8;
-    h.work = reinterpret_cast<u64 *>(c);
-    c += 8;
-    h.fcnt = reinterpret_cast<unsigned *>(c);
-    c += f * 4;
-    h.doneA = reinterpret_cast<unsigned *>(c);
-    c += nb * 4;
-    h.stage = reinterpret_cast<int *>(c);
-    return h;
-}
-
-template <typename T>
-cudaError_t scatter_slice(cudaStream_t s, const int32_t *idx, const T *b, T *a, int64_t n,
-                          int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty,
-                          const ScatterPlan &pl, void *scratch) {
-    SliceHdr h = slice_hdr(scratch, pl);
-    char *sc = static_cast<char *>(scratch) + pl.hdr;
-    const size_t pk = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t pv = ((size_t)n * sizeof(T) + 255) & ~(size_t)255;
-    int32_t *ck = reinterpret_cast<int32_t *>(sc);
-    T *cv = reinterpret_cast<T *>(sc + pk);
-    int32_t *fk = reinterpret_cast<int32_t *>(sc + pk + pv);
-    T *fv = reinterpret_cast<T *>(sc + 2 * pk + pv);
-    cudaError_t e = cudaMemsetAsync(h.fcnt, 0, (size_t)pl.nf * 4, s);
-    if (e != cudaSuccess) return e;
-    // attributes are per device: set on every call (host-side, cheap)
-    cudaFuncSetAttribute(scat_fhist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SL_MAXF * 4);
-    const int pdsm = SB_T * 16 * (int)(sizeof(T) + 4);
-    cudaFuncSetAttribute(scat_part_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-    const int sdyn = SL_SLICE + 16 + (int)(SL_SLICE / sizeof(T) / 32 + 2) * 4;
-    e = cudaFuncSetAttribute(scat_slice_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sdyn);
+cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
+                               void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
+                               u64 *dirty, const ScatterPlan &pl, void *scratch) {
+    char *sc = static_cast<char *>(scratch);
+    u64 *fill = reinterpret_cast<u64 *>(sc);
+    unsigned *ctr = reinterpret_cast<unsigned *>(sc + (size_t)pl.nb * 8);
+    unsigned *pool = ctr + 4;
+    unsigned *dir = ctr + 8;
+    u64 *items = reinterpret_cast<u64 *>(sc + pl.state);
+    int32_t *pk = reinterpret_cast<int32_t *>(sc + pl.hdr);
+    char *pv = sc + pl.hdr + (size_t)pl.npool * PG_P * 4;
+    // the partition state starts zeroed (the items kernel re-zeroes what a
+    // launch used; the memset keeps it exact whatever earlier launches of
+    // another layout left in the scratch)
+    cudaError_t e = cudaMemsetAsync(sc, 0, pl.state, s);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
-    scat_fhist_kernel<<<nsm, 1024, pl.nf * 4, s>>>(idx, n, lo, hi, pl.fs, pl.nf, h.fcnt);
-    scat_fscan_kernel<<<1, 1024, 0, s>>>(h, pl.nf, pl.nb);
-    const int64_t tile = (int64_t)SB_T * 16;
-    const int64_t tiles = (n + tile - 1) / tile;
-    const int pg = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
-    scat_part_kernel<T, 16><<<pg, SB_T, pdsm, s>>>(idx, b, n, lo, hi, pl.shift, pl.nb, h.ccur, ck, cv);
-    scat_slice_kernel<T><<<2 * nsm, SL_T, sdyn, s>>>(h, pl.nb, pl.nf, pl.fs, lo, hi, ck, cv, fk, fv, a,
-                                                 bitmap, dirty);
-    return cudaGetLastError();
-}
-}  // namespace
-
-cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
-                               void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
-                               u64 *dirty, const ScatterPlan &pl, void *scratch, uint8_t *bytemap,
-                               uint8_t epoch) {
-    if (pl.slice)
-        return is_f64 ? scatter_slice<double>(s, idx, static_cast<const double *>(b),
-                                              static_cast<double *>(a), n, lo, hi, bitmap, dirty, pl,
-                                              scratch)
-                      : scatter_slice<int32_t>(s, idx, static_cast<const int32_t *>(b),
-                                               static_cast<int32_t *>(a), n, lo, hi, bitmap, dirty,
-                                               pl, scratch);
-    char *sc = static_cast<char *>(scratch);
-    u64 *counts = reinterpret_cast<u64 *>(sc);
-    u64 *cursor = counts + pl.nb;
-    u64 *base = cursor + pl.nb;  // nb + 1
-    u64 *work = base + pl.nb + 1;
-    const size_t hdr = ((size_t)(3 * pl.nb + 2) * 8 + 255) & ~(size_t)255;
-    int32_t *pidx = reinterpret_cast<int32_t *>(sc + hdr);
-    char *pv = sc + hdr + (((size_t)n * 4 + 255) & ~(size_t)255);
-    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)pl.nb * 8, s);
-    if (e != cudaSuccess) return e;
-    scat_hist_kernel<<<148 * 8, 256, 0, s>>>(idx, n, lo, hi, pl.shift, pl.nb, counts);
-    scat_scan_kernel<<<1, 1024, 0, s>>>(counts, pl.nb, base, cursor, work);
-    // partition elements per thread (JACC_SCATTER_PART_E: 8, 12 or 16);
-    // 16 measured best (tools/tune_scatter.py: 5.51 ms vs 5.76 ms for 8)
-    static int pe = -1;
-    if (pe < 0) {
-        const char *e = getenv("JACC_SCATTER_PART_E");
-        pe = e ? atoi(e) : 16;
-        if (pe != 8 && pe != 12) pe = 16;
-    }
-    const int64_t tile = (int64_t)SB_T * pe;
-    const int64_t tiles = (n + tile - 1) / tile;
-    const size_t dsm = (size_t)tile * ((is_f64 ? 8 : 4) + 4);
-    static int pbps = -1;  // partition CTAs per SM in the grid (JACC_SCATTER_PART_BPS)
-    if (pbps < 0) {
-        const char *e = getenv("JACC_SCATTER_PART_BPS");
-        pbps = e ? std::max(1, std::min(16, atoi(e))) : 8;
-    }
-    const int pg = (int)(tiles < 148 * pbps ? tiles : 148 * pbps);
-#define PART_LAUNCH(T, E)                                                                          \
-    do {                                                                                           \
-        /* always: dynamic + 16 KB static smem may pass the 48 KB default */                      \
-            cudaFuncSetAttribute(scat_part_kernel<T, E>,                                           \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);           \
-        scat_part_kernel<T, E><<<pg, SB_T, dsm, s>>>(idx, static_cast<const T *>(b), n, lo, hi,    \
-                                                     pl.shift, pl.nb, cursor, pidx,                \
-                                                     reinterpret_cast<T *>(pv));                   \
-    } while (0)
-#define PART_E(T)                                                                                  \
-    do {                                                                                           \
-        if (pe == 12) PART_LAUNCH(T, 12);                                                          \
-        else if (pe == 16) PART_LAUNCH(T, 16);                                                     \
-        else PART_LAUNCH(T, 8);                                                                    \
-    } while (0)
-    // dirty bits: a bucket-parallel pass over the partitioned keys
-    // (default), or the epoch byte-map written by the apply and packed
-    // (JACC_SCATTER_BYTEMAP=1, or when no byte-map exists)
-    const bool use_bytemap = pl.bytemap && bytemap;
-    // apply chunk and CTAs per SM (JACC_SCATTER_APPLY_CH, JACC_SCATTER_APPLY_BPS)
-    static int ach = -1, abps = -1;
-    if (ach < 0) {
-        const char *e1 = getenv("JACC_SCATTER_APPLY_CH"), *e2 = getenv("JACC_SCATTER_APPLY_BPS");
-        ach = e1 ? std::max(256, atoi(e1)) : SA_CH;
-        abps = e2 ? std::max(1, std::min(8, atoi(e2))) : 3;  // 3: 4.17 ms vs 5.1 ms at 8 (fewer chunks in flight)
-    }
-    const int ag = 148 * abps;
+    const int64_t tiles = (n + (int64_t)SB_T * SB_E - 1) / ((int64_t)SB_T * SB_E);
+    const int pg = (int)std::min<int64_t>(tiles, (int64_t)nsm * 8);
+    const int esz = is_f64 ? 8 : 4;
+    const int pdsm = SB_T * SB_E * (esz + 4);
+    const int adsm = (int)((((int64_t)1 << pl.shift) >> 5) + 2) * 4;
+    // attributes are per device: set on every call (host-side, cheap)
     if (is_f64) {
-        PART_E(double);
-        if (use_bytemap)
-            scat_apply_kernel<double, true><<<ag, 256, 0, s>>>(
-                pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
-                static_cast<double *>(a), bytemap, epoch, dirty, ach);
-        else
-            scat_apply_kernel<double, false><<<ag, 256, 0, s>>>(
-                pidx, reinterpret_cast<const double *>(pv), base, pl.nb, work,
-                static_cast<double *>(a), bytemap, epoch, dirty, ach);
+        cudaFuncSetAttribute(scat_part_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+        cudaFuncSetAttribute(scat_apply_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, adsm);
+        scat_part_kernel<double><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo, hi,
+                                                        pl.shift, pl.nb, (int)pl.kmax, fill, pool, dir,
+                                                        pk, reinterpret_cast<double *>(pv));
     } else {
-        PART_E(int32_t);
-        if (use_bytemap)
-            scat_apply_kernel<int32_t, true><<<ag, 256, 0, s>>>(
-                pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
-                static_cast<int32_t *>(a), bytemap, epoch, dirty, ach);
-        else
-            scat_apply_kernel<int32_t, false><<<ag, 256, 0, s>>>(
-                pidx, reinterpret_cast<const int32_t *>(pv), base, pl.nb, work,
-                static_cast<int32_t *>(a), bytemap, epoch, dirty, ach);
+        cudaFuncSetAttribute(scat_part_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+        cudaFuncSetAttribute(scat_apply_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, adsm);
+        scat_part_kernel<int32_t><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo, hi,
+                                                         pl.shift, pl.nb, (int)pl.kmax, fill, pool, dir,
+                                                         pk, reinterpret_cast<int32_t *>(pv));
     }
-#undef PART_E
-#undef PART_LAUNCH
-    if (use_bytemap) {
-        scat_pack_kernel<<<148 * 8, 256, 0, s>>>(bytemap, epoch, lo, hi, bitmap);
-    } else {
-        const int pb = pl.shift > SBITS_LB ? SBITS_LB : pl.shift;
-        const int smem = (int)((((int64_t)1 << pb) >> 5) + 2) * 4;
-        cudaFuncSetAttribute(scat_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        const int64_t items = (int64_t)pl.nb << (pl.shift - pb);
-        int dev = 0, nsm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nsm <= 0) nsm = 148;
-        const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
-        scat_bits_kernel<<<g, 1024, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap);
-    }
+    scat_items_kernel<<<1, 1024, 0, s>>>(fill, pool, dir, pl.nb, (int)pl.kmax, items, ctr);
+    if (is_f64)
+        scat_apply_kernel<double><<<nsm, SA_T, adsm, s>>>(items, ctr, pk, reinterpret_cast<const double *>(pv),
+                                                          static_cast<double *>(a), lo, hi, pl.shift,
+                                                          bitmap, dirty);
+    else
+        scat_apply_kernel<int32_t><<<nsm, SA_T, adsm, s>>>(items, ctr, pk, reinterpret_cast<const int32_t *>(pv),
+                                                           static_cast<int32_t *>(a), lo, hi, pl.shift,
+                                                           bitmap, dirty);
     return cudaGetLastError();
 }
 

@@ -60,35 +60,29 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
                             int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty);
 
 // BK4b Same loop, executed as a destination-binned pipeline for arrays far
-// larger than L2: (1) histogram of owned updates per 8 MiB bucket of a,
-// (2) scan, (3) stable-per-CTA partition of (k, b[i]) pairs into bucket
-// order through shared memory (coalesced writes), (4) apply the pairs
-// bucket by bucket, so the read-modify-writes of a hit L2 and every line of
-// a moves to/from HBM about once.  Write tracking (bitmap + range) is fused
-// into (4).  is_f64: T = double, else int32.
-//
-// BK4c Owner-slice apply (opt-in: JACC_SCATTER_SLICE=1, dense updates; measured
-// slower than BK4b at 2^28): the partition above
-// into 16 MiB coarse buckets, then one persistent kernel whose work queue
-// interleaves A items (fine-partition 4096 pairs of a coarse bucket into its
-// 128 slices of 128 KB) and B items (one CTA loads a slice of a into shared
-// memory, adds the slice's updates there -- shared-memory atomics instead of
-// L2 atomics -- sets the slice's dirty bits in shared memory and writes the
-// slice and its bitmap words back).  No byte-map.
+// larger than L2, in one pass over the updates: (1) partition the owned
+// (k, b[i]) pairs into buckets of 2^shift elements of a (shared-memory
+// staging, bucket-contiguous writes) into pages of 8192 pairs that each
+// bucket claims from a pool as its stream grows (no histogram pass); (2) a
+// one-block kernel lists the pages bucket by bucket; (3) one persistent
+// kernel applies the pages in that order, so the read-modify-writes of a hit
+// L2 and every line of a moves to/from HBM about once, and after each
+// bucket rebuilds its dirty-bitmap words in shared memory from the bucket's
+// keys while they are still in L2 (no extra HBM pass).  Dirty range fused.
+// is_f64: T = double, else int32.  The scratch's state region is zeroed by
+// the wrapper on every call.
 struct ScatterPlan {
     bool binned;
-    bool slice;       // BK4c owner-slice apply
-    int shift, nb;    // coarse bucket = 2^shift elements, nb buckets
-    size_t scratch;   // bytes of pair scratch
-    size_t bytemap;   // bytes of the epoch byte-map (elements of a, rounded to 32; 0 = none)
-    int fs, nf;       // BK4c: slice = 2^fs elements, nf slices
-    size_t hdr;       // BK4c: header bytes at the start of the scratch
+    int shift, nb;      // bucket = 2^shift elements, nb buckets
+    int64_t kmax;       // page-directory entries per bucket
+    int64_t npool;      // pages in the pool
+    size_t state, hdr;  // bytes: zeroed state | + item list (pages follow)
+    size_t scratch;     // total scratch bytes
 };
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem);
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
-                               u64 *dirty, const ScatterPlan &pl, void *scratch, uint8_t *bytemap,
-                               uint8_t epoch);
+                               u64 *dirty, const ScatterPlan &pl, void *scratch);
 
 // NEXT-2  Himeno benchmark (DESIGN R-17), fp32, row-major
 // [I][J][K] arrays (a: 4, b and c: 3 stacked arrays).  Stencil loop over

@@ -432,16 +432,6 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 if (cudaMalloc(&dv.scratch, sp.scratch) == cudaSuccess) dv.scratch_bytes = sp.scratch;
                 else cudaGetLastError();
             }
-            const size_t bmap = (size_t)((W->nelem + 31) / 32) * 32;  // whole region
-            if (sp.bytemap && !W->bytemap[d]) {
-                if (cudaMalloc(&W->bytemap[d], bmap) == cudaSuccess) {
-                    CK(cudaMemsetAsync(W->bytemap[d], 0, bmap, dv.s));
-                    W->epoch[d] = 0;
-                } else {
-                    W->bytemap[d] = nullptr;
-                    cudaGetLastError();
-                }
-            }
         }
     }
     // ---- NEXT-3 phase 1: every device scatters its iteration block into its
@@ -635,29 +625,12 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 const char *b = L.a[1].reg->rep[d] + (L.a[1].off + p.i0) * (int64_t)W->elem;
                 const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
                 jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
-                // the epoch byte-map state is host-side: no byte-map path in a
-                // captured graph (the default bits pass and the owner-slice
-                // path have none, and run captured when their scratch was
-                // reserved before the capture)
-                if (R.capturing && sp.bytemap) sp.binned = false;
                 if (R.nq > 1) sp.binned = false;     // per-device scratch is not per queue
-                if (sp.binned && (dv.scratch_bytes < sp.scratch || (sp.bytemap && !W->bytemap[d])))
+                if (sp.binned && dv.scratch_bytes < sp.scratch)
                     sp.binned = false;  // scratch could not be reserved up front: direct kernel
-                if (sp.binned && sp.slice) {
+                if (sp.binned) {
                     CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
-                                              drec, sp, dv.scratch, nullptr, 0));
-                } else if (sp.binned && !sp.bytemap) {
-                    CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
-                                              drec, sp, dv.scratch, nullptr, 0));
-                } else if (sp.binned) {
-                    if (W->epoch[d] == 255) {  // wrap: clear stale epochs
-                        CK(cudaMemsetAsync(W->bytemap[d], 0, (size_t)((W->nelem + 31) / 32) * 32, dv.s));
-                        W->epoch[d] = 0;
-                    }
-                    W->epoch[d]++;
-                    CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
-                                              drec, sp, dv.scratch, W->bytemap[d],
-                                              W->epoch[d]));
+                                              drec, sp, dv.scratch));
                 } else if (f64) {
                     CK(jk::scatter_add_f64(dv.s, ix, reinterpret_cast<const double *>(b),
                                            reinterpret_cast<double *>(W->rep[d]), p.i1 - p.i0, lo,

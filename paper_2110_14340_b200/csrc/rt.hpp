@@ -269,10 +269,8 @@ struct Region {
     std::vector<u64 *> dirty;          // per device: 2 slots of [min, ~max] (32 B)
     std::vector<int> dslot;            // per device: slot of the most recent launch
     std::vector<uint32_t *> bitmap;    // per device, lazily allocated
-    std::vector<uint8_t *> bytemap;    // per device epoch byte-map (binned scatter)
     std::vector<char *> delta;         // per device delta array (iteration-split scatter)
     std::vector<uint32_t *> dbm;       // per device delta bitmap
-    std::vector<uint8_t> epoch;
     std::vector<IntervalSet> valid;    // per device
 };
 
@@ -513,7 +511,6 @@ inline void free_region(Region *r) {
         if (r->rep[d]) cudaFree(r->rep[d]);
         if (r->dirty[d]) cudaFree(r->dirty[d]);
         if (r->bitmap[d]) cudaFree(r->bitmap[d]);
-        if (r->bytemap[d]) cudaFree(r->bytemap[d]);
         if (r->delta[d]) cudaFree(r->delta[d]);
         if (r->dbm[d]) cudaFree(r->dbm[d]);
     }

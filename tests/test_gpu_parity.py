@@ -518,17 +518,14 @@ def test_scatter_permutation_exact(J):
     assert np.array_equal(a, ref)
 
 
-@pytest.mark.parametrize("binned,slice_,bytemap", [("0", "0", "0"), ("1", "0", "0"),
-                                                   ("1", "0", "1"), ("1", "1", "0")])
+@pytest.mark.parametrize("binned", ["0", "1"])
 @pytest.mark.parametrize("n", [1, 3])
 @pytest.mark.parametrize("lo", [0, 1, 2, 3, 5])
-def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, slice_, bytemap, n, lo):
-    """Direct, destination-binned (dirty bits by the bucket pass, or by the
-    byte-map) and owner-slice scatter pipelines, iteration ranges starting
-    at any element (int4 head/tail handling)."""
+def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, n, lo):
+    """Direct and destination-binned (paged partition, apply with the bits
+    items) scatter, iteration ranges starting at any element (int4
+    head/tail handling)."""
     monkeypatch.setenv("JACC_SCATTER_BINNED", binned)
-    monkeypatch.setenv("JACC_SCATTER_SLICE", slice_)
-    monkeypatch.setenv("JACC_SCATTER_BYTEMAP", bytemap)
     N, M = 30_011, 4099
     idx = synth.index_i32(N, M, 75, 5)
     b = synth.dyadic_f64(N, 75, 6)
@@ -551,16 +548,11 @@ def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, slice_, byt
     assert np.array_equal(a, ref)
 
 
-@pytest.mark.parametrize("slice_,bytemap", [("0", "0"), ("0", "1"), ("1", "0")])
 @pytest.mark.parametrize("dtype", ["f64", "i32"])
 @pytest.mark.parametrize("n", [1, 2, 3])
-def test_scatter_binned_large(J, monkeypatch, dtype, n, slice_, bytemap):
-    """Arrays larger than L2 take the binned pipeline by default (dirty bits
-    by the bucket pass; the byte-map with JACC_SCATTER_BYTEMAP=1; the
-    owner-slice apply with JACC_SCATTER_SLICE=1); n=3 gives owned spans off
-    word and bucket boundaries."""
-    monkeypatch.setenv("JACC_SCATTER_SLICE", slice_)
-    monkeypatch.setenv("JACC_SCATTER_BYTEMAP", bytemap)
+def test_scatter_binned_large(J, dtype, n):
+    """Arrays larger than L2 take the binned pipeline by default; n=3 gives
+    owned spans off word and bucket boundaries."""
     M = 2**25 if dtype == "f64" else 2**26
     N = 2**23
     idx = synth.index_i32(N, M, 76, 5)
@@ -581,12 +573,12 @@ def test_scatter_binned_large(J, monkeypatch, dtype, n, slice_, bytemap):
 
 @pytest.mark.parametrize("dtype", ["f64", "i32"])
 @pytest.mark.parametrize("n", [1, 3, 8])
-def test_scatter_slice_ragged(J, monkeypatch, dtype, n):
-    """Owner-slice pipeline over several coarse buckets with a ragged last
-    bucket and slice, owned spans starting off word boundaries (n=3, 8),
-    skewed index mix (a hot band plus uniform), exact inputs."""
+def test_scatter_binned_ragged_skewed(J, monkeypatch, dtype, n):
+    """Binned pipeline over several buckets with a ragged last bucket,
+    owned spans starting off word boundaries (n=3, 8) and a skewed index mix
+    (a hot band holding a quarter of the updates: one bucket claims many
+    more pages than the others), exact inputs."""
     monkeypatch.setenv("JACC_SCATTER_BINNED", "1")
-    monkeypatch.setenv("JACC_SCATTER_SLICE", "1")
     M = 3 * 2**21 + 777 if dtype == "f64" else 3 * 2**22 + 777
     N = 2**22 + 3
     idx = synth.index_i32(N, M, 79, 5)
@@ -596,6 +588,34 @@ def test_scatter_slice_ragged(J, monkeypatch, dtype, n):
         b, a0 = synth.dyadic_f64(N, 79, 6), synth.dyadic_f64(M, 79, 7)
     else:
         b, a0 = synth.int_i32(N, -1000, 1000, 79, 6), synth.int_i32(M, -10**6, 10**6, 79, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, bms, drs, reps = _scatter(J, idx, b, a0, n)
+    assert np.array_equal(a, ref)
+    for d in range(n):
+        lo, hi = orc.partition(M, n, d)
+        bm, mn, mx = orc.scatter_add_filtered(idx, b, a0.copy(), lo, hi - 1)
+        assert np.array_equal(bms[d], bm) and drs[d] == (mn, mx)
+        assert np.array_equal(reps[d], ref)
+
+
+@pytest.mark.parametrize("case", ["one_bucket", "one_element", "empty_owned"])
+@pytest.mark.parametrize("n", [1, 2])
+def test_scatter_binned_extreme_skew(J, monkeypatch, case, n):
+    """Page allocation under extreme skew: every update in one bucket (a
+    single bucket claims every page of the pool), every update on ONE
+    element (maximum collisions; int32 exact), and updates that miss a
+    device's slice entirely (empty buckets, no bits items)."""
+    monkeypatch.setenv("JACC_SCATTER_BINNED", "1")
+    N, M = 3_000_017, 5 * 2**20 + 3
+    if case == "one_bucket":
+        idx = synth.index_i32(N, 2**20, 116, 5) + np.int32(2**21)
+    elif case == "one_element":
+        idx = np.full(N, 2**21 + 7, dtype=np.int32)
+    else:
+        idx = synth.index_i32(N, 2**20, 116, 5)   # all in device 0's slice
+    b = synth.int_i32(N, -1000, 1000, 116, 6)
+    a0 = synth.int_i32(M, -10**6, 10**6, 116, 7)
     ref = a0.copy()
     orc.scatter_add(idx, b, ref)
     a, bms, drs, reps = _scatter(J, idx, b, a0, n)

@@ -52,17 +52,52 @@ def main():
             J.jacc_update_device(a)
         for _ in range(reps):
             J.jacc_launch(J.JACC_LOOP_GEMM_F64, None, [J.arg(IN, A), J.arg(IN, B), J.arg(OUT, C)], 0)
-    elif which == "scatter":
+    elif which in ("scatter", "scatter_i32"):
         S = 2**28
         idx = synth.index_i32(S, S, 3, 5)
-        b = synth.dyadic_f64(S, 3, 6)
-        a = synth.dyadic_f64(S, 3, 7)
+        if which == "scatter":
+            b, a, loop = synth.dyadic_f64(S, 3, 6), synth.dyadic_f64(S, 3, 7), J.JACC_LOOP_SCATTER_ADD_F64
+        else:
+            b = synth.int_i32(S, -1000, 1000, 3, 6)
+            a = synth.int_i32(S, -10**6, 10**6, 3, 7)
+            loop = J.JACC_LOOP_SCATTER_ADD_I32
         for arr in (idx, b, a):
             J.jacc_data_create(arr)
             J.jacc_update_device(arr)
         for _ in range(reps):
-            J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, J.make_range(0, S),
-                          [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)], 0)
+            J.jacc_launch(loop, J.make_range(0, S), [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)], 0)
+    elif which == "merge":
+        # BK5 in isolation: two virtual devices, EAGER, loop restricted to
+        # device 0's block (device 1 idle): merge_range_kernel, then the
+        # dense and sparse merge_bitmap_kernel
+        J.jacc_set_merge_policy(J.JACC_MERGE_EAGER)
+        N = 16384
+        A, B = synth.polybench_jacobi2d(N)
+        for a in (A, B):
+            J.jacc_data_create(a)
+            J.jacc_update_device(a)
+        lo, hi = J.jacc_partition(N, n, 0)
+        for _ in range(reps):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, J.make_range((lo + 1, 1), (hi, N - 1)),
+                          [J.arg(IN, A), J.arg(OUT, B)], 0)
+        J.jacc_wait()
+        J.jacc_data_delete(A)
+        J.jacc_data_delete(B)
+        del A, B
+        M = 2**28
+        for nupd in (2**27, 2**20):
+            idx = synth.index_i32(nupd, M // 2, 4, 5)
+            b = synth.dyadic_f64(nupd, 4, 6)
+            a = synth.dyadic_f64(M, 4, 7)
+            for arr in (idx, b, a):
+                J.jacc_data_create(arr)
+                J.jacc_update_device(arr)
+            for _ in range(reps):
+                J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, J.make_range(0, nupd),
+                              [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)], 0)
+            J.jacc_wait()
+            for arr in (idx, b, a):
+                J.jacc_data_delete(arr)
     elif which == "himeno":
         I, Jd, K = 1025, 513, 513
         arrs = synth.himeno_init(I, Jd, K)
