@@ -583,11 +583,14 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
 // while its keys are still L2-resident.
 // ---------------------------------------------------------------------------
 constexpr int SB_T = 256;        // partition CTA; tile = SB_T * SB_E updates
-constexpr int SB_E = 16;
+constexpr int SB_E = 8;
+constexpr int SB_MINB = 4;       // partition CTAs per SM (registers, shared memory)
 constexpr int SB_MAXB = 1024;    // max buckets
 constexpr int PG_LOG = 13;       // pairs per page = 8192 (>= a tile: a tile's
 constexpr int PG_P = 1 << PG_LOG;  //  bucket segment spans at most two pages)
 constexpr int SA_T = 1024;       // apply CTA (one per SM)
+constexpr int SA_B = 4;          // work items per dequeue
+constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;  // buckets per thread in the reservation
 static_assert(SB_T * SB_E <= PG_P, "a tile segment must fit in two pages");
 
 // warp 0 computes the exclusive scan of hist[0..nb) into off[]
@@ -614,29 +617,38 @@ __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off,
     if (lane == 31) *total = inc;
 }
 
+// shared-memory layout of the partition: per-bucket state sized by nb
+__host__ __device__ constexpr size_t part_smem(int nb, int esz) {
+    return (size_t)nb * 8 + (size_t)((nb + 1) & ~1) * 16 + (size_t)SB_T * SB_E * (esz + 4);
+}
+
 // Partition.  Per tile of SB_T*SB_E updates: keys (then the values of the
 // owned ones) into registers, per-bucket ranks by shared-memory atomics,
-// warp scan, then one thread per non-empty bucket reserves the tile's
-// segment of the bucket's stream (atomicAdd on fill[b]) and claims from the
-// pool every page whose first slot falls inside the segment, publishing it
-// in dir[b*kmax + k] (page id + 1).  The page holding the segment's first
-// slot, when it starts before the segment, was claimed by the CTA that
-// reserved that slot; its reservation precedes ours and it publishes right
-// after reserving (before any wait of its own), so the wait below always
-// ends.  The pairs are staged in bucket order in shared memory and written
-// out bucket-contiguously.
+// warp scan; one thread per non-empty bucket reserves the tile's segment of
+// the bucket's stream (atomicAdd on fill[b], issued before the staging so
+// its round trip overlaps it) and claims from the pool every page whose
+// first slot falls inside the segment, publishing it in dir[b*kmax + k]
+// (page id + 1).  The page holding the segment's first slot, when it starts
+// before the segment, was claimed by the CTA that reserved that slot; its
+// reservation precedes ours and it publishes right after its reservation
+// returns (before any wait of its own), so the wait below always ends.
+// Pairs are staged in bucket order in shared memory and written out
+// bucket-contiguously.  Several small CTAs per SM keep loads of one tile in
+// flight while others stage or wait on their reservation.
 template <typename T>
-__global__ void __launch_bounds__(SB_T) scat_part_kernel(
+__global__ void __launch_bounds__(SB_T, SB_MINB) scat_part_kernel(
     const int32_t *__restrict__ idx, const T *__restrict__ b, int64_t n, int64_t lo, int64_t hi,
     int shift, int nb, int kmax, u64 *fill, unsigned *pool, unsigned *dir,
     int32_t *__restrict__ pk, T *__restrict__ pv) {
     constexpr int E = SB_E, TILE = SB_T * E;
-    __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB], gp0[SB_MAXB], gp1[SB_MAXB];
-    __shared__ u64 gv0[SB_MAXB];
+    extern __shared__ __align__(16) unsigned char sdyn[];
+    u64 *gv0 = reinterpret_cast<u64 *>(sdyn);
+    const int nb2 = (nb + 1) & ~1;
+    unsigned *hist = reinterpret_cast<unsigned *>(sdyn + (size_t)nb * 8);
+    unsigned *loff = hist + nb2, *gp0 = loff + nb2, *gp1 = gp0 + nb2;
+    T *sv = reinterpret_cast<T *>(gp1 + nb2);
+    int32_t *sk = reinterpret_cast<int32_t *>(sv + TILE);
     __shared__ unsigned total;
-    extern __shared__ __align__(16) unsigned char sdyn[];  // [TILE] T, [TILE] i32
-    T *sv = reinterpret_cast<T *>(sdyn);
-    int32_t *sk = reinterpret_cast<int32_t *>(sdyn + TILE * sizeof(T));
     const int tid = threadIdx.x;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -660,32 +672,15 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(
             if (k[j] >= lo && k[j] < hi) rk[j] = atomicAdd(&hist[(int)(((int64_t)k[j] - lo) >> shift)], 1u);
         __syncthreads();
         if (tid < 32) warp_exscan(hist, loff, nb, &total);
-        // reserve + claim (no waiting), then resolve the first page (may wait)
-        for (int i = tid; i < nb; i += SB_T) {
-            const unsigned c = hist[i];
-            if (!c) continue;
-            const u64 v0 = atomicAdd(&fill[i], (u64)c);
-            const u64 k0 = v0 >> PG_LOG, k1 = (v0 + c - 1) >> PG_LOG;
-            unsigned p0 = 0, p1 = 0;
-            for (u64 kk = k0; kk <= k1; kk++)
-                if ((kk << PG_LOG) >= v0) {
-                    const unsigned pid = atomicAdd(pool, 1u) + 1u;
-                    atomicExch(&dir[(size_t)i * kmax + kk], pid);
-                    if (kk == k0) p0 = pid;
-                    else p1 = pid;
-                }
-            gv0[i] = v0;
-            gp0[i] = p0;
-            gp1[i] = p1;
+        // reserve now; the results are consumed after the staging
+        u64 v0[SB_RES];
+#pragma unroll
+        for (int r = 0; r < SB_RES; r++) {
+            const int i = tid + r * SB_T;
+            const unsigned c = i < nb ? hist[i] : 0u;
+            v0[r] = c ? atomicAdd(&fill[i], (u64)c) : 0;
         }
-        for (int i = tid; i < nb; i += SB_T) {
-            if (!hist[i] || gp0[i]) continue;
-            unsigned *d = dir + (size_t)i * kmax + (gv0[i] >> PG_LOG);
-            unsigned p;
-            while ((p = atomicOr(d, 0u)) == 0) __nanosleep(64);  // read at L2
-            gp0[i] = p;
-        }
-        __syncthreads();
+        __syncthreads();  // loff
 #pragma unroll
         for (int j = 0; j < E; j++)
             if (k[j] >= lo && k[j] < hi) {
@@ -693,6 +688,29 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(
                 sk[pos] = k[j];
                 sv[pos] = v[j];
             }
+        // claim (no waiting), then resolve the first page (may wait)
+#pragma unroll
+        for (int r = 0; r < SB_RES; r++) {
+            const int i = tid + r * SB_T;
+            const unsigned c = i < nb ? hist[i] : 0u;
+            if (!c) continue;
+            const u64 k0 = v0[r] >> PG_LOG, k1 = (v0[r] + c - 1) >> PG_LOG;
+            unsigned p0 = 0, p1 = 0;
+            for (u64 kk = k0; kk <= k1; kk++)
+                if ((kk << PG_LOG) >= v0[r]) {
+                    const unsigned pid = atomicAdd(pool, 1u) + 1u;
+                    atomicExch(&dir[(size_t)i * kmax + kk], pid);
+                    if (kk == k0) p0 = pid;
+                    else p1 = pid;
+                }
+            gv0[i] = v0[r];
+            gp1[i] = p1;
+            if (!p0) {
+                unsigned *d = dir + (size_t)i * kmax + k0;
+                while ((p0 = atomicOr(d, 0u)) == 0) __nanosleep(64);  // read at L2
+            }
+            gp0[i] = p0;
+        }
         __syncthreads();
         const unsigned cnt = total;
         for (unsigned pos = tid; pos < cnt; pos += SB_T) {
@@ -708,126 +726,134 @@ __global__ void __launch_bounds__(SB_T) scat_part_kernel(
     }
 }
 
-// One block: the apply's work list.  For every non-empty bucket b, in
-// order, its pages (apply item = page id << 16 | pairs-1) then one bits item
-// (IT_BITS | b << 32 | page count).  Also clears the fill/pool/dir state for
-// the next launch and zeroes the apply's work counter; ctr[1] = item count.
-constexpr u64 IT_BITS = 1ull << 63;
-__global__ void __launch_bounds__(1024) scat_items_kernel(u64 *fill, unsigned *pool, unsigned *dir,
-                                                          int nb, int kmax, u64 *items,
-                                                          unsigned *ctr) {
-    __shared__ unsigned wsum[32];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    // buckets per thread: nb <= 1024
-    const u64 c = t < nb ? fill[t] : 0;
-    const unsigned np = (unsigned)((c + PG_P - 1) >> PG_LOG);
-    const unsigned own = np ? np + 1 : 0;  // pages + the bits item
-    unsigned inc = own;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-    }
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        const unsigned x = wsum[lane];
-        unsigned y = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned v = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += v;
-        }
-        wsum[lane] = y - x;
-    }
-    __syncthreads();
-    const unsigned base = wsum[w] + inc - own;
-    if (t < nb && np) {
-        for (unsigned k = 0; k < np; k++) {
-            unsigned *e = dir + (size_t)t * kmax + k;
-            const unsigned pid = *e - 1u;
-            *e = 0;
-            const u64 cnt = (k + 1 < np) ? (u64)PG_P : c - ((u64)k << PG_LOG);
-            items[base + k] = ((u64)pid << 16) | (cnt - 1);
-        }
-        items[base + np] = IT_BITS | ((u64)t << 32) | np;
-        fill[t] = 0;
-    }
-    if (t == nb - 1) ctr[1] = base + own;  // number of items
-    if (t == 0) {
-        *pool = 0;
-        ctr[0] = 0;  // work counter
-    }
-}
-
-// Apply (persistent, one CTA of SA_T threads per SM, items from a dynamic
-// counter in list order).  Apply item: a[k] += v for the page's pairs (L2
-// atomics; the buckets in flight are L2-resident).  Bits item of bucket b:
-// the bucket's keys (just applied, still in L2) set bits of a shared-memory
-// copy of the bucket's bitmap words, which are then written out once
-// (plain stores; the first/last word of a bucket may be shared with the
-// neighbour bucket when lo is not 32-aligned: atomicOr into the zeroed
-// bitmap).  Dirty range: min/max over the applied keys.
+// Apply (persistent, one CTA of SA_T threads per SM).  Work items, in list
+// order: for every non-empty bucket b, its pages, then one bits item.  Each
+// CTA derives the list from fill[] (a block scan into shared memory) and
+// maps a dequeued item to (bucket, page) by binary search; page ids come from
+// the partition's directory.  Apply item: a[k] += v for the page's pairs (L2
+// atomics; the bucket in flight is L2-resident; keys are loaded with the
+// default policy so they stay in L2 for the bits item).  Bits item: the
+// bucket's keys, still L2-resident, set bits of a shared-memory copy of the
+// bucket's dirty-bitmap words, written out once (plain stores; a bucket's
+// first/last word may be shared with its neighbour when lo is not
+// 32-aligned: atomicOr into the zeroed bitmap).  Dirty range: min/max over
+// the applied keys.
 template <typename T>
 __global__ void __launch_bounds__(SA_T, 1) scat_apply_kernel(
-    const u64 *__restrict__ items, unsigned *ctr, const int32_t *__restrict__ pk,
-    const T *__restrict__ pv, T *a, int64_t lo, int64_t hi, int shift, uint32_t *bitmap,
-    u64 *dirty) {
+    const u64 *__restrict__ fill, const unsigned *__restrict__ dir, int nb, int kmax, unsigned *work,
+    const int32_t *__restrict__ pk, const T *__restrict__ pv, T *a, int64_t lo, int64_t hi, int shift,
+    uint32_t *bitmap, u64 *dirty) {
     extern __shared__ uint32_t sw[];
-    __shared__ unsigned sj;
-    const unsigned nitems = ctr[1];
+    __shared__ unsigned ibase[SB_MAXB + 1];
+    __shared__ unsigned wsum[32];
+    __shared__ unsigned s_b[SA_B], s_q[SA_B], s_np[SA_B], s_pid[SA_B], s_cnt[SA_B];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    {   // item list prefix: bucket b owns np_b page items + 1 bits item (if np_b > 0)
+        const u64 c = t < nb ? fill[t] : 0;
+        const unsigned np = (unsigned)((c + PG_P - 1) >> PG_LOG);
+        const unsigned own = np ? np + 1 : 0;
+        unsigned inc = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned x = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += x;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const unsigned x = wsum[lane];
+            unsigned y = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += z;
+            }
+            wsum[lane] = y - x;
+        }
+        __syncthreads();
+        if (t < nb) ibase[t] = wsum[w] + inc - own;
+        if (t == nb - 1) ibase[nb] = wsum[w] + inc;
+        __syncthreads();
+    }
+    const unsigned nitems = ibase[nb];
     u64 mn = kU64Max, mx = 0;
     for (;;) {
-        if (threadIdx.x == 0) sj = atomicAdd(&ctr[0], 1u);
+        // thread 0 takes SA_B consecutive items per dequeue (one counter
+        // round trip per SA_B pages) and decodes them
+        if (t == 0) {
+            const unsigned j0 = atomicAdd(work, (unsigned)SA_B);
+            for (int u = 0; u < SA_B; u++) {
+                const unsigned j = j0 + u;
+                s_b[u] = 0xffffffffu;
+                if (j >= nitems) continue;
+                int l = 0, r = nb - 1;  // last bucket with ibase[b] <= j
+                while (l < r) {
+                    const int m = (l + r + 1) >> 1;
+                    if (ibase[m] <= j) l = m;
+                    else r = m - 1;
+                }
+                const u64 c = fill[l];
+                const unsigned np = (unsigned)((c + PG_P - 1) >> PG_LOG);
+                const unsigned q = j - ibase[l];
+                s_b[u] = (unsigned)l;
+                s_np[u] = np;
+                s_q[u] = q;
+                if (q < np) {
+                    s_pid[u] = dir[(size_t)l * kmax + q] - 1u;
+                    s_cnt[u] = q + 1 < np ? (unsigned)PG_P : (unsigned)(c - ((u64)q << PG_LOG));
+                }
+            }
+        }
         __syncthreads();
-        const unsigned j = sj;
-        __syncthreads();
-        if (j >= nitems) break;
-        const u64 it = items[j];
-        if (!(it & IT_BITS)) {
-            const size_t p0 = (size_t)(it >> 16) << PG_LOG;
-            const int cnt = (int)(it & 0xffff) + 1;
+        if (s_b[0] == 0xffffffffu) break;
+        for (int u = 0; u < SA_B; u++) {
+            const unsigned bk = s_b[u], q = s_q[u], np = s_np[u];
+            if (bk == 0xffffffffu) break;
+            if (q < np) {
+                const size_t p0 = (size_t)s_pid[u] << PG_LOG;
+                const unsigned cnt = s_cnt[u];
 #pragma unroll 4
-            for (int p = threadIdx.x; p < cnt; p += SA_T) {
-                const int32_t k = __ldcs(pk + p0 + p);
-                atomicAdd(a + k, __ldcs(pv + p0 + p));
-                mn = (u64)k < mn ? (u64)k : mn;
-                mx = (u64)k > mx ? (u64)k : mx;
+                for (unsigned p = t; p < cnt; p += SA_T) {
+                    const int32_t k = pk[p0 + p];
+                    atomicAdd(a + k, __ldcs(pv + p0 + p));
+                    mn = (u64)k < mn ? (u64)k : mn;
+                    mx = (u64)k > mx ? (u64)k : mx;
+                }
+                continue;
             }
-            continue;
-        }
-        const int bk = (int)((it >> 32) & 0xffff);
-        const unsigned np = (unsigned)(it & 0xffffffffu);
-        const int64_t e0 = lo + ((int64_t)bk << shift);
-        const int64_t e1 = e0 + ((int64_t)1 << shift) < hi ? e0 + ((int64_t)1 << shift) : hi;
-        const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
-        for (int i = threadIdx.x; i < nw; i += SA_T) sw[i] = 0;
-        __syncthreads();
-        for (unsigned q = 0; q < np; q++) {
-            const u64 ip = items[j - np + q];
-            const int4 *k4 = reinterpret_cast<const int4 *>(pk + ((size_t)(ip >> 16) << PG_LOG));
-            const int cnt = (int)(ip & 0xffff) + 1;
-            const int n4 = cnt >> 2;
-            for (int p = threadIdx.x; p < n4; p += SA_T) {
-                const int4 k = __ldcg(k4 + p);
-                atomicOr(&sw[(k.x >> 5) - w0], 1u << (k.x & 31));
-                atomicOr(&sw[(k.y >> 5) - w0], 1u << (k.y & 31));
-                atomicOr(&sw[(k.z >> 5) - w0], 1u << (k.z & 31));
-                atomicOr(&sw[(k.w >> 5) - w0], 1u << (k.w & 31));
+            const int64_t e0 = lo + ((int64_t)bk << shift);
+            const int64_t e1 = e0 + ((int64_t)1 << shift) < hi ? e0 + ((int64_t)1 << shift) : hi;
+            const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
+            for (int i = t; i < nw; i += SA_T) sw[i] = 0;
+            const u64 c = fill[bk];
+            __syncthreads();
+            for (unsigned qq = 0; qq < np; qq++) {
+                const unsigned pg = dir[(size_t)bk * kmax + qq] - 1u;
+                const int4 *k4 = reinterpret_cast<const int4 *>(pk + ((size_t)pg << PG_LOG));
+                const int n1 = qq + 1 < np ? PG_P : (int)(c - ((u64)qq << PG_LOG));
+                const int n4 = n1 >> 2;
+                for (int p = t; p < n4; p += SA_T) {
+                    const int4 k = __ldcs(k4 + p);
+                    atomicOr(&sw[(k.x >> 5) - w0], 1u << (k.x & 31));
+                    atomicOr(&sw[(k.y >> 5) - w0], 1u << (k.y & 31));
+                    atomicOr(&sw[(k.z >> 5) - w0], 1u << (k.z & 31));
+                    atomicOr(&sw[(k.w >> 5) - w0], 1u << (k.w & 31));
+                }
+                if (t < (n1 & 3)) {
+                    const int32_t k = __ldcs(reinterpret_cast<const int32_t *>(k4) + 4 * n4 + t);
+                    atomicOr(&sw[(k >> 5) - w0], 1u << (k & 31));
+                }
             }
-            if (threadIdx.x < (cnt & 3)) {
-                const int32_t k = __ldcg(reinterpret_cast<const int32_t *>(k4) + 4 * n4 + threadIdx.x);
-                atomicOr(&sw[(k >> 5) - w0], 1u << (k & 31));
+            __syncthreads();
+            for (int i = t; i < nw; i += SA_T) {
+                const uint32_t x = sw[i];
+                if (i == 0 || i == nw - 1) {
+                    if (x) atomicOr(bitmap + w0 + i, x);
+                } else {
+                    bitmap[w0 + i] = x;
+                }
             }
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < nw; i += SA_T) {
-            const uint32_t v = sw[i];
-            if (i == 0 || i == nw - 1) {
-                if (v) atomicOr(bitmap + w0 + i, v);
-            } else {
-                bitmap[w0 + i] = v;
-            }
+            __syncthreads();  // sw is reused by the next bits item
         }
         __syncthreads();
     }
@@ -1338,24 +1364,46 @@ template <typename T>
 __global__ void __launch_bounds__(256) merge_bitmap_kernel(const T *__restrict__ src, PeerPtrs dsts,
                                                            const uint32_t *__restrict__ bitmap,
                                                            int64_t lo, int64_t hi) {
-    // one warp per group of 32 words: lane l reads word w0+l, then the warp
-    // walks the words; each dirty element is stored by its own lane, so the
-    // 32 elements of a word go out as one coalesced 128/256-byte segment.
+    // One warp per group of 32 words (1024 elements); lane l holds word
+    // w0+l.  Sparse groups (<= 96 set bits): every lane copies its own
+    // word's elements (32 independent chains).  Dense groups: the warp walks
+    // the words 8 at a time, lane l moving element l of each, so the 8 loads
+    // are in flight together and each word goes out as one coalesced
+    // 128/256-byte segment per peer.
     const int lane = threadIdx.x & 31;
     const int64_t wlo = lo >> 5, whi = (hi + 31) >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t w0 = wlo + gw * 32; w0 < whi; w0 += nw * 32) {
         const uint32_t mine = (w0 + lane < whi) ? __ldg(bitmap + w0 + lane) : 0u;
-        unsigned any = __ballot_sync(0xffffffffu, mine != 0u);
-        while (any) {
-            const int j = __ffs(any) - 1;
-            any &= any - 1;
-            const uint32_t bits = __shfl_sync(0xffffffffu, mine, j);
-            if ((bits >> lane) & 1u) {
-                const int64_t e = ((w0 + j) << 5) + lane;
+        const int tot = __reduce_add_sync(0xffffffffu, __popc(mine));
+        if (tot == 0) continue;
+        if (tot <= 96) {
+            uint32_t m = mine;
+            while (m) {
+                const int bp = __ffs(m) - 1;
+                m &= m - 1;
+                const int64_t e = ((w0 + lane) << 5) + bp;
                 const T v = src[e];
                 for (int d = 0; d < dsts.n; d++) static_cast<T *>(dsts.p[d])[e] = v;
+            }
+            continue;
+        }
+#pragma unroll 1
+        for (int j0 = 0; j0 < 32; j0 += 8) {
+            T v[8];
+            bool on[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint32_t bits = __shfl_sync(0xffffffffu, mine, j0 + u);
+                on[u] = (bits >> lane) & 1u;
+                if (on[u]) v[u] = __ldcs(src + ((w0 + j0 + u) << 5) + lane);
+            }
+            for (int d = 0; d < dsts.n; d++) {
+                T *dp = static_cast<T *>(dsts.p[d]);
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (on[u]) dp[((w0 + j0 + u) << 5) + lane] = v[u];
             }
         }
     }
@@ -1582,9 +1630,9 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
     p.nb = (int)nb;
     p.kmax = (n + PG_P - 1) / PG_P + 1;      // pages one bucket can need
     p.npool = (n + PG_P - 1) / PG_P + p.nb;  // every bucket: <= 1 partial page
-    // fill u64[nb] | ctr u32[4] | pool u32[4] | dir u32[nb*kmax] || items u64[npool+nb] || pages
-    p.state = ((size_t)p.nb * 8 + 32 + (size_t)p.nb * p.kmax * 4 + 255) & ~(size_t)255;
-    p.hdr = (p.state + (size_t)(p.npool + p.nb) * 8 + 255) & ~(size_t)255;
+    // fill u64[nb] | ctr u32[4] (work, pool) | dir u32[nb*kmax] || pages: keys, values
+    p.state = ((size_t)p.nb * 8 + 16 + (size_t)p.nb * p.kmax * 4 + 255) & ~(size_t)255;
+    p.hdr = p.state;
     p.scratch = p.hdr + (size_t)p.npool * PG_P * (4 + (size_t)elem);
     return p;
 }
@@ -1594,15 +1642,12 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
                                u64 *dirty, const ScatterPlan &pl, void *scratch) {
     char *sc = static_cast<char *>(scratch);
     u64 *fill = reinterpret_cast<u64 *>(sc);
-    unsigned *ctr = reinterpret_cast<unsigned *>(sc + (size_t)pl.nb * 8);
-    unsigned *pool = ctr + 4;
-    unsigned *dir = ctr + 8;
-    u64 *items = reinterpret_cast<u64 *>(sc + pl.state);
+    unsigned *work = reinterpret_cast<unsigned *>(sc + (size_t)pl.nb * 8);
+    unsigned *pool = work + 1;
+    unsigned *dir = work + 4;
     int32_t *pk = reinterpret_cast<int32_t *>(sc + pl.hdr);
     char *pv = sc + pl.hdr + (size_t)pl.npool * PG_P * 4;
-    // the partition state starts zeroed (the items kernel re-zeroes what a
-    // launch used; the memset keeps it exact whatever earlier launches of
-    // another layout left in the scratch)
+    // the partition state (fill, counters, page directory) starts zeroed
     cudaError_t e = cudaMemsetAsync(sc, 0, pl.state, s);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0;
@@ -1610,33 +1655,32 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
     const int64_t tiles = (n + (int64_t)SB_T * SB_E - 1) / ((int64_t)SB_T * SB_E);
-    const int pg = (int)std::min<int64_t>(tiles, (int64_t)nsm * 8);
-    const int esz = is_f64 ? 8 : 4;
-    const int pdsm = SB_T * SB_E * (esz + 4);
+    const int pg = (int)std::min<int64_t>(tiles, (int64_t)nsm * SB_MINB * 2);
+    const int pdsm = (int)part_smem(pl.nb, is_f64 ? 8 : 4);
     const int adsm = (int)((((int64_t)1 << pl.shift) >> 5) + 2) * 4;
+    const int kmax = (int)pl.kmax;
     // attributes are per device: set on every call (host-side, cheap)
     if (is_f64) {
         cudaFuncSetAttribute(scat_part_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
         cudaFuncSetAttribute(scat_apply_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, adsm);
         scat_part_kernel<double><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo, hi,
-                                                        pl.shift, pl.nb, (int)pl.kmax, fill, pool, dir,
-                                                        pk, reinterpret_cast<double *>(pv));
+                                                        pl.shift, pl.nb, kmax, fill, pool, dir, pk,
+                                                        reinterpret_cast<double *>(pv));
+        scat_apply_kernel<double><<<nsm, SA_T, adsm, s>>>(fill, dir, pl.nb, kmax, work, pk,
+                                                          reinterpret_cast<const double *>(pv),
+                                                          static_cast<double *>(a), lo, hi, pl.shift,
+                                                          bitmap, dirty);
     } else {
         cudaFuncSetAttribute(scat_part_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
         cudaFuncSetAttribute(scat_apply_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, adsm);
         scat_part_kernel<int32_t><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo, hi,
-                                                         pl.shift, pl.nb, (int)pl.kmax, fill, pool, dir,
-                                                         pk, reinterpret_cast<int32_t *>(pv));
-    }
-    scat_items_kernel<<<1, 1024, 0, s>>>(fill, pool, dir, pl.nb, (int)pl.kmax, items, ctr);
-    if (is_f64)
-        scat_apply_kernel<double><<<nsm, SA_T, adsm, s>>>(items, ctr, pk, reinterpret_cast<const double *>(pv),
-                                                          static_cast<double *>(a), lo, hi, pl.shift,
-                                                          bitmap, dirty);
-    else
-        scat_apply_kernel<int32_t><<<nsm, SA_T, adsm, s>>>(items, ctr, pk, reinterpret_cast<const int32_t *>(pv),
+                                                         pl.shift, pl.nb, kmax, fill, pool, dir, pk,
+                                                         reinterpret_cast<int32_t *>(pv));
+        scat_apply_kernel<int32_t><<<nsm, SA_T, adsm, s>>>(fill, dir, pl.nb, kmax, work, pk,
+                                                           reinterpret_cast<const int32_t *>(pv),
                                                            static_cast<int32_t *>(a), lo, hi, pl.shift,
                                                            bitmap, dirty);
+    }
     return cudaGetLastError();
 }
 

@@ -63,9 +63,8 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
 // larger than L2, in one pass over the updates: (1) partition the owned
 // (k, b[i]) pairs into buckets of 2^shift elements of a (shared-memory
 // staging, bucket-contiguous writes) into pages of 8192 pairs that each
-// bucket claims from a pool as its stream grows (no histogram pass); (2) a
-// one-block kernel lists the pages bucket by bucket; (3) one persistent
-// kernel applies the pages in that order, so the read-modify-writes of a hit
+// bucket claims from a pool as its stream grows (no histogram pass); (2) one
+// persistent kernel applies the pages bucket by bucket, so the read-modify-writes of a hit
 // L2 and every line of a moves to/from HBM about once, and after each
 // bucket rebuilds its dirty-bitmap words in shared memory from the bucket's
 // keys while they are still in L2 (no extra HBM pass).  Dirty range fused.
@@ -76,7 +75,7 @@ struct ScatterPlan {
     int shift, nb;      // bucket = 2^shift elements, nb buckets
     int64_t kmax;       // page-directory entries per bucket
     int64_t npool;      // pages in the pool
-    size_t state, hdr;  // bytes: zeroed state | + item list (pages follow)
+    size_t state, hdr;  // bytes: zeroed state (fill, counters, directory); pages at hdr
     size_t scratch;     // total scratch bytes
 };
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem);
