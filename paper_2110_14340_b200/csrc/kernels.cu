@@ -12,6 +12,9 @@
 // contracted (DESIGN R-14): results are bit-identical to the oracle.
 #include "kernels.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 #include <algorithm>
 #include <cstdlib>
@@ -515,6 +518,200 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, ST, WM, WN>::NT)
 }
 
 // ---------------------------------------------------------------------------
+// BK3  fp64 GEMM, Blackwell data movement: a persistent CTA per SM, one
+// producer warp whose elected lane streams the A and B tiles of every k-step
+// into a TG_ST-stage shared-memory ring with TMA (cp.async.bulk.tensor,
+// completion counted on a per-stage "full" mbarrier), and TG_CW consumer
+// warps that wait on "full", run the DMMA fragments (mma.sync m8n8k4 f64 --
+// tcgen05 has no f64 kind) and release the stage on its "empty" mbarrier.
+// No CTA-wide barrier in the main loop; the next tile's loads stream while
+// the consumers store the previous tile (epilogue: dirty range and the
+// EAGER peer push fused, as in the cp.async kernel).
+// TMA boxes give conflict-free fragment reads without padding: A as
+// [k/4][BM rows][4] (32-byte rows: a fragment is 256 contiguous bytes), B as
+// [n/8][BK rows][8] (64-byte rows: a fragment's 4 k-rows are contiguous).
+// ---------------------------------------------------------------------------
+constexpr int TG_BM = 128, TG_BN = 128, TG_BK = 16, TG_ST = 6;
+constexpr int TG_WM = 64, TG_WN = 32;
+constexpr int TG_CW = (TG_BM / TG_WM) * (TG_BN / TG_WN);  // 8 consumer warps
+constexpr int TG_NT = (TG_CW + 1) * 32;
+constexpr int TG_ABYTES = TG_BM * TG_BK * 8, TG_BBYTES = TG_BK * TG_BN * 8;
+constexpr int TG_SMEM = TG_ST * (TG_ABYTES + TG_BBYTES) + 2 * TG_ST * 8 + 2 * TG_CW * 8;
+constexpr int TG_GROUP = 8;  // grouped rasterisation of the persistent tile order
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(u64 *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64 *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64 *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *bar, unsigned parity) {
+    const unsigned a = smem_u32(bar);
+    unsigned ok = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, u64 *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tg_tile(int64_t t, int64_t tilesM, int64_t tilesN, int64_t &tm, int64_t &tn) {
+    const int64_t per = (int64_t)TG_GROUP * tilesN, g = t / per;
+    const int64_t gm = tilesM - g * TG_GROUP < TG_GROUP ? tilesM - g * TG_GROUP : TG_GROUP;
+    tm = g * TG_GROUP + (t % per) % gm;
+    tn = (t % per) / gm;
+}
+
+__global__ void __launch_bounds__(TG_NT, 1)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                    double *__restrict__ C, int64_t N, int64_t K, int64_t r0, int64_t r1, int64_t c0,
+                    int64_t c1, u64 *dirty, PeerPtrs push) {
+    // no static shared memory in this kernel: the dynamic window starts at
+    // the CTA's shared base (1 KB aligned), as TMA destinations require
+    extern __shared__ __align__(1024) double tsm[];
+    double *As = tsm;                                   // [ST][BK/4][BM][4]
+    double *Bs = tsm + TG_ST * (TG_ABYTES / 8);         // [ST][BN/8][BK][8]
+    u64 *full = reinterpret_cast<u64 *>(tsm + TG_ST * ((TG_ABYTES + TG_BBYTES) / 8));
+    u64 *empty = full + TG_ST;
+    u64 *smn = empty + TG_ST, *smx = smn + TG_CW;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TG_ST; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], TG_CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t tilesM = (r1 - r0 + TG_BM - 1) / TG_BM, tilesN = (c1 - c0 + TG_BN - 1) / TG_BN;
+    const int64_t ntiles = tilesM * tilesN;
+    const int KT = (int)((K + TG_BK - 1) / TG_BK);
+    if (warp == TG_CW) {
+        // ---- producer: one elected lane issues every TMA ----
+        if (lane == 0) {
+            unsigned it = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int64_t tm, tn;
+                tg_tile(t, tilesM, tilesN, tm, tn);
+                const int m0 = (int)(r0 + tm * TG_BM), n0 = (int)(c0 + tn * TG_BN);
+                for (int kt = 0; kt < KT; kt++, it++) {
+                    const unsigned s = it % TG_ST, round = it / TG_ST;
+                    if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+                    mbar_expect_tx(&full[s], TG_ABYTES + TG_BBYTES);
+                    double *as = As + (size_t)s * (TG_ABYTES / 8);
+                    double *bs = Bs + (size_t)s * (TG_BBYTES / 8);
+#pragma unroll
+                    for (int kc = 0; kc < TG_BK / 4; kc++)
+                        tma_load_2d(as + kc * TG_BM * 4, &ta, kt * TG_BK + kc * 4, m0, &full[s]);
+#pragma unroll
+                    for (int nc = 0; nc < TG_BN / 8; nc++)
+                        tma_load_2d(bs + nc * TG_BK * 8, &tb, n0 + nc * 8, kt * TG_BK, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+    // ---- consumers ----
+    constexpr int MI = TG_WM / 8, NJ = TG_WN / 8, WCOLS = TG_BN / TG_WN;
+    const int wm = warp / WCOLS, wn = warp % WCOLS;
+    const int ar = lane >> 2, ac = lane & 3;
+    u64 mn = kU64Max, mx = 0;
+    unsigned it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int64_t tm, tn;
+        tg_tile(t, tilesM, tilesN, tm, tn);
+        const int64_t m0 = r0 + tm * TG_BM, n0 = c0 + tn * TG_BN;
+        double acc[MI][NJ][2];
+#pragma unroll
+        for (int i = 0; i < MI; i++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kt = 0; kt < KT; kt++, it++) {
+            const unsigned s = it % TG_ST;
+            mbar_wait(&full[s], (it / TG_ST) & 1);
+            const double *as = As + (size_t)s * (TG_ABYTES / 8) + (wm * TG_WM + ar) * 4 + ac;
+            const double *bs = Bs + (size_t)s * (TG_BBYTES / 8) + (wn * NJ) * TG_BK * 8 + ac * 8 + ar;
+#pragma unroll
+            for (int kc = 0; kc < TG_BK / 4; kc++) {
+                double a[MI], b[NJ];
+#pragma unroll
+                for (int i = 0; i < MI; i++) a[i] = as[kc * TG_BM * 4 + i * 8 * 4];
+#pragma unroll
+                for (int j = 0; j < NJ; j++) b[j] = bs[j * TG_BK * 8 + kc * 4 * 8];
+#pragma unroll
+                for (int i = 0; i < MI; i++)
+#pragma unroll
+                    for (int j = 0; j < NJ; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // epilogue: C rows in [r0, r1), cols in [c0, c1) (N even, c0 even:
+        // every fragment pair is one aligned 16-byte store); EAGER peer push
+#pragma unroll
+        for (int i = 0; i < MI; i++) {
+            const int64_t m = m0 + wm * TG_WM + i * 8 + ar;
+            if (m >= r1) continue;
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+                const int64_t n = n0 + wn * TG_WN + j * 8 + ac * 2;
+                const int64_t f = m * N + n;
+                if (n + 1 < c1) {
+                    const double2 v2 = make_double2(acc[i][j][0], acc[i][j][1]);
+                    *reinterpret_cast<double2 *>(C + f) = v2;
+                    for (int q = 0; q < push.n; q++)
+                        *reinterpret_cast<double2 *>(static_cast<double *>(push.p[q]) + f) = v2;
+                    mn = (u64)f < mn ? (u64)f : mn;
+                    mx = (u64)(f + 1) > mx ? (u64)(f + 1) : mx;
+                } else if (n < c1) {
+                    C[f] = acc[i][j][0];
+                    for (int q = 0; q < push.n; q++) static_cast<double *>(push.p[q])[f] = acc[i][j][0];
+                    mn = (u64)f < mn ? (u64)f : mn;
+                    mx = (u64)f > mx ? (u64)f : mx;
+                }
+            }
+        }
+    }
+    // dirty range over the consumer warps (named barrier: the producer warp
+    // has left)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        u64 *nx = reinterpret_cast<u64 *>(reinterpret_cast<uintptr_t>(dirty) ^ 16u);
+        nx[0] = kU64Max;
+        nx[1] = kU64Max;
+    }
+    mn = warp_min_u64(mn);
+    mx = warp_max_u64(mx);
+    if (lane == 0) {
+        smn[warp] = mn;
+        smx[warp] = mx;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TG_CW * 32) : "memory");
+    if (threadIdx.x == 0) {
+        u64 a = smn[0], b = smx[0];
+        for (int i = 1; i < TG_CW; i++) {
+            a = smn[i] < a ? smn[i] : a;
+            b = smx[i] > b ? smx[i] : b;
+        }
+        if (a != kU64Max) {
+            atomicMin(&dirty[0], a);
+            atomicMin(&dirty[1], ~b);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // BK4  owner-filtered scatter-add with warp-aggregated dirty bitmap
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -583,15 +780,16 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
 // while its keys are still L2-resident.
 // ---------------------------------------------------------------------------
 constexpr int SB_T = 256;        // partition CTA; tile = SB_T * SB_E updates
-constexpr int SB_E = 8;
-constexpr int SB_MINB = 4;       // partition CTAs per SM (registers, shared memory)
+constexpr int SB_E = 16;
+constexpr int SB_MINB = 2;       // partition CTAs per SM (persistent grid)
 constexpr int SB_MAXB = 1024;    // max buckets
-constexpr int PG_LOG = 13;       // pairs per page = 8192 (>= a tile: a tile's
-constexpr int PG_P = 1 << PG_LOG;  //  bucket segment spans at most two pages)
-constexpr int SA_T = 1024;       // apply CTA (one per SM)
-constexpr int SA_B = 4;          // work items per dequeue
+constexpr int MP_LOG = 9;        // mini-page = 512 pairs
+constexpr int MP = 1 << MP_LOG;
 constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;  // buckets per thread in the reservation
-static_assert(SB_T * SB_E <= PG_P, "a tile segment must fit in two pages");
+constexpr int SA_T = 1024;       // apply CTA (one per SM)
+constexpr int SA_G = 16;         // mini-pages per apply item (<= 8192 pairs)
+constexpr int SA_B = 2;          // apply items per dequeue
+static_assert(SA_T % SA_G == 0 && MP % (SA_T / SA_G) == 0, "apply item shape");
 
 // warp 0 computes the exclusive scan of hist[0..nb) into off[]
 __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off, int nb,
@@ -617,39 +815,73 @@ __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off,
     if (lane == 31) *total = inc;
 }
 
-// shared-memory layout of the partition: per-bucket state sized by nb
-__host__ __device__ constexpr size_t part_smem(int nb, int esz) {
-    return (size_t)nb * 8 + (size_t)((nb + 1) & ~1) * 16 + (size_t)SB_T * SB_E * (esz + 4);
+// block-wide exclusive scan of v (one value per thread, blockDim.x <= 1024);
+// returns the exclusive prefix, *tot = the sum
+__device__ __forceinline__ unsigned block_exscan(unsigned v, unsigned *wsum, unsigned *tot) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    unsigned inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned x = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += x;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const unsigned x = lane < nw ? wsum[lane] : 0u;
+        unsigned y = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
+        }
+        wsum[lane] = y - x;
+        if (lane == 31) *tot = y;
+    }
+    __syncthreads();
+    const unsigned r = wsum[w] + inc - v;
+    __syncthreads();
+    return r;
 }
 
-// Partition.  Per tile of SB_T*SB_E updates: keys (then the values of the
-// owned ones) into registers, per-bucket ranks by shared-memory atomics,
-// warp scan; one thread per non-empty bucket reserves the tile's segment of
-// the bucket's stream (atomicAdd on fill[b], issued before the staging so
-// its round trip overlaps it) and claims from the pool every page whose
-// first slot falls inside the segment, publishing it in dir[b*kmax + k]
-// (page id + 1).  The page holding the segment's first slot, when it starts
-// before the segment, was claimed by the CTA that reserved that slot; its
-// reservation precedes ours and it publishes right after its reservation
-// returns (before any wait of its own), so the wait below always ends.
-// Pairs are staged in bucket order in shared memory and written out
-// bucket-contiguously.  Several small CTAs per SM keep loads of one tile in
-// flight while others stage or wait on their reservation.
+// shared-memory layout of the partition: per-bucket state sized by nb
+__host__ __device__ constexpr size_t part_smem(int nb, int esz) {
+    return (size_t)((nb + 1) & ~1) * 4 * 7 + (size_t)SB_T * SB_E * (esz + 4);
+}
+
+// Partition (persistent: SB_MINB CTAs per SM, tiles grid-strided).  Each
+// CTA owns a static range of `cap` mini-pages of MP pairs and keeps, per
+// bucket, a current mini-page and its fill in shared memory, so reserving a
+// tile's bucket segments needs no global round trip: a segment continues
+// the bucket's current mini-page and takes consecutive fresh mini-pages from
+// the CTA's range when it fills.  Per tile: keys (then the owned values)
+// into registers, ranks by shared-memory atomics, warp scan, reservation,
+// staging in bucket order in shared memory, bucket-contiguous write-out.
+// Claimed mini-pages are logged (pbucket[pid] = bucket, np[b] += 1); each
+// gets its pair count in pcnt once: MP when it is left full, its fill when
+// it is the bucket's current page at the end.
+constexpr unsigned MP_NONE = 0xffffffffu;
 template <typename T>
 __global__ void __launch_bounds__(SB_T, SB_MINB) scat_part_kernel(
     const int32_t *__restrict__ idx, const T *__restrict__ b, int64_t n, int64_t lo, int64_t hi,
-    int shift, int nb, int kmax, u64 *fill, unsigned *pool, unsigned *dir,
-    int32_t *__restrict__ pk, T *__restrict__ pv) {
+    int shift, int nb, unsigned cap, unsigned *np, unsigned *used, unsigned *pbucket,
+    unsigned *pcnt, int32_t *__restrict__ pk, T *__restrict__ pv) {
     constexpr int E = SB_E, TILE = SB_T * E;
     extern __shared__ __align__(16) unsigned char sdyn[];
-    u64 *gv0 = reinterpret_cast<u64 *>(sdyn);
     const int nb2 = (nb + 1) & ~1;
-    unsigned *hist = reinterpret_cast<unsigned *>(sdyn + (size_t)nb * 8);
-    unsigned *loff = hist + nb2, *gp0 = loff + nb2, *gp1 = gp0 + nb2;
-    T *sv = reinterpret_cast<T *>(gp1 + nb2);
+    unsigned *hist = reinterpret_cast<unsigned *>(sdyn);
+    unsigned *loff = hist + nb2, *cpg = loff + nb2, *cfill = cpg + nb2;   // current page, its fill
+    unsigned *opg = cfill + nb2, *ofill = opg + nb2, *npg = ofill + nb2;  // this tile: old page/fill, first fresh page
+    T *sv = reinterpret_cast<T *>(npg + nb2);
     int32_t *sk = reinterpret_cast<int32_t *>(sv + TILE);
-    __shared__ unsigned total;
+    __shared__ unsigned total, next;  // next: first unclaimed mini-page of this CTA's range
     const int tid = threadIdx.x;
+    const unsigned pbase = blockIdx.x * cap;
+    for (int i = tid; i < nb; i += SB_T) {
+        cpg[i] = MP_NONE;
+        cfill[i] = MP;  // no room: the first segment claims
+    }
+    if (tid == 0) next = 0;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int32_t k[E];
@@ -672,15 +904,29 @@ __global__ void __launch_bounds__(SB_T, SB_MINB) scat_part_kernel(
             if (k[j] >= lo && k[j] < hi) rk[j] = atomicAdd(&hist[(int)(((int64_t)k[j] - lo) >> shift)], 1u);
         __syncthreads();
         if (tid < 32) warp_exscan(hist, loff, nb, &total);
-        // reserve now; the results are consumed after the staging
-        u64 v0[SB_RES];
-#pragma unroll
-        for (int r = 0; r < SB_RES; r++) {
-            const int i = tid + r * SB_T;
-            const unsigned c = i < nb ? hist[i] : 0u;
-            v0[r] = c ? atomicAdd(&fill[i], (u64)c) : 0;
+        for (int i = tid; i < nb; i += SB_T) {
+            const unsigned c = hist[i];
+            if (!c) continue;
+            const unsigned f = cfill[i], room = MP - f;
+            opg[i] = cpg[i];
+            ofill[i] = f;
+            if (c <= room) {
+                cfill[i] = f + c;
+                continue;
+            }
+            const unsigned kn = (c - room + MP - 1) >> MP_LOG;  // fresh mini-pages
+            const unsigned p = pbase + atomicAdd(&next, kn);
+            npg[i] = p;
+            if (cpg[i] != MP_NONE) pcnt[cpg[i]] = MP;  // left full
+            for (unsigned q = 0; q < kn; q++) {
+                pbucket[p + q] = (unsigned)i;
+                if (q + 1 < kn) pcnt[p + q] = MP;
+            }
+            atomicAdd(&np[i], kn);
+            cpg[i] = p + kn - 1;
+            cfill[i] = c - room - ((kn - 1) << MP_LOG);
         }
-        __syncthreads();  // loff
+        __syncthreads();
 #pragma unroll
         for (int j = 0; j < E; j++)
             if (k[j] >= lo && k[j] < hi) {
@@ -688,98 +934,79 @@ __global__ void __launch_bounds__(SB_T, SB_MINB) scat_part_kernel(
                 sk[pos] = k[j];
                 sv[pos] = v[j];
             }
-        // claim (no waiting), then resolve the first page (may wait)
-#pragma unroll
-        for (int r = 0; r < SB_RES; r++) {
-            const int i = tid + r * SB_T;
-            const unsigned c = i < nb ? hist[i] : 0u;
-            if (!c) continue;
-            const u64 k0 = v0[r] >> PG_LOG, k1 = (v0[r] + c - 1) >> PG_LOG;
-            unsigned p0 = 0, p1 = 0;
-            for (u64 kk = k0; kk <= k1; kk++)
-                if ((kk << PG_LOG) >= v0[r]) {
-                    const unsigned pid = atomicAdd(pool, 1u) + 1u;
-                    atomicExch(&dir[(size_t)i * kmax + kk], pid);
-                    if (kk == k0) p0 = pid;
-                    else p1 = pid;
-                }
-            gv0[i] = v0[r];
-            gp1[i] = p1;
-            if (!p0) {
-                unsigned *d = dir + (size_t)i * kmax + k0;
-                while ((p0 = atomicOr(d, 0u)) == 0) __nanosleep(64);  // read at L2
-            }
-            gp0[i] = p0;
-        }
         __syncthreads();
         const unsigned cnt = total;
         for (unsigned pos = tid; pos < cnt; pos += SB_T) {
             const int32_t kk = sk[pos];
             const int bb = (int)(((int64_t)kk - lo) >> shift);
-            const u64 vs = gv0[bb] + (pos - loff[bb]);
-            const unsigned pid = (vs >> PG_LOG) == (gv0[bb] >> PG_LOG) ? gp0[bb] : gp1[bb];
-            const size_t g = ((size_t)(pid - 1) << PG_LOG) | (size_t)(vs & (PG_P - 1));
+            const unsigned vv = ofill[bb] + (pos - loff[bb]);  // slot counted from the old page
+            const unsigned pg = vv < MP ? opg[bb] : npg[bb] + ((vv - MP) >> MP_LOG);
+            const size_t g = ((size_t)pg << MP_LOG) | (vv & (MP - 1));
             pk[g] = kk;
             pv[g] = sv[pos];
         }
         __syncthreads();
     }
+    for (int i = tid; i < nb; i += SB_T)
+        if (cpg[i] != MP_NONE) pcnt[cpg[i]] = cfill[i];
+    if (tid == 0) used[blockIdx.x] = next;
+}
+
+// Page list: every claimed mini-page, grouped by bucket (order inside a
+// bucket is free).  Block c walks partition CTA c's range.
+__global__ void __launch_bounds__(1024) scat_plist_kernel(const unsigned *__restrict__ np,
+                                                          const unsigned *__restrict__ used,
+                                                          const unsigned *__restrict__ pbucket,
+                                                          unsigned *cursor, unsigned *plist, int nb,
+                                                          unsigned cap) {
+    __shared__ unsigned pfx[SB_MAXB], wsum[32], tot;
+    const int t = threadIdx.x;
+    const unsigned x = block_exscan(t < nb ? np[t] : 0u, wsum, &tot);
+    if (t < nb) pfx[t] = x;
+    __syncthreads();
+    const unsigned base = blockIdx.x * cap, u = used[blockIdx.x];
+    for (unsigned j = t; j < u; j += blockDim.x) {
+        const unsigned bk = pbucket[base + j];
+        plist[pfx[bk] + atomicAdd(&cursor[bk], 1u)] = base + j;
+    }
 }
 
 // Apply (persistent, one CTA of SA_T threads per SM).  Work items, in list
-// order: for every non-empty bucket b, its pages, then one bits item.  Each
-// CTA derives the list from fill[] (a block scan into shared memory) and
-// maps a dequeued item to (bucket, page) by binary search; page ids come from
-// the partition's directory.  Apply item: a[k] += v for the page's pairs (L2
-// atomics; the bucket in flight is L2-resident; keys are loaded with the
-// default policy so they stay in L2 for the bits item).  Bits item: the
-// bucket's keys, still L2-resident, set bits of a shared-memory copy of the
-// bucket's dirty-bitmap words, written out once (plain stores; a bucket's
-// first/last word may be shared with its neighbour when lo is not
-// 32-aligned: atomicOr into the zeroed bitmap).  Dirty range: min/max over
-// the applied keys.
+// order: for every bucket with pages, its pages in groups of SA_G (apply
+// items), then one bits item.  Each CTA derives the list from np[] (block
+// scans into shared memory) and maps a dequeued item to (bucket, group) by
+// binary search.  Apply item: every thread loads all its pairs of the
+// group first (MP/64 keys and values in flight), then issues their REDs
+// (a[k] += v; the buckets in flight are L2-resident).  Bits item: the
+// bucket's keys set bits of a shared-memory copy of the bucket's
+// dirty-bitmap words, written out once (plain stores; a bucket's first/last
+// word may be shared with its neighbour when lo is not 32-aligned: atomicOr
+// into the zeroed bitmap).  Dirty range: min/max over the applied keys.
 template <typename T>
 __global__ void __launch_bounds__(SA_T, 1) scat_apply_kernel(
-    const u64 *__restrict__ fill, const unsigned *__restrict__ dir, int nb, int kmax, unsigned *work,
-    const int32_t *__restrict__ pk, const T *__restrict__ pv, T *a, int64_t lo, int64_t hi, int shift,
-    uint32_t *bitmap, u64 *dirty) {
+    const unsigned *__restrict__ np, const unsigned *__restrict__ plist,
+    const unsigned *__restrict__ pcnt, int nb, unsigned *work, const int32_t *__restrict__ pk,
+    const T *__restrict__ pv, T *a, int64_t lo, int64_t hi, int shift, uint32_t *bitmap, u64 *dirty) {
+    constexpr int TPP = SA_T / SA_G;   // threads per mini-page
+    constexpr int PER = MP / TPP;      // pairs per thread per mini-page
     extern __shared__ uint32_t sw[];
-    __shared__ unsigned ibase[SB_MAXB + 1];
-    __shared__ unsigned wsum[32];
-    __shared__ unsigned s_b[SA_B], s_q[SA_B], s_np[SA_B], s_pid[SA_B], s_cnt[SA_B];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    {   // item list prefix: bucket b owns np_b page items + 1 bits item (if np_b > 0)
-        const u64 c = t < nb ? fill[t] : 0;
-        const unsigned np = (unsigned)((c + PG_P - 1) >> PG_LOG);
-        const unsigned own = np ? np + 1 : 0;
-        unsigned inc = own;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned x = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += x;
-        }
-        if (lane == 31) wsum[w] = inc;
-        __syncthreads();
-        if (w == 0) {
-            const unsigned x = wsum[lane];
-            unsigned y = x;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned z = __shfl_up_sync(0xffffffffu, y, o);
-                if (lane >= o) y += z;
-            }
-            wsum[lane] = y - x;
-        }
-        __syncthreads();
-        if (t < nb) ibase[t] = wsum[w] + inc - own;
-        if (t == nb - 1) ibase[nb] = wsum[w] + inc;
+    __shared__ unsigned ibase[SB_MAXB + 1], pfx[SB_MAXB + 1], wsum[32], tot;
+    __shared__ unsigned s_b[SA_B], s_q[SA_B];
+    const int t = threadIdx.x;
+    {
+        const unsigned c = t < nb ? np[t] : 0u;
+        const unsigned x = block_exscan(c, wsum, &tot);
+        if (t < nb) pfx[t] = x;
+        if (t == 0) pfx[nb] = tot;
+        const unsigned own = c ? (c + SA_G - 1) / SA_G + 1 : 0u;
+        const unsigned y = block_exscan(own, wsum, &tot);
+        if (t < nb) ibase[t] = y;
+        if (t == 0) ibase[nb] = tot;
         __syncthreads();
     }
     const unsigned nitems = ibase[nb];
     u64 mn = kU64Max, mx = 0;
     for (;;) {
-        // thread 0 takes SA_B consecutive items per dequeue (one counter
-        // round trip per SA_B pages) and decodes them
         if (t == 0) {
             const unsigned j0 = atomicAdd(work, (unsigned)SA_B);
             for (int u = 0; u < SA_B; u++) {
@@ -792,32 +1019,43 @@ __global__ void __launch_bounds__(SA_T, 1) scat_apply_kernel(
                     if (ibase[m] <= j) l = m;
                     else r = m - 1;
                 }
-                const u64 c = fill[l];
-                const unsigned np = (unsigned)((c + PG_P - 1) >> PG_LOG);
-                const unsigned q = j - ibase[l];
                 s_b[u] = (unsigned)l;
-                s_np[u] = np;
-                s_q[u] = q;
-                if (q < np) {
-                    s_pid[u] = dir[(size_t)l * kmax + q] - 1u;
-                    s_cnt[u] = q + 1 < np ? (unsigned)PG_P : (unsigned)(c - ((u64)q << PG_LOG));
-                }
+                s_q[u] = j - ibase[l];
             }
         }
         __syncthreads();
         if (s_b[0] == 0xffffffffu) break;
         for (int u = 0; u < SA_B; u++) {
-            const unsigned bk = s_b[u], q = s_q[u], np = s_np[u];
+            const unsigned bk = s_b[u];
             if (bk == 0xffffffffu) break;
-            if (q < np) {
-                const size_t p0 = (size_t)s_pid[u] << PG_LOG;
-                const unsigned cnt = s_cnt[u];
-#pragma unroll 4
-                for (unsigned p = t; p < cnt; p += SA_T) {
-                    const int32_t k = pk[p0 + p];
-                    atomicAdd(a + k, __ldcs(pv + p0 + p));
-                    mn = (u64)k < mn ? (u64)k : mn;
-                    mx = (u64)k > mx ? (u64)k : mx;
+            const unsigned q = s_q[u], p0 = pfx[bk], npb = pfx[bk + 1] - p0;
+            const unsigned ng = (npb + SA_G - 1) / SA_G;
+            if (q < ng) {
+                const unsigned g = q * SA_G + (unsigned)(t / TPP);
+                if (g < npb) {
+                    const unsigned pid = plist[p0 + g];
+                    const unsigned pc = pcnt[pid];
+                    const size_t base = (size_t)pid << MP_LOG;
+                    const int off = t % TPP;
+                    int32_t kk[PER];
+                    T vv[PER];
+#pragma unroll
+                    for (int e = 0; e < PER; e++) {
+                        const unsigned s = off + e * TPP;
+                        kk[e] = s < pc ? pk[base + s] : -1;
+                    }
+#pragma unroll
+                    for (int e = 0; e < PER; e++) {
+                        const unsigned s = off + e * TPP;
+                        if (s < pc) vv[e] = __ldcs(pv + base + s);
+                    }
+#pragma unroll
+                    for (int e = 0; e < PER; e++)
+                        if (kk[e] >= 0) {
+                            atomicAdd(a + kk[e], vv[e]);
+                            mn = (u64)kk[e] < mn ? (u64)kk[e] : mn;
+                            mx = (u64)kk[e] > mx ? (u64)kk[e] : mx;
+                        }
                 }
                 continue;
             }
@@ -825,22 +1063,13 @@ __global__ void __launch_bounds__(SA_T, 1) scat_apply_kernel(
             const int64_t e1 = e0 + ((int64_t)1 << shift) < hi ? e0 + ((int64_t)1 << shift) : hi;
             const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
             for (int i = t; i < nw; i += SA_T) sw[i] = 0;
-            const u64 c = fill[bk];
             __syncthreads();
-            for (unsigned qq = 0; qq < np; qq++) {
-                const unsigned pg = dir[(size_t)bk * kmax + qq] - 1u;
-                const int4 *k4 = reinterpret_cast<const int4 *>(pk + ((size_t)pg << PG_LOG));
-                const int n1 = qq + 1 < np ? PG_P : (int)(c - ((u64)qq << PG_LOG));
-                const int n4 = n1 >> 2;
-                for (int p = t; p < n4; p += SA_T) {
-                    const int4 k = __ldcs(k4 + p);
-                    atomicOr(&sw[(k.x >> 5) - w0], 1u << (k.x & 31));
-                    atomicOr(&sw[(k.y >> 5) - w0], 1u << (k.y & 31));
-                    atomicOr(&sw[(k.z >> 5) - w0], 1u << (k.z & 31));
-                    atomicOr(&sw[(k.w >> 5) - w0], 1u << (k.w & 31));
-                }
-                if (t < (n1 & 3)) {
-                    const int32_t k = __ldcs(reinterpret_cast<const int32_t *>(k4) + 4 * n4 + t);
+            for (unsigned g = t / TPP; g < npb; g += SA_G) {
+                const unsigned pid = plist[p0 + g];
+                const unsigned pc = pcnt[pid];
+                const size_t base = (size_t)pid << MP_LOG;
+                for (unsigned s = t % TPP; s < pc; s += TPP) {
+                    const int32_t k = __ldcs(pk + base + s);
                     atomicOr(&sw[(k >> 5) - w0], 1u << (k & 31));
                 }
             }
@@ -1525,6 +1754,66 @@ static cudaError_t gemm_launch(cudaStream_t s, bool v16, const double *A, const 
     return cudaGetLastError();
 }
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// TMA + mbarrier pipeline (gemm_tma_kernel); false when the shapes or the
+// driver do not allow it (the caller then runs the cp.async kernel)
+bool gemm_tma_launch(cudaStream_t s, const double *A, const double *B, double *C, int64_t M,
+                     int64_t N, int64_t K, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                     u64 *dirty, PeerPtrs push, cudaError_t &err) {
+    (void)M;
+    auto enc = tmap_encode();
+    if (!enc || K % 2 || N % 2 || c0 % 2 || (uintptr_t)A % 16 || (uintptr_t)B % 16 ||
+        (uintptr_t)C % 16 || r1 > INT32_MAX || c1 > INT32_MAX || K > INT32_MAX)
+        return false;
+    CUtensorMap ta, tb;
+    const cuuint32_t one[2] = {1, 1};
+    {   // A: rows [0, r1) x K, box {4 k, BM rows}
+        const cuuint64_t dim[2] = {(cuuint64_t)K, (cuuint64_t)r1};
+        const cuuint64_t str[1] = {(cuuint64_t)K * 8};
+        const cuuint32_t box[2] = {4, (cuuint32_t)TG_BM};
+        if (enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(A), dim, str, box, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    {   // B: K x cols [0, c1), box {8 cols, BK rows}
+        const cuuint64_t dim[2] = {(cuuint64_t)c1, (cuuint64_t)K};
+        const cuuint64_t str[1] = {(cuuint64_t)N * 8};
+        const cuuint32_t box[2] = {8, (cuuint32_t)TG_BK};
+        if (enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(B), dim, str, box, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+    cudaFuncSetAttribute(gemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM);
+    const int64_t tiles = ((r1 - r0 + TG_BM - 1) / TG_BM) * ((c1 - c0 + TG_BN - 1) / TG_BN);
+    const int grid = (int)std::min<int64_t>(tiles, nsm);
+    gemm_tma_kernel<<<grid, TG_NT, TG_SMEM, s>>>(ta, tb, C, N, K, r0, r1, c0, c1, dirty, push);
+    err = cudaGetLastError();
+    return true;
+}
+}  // namespace
+
 cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C, int64_t M,
                      int64_t N, int64_t K, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
                      u64 *dirty, PeerPtrs push) {
@@ -1535,6 +1824,10 @@ cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C
     if (variant < 0) {
         const char *e = getenv("JACC_GEMM_VARIANT");
         variant = e ? atoi(e) : 0;
+    }
+    if (variant == 0) {
+        cudaError_t err = cudaSuccess;
+        if (gemm_tma_launch(s, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push, err)) return err;
     }
     switch (variant) {
     case 1: return gemm_launch<64, 64, 32, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
@@ -1614,7 +1907,7 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
 }
 
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
-    ScatterPlan p{false, 0, 0, 0, 0, 0, 0, 0};
+    ScatterPlan p{};
     const int64_t span = hi - lo;
     const char *force = getenv("JACC_SCATTER_BINNED");  // "0" never, "1" always (tests)
     if (span <= 0 || n <= 0 || (force && force[0] == '0')) return p;
@@ -1625,15 +1918,24 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
     const int shift = 20;
     const int64_t nb = (span + ((int64_t)1 << shift) - 1) >> shift;
     if (nb > SB_MAXB) return p;  // > 2^30 owned elements: the direct kernel
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+    const int64_t tile = (int64_t)SB_T * SB_E, tiles = (n + tile - 1) / tile;
+    p.grid = (int)std::min<int64_t>(tiles, (int64_t)nsm * SB_MINB);
+    const int64_t per_cta = (tiles + p.grid - 1) / p.grid;         // tiles per partition CTA
+    p.cap = (per_cta * tile + MP - 1) / MP + nb;                   // its mini-pages, worst case
+    p.npool = p.cap * p.grid;
+    if (p.npool >= ((int64_t)1 << 31)) return p;
     p.binned = true;
     p.shift = shift;
     p.nb = (int)nb;
-    p.kmax = (n + PG_P - 1) / PG_P + 1;      // pages one bucket can need
-    p.npool = (n + PG_P - 1) / PG_P + p.nb;  // every bucket: <= 1 partial page
-    // fill u64[nb] | ctr u32[4] (work, pool) | dir u32[nb*kmax] || pages: keys, values
-    p.state = ((size_t)p.nb * 8 + 16 + (size_t)p.nb * p.kmax * 4 + 255) & ~(size_t)255;
-    p.hdr = p.state;
-    p.scratch = p.hdr + (size_t)p.npool * PG_P * (4 + (size_t)elem);
+    // zeroed state: np u32[nb] | cursor u32[nb] | work u32 ; then used u32[grid],
+    // pbucket u32[npool], pcnt u32[npool], plist u32[npool]; pages (keys, values)
+    p.state = (((size_t)nb * 8 + 16) + 255) & ~(size_t)255;
+    p.hdr = (p.state + (size_t)p.grid * 4 + (size_t)p.npool * 12 + 255) & ~(size_t)255;
+    p.scratch = p.hdr + (size_t)p.npool * MP * (4 + (size_t)elem);
     return p;
 }
 
@@ -1641,46 +1943,49 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
                                u64 *dirty, const ScatterPlan &pl, void *scratch) {
     char *sc = static_cast<char *>(scratch);
-    u64 *fill = reinterpret_cast<u64 *>(sc);
-    unsigned *work = reinterpret_cast<unsigned *>(sc + (size_t)pl.nb * 8);
-    unsigned *pool = work + 1;
-    unsigned *dir = work + 4;
+    unsigned *np = reinterpret_cast<unsigned *>(sc);
+    unsigned *cursor = np + pl.nb;
+    unsigned *work = cursor + pl.nb;
+    unsigned *used = reinterpret_cast<unsigned *>(sc + pl.state);
+    unsigned *pbucket = used + pl.grid;
+    unsigned *pcnt = pbucket + pl.npool;
+    unsigned *plist = pcnt + pl.npool;
     int32_t *pk = reinterpret_cast<int32_t *>(sc + pl.hdr);
-    char *pv = sc + pl.hdr + (size_t)pl.npool * PG_P * 4;
-    // the partition state (fill, counters, page directory) starts zeroed
-    cudaError_t e = cudaMemsetAsync(sc, 0, pl.state, s);
+    char *pv = sc + pl.hdr + (size_t)pl.npool * MP * 4;
+    cudaError_t e = cudaMemsetAsync(sc, 0, pl.state, s);  // counters start at zero
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
-    const int64_t tiles = (n + (int64_t)SB_T * SB_E - 1) / ((int64_t)SB_T * SB_E);
-    const int pg = (int)std::min<int64_t>(tiles, (int64_t)nsm * SB_MINB * 2);
     const int pdsm = (int)part_smem(pl.nb, is_f64 ? 8 : 4);
     const int adsm = (int)((((int64_t)1 << pl.shift) >> 5) + 2) * 4;
-    const int kmax = (int)pl.kmax;
+    const unsigned cap = (unsigned)pl.cap;
     // attributes are per device: set on every call (host-side, cheap)
     if (is_f64) {
         cudaFuncSetAttribute(scat_part_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
         cudaFuncSetAttribute(scat_apply_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, adsm);
-        scat_part_kernel<double><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo, hi,
-                                                        pl.shift, pl.nb, kmax, fill, pool, dir, pk,
-                                                        reinterpret_cast<double *>(pv));
-        scat_apply_kernel<double><<<nsm, SA_T, adsm, s>>>(fill, dir, pl.nb, kmax, work, pk,
-                                                          reinterpret_cast<const double *>(pv),
-                                                          static_cast<double *>(a), lo, hi, pl.shift,
-                                                          bitmap, dirty);
+        scat_part_kernel<double><<<pl.grid, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo, hi,
+                                                             pl.shift, pl.nb, cap, np, used, pbucket,
+                                                             pcnt, pk, reinterpret_cast<double *>(pv));
     } else {
         cudaFuncSetAttribute(scat_part_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
         cudaFuncSetAttribute(scat_apply_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, adsm);
-        scat_part_kernel<int32_t><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo, hi,
-                                                         pl.shift, pl.nb, kmax, fill, pool, dir, pk,
-                                                         reinterpret_cast<int32_t *>(pv));
-        scat_apply_kernel<int32_t><<<nsm, SA_T, adsm, s>>>(fill, dir, pl.nb, kmax, work, pk,
+        scat_part_kernel<int32_t><<<pl.grid, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo, hi,
+                                                              pl.shift, pl.nb, cap, np, used, pbucket,
+                                                              pcnt, pk, reinterpret_cast<int32_t *>(pv));
+    }
+    scat_plist_kernel<<<pl.grid, 1024, 0, s>>>(np, used, pbucket, cursor, plist, pl.nb, cap);
+    if (is_f64)
+        scat_apply_kernel<double><<<nsm, SA_T, adsm, s>>>(np, plist, pcnt, pl.nb, work, pk,
+                                                          reinterpret_cast<const double *>(pv),
+                                                          static_cast<double *>(a), lo, hi, pl.shift,
+                                                          bitmap, dirty);
+    else
+        scat_apply_kernel<int32_t><<<nsm, SA_T, adsm, s>>>(np, plist, pcnt, pl.nb, work, pk,
                                                            reinterpret_cast<const int32_t *>(pv),
                                                            static_cast<int32_t *>(a), lo, hi, pl.shift,
                                                            bitmap, dirty);
-    }
     return cudaGetLastError();
 }
 
