@@ -48,7 +48,7 @@ FP64_PER_BF16 = 40.0 / 2250.0   # nominal fp64 tensor / dense bf16 ratio (guide)
 DOT_L = 2**30
 GEMM_N = 8192
 SCAT_N = 2**28
-HIMENO = (1025, 513, 513)
+HIMENO = (1024, 512, 512)  # Size XL grid (DESIGN R-17)
 
 
 def algo_bytes_per_sweep_dev(N, n, d):

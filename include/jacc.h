@@ -337,6 +337,20 @@ jacc_status jacc_profile_totals(int dev, double *kernel_s, double *merge_s,
                                 uint64_t *launches, uint64_t *bytes_merged);
 jacc_status jacc_profile_reset(void);
 
+/* D13 trace: with a path, turn profiling on and append one JSON
+ * line per launch to the file once its CUDA events resolve:
+ *   {"event", "kernel_id", "kernel", "queue", "waits": [queues waited on],
+ *    "peer_waits": [devices whose previous launch it waited on],
+ *    "t_kernel_s", "t_comm_s" (max over devices), "mode": "multi"|"dup",
+ *    "merge": "eager"|"halo", "bytes_exchanged", "devices"}
+ * NULL (or jacc_finalize) closes the file after a summary line
+ *   {"summary": {"events", "total_kernel_s", "total_comm_s",
+ *                "per_kernel_modes": {name: {"multi": k, "dup": m}}}}.
+ * Every jacc_launch is also an NVTX range named after its loop.
+ * Errors: JACC_ERR_INVALID (file cannot be opened), JACC_ERR_STATE while
+ * capturing a graph. */
+jacc_status jacc_set_trace(const char *path);
+
 /* The CUDA stream (cudaStream_t) logical device `dev` runs on, and its
  * CUDA ordinal, so callers can time the path with their own events. */
 jacc_status jacc_get_stream(int dev, void **stream, int *cuda_ordinal);

@@ -111,6 +111,13 @@ jacc_status jacc_finalize(void) {
     R.graphs.clear();
     for (auto &kv : R.table) free_region(kv.second.get());
     R.table.clear();
+    if (!R.poisoned) {
+        try {
+            flush_prof();
+        } catch (Fail &) {
+        }
+    }
+    close_trace();
     for (auto &p : R.prof) {
         R.evpool.push_back(p.k0);
         R.evpool.push_back(p.k1);
@@ -384,6 +391,10 @@ jacc_status jacc_data_delete(void *host) {
 }
 
 jacc_status jacc_update_device(void *host, size_t off, size_t bytes) {
+    struct Nvtx {
+        Nvtx() { nvtxRangePushA("jacc_update_device"); }
+        ~Nvtx() { nvtxRangePop(); }
+    } nvtx;
     return guard([&]() -> jacc_status {
         if (R.capturing) return JACC_ERR_STATE;
         Region *r = lookup(host);
@@ -406,6 +417,10 @@ jacc_status jacc_update_device(void *host, size_t off, size_t bytes) {
 }
 
 jacc_status jacc_update_host(void *host, size_t off, size_t bytes) {
+    struct Nvtx {
+        Nvtx() { nvtxRangePushA("jacc_update_host"); }
+        ~Nvtx() { nvtxRangePop(); }
+    } nvtx;
     return guard([&]() -> jacc_status {
         if (R.capturing) return JACC_ERR_STATE;
         Region *r = lookup(host);
@@ -518,6 +533,22 @@ jacc_status jacc_last_timing(double *tk, double *tm, uint64_t *bytes) {
         if (tk) *tk = R.last_valid ? R.last_k : 0.0;
         if (tm) *tm = R.last_valid ? R.last_m : 0.0;
         if (bytes) *bytes = R.last_bytes;
+        return JACC_OK;
+    });
+}
+
+jacc_status jacc_set_trace(const char *path) {
+    return guard([&]() -> jacc_status {
+        if (R.capturing) return JACC_ERR_STATE;
+        flush_prof();
+        close_trace();
+        if (!path) return JACC_OK;
+        R.trace = fopen(path, "w");
+        if (!R.trace) return JACC_ERR_INVALID;
+        R.trace_events = 0;
+        R.trace_k = R.trace_c = 0;
+        R.trace_modes.clear();
+        R.profiling = true;
         return JACC_OK;
     });
 }

@@ -1545,14 +1545,16 @@ __global__ void __launch_bounds__(256) merge_range_kernel(const char *__restrict
     const int64_t nv = (ve - vs) >> 4;
     const int4 *s4 = reinterpret_cast<const int4 *>(src + vs);
     int64_t q = tid;
-    for (; q + 3 * nth < nv; q += 4 * nth) {
-        int4 v[4];
+    // 8 independent 16-byte loads in flight per thread (tools/merge_probe.cu:
+    // 8-way unroll at 16 CTAs/SM copies at 0.97 of the HBM copy peak)
+    for (; q + 7 * nth < nv; q += 8 * nth) {
+        int4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; u++) v[u] = __ldcs(s4 + q + u * nth);
+        for (int u = 0; u < 8; u++) v[u] = __ldcs(s4 + q + u * nth);
         for (int d = 0; d < dsts.n; d++) {
             int4 *d4 = reinterpret_cast<int4 *>(static_cast<char *>(dsts.p[d]) + vs);
 #pragma unroll
-            for (int u = 0; u < 4; u++) d4[q + u * nth] = v[u];
+            for (int u = 0; u < 8; u++) d4[q + u * nth] = v[u];
         }
     }
     for (; q < nv; q += nth) {
@@ -1684,6 +1686,9 @@ cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N, 
     const bool v2 = (N % 2 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0) &&
                     (!push_top || (uintptr_t)push_top % 16 == 0) &&
                     (!push_bot || (uintptr_t)push_bot % 16 == 0);
+#ifdef JACC_TUNING_VARIANTS
+    // tile-shape variants measured on the box (tools/tune_jacobi.py; build
+    // with -DJACC_TUNING_VARIANTS); not compiled into the product
     static int variant = -1;
     if (variant < 0) {
         const char *e = getenv("JACC_JACOBI_VARIANT");
@@ -1692,20 +1697,14 @@ cudaError_t jacobi2d(cudaStream_t s, const double *src, double *dst, int64_t N, 
     switch (variant) {
     case 1: return jacobi2d_launch<4, 32, 3, 6>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
     case 2: return jacobi2d_launch<4, 64, 3, 7>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    case 3: return jacobi2d_launch<4, 32, 4, 6>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    case 4: return jacobi2d_launch<4, 16, 2, 8>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
     case 5: return jacobi2d_launch<8, 32, 3, 3>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    case 6: return jacobi2d_launch<2, 32, 3, 12>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    case 7: return jacobi2d_launch<4, 32, 6, 4>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    case 8: return jacobi2d_launch<4, 32, 3, 7, false>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    case 9: return jacobi2d_launch<4, 16, 3, 8>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    case 10: return jacobi2d_launch<4, 24, 3, 7>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    case 11: return jacobi2d_launch<8, 32, 3, 3, false>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
     case 12: return jacobi2d_launch<4, 32, 3, 7, true>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
-    // default: measured best (tools/tune_jacobi.py): 4 warps x 32 rows,
-    // 3 rows of prefetch, 7 CTAs/SM, plain (write-back) stores
-    default: return jacobi2d_launch<4, 32, 3, 7, false>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
+    default: break;
     }
+#endif
+    // measured best (tools/tune_jacobi.py): 4 warps x 32 rows, 3 rows of
+    // prefetch, 7 CTAs/SM, plain (write-back) stores
+    return jacobi2d_launch<4, 32, 3, 7, false>(s, v2, src, dst, N, r0, r1, c0, c1, dirty, push_top, push_bot);
 }
 
 cudaError_t reduce_f64(cudaStream_t s, const double *x, const double *y, int64_t n,
@@ -1820,39 +1819,14 @@ cudaError_t gemm_f64(cudaStream_t s, const double *A, const double *B, double *C
     if (r1 <= r0 || c1 <= c0 || K <= 0) return cudaSuccess;
     const bool v16 = (K % 2 == 0) && (N % 2 == 0) && (c0 % 2 == 0) && ((uintptr_t)A % 16 == 0) &&
                      ((uintptr_t)B % 16 == 0) && ((uintptr_t)C % 16 == 0);
-    static int variant = -1;
-    if (variant < 0) {
-        const char *e = getenv("JACC_GEMM_VARIANT");
-        variant = e ? atoi(e) : 0;
-    }
-    if (variant == 0) {
+    {
         cudaError_t err = cudaSuccess;
         if (gemm_tma_launch(s, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push, err)) return err;
     }
-    switch (variant) {
-    case 1: return gemm_launch<64, 64, 32, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 2: return gemm_launch<128, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 3: return gemm_launch<128, 128, 16, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 4: return gemm_launch<64, 128, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 5: return gemm_launch<64, 64, 16, 4, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 6: return gemm_launch<128, 128, 32, 3, 64, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 7: return gemm_launch<64, 64, 16, 3, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 8: return gemm_launch<64, 64, 16, 3, 32, 32, 16>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 9: return gemm_launch<64, 64, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 10: return gemm_launch<64, 128, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 11: return gemm_launch<64, 128, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 12: return gemm_launch<128, 128, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 13: return gemm_launch<64, 256, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 14: return gemm_launch<128, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 15: return gemm_launch<64, 64, 16, 3, 32, 32>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 16: return gemm_launch<64, 128, 16, 4, 32, 64, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 17: return gemm_launch<128, 128, 16, 3, 32, 64, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    case 18: return gemm_launch<64, 128, 16, 4, 32, 32, 16>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    // default: 64x128 CTA tile, 8 warps of 32x32, 4-stage cp.async ring,
-    // grouped rasterisation (tools/tune_gemm.py: 33.0 TFLOP/s vs 32.2 for
-    // the 64x64x3 tile, variant 15)
-    default: return gemm_launch<64, 128, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
-    }
+    // shapes TMA cannot describe (odd K or N, unaligned bases): the cp.async
+    // kernel, 64x128 CTA tile, 8 warps of 32x32, 4-stage ring, grouped
+    // rasterisation (tools/tune_gemm.py: 33.0 TFLOP/s at 8192^3)
+    return gemm_launch<64, 128, 16, 4, 32, 32, 8>(s, v16, A, B, C, M, N, K, r0, r1, c0, c1, dirty, push);
 }
 
 cudaError_t scatter_add_f64(cudaStream_t s, const int32_t *idx, const double *b, double *a,
@@ -1879,19 +1853,8 @@ cudaError_t himeno_stencil(cudaStream_t s, const float *p, const float *a, const
                            unsigned *ticket, double *out, u64 *dirty) {
     if (i1 <= i0 || j1 <= j0 || k1 <= k0) return cudaErrorInvalidValue;
     static_assert(kHimenoGrid <= kHimenoPartials, "partials buffer");
-    static int variant = -1;  // JACC_HIMENO_VARIANT: 1 = one CTA/SM (more registers)
-    if (variant < 0) {
-        const char *e = getenv("JACC_HIMENO_VARIANT");
-        variant = e ? atoi(e) : 0;
-    }
-    if (variant == 1)
-        himeno_stencil_kernel<1><<<kHimenoGrid, HT, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0,
-                                                            i1, j0, j1, k0, k1, omega, partials,
-                                                            ticket, out, dirty);
-    else
-        himeno_stencil_kernel<2><<<kHimenoGrid, HT, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0,
-                                                            i1, j0, j1, k0, k1, omega, partials,
-                                                            ticket, out, dirty);
+    himeno_stencil_kernel<2><<<kHimenoGrid, HT, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0, i1, j0,
+                                                        j1, k0, k1, omega, partials, ticket, out, dirty);
     return cudaGetLastError();
 }
 
@@ -1992,7 +1955,7 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
 cudaError_t merge_range(cudaStream_t s, const void *src, PeerPtrs dsts, const u64 *dirty,
                         int64_t elem, int64_t lo, int64_t hi) {
     if (hi <= lo || dsts.n == 0) return cudaSuccess;
-    merge_range_kernel<<<grid_for((hi - lo) * elem, 256 * 16 * 4, 148 * 8), 256, 0, s>>>(
+    merge_range_kernel<<<grid_for((hi - lo) * elem, 256 * 16 * 8, 148 * 16), 256, 0, s>>>(
         static_cast<const char *>(src), dsts, dirty, elem, lo, hi);
     return cudaGetLastError();
 }

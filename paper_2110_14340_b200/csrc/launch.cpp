@@ -340,6 +340,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
         }
     } swap;
     int qsel = 0;
+    std::vector<int> waits;
     const bool multiq = R.nq > 1;
     if (multiq) {
         std::vector<int64_t> rd, wr;
@@ -349,7 +350,6 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             if (L.a[k].kind == JACC_ARG_ARRAY_IN || L.a[k].kind == JACC_ARG_ARRAY_INOUT) rd.push_back(key);
             if (L.a[k].kind == JACC_ARG_ARRAY_OUT || L.a[k].kind == JACC_ARG_ARRAY_INOUT) wr.push_back(key);
         }
-        std::vector<int> waits;
         qsel = R.sched.schedule(rd, wr, async_id >= 0 ? async_id % R.nq : -1, waits);
         swap.saved.assign(n, nullptr);
         swap.partials.assign(n, nullptr);
@@ -762,6 +762,14 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             }
         }
     }
+    if (prof) {
+        TraceRec tr{R.trace_events++, loop_id, D->name, qsel, waits, {}, L.dup, R.policy, merged_bytes,
+                    R.last_start, R.prof.size()};
+        for (int q = 0; q < n; q++)
+            if (!multiq && (comm[R.mp ? R.me : 0][q] || R.comm_prev[R.mp ? R.me : 0][q]) && q != (R.mp ? R.me : 0))
+                tr.peers.push_back(q);
+        R.trace_pending.push_back(std::move(tr));
+    }
     R.dev[R.mp ? R.me : 0].bytes_merged += merged_bytes;
     R.last_bytes = merged_bytes;
     R.comm_prev = comm;
@@ -824,7 +832,11 @@ extern "C" {
 
 jacc_status jacc_launch(int loop_id, const jacc_range *range, const jacc_arg *args, int nargs,
                         int async_id) {
-    return guard([&]() { return do_launch(loop_id, range, args, nargs, async_id); });
+    const Desc *D = find_desc(loop_id);
+    nvtxRangePushA(D ? D->name : "jacc_launch");  // NVTX range per launch (host issue)
+    const jacc_status st = guard([&]() { return do_launch(loop_id, range, args, nargs, async_id); });
+    nvtxRangePop();
+    return st;
 }
 
 jacc_status jacc_wait(int async_id) {

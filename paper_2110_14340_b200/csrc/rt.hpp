@@ -41,6 +41,7 @@
 
 #include "jacc.h"
 #include "kernels.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 namespace jrt {
 
@@ -279,6 +280,22 @@ struct ProfRec {
     cudaEvent_t k0, k1, m1;
 };
 
+// D13 timing record of one launch, written as a JSON line once its events
+// resolve ({event, kernel_id, queue, waits[], t_kernel_s,
+// t_comm_s, mode, bytes_exchanged}; jacc_set_trace)
+struct TraceRec {
+    uint64_t event;
+    int loop_id;
+    const char *name;
+    int queue;
+    std::vector<int> waits;  // queues this launch waited on (NEXT-4)
+    std::vector<int> peers;  // devices whose previous launch it waited on (merge ordering)
+    bool dup;
+    int policy;
+    uint64_t bytes;
+    size_t p0, p1;           // its ProfRecs: R.prof[p0, p1)
+};
+
 // one adaptive observation in flight: a launch's per-device events
 struct AdaptRec {
     std::string key;
@@ -318,6 +335,11 @@ struct Runtime {
     std::vector<std::vector<char>> comm_prev;  // [d][q]
     bool profiling = false;
     std::vector<ProfRec> prof;                 // unresolved event records
+    FILE *trace = nullptr;                     // JSON-lines trace (jacc_set_trace)
+    std::vector<TraceRec> trace_pending;
+    uint64_t trace_events = 0;
+    double trace_k = 0, trace_c = 0;           // summary totals (max over devices per launch)
+    std::map<std::string, std::pair<uint64_t, uint64_t>> trace_modes;  // name -> (multi, dup)
     size_t last_start = 0;                     // first record of the last launch
     std::vector<cudaEvent_t> evpool;
     double last_k = 0, last_m = 0;
@@ -472,9 +494,53 @@ inline cudaEvent_t pool_event() {
 
 // resolve the accumulated profiling records into totals (syncs on them;
 // called only on query, so timing never adds a host sync per launch)
+inline void write_trace(const std::vector<float> &ks, const std::vector<float> &ms) {
+    for (auto &t : R.trace_pending) {
+        double tk = 0, tc = 0;
+        for (size_t i = t.p0; i < t.p1 && i < ks.size(); i++) {
+            tk = std::max(tk, (double)ks[i] * 1e-3);
+            tc = std::max(tc, (double)ms[i] * 1e-3);
+        }
+        R.trace_k += tk;
+        R.trace_c += tc;
+        auto &mc = R.trace_modes[t.name];
+        (t.dup ? mc.second : mc.first)++;
+        if (!R.trace) continue;
+        std::string w, pe;
+        for (size_t i = 0; i < t.waits.size(); i++) w += (i ? "," : "") + std::to_string(t.waits[i]);
+        for (size_t i = 0; i < t.peers.size(); i++) pe += (i ? "," : "") + std::to_string(t.peers[i]);
+        fprintf(R.trace,
+                "{\"event\": %llu, \"kernel_id\": %d, \"kernel\": \"%s\", \"queue\": %d, "
+                "\"waits\": [%s], \"peer_waits\": [%s], \"t_kernel_s\": %.9g, \"t_comm_s\": %.9g, "
+                "\"mode\": \"%s\", \"merge\": \"%s\", \"bytes_exchanged\": %llu, \"devices\": %d}\n",
+                (unsigned long long)t.event, t.loop_id, t.name, t.queue, w.c_str(), pe.c_str(), tk, tc,
+                t.dup ? "dup" : "multi", t.policy == JACC_MERGE_HALO ? "halo" : "eager",
+                (unsigned long long)t.bytes, R.n);
+    }
+    R.trace_pending.clear();
+    if (R.trace) fflush(R.trace);
+}
+
+inline void close_trace() {
+    if (!R.trace) return;
+    std::string pm;
+    for (auto &kv : R.trace_modes)
+        pm += (pm.empty() ? "" : ", ") + std::string("\"") + kv.first + "\": {\"multi\": " +
+              std::to_string(kv.second.first) + ", \"dup\": " + std::to_string(kv.second.second) + "}";
+    fprintf(R.trace, "{\"summary\": {\"events\": %llu, \"total_kernel_s\": %.9g, \"total_comm_s\": %.9g, "
+                     "\"per_kernel_modes\": {%s}}}\n",
+            (unsigned long long)R.trace_events, R.trace_k, R.trace_c, pm.c_str());
+    fclose(R.trace);
+    R.trace = nullptr;
+}
+
 inline void flush_prof() {
-    if (R.prof.empty()) return;
+    if (R.prof.empty()) {
+        R.trace_pending.clear();
+        return;
+    }
     double kmax = 0, mmax = 0;
+    std::vector<float> ks(R.prof.size()), ms(R.prof.size());
     for (size_t i = 0; i < R.prof.size(); i++) {
         auto &p = R.prof[i];
         set_dev(p.dev);
@@ -482,6 +548,8 @@ inline void flush_prof() {
         float k = 0, m = 0;
         CK(cudaEventElapsedTime(&k, p.k0, p.k1));
         CK(cudaEventElapsedTime(&m, p.k1, p.m1));
+        ks[i] = k;
+        ms[i] = m;
         R.dev[p.dev].kernel_s += k * 1e-3;
         R.dev[p.dev].merge_s += m * 1e-3;
         if (i >= R.last_start) {
@@ -497,6 +565,7 @@ inline void flush_prof() {
         R.last_m = mmax;
         R.last_valid = true;
     }
+    write_trace(ks, ms);
     R.prof.clear();
     R.last_start = 0;
 }

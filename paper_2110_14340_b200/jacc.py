@@ -58,7 +58,7 @@ EXPORTS = [
     "jacc_adaptive_replay", "jacc_adaptive_history",
     "jacc_graph_begin", "jacc_graph_end", "jacc_graph_replay", "jacc_graph_destroy",
     "jacc_select_split_dim", "jacc_exchange_plan", "jacc_set_split_dim",
-    "jacc_set_scatter_split", "jacc_set_queues", "jacc_queue_replay", "jacc_get_info",
+    "jacc_set_scatter_split", "jacc_set_queues", "jacc_queue_replay", "jacc_get_info", "jacc_set_trace",
 ]
 JACC_MAX_QUEUES = 32
 JACC_ASYNC_AUTO = -2
@@ -136,6 +136,8 @@ for _name, _args in {
     "jacc_graph_replay": [_I, _I],
     "jacc_graph_destroy": [_I],
     "jacc_adaptive_history": [_I, _I, _P, _P, _P, _P, ctypes.POINTER(_I), ctypes.POINTER(_I)],
+    "jacc_set_trace": [ctypes.c_char_p],
+    "jacc_get_info": [ctypes.POINTER(jacc_info)],
 }.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
@@ -312,6 +314,12 @@ def jacc_get_stream(dev):
     s, o = ctypes.c_void_p(), ctypes.c_int()
     _ck(lib.jacc_get_stream(dev, ctypes.byref(s), ctypes.byref(o)), "jacc_get_stream")
     return s.value, o.value
+
+
+def jacc_set_trace(path):
+    """JSON-lines trace of every launch (D13); None closes it."""
+    p = None if path is None else str(path).encode()
+    return _ck(lib.jacc_set_trace(p), "jacc_set_trace")
 
 
 def jacc_get_info():

@@ -844,12 +844,14 @@ def test_himeno_subrange(J):
     assert np.array_equal(gp, p_ref)
 
 
-def test_himeno_XL_full_size(J):
-    """The paper's Size XL (1024x512x512) with the benchmark's
-    initial state, one iteration at n=1 (the bench launch configuration):
-    wrk2 and p bit-exact vs the oracle, gosa within 1e-12 of the compensated
-    reference."""
-    I, Jd, K = 1025, 513, 513
+@pytest.mark.parametrize("shape", [(1024, 512, 512), (1025, 513, 513)])
+def test_himeno_XL_full_size(J, shape):
+    """The paper's Size XL grid (1024x512x512; DESIGN R-17) with the
+    benchmark's initial state, one iteration at n=1 (the bench launch
+    configuration), and himenoBMT's 1025x513x513 allocation (rows off
+    16-byte alignment): wrk2 and p bit-exact vs the oracle, gosa within
+    1e-12 of the compensated reference."""
+    I, Jd, K = shape
     arrs = synth.himeno_init(I, Jd, K)
     gp, gw, gosas, _ = _himeno_gpu(J, arrs, 1, 1, 0)
     p, a, b, c, w1, bd = arrs
@@ -1385,3 +1387,48 @@ def test_async_queues_cross_device_same_queue(J, nq):
         J.jacc_update_host(A)
         J.jacc_update_host(B)
     assert np.array_equal(A, Ar) and np.array_equal(B, Br)
+
+
+# --------------------------------------------------------------------------
+# D13 trace records and runtime facts (jacc_get_info)
+# --------------------------------------------------------------------------
+def test_trace_json_lines(J, tmp_path):
+    import json
+    N = 130
+    A = synth.uniform_f64(N * N, 117, 1).reshape(N, N)
+    B = synth.uniform_f64(N * N, 117, 2).reshape(N, N)
+    x = synth.dyadic_f64(5000, 117, 3)
+    path = tmp_path / "trace.jsonl"
+    with runtime(J, 3, 1):
+        _create(J, A, B, x)
+        J.jacc_set_trace(path)
+        for _ in range(2):
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, A), _out(J, B)], 0)
+            J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, None, [_in(J, B), _out(J, A)], 0)
+        s = np.zeros(1)
+        J.jacc_launch(J.JACC_LOOP_SUM_F64, J.make_range(0, 5000),
+                      [_in(J, x), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s)])
+        J.jacc_set_trace(None)
+        info = J.jacc_get_info()
+    lines = [json.loads(l) for l in open(path)]
+    ev, summ = lines[:-1], lines[-1]["summary"]
+    assert [e["event"] for e in ev] == list(range(5))
+    assert [e["kernel"] for e in ev] == ["jacobi2d_f64"] * 4 + ["sum_f64"]
+    for e in ev[:4]:
+        assert e["merge"] == "halo" and e["mode"] == "multi" and e["devices"] == 3
+        assert e["t_kernel_s"] > 0 and e["t_comm_s"] >= 0
+        # HALO: device pushes of two boundary rows per interior boundary
+        assert e["bytes_exchanged"] == 2 * 2 * 8 * (N - 2)
+    assert ev[4]["bytes_exchanged"] == 0
+    assert summ["events"] == 5
+    assert summ["per_kernel_modes"]["jacobi2d_f64"] == {"multi": 4, "dup": 0}
+    assert abs(summ["total_kernel_s"] - sum(e["t_kernel_s"] for e in ev)) < 1e-6
+    assert info["n_devices"] == 3 and info["distinct_gpus"] == 0 and info["combine"] == "peer"
+    assert s[0] == orc.sum_f64(x, 0.0)
+
+
+def test_info_single_device(J):
+    with runtime(J, 1):
+        info = J.jacc_get_info()
+    assert info == {"n_devices": 1, "distinct_gpus": 1, "combine": "peer", "peer_pairs": 0,
+                    "multiprocess": 0, "rank": 0}

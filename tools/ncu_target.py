@@ -99,7 +99,7 @@ def main():
             for arr in (idx, b, a):
                 J.jacc_data_delete(arr)
     elif which == "himeno":
-        I, Jd, K = 1025, 513, 513
+        I, Jd, K = 1024, 512, 512
         arrs = synth.himeno_init(I, Jd, K)
         w2 = np.zeros_like(arrs[0])
         for arr in list(arrs) + [w2]:

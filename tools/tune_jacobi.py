@@ -1,4 +1,5 @@
-"""Time the Jacobi-2D sweep variants (JACC_JACOBI_VARIANT) at J16K, n=1.
+"""Time the Jacobi-2D sweep variants (JACC_JACOBI_VARIANT) at J16K, n=1; the
+variants exist only in a build with -DJACC_TUNING_VARIANTS (not the product).
     python tools/tune_jacobi.py            # all variants, one process each
 """
 import json
