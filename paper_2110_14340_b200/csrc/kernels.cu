@@ -771,25 +771,92 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
 }
 
 // ---------------------------------------------------------------------------
-// BK4b destination-binned scatter, single pass over the updates (see
-// kernels.cuh).  Owned pairs are partitioned into buckets of 2^shift
-// elements of `a`, written into pages of PG_P pairs that each bucket claims
-// from a pool as its stream grows; the apply walks the buckets in order so
-// the read-modify-writes of `a` are L2 hits, and after each bucket's pages a
-// bits item rebuilds that bucket's dirty-bitmap words in shared memory
-// while its keys are still L2-resident.
+// BK4b destination-binned scatter (see kernels.cuh).  Owned pairs are binned
+// by bucket of 2^shift elements of `a`: (1) histogram of the owned keys per
+// bucket, (2) scan -> bucket bases, (3) partition through shared-memory
+// staging into bucket-contiguous streams (one global stream per bucket, so
+// every tile's segment extends the bucket's current lines: full-line
+// writes), (4) apply the pairs in stream order through a dynamic chunk
+// counter (the chunks in flight span ~one bucket: the read-modify-writes of
+// `a` are L2 hits), (5) dirty bits per bucket from the partitioned keys.
+// Index arithmetic is 32-bit where the values allow (keys, spans < 2^31):
+// the partition is issue-limited as much as latency-limited.
 // ---------------------------------------------------------------------------
 constexpr int SB_T = 256;        // partition CTA; tile = SB_T * SB_E updates
 constexpr int SB_E = 16;
-constexpr int SB_MINB = 2;       // partition CTAs per SM (persistent grid)
 constexpr int SB_MAXB = 1024;    // max buckets
-constexpr int MP_LOG = 9;        // mini-page = 512 pairs
-constexpr int MP = 1 << MP_LOG;
-constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;  // buckets per thread in the reservation
-constexpr int SA_T = 1024;       // apply CTA (one per SM)
-constexpr int SA_G = 16;         // mini-pages per apply item (<= 8192 pairs)
-constexpr int SA_B = 2;          // apply items per dequeue
-static_assert(SA_T % SA_G == 0 && MP % (SA_T / SA_G) == 0, "apply item shape");
+constexpr int SA_CH = 4096;      // apply chunk (pairs)
+constexpr int SA_BPS = 3;        // apply CTAs of 256 threads per SM
+constexpr int SBITS_LB = 20;     // bits pass: 2^20 elements (128 KB of bits) per CTA item
+
+__device__ __forceinline__ bool owned(int32_t k, int32_t lo, unsigned span) {
+    return (unsigned)(k - lo) < span;
+}
+
+__global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restrict__ idx, int64_t n,
+                                                        int32_t lo, unsigned span, int shift, int nb,
+                                                        u64 *counts) {
+    __shared__ unsigned h[SB_MAXB];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t hd = (int64_t)((16 - ((uintptr_t)idx & 15)) & 15) >> 2;
+    if (hd > n) hd = n;
+    const int64_t n4 = (n - hd) >> 2;
+    const int4 *idx4 = reinterpret_cast<const int4 *>(idx + hd);
+    auto put = [&](int32_t k) {
+        if (owned(k, lo, span)) atomicAdd(&h[(unsigned)(k - lo) >> shift], 1u);
+    };
+    if (tid < hd) put(idx[tid]);
+#pragma unroll 4
+    for (int64_t q = tid; q < n4; q += nth) {
+        const int4 k = __ldcs(idx4 + q);
+        put(k.x);
+        put(k.y);
+        put(k.z);
+        put(k.w);
+    }
+    for (int64_t i = hd + 4 * n4 + tid; i < n; i += nth) put(idx[i]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+        if (h[i]) atomicAdd(&counts[i], (u64)h[i]);
+}
+
+// exclusive scan of counts[0..nb) -> base[0..nb] and cursor = base (one
+// block of 1024 threads: nb <= SB_MAXB); also zeroes the apply's counter
+__global__ void __launch_bounds__(1024) scat_scan_kernel(const u64 *counts, int nb, u64 *base,
+                                                         u64 *cursor, u64 *work) {
+    __shared__ u64 wsum[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const u64 c = t < nb ? counts[t] : 0;
+    u64 inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const u64 x = wsum[lane];
+        u64 y = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 v = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += v;
+        }
+        wsum[lane] = y - x;
+    }
+    __syncthreads();
+    const u64 ex = wsum[w] + inc - c;
+    if (t < nb) {
+        base[t] = ex;
+        cursor[t] = ex;
+    }
+    if (t == nb - 1) base[nb] = ex + c;
+    if (t == 0) *work = 0;
+}
 
 // warp 0 computes the exclusive scan of hist[0..nb) into off[]
 __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off, int nb,
@@ -815,122 +882,55 @@ __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off,
     if (lane == 31) *total = inc;
 }
 
-// block-wide exclusive scan of v (one value per thread, blockDim.x <= 1024);
-// returns the exclusive prefix, *tot = the sum
-__device__ __forceinline__ unsigned block_exscan(unsigned v, unsigned *wsum, unsigned *tot) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    unsigned inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned x = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += x;
-    }
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        const unsigned x = lane < nw ? wsum[lane] : 0u;
-        unsigned y = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned z = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += z;
-        }
-        wsum[lane] = y - x;
-        if (lane == 31) *tot = y;
-    }
-    __syncthreads();
-    const unsigned r = wsum[w] + inc - v;
-    __syncthreads();
-    return r;
-}
-
-// shared-memory layout of the partition: per-bucket state sized by nb
-__host__ __device__ constexpr size_t part_smem(int nb, int esz) {
-    return (size_t)((nb + 1) & ~1) * 4 * 7 + (size_t)SB_T * SB_E * (esz + 4);
-}
-
-// Partition (persistent: SB_MINB CTAs per SM, tiles grid-strided).  Each
-// CTA owns a static range of `cap` mini-pages of MP pairs and keeps, per
-// bucket, a current mini-page and its fill in shared memory, so reserving a
-// tile's bucket segments needs no global round trip: a segment continues
-// the bucket's current mini-page and takes consecutive fresh mini-pages from
-// the CTA's range when it fills.  Per tile: keys (then the owned values)
-// into registers, ranks by shared-memory atomics, warp scan, reservation,
-// staging in bucket order in shared memory, bucket-contiguous write-out.
-// Claimed mini-pages are logged (pbucket[pid] = bucket, np[b] += 1); each
-// gets its pair count in pcnt once: MP when it is left full, its fill when
-// it is the bucket's current page at the end.
-constexpr unsigned MP_NONE = 0xffffffffu;
+// Partition.  Per tile: all keys of a thread, then the values of its owned
+// ones (two batches of independent loads), ranks by shared-memory atomics,
+// warp scan, one cursor reservation per non-empty bucket (global atomic;
+// gdst[b] = stream position of the tile's segment minus its staging offset),
+// staging in bucket order, bucket-contiguous write-out.
 template <typename T>
-__global__ void __launch_bounds__(SB_T, SB_MINB) scat_part_kernel(
-    const int32_t *__restrict__ idx, const T *__restrict__ b, int64_t n, int64_t lo, int64_t hi,
-    int shift, int nb, unsigned cap, unsigned *np, unsigned *used, unsigned *pbucket,
-    unsigned *pcnt, int32_t *__restrict__ pk, T *__restrict__ pv) {
+__global__ void __launch_bounds__(SB_T, 2) scat_part_kernel(const int32_t *__restrict__ idx,
+                                                            const T *__restrict__ b, int64_t n,
+                                                            int32_t lo, unsigned span, int shift,
+                                                            int nb, u64 *cursor,
+                                                            int32_t *__restrict__ pidx,
+                                                            T *__restrict__ pval) {
     constexpr int E = SB_E, TILE = SB_T * E;
-    extern __shared__ __align__(16) unsigned char sdyn[];
-    const int nb2 = (nb + 1) & ~1;
-    unsigned *hist = reinterpret_cast<unsigned *>(sdyn);
-    unsigned *loff = hist + nb2, *cpg = loff + nb2, *cfill = cpg + nb2;   // current page, its fill
-    unsigned *opg = cfill + nb2, *ofill = opg + nb2, *npg = ofill + nb2;  // this tile: old page/fill, first fresh page
-    T *sv = reinterpret_cast<T *>(npg + nb2);
-    int32_t *sk = reinterpret_cast<int32_t *>(sv + TILE);
-    __shared__ unsigned total, next;  // next: first unclaimed mini-page of this CTA's range
+    __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB];
+    __shared__ u64 gdst[SB_MAXB];
+    __shared__ unsigned total;
+    extern __shared__ __align__(16) unsigned char sdyn[];  // [TILE] T, [TILE] i32
+    T *sv = reinterpret_cast<T *>(sdyn);
+    int32_t *sk = reinterpret_cast<int32_t *>(sdyn + TILE * sizeof(T));
     const int tid = threadIdx.x;
-    const unsigned pbase = blockIdx.x * cap;
-    for (int i = tid; i < nb; i += SB_T) {
-        cpg[i] = MP_NONE;
-        cfill[i] = MP;  // no room: the first segment claims
-    }
-    if (tid == 0) next = 0;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int32_t *ti = idx + t * TILE + tid;
+        const T *tb = b + t * TILE + tid;
+        const int rem = (int)(n - t * TILE < TILE ? n - t * TILE : TILE) - tid;  // valid: j*SB_T < rem
         int32_t k[E];
         T v[E];
 #pragma unroll
-        for (int j = 0; j < E; j++) {
-            const int64_t i = t * TILE + j * SB_T + tid;
-            k[j] = i < n ? __ldcs(idx + i) : (int32_t)lo - 1;  // lo-1: not owned
-        }
+        for (int j = 0; j < E; j++) k[j] = j * SB_T < rem ? __ldcs(ti + j * SB_T) : lo - 1;
 #pragma unroll
-        for (int j = 0; j < E; j++) {
-            const int64_t i = t * TILE + j * SB_T + tid;
-            if (k[j] >= lo && k[j] < hi) v[j] = __ldcs(b + i);
-        }
+        for (int j = 0; j < E; j++)
+            if (owned(k[j], lo, span)) v[j] = __ldcs(tb + j * SB_T);
         for (int i = tid; i < nb; i += SB_T) hist[i] = 0;
         __syncthreads();
         unsigned rk[E];
 #pragma unroll
         for (int j = 0; j < E; j++)
-            if (k[j] >= lo && k[j] < hi) rk[j] = atomicAdd(&hist[(int)(((int64_t)k[j] - lo) >> shift)], 1u);
+            if (owned(k[j], lo, span)) rk[j] = atomicAdd(&hist[(unsigned)(k[j] - lo) >> shift], 1u);
         __syncthreads();
         if (tid < 32) warp_exscan(hist, loff, nb, &total);
+        __syncthreads();
         for (int i = tid; i < nb; i += SB_T) {
             const unsigned c = hist[i];
-            if (!c) continue;
-            const unsigned f = cfill[i], room = MP - f;
-            opg[i] = cpg[i];
-            ofill[i] = f;
-            if (c <= room) {
-                cfill[i] = f + c;
-                continue;
-            }
-            const unsigned kn = (c - room + MP - 1) >> MP_LOG;  // fresh mini-pages
-            const unsigned p = pbase + atomicAdd(&next, kn);
-            npg[i] = p;
-            if (cpg[i] != MP_NONE) pcnt[cpg[i]] = MP;  // left full
-            for (unsigned q = 0; q < kn; q++) {
-                pbucket[p + q] = (unsigned)i;
-                if (q + 1 < kn) pcnt[p + q] = MP;
-            }
-            atomicAdd(&np[i], kn);
-            cpg[i] = p + kn - 1;
-            cfill[i] = c - room - ((kn - 1) << MP_LOG);
+            if (c) gdst[i] = atomicAdd(&cursor[i], (u64)c) - loff[i];
         }
-        __syncthreads();
 #pragma unroll
         for (int j = 0; j < E; j++)
-            if (k[j] >= lo && k[j] < hi) {
-                const unsigned pos = loff[(int)(((int64_t)k[j] - lo) >> shift)] + rk[j];
+            if (owned(k[j], lo, span)) {
+                const unsigned pos = loff[(unsigned)(k[j] - lo) >> shift] + rk[j];
                 sk[pos] = k[j];
                 sv[pos] = v[j];
             }
@@ -938,155 +938,106 @@ __global__ void __launch_bounds__(SB_T, SB_MINB) scat_part_kernel(
         const unsigned cnt = total;
         for (unsigned pos = tid; pos < cnt; pos += SB_T) {
             const int32_t kk = sk[pos];
-            const int bb = (int)(((int64_t)kk - lo) >> shift);
-            const unsigned vv = ofill[bb] + (pos - loff[bb]);  // slot counted from the old page
-            const unsigned pg = vv < MP ? opg[bb] : npg[bb] + ((vv - MP) >> MP_LOG);
-            const size_t g = ((size_t)pg << MP_LOG) | (vv & (MP - 1));
-            pk[g] = kk;
-            pv[g] = sv[pos];
+            const u64 g = gdst[(unsigned)(kk - lo) >> shift] + pos;
+            pidx[g] = kk;
+            pval[g] = sv[pos];
         }
         __syncthreads();
     }
-    for (int i = tid; i < nb; i += SB_T)
-        if (cpg[i] != MP_NONE) pcnt[cpg[i]] = cfill[i];
-    if (tid == 0) used[blockIdx.x] = next;
 }
 
-// Page list: every claimed mini-page, grouped by bucket (order inside a
-// bucket is free).  Block c walks partition CTA c's range.
-__global__ void __launch_bounds__(1024) scat_plist_kernel(const unsigned *__restrict__ np,
-                                                          const unsigned *__restrict__ used,
-                                                          const unsigned *__restrict__ pbucket,
-                                                          unsigned *cursor, unsigned *plist, int nb,
-                                                          unsigned cap) {
-    __shared__ unsigned pfx[SB_MAXB], wsum[32], tot;
-    const int t = threadIdx.x;
-    const unsigned x = block_exscan(t < nb ? np[t] : 0u, wsum, &tot);
-    if (t < nb) pfx[t] = x;
-    __syncthreads();
-    const unsigned base = blockIdx.x * cap, u = used[blockIdx.x];
-    for (unsigned j = t; j < u; j += blockDim.x) {
-        const unsigned bk = pbucket[base + j];
-        plist[pfx[bk] + atomicAdd(&cursor[bk], 1u)] = base + j;
-    }
-}
-
-// Apply (persistent, one CTA of SA_T threads per SM).  Work items, in list
-// order: for every bucket with pages, its pages in groups of SA_G (apply
-// items), then one bits item.  Each CTA derives the list from np[] (block
-// scans into shared memory) and maps a dequeued item to (bucket, group) by
-// binary search.  Apply item: every thread loads all its pairs of the
-// group first (MP/64 keys and values in flight), then issues their REDs
-// (a[k] += v; the buckets in flight are L2-resident).  Bits item: the
-// bucket's keys set bits of a shared-memory copy of the bucket's
-// dirty-bitmap words, written out once (plain stores; a bucket's first/last
-// word may be shared with its neighbour when lo is not 32-aligned: atomicOr
-// into the zeroed bitmap).  Dirty range: min/max over the applied keys.
+// Apply: pairs in stream (bucket) order through a dynamic chunk counter, so
+// the chunks in flight span ~one bucket of `a` and its read-modify-writes
+// hit L2; every thread loads all its pairs of the chunk before issuing
+// their REDs (SA_CH/256 keys and values in flight).
 template <typename T>
-__global__ void __launch_bounds__(SA_T, 1) scat_apply_kernel(
-    const unsigned *__restrict__ np, const unsigned *__restrict__ plist,
-    const unsigned *__restrict__ pcnt, int nb, unsigned *work, const int32_t *__restrict__ pk,
-    const T *__restrict__ pv, T *a, int64_t lo, int64_t hi, int shift, uint32_t *bitmap, u64 *dirty) {
-    constexpr int TPP = SA_T / SA_G;   // threads per mini-page
-    constexpr int PER = MP / TPP;      // pairs per thread per mini-page
-    extern __shared__ uint32_t sw[];
-    __shared__ unsigned ibase[SB_MAXB + 1], pfx[SB_MAXB + 1], wsum[32], tot;
-    __shared__ unsigned s_b[SA_B], s_q[SA_B];
-    const int t = threadIdx.x;
-    {
-        const unsigned c = t < nb ? np[t] : 0u;
-        const unsigned x = block_exscan(c, wsum, &tot);
-        if (t < nb) pfx[t] = x;
-        if (t == 0) pfx[nb] = tot;
-        const unsigned own = c ? (c + SA_G - 1) / SA_G + 1 : 0u;
-        const unsigned y = block_exscan(own, wsum, &tot);
-        if (t < nb) ibase[t] = y;
-        if (t == 0) ibase[nb] = tot;
-        __syncthreads();
-    }
-    const unsigned nitems = ibase[nb];
+__global__ void __launch_bounds__(256) scat_apply_kernel(const int32_t *__restrict__ pidx,
+                                                         const T *__restrict__ pval, const u64 *base,
+                                                         int nb, u64 *work, T *a, u64 *dirty) {
+    constexpr int PER = SA_CH / 256;
+    __shared__ u64 chunk;
+    const int64_t m = (int64_t)base[nb];
+    const int64_t nchunks = (m + SA_CH - 1) / SA_CH;
     u64 mn = kU64Max, mx = 0;
     for (;;) {
-        if (t == 0) {
-            const unsigned j0 = atomicAdd(work, (unsigned)SA_B);
-            for (int u = 0; u < SA_B; u++) {
-                const unsigned j = j0 + u;
-                s_b[u] = 0xffffffffu;
-                if (j >= nitems) continue;
-                int l = 0, r = nb - 1;  // last bucket with ibase[b] <= j
-                while (l < r) {
-                    const int m = (l + r + 1) >> 1;
-                    if (ibase[m] <= j) l = m;
-                    else r = m - 1;
-                }
-                s_b[u] = (unsigned)l;
-                s_q[u] = j - ibase[l];
+        if (threadIdx.x == 0) chunk = atomicAdd(work, 1ull);
+        __syncthreads();
+        const int64_t c = (int64_t)chunk;
+        __syncthreads();
+        if (c >= nchunks) break;
+        const int64_t p0 = c * SA_CH;
+        const int cnt = (int)(m - p0 < SA_CH ? m - p0 : SA_CH);
+        const int32_t *ck = pidx + p0 + threadIdx.x;
+        const T *cv = pval + p0 + threadIdx.x;
+        int32_t kk[PER];
+        T vv[PER];
+#pragma unroll
+        for (int e = 0; e < PER; e++) kk[e] = e * 256 + (int)threadIdx.x < cnt ? __ldcs(ck + e * 256) : -1;
+#pragma unroll
+        for (int e = 0; e < PER; e++)
+            if (kk[e] >= 0) vv[e] = __ldcs(cv + e * 256);
+#pragma unroll
+        for (int e = 0; e < PER; e++)
+            if (kk[e] >= 0) {
+                atomicAdd(a + kk[e], vv[e]);
+                mn = (u64)kk[e] < mn ? (u64)kk[e] : mn;
+                mx = (u64)kk[e] > mx ? (u64)kk[e] : mx;
             }
+    }
+    publish_dirty<8>(mn, mx, dirty);
+}
+
+// Dirty bitmap from the bucket-ordered keys: CTA item (bucket, part) owns
+// 2^SBITS_LB elements of the bucket (a 128 KB bitmap in shared memory),
+// scans the bucket's keys (16-byte loads), sets its bits with shared-memory
+// atomicOr and writes its words once (a part's first/last word may be
+// shared with the neighbour part when lo is not 32-aligned: atomicOr into
+// the zeroed bitmap).
+__global__ void __launch_bounds__(1024) scat_bits_kernel(const int32_t *__restrict__ pidx,
+                                                         const u64 *__restrict__ base, int nb,
+                                                         int shift, int64_t lo, int64_t hi,
+                                                         uint32_t *bitmap) {
+    extern __shared__ uint32_t sw[];
+    const int lp = shift > SBITS_LB ? shift - SBITS_LB : 0;  // log2 parts per bucket
+    const int pb = shift > SBITS_LB ? SBITS_LB : shift;      // log2 elements per part
+    const int64_t items = (int64_t)nb << lp;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int bk = (int)(it >> lp), q = (int)(it & ((1 << lp) - 1));
+        const int64_t e0 = lo + ((int64_t)bk << shift) + ((int64_t)q << pb);
+        if (e0 >= hi) continue;  // uniform per CTA
+        const int64_t e1 = e0 + ((int64_t)1 << pb) < hi ? e0 + ((int64_t)1 << pb) : hi;
+        const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
+        for (int i = threadIdx.x; i < nw; i += 1024) sw[i] = 0;
+        __syncthreads();
+        const u64 p0 = base[bk], p1 = base[bk + 1];
+        auto put = [&](int64_t k) {
+            if (k >= e0 && k < e1) atomicOr(&sw[(k >> 5) - w0], 1u << (k & 31));
+        };
+        u64 pa = (p0 + 3) & ~(u64)3;  // 16-byte loads for the aligned body
+        if (pa > p1) pa = p1;
+        const u64 n4 = (p1 - pa) >> 2, pt = pa + 4 * n4;
+        if (threadIdx.x < pa - p0) put(pidx[p0 + threadIdx.x]);
+        if (threadIdx.x < p1 - pt) put(pidx[pt + threadIdx.x]);
+        const int4 *k4 = reinterpret_cast<const int4 *>(pidx + pa);
+#pragma unroll 4
+        for (u64 q4 = threadIdx.x; q4 < n4; q4 += 1024) {
+            const int4 k = __ldcs(k4 + q4);
+            put(k.x);
+            put(k.y);
+            put(k.z);
+            put(k.w);
         }
         __syncthreads();
-        if (s_b[0] == 0xffffffffu) break;
-        for (int u = 0; u < SA_B; u++) {
-            const unsigned bk = s_b[u];
-            if (bk == 0xffffffffu) break;
-            const unsigned q = s_q[u], p0 = pfx[bk], npb = pfx[bk + 1] - p0;
-            const unsigned ng = (npb + SA_G - 1) / SA_G;
-            if (q < ng) {
-                const unsigned g = q * SA_G + (unsigned)(t / TPP);
-                if (g < npb) {
-                    const unsigned pid = plist[p0 + g];
-                    const unsigned pc = pcnt[pid];
-                    const size_t base = (size_t)pid << MP_LOG;
-                    const int off = t % TPP;
-                    int32_t kk[PER];
-                    T vv[PER];
-#pragma unroll
-                    for (int e = 0; e < PER; e++) {
-                        const unsigned s = off + e * TPP;
-                        kk[e] = s < pc ? pk[base + s] : -1;
-                    }
-#pragma unroll
-                    for (int e = 0; e < PER; e++) {
-                        const unsigned s = off + e * TPP;
-                        if (s < pc) vv[e] = __ldcs(pv + base + s);
-                    }
-#pragma unroll
-                    for (int e = 0; e < PER; e++)
-                        if (kk[e] >= 0) {
-                            atomicAdd(a + kk[e], vv[e]);
-                            mn = (u64)kk[e] < mn ? (u64)kk[e] : mn;
-                            mx = (u64)kk[e] > mx ? (u64)kk[e] : mx;
-                        }
-                }
-                continue;
+        for (int i = threadIdx.x; i < nw; i += 1024) {
+            const uint32_t v = sw[i];
+            if (i == 0 || i == nw - 1) {
+                if (v) atomicOr(bitmap + w0 + i, v);
+            } else {
+                bitmap[w0 + i] = v;
             }
-            const int64_t e0 = lo + ((int64_t)bk << shift);
-            const int64_t e1 = e0 + ((int64_t)1 << shift) < hi ? e0 + ((int64_t)1 << shift) : hi;
-            const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
-            for (int i = t; i < nw; i += SA_T) sw[i] = 0;
-            __syncthreads();
-            for (unsigned g = t / TPP; g < npb; g += SA_G) {
-                const unsigned pid = plist[p0 + g];
-                const unsigned pc = pcnt[pid];
-                const size_t base = (size_t)pid << MP_LOG;
-                for (unsigned s = t % TPP; s < pc; s += TPP) {
-                    const int32_t k = __ldcs(pk + base + s);
-                    atomicOr(&sw[(k >> 5) - w0], 1u << (k & 31));
-                }
-            }
-            __syncthreads();
-            for (int i = t; i < nw; i += SA_T) {
-                const uint32_t x = sw[i];
-                if (i == 0 || i == nw - 1) {
-                    if (x) atomicOr(bitmap + w0 + i, x);
-                } else {
-                    bitmap[w0 + i] = x;
-                }
-            }
-            __syncthreads();  // sw is reused by the next bits item
         }
         __syncthreads();
     }
-    publish_dirty<SA_T / 32>(mn, mx, dirty);
 }
 
 // ---------------------------------------------------------------------------
@@ -1876,29 +1827,16 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
     if (span <= 0 || n <= 0 || (force && force[0] == '0')) return p;
     if (!(force && force[0] == '1') && (n < (1 << 22) || span * elem <= (int64_t)96 << 20))
         return p;  // a fits in L2: the direct kernel is already L2-resident
-    // buckets of 2^20 elements (8 MiB of fp64, 4 MiB of int32): a bucket's
-    // dirty-bitmap words (128 KiB) fit one apply CTA's shared memory
-    const int shift = 20;
-    const int64_t nb = (span + ((int64_t)1 << shift) - 1) >> shift;
-    if (nb > SB_MAXB) return p;  // > 2^30 owned elements: the direct kernel
-    int dev = 0, nsm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-    const int64_t tile = (int64_t)SB_T * SB_E, tiles = (n + tile - 1) / tile;
-    p.grid = (int)std::min<int64_t>(tiles, (int64_t)nsm * SB_MINB);
-    const int64_t per_cta = (tiles + p.grid - 1) / p.grid;         // tiles per partition CTA
-    p.cap = (per_cta * tile + MP - 1) / MP + nb;                   // its mini-pages, worst case
-    p.npool = p.cap * p.grid;
-    if (p.npool >= ((int64_t)1 << 31)) return p;
+    if (hi > INT32_MAX) return p;  // keys are int32: never, kept for the 32-bit arithmetic
+    // buckets of 8 MiB of `a` (round 1: 8 MiB 4.18 ms vs 16 MiB 4.38, 4 MiB 5.73)
+    int shift = 0;
+    while (((int64_t)elem << shift) < ((int64_t)8 << 20)) shift++;
+    while (((span + ((int64_t)1 << shift) - 1) >> shift) > SB_MAXB) shift++;
     p.binned = true;
     p.shift = shift;
-    p.nb = (int)nb;
-    // zeroed state: np u32[nb] | cursor u32[nb] | work u32 ; then used u32[grid],
-    // pbucket u32[npool], pcnt u32[npool], plist u32[npool]; pages (keys, values)
-    p.state = (((size_t)nb * 8 + 16) + 255) & ~(size_t)255;
-    p.hdr = (p.state + (size_t)p.grid * 4 + (size_t)p.npool * 12 + 255) & ~(size_t)255;
-    p.scratch = p.hdr + (size_t)p.npool * MP * (4 + (size_t)elem);
+    p.nb = (int)((span + ((int64_t)1 << shift) - 1) >> shift);
+    p.hdr = ((size_t)(3 * p.nb + 2) * 8 + 255) & ~(size_t)255;
+    p.scratch = p.hdr + (((size_t)n * 4 + 255) & ~(size_t)255) + (size_t)n * elem;
     return p;
 }
 
@@ -1906,49 +1844,49 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
                                u64 *dirty, const ScatterPlan &pl, void *scratch) {
     char *sc = static_cast<char *>(scratch);
-    unsigned *np = reinterpret_cast<unsigned *>(sc);
-    unsigned *cursor = np + pl.nb;
-    unsigned *work = cursor + pl.nb;
-    unsigned *used = reinterpret_cast<unsigned *>(sc + pl.state);
-    unsigned *pbucket = used + pl.grid;
-    unsigned *pcnt = pbucket + pl.npool;
-    unsigned *plist = pcnt + pl.npool;
-    int32_t *pk = reinterpret_cast<int32_t *>(sc + pl.hdr);
-    char *pv = sc + pl.hdr + (size_t)pl.npool * MP * 4;
-    cudaError_t e = cudaMemsetAsync(sc, 0, pl.state, s);  // counters start at zero
+    u64 *counts = reinterpret_cast<u64 *>(sc);
+    u64 *cursor = counts + pl.nb;
+    u64 *base = cursor + pl.nb;  // nb + 1
+    u64 *work = base + pl.nb + 1;
+    int32_t *pidx = reinterpret_cast<int32_t *>(sc + pl.hdr);
+    char *pv = sc + pl.hdr + (((size_t)n * 4 + 255) & ~(size_t)255);
+    const int32_t lo32 = (int32_t)lo;
+    const unsigned span = (unsigned)(hi - lo);
+    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)pl.nb * 8, s);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
-    const int pdsm = (int)part_smem(pl.nb, is_f64 ? 8 : 4);
-    const int adsm = (int)((((int64_t)1 << pl.shift) >> 5) + 2) * 4;
-    const unsigned cap = (unsigned)pl.cap;
+    scat_hist_kernel<<<nsm * 8, 256, 0, s>>>(idx, n, lo32, span, pl.shift, pl.nb, counts);
+    scat_scan_kernel<<<1, 1024, 0, s>>>(counts, pl.nb, base, cursor, work);
+    const int64_t tile = (int64_t)SB_T * SB_E;
+    const int pg = (int)std::min<int64_t>((n + tile - 1) / tile, (int64_t)nsm * 8);
+    const int pdsm = (int)tile * ((is_f64 ? 8 : 4) + 4);
     // attributes are per device: set on every call (host-side, cheap)
     if (is_f64) {
         cudaFuncSetAttribute(scat_part_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-        cudaFuncSetAttribute(scat_apply_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, adsm);
-        scat_part_kernel<double><<<pl.grid, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo, hi,
-                                                             pl.shift, pl.nb, cap, np, used, pbucket,
-                                                             pcnt, pk, reinterpret_cast<double *>(pv));
+        scat_part_kernel<double><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo32, span,
+                                                        pl.shift, pl.nb, cursor, pidx,
+                                                        reinterpret_cast<double *>(pv));
+        scat_apply_kernel<double><<<nsm * SA_BPS, 256, 0, s>>>(pidx, reinterpret_cast<const double *>(pv),
+                                                               base, pl.nb, work, static_cast<double *>(a),
+                                                               dirty);
     } else {
         cudaFuncSetAttribute(scat_part_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-        cudaFuncSetAttribute(scat_apply_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, adsm);
-        scat_part_kernel<int32_t><<<pl.grid, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo, hi,
-                                                              pl.shift, pl.nb, cap, np, used, pbucket,
-                                                              pcnt, pk, reinterpret_cast<int32_t *>(pv));
+        scat_part_kernel<int32_t><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32, span,
+                                                         pl.shift, pl.nb, cursor, pidx,
+                                                         reinterpret_cast<int32_t *>(pv));
+        scat_apply_kernel<int32_t><<<nsm * SA_BPS, 256, 0, s>>>(pidx, reinterpret_cast<const int32_t *>(pv),
+                                                                base, pl.nb, work,
+                                                                static_cast<int32_t *>(a), dirty);
     }
-    scat_plist_kernel<<<pl.grid, 1024, 0, s>>>(np, used, pbucket, cursor, plist, pl.nb, cap);
-    if (is_f64)
-        scat_apply_kernel<double><<<nsm, SA_T, adsm, s>>>(np, plist, pcnt, pl.nb, work, pk,
-                                                          reinterpret_cast<const double *>(pv),
-                                                          static_cast<double *>(a), lo, hi, pl.shift,
-                                                          bitmap, dirty);
-    else
-        scat_apply_kernel<int32_t><<<nsm, SA_T, adsm, s>>>(np, plist, pcnt, pl.nb, work, pk,
-                                                           reinterpret_cast<const int32_t *>(pv),
-                                                           static_cast<int32_t *>(a), lo, hi, pl.shift,
-                                                           bitmap, dirty);
+    const int pb = pl.shift > SBITS_LB ? SBITS_LB : pl.shift;
+    const int smem = (int)((((int64_t)1 << pb) >> 5) + 2) * 4;
+    cudaFuncSetAttribute(scat_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int64_t items = (int64_t)pl.nb << (pl.shift - pb);
+    const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
+    scat_bits_kernel<<<g, 1024, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap);
     return cudaGetLastError();
 }
 

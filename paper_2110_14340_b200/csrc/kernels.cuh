@@ -60,25 +60,18 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
                             int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap, u64 *dirty);
 
 // BK4b Same loop, executed as a destination-binned pipeline for arrays far
-// larger than L2, in one pass over the updates: (1) a persistent partition
-// writes the owned (k, b[i]) pairs, bucket-contiguously through shared-memory
-// staging, into mini-pages of 512 pairs; every CTA hands out mini-pages of
-// its own static range to its buckets as they fill (no histogram pass, no
-// global round trip per tile); (2) the claimed mini-pages are listed bucket
-// by bucket; (3) one persistent kernel applies them bucket by bucket (buckets
-// of 2^shift elements), so the read-modify-writes of a hit L2 and every line
-// of a moves to/from HBM about once, and after each bucket rebuilds its
-// dirty-bitmap words in shared memory from the bucket's keys.  Dirty range
-// fused.  is_f64: T = double, else int32.  The scratch's state region is
-// zeroed by the wrapper on every call.
+// larger than L2: (1) histogram of the owned keys per 8 MiB bucket of a,
+// (2) scan, (3) partition of the (k, b[i]) pairs into bucket-contiguous
+// streams through shared-memory staging (coalesced, full-line writes),
+// (4) apply the pairs in stream order, so the read-modify-writes of a hit
+// L2 and every line of a moves to/from HBM about once, (5) dirty bits per
+// bucket part in shared memory, each bitmap word written once.  Dirty range
+// fused into (4).  is_f64: T = double, else int32.
 struct ScatterPlan {
     bool binned;
     int shift, nb;      // bucket = 2^shift elements, nb buckets
-    int grid;           // partition CTAs
-    int64_t cap;        // mini-pages per partition CTA
-    int64_t npool;      // mini-pages in all
-    size_t state, hdr;  // bytes: zeroed counters | page log and list; pages at hdr
-    size_t scratch;     // total scratch bytes
+    size_t hdr;         // bytes of counters/bases at the start of the scratch
+    size_t scratch;     // total scratch bytes (header + n keys + n values)
 };
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem);
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
