@@ -624,6 +624,31 @@ def _hbm_roof(achieved, peak, peak_src, kernels, algo, k, traffic_keys):
             "peak_source": peak_src}
 
 
+def cublas_dgemm_tflops(torch, A, B, reps=5):
+    """cuBLAS DGEMM (torch.matmul on fp64 device tensors) on the same inputs:
+    the measured fp64 tensor-pipe reference for the GEMM roofline (a library
+    GEMM used as the denominator only, never on the product path)."""
+    try:
+        a = torch.from_numpy(A).cuda()
+        b = torch.from_numpy(B).cuda()
+        torch.matmul(a, b)
+        torch.cuda.synchronize()
+        best = None
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            best = t if best is None or t < best else best
+        del a, b
+        torch.cuda.empty_cache()
+        return 2 * A.shape[0] * A.shape[1] * B.shape[1] / best / 1e12
+    except Exception:
+        return None
+
+
 def run_loops(J, C, n, peaks, args):
     """The other BASELINE configs (DOT 2^30, GEMM 8192^3, SCAT 2^28 f64 and
     int32) and Himeno XL, timed through the same C-ABI.  Each entry carries
@@ -672,6 +697,9 @@ def run_loops(J, C, n, peaks, args):
     t, k, m = _time_loop(J, C, launch, 3)
     fl = 2 * G**3
     dg, dsrc = load_dgemm_peak()
+    dg_run = cublas_dgemm_tflops(C.torch, Ag, Bg)  # same box, same run: the fp64 reference
+    if dg_run:
+        dg, dsrc = dg_run, "torch.matmul fp64 (cuBLAS DGEMM) 8192^3 timed in this run"
     scaled = float(peaks.get("bf16_tflops", 0)) * FP64_PER_BF16
     te = _e2e(J, C, [Ag, Bg], launch, [Cg], reps=1)
     traffic, tsrc = load_traffic("gemm")
