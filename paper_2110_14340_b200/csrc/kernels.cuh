@@ -65,8 +65,10 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
 // streams through shared-memory staging (coalesced, full-line writes),
 // (4) apply the pairs in stream order, so the read-modify-writes of a hit
 // L2 and every line of a moves to/from HBM about once, (5) dirty bits per
-// bucket part in shared memory, each bitmap word written once.  Dirty range
-// fused into (4).  is_f64: T = double, else int32.
+// bucket part in shared memory, each bitmap word written once; (5) runs on
+// stream s2 (fork/join events) beside (4) and follows its progress, reading
+// the keys (4) just brought into L2 (s2 == nullptr: after (4) on s).  Dirty
+// range fused into (4).  is_f64: T = double, else int32.
 struct ScatterPlan {
     bool binned;
     int shift, nb;      // bucket = 2^shift elements, nb buckets
@@ -76,7 +78,8 @@ struct ScatterPlan {
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem);
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
-                               u64 *dirty, const ScatterPlan &pl, void *scratch);
+                               u64 *dirty, const ScatterPlan &pl, void *scratch, cudaStream_t s2,
+                               cudaEvent_t fork, cudaEvent_t join);
 
 // NEXT-2  Himeno benchmark (DESIGN R-17), fp32, row-major
 // [I][J][K] arrays (a: 4, b and c: 3 stacked arrays).  Stencil loop over

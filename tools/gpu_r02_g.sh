@@ -4,6 +4,12 @@
 # sync overhead probe; isolated ncu of the BK5 merge kernels
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
+for l in scat_f64 scat_i32; do timeout 300 python tools/time_loop.py $l 5 >> gpurun_out/time_g.jsonl 2>> gpurun_out/time_g.err; done
+cat gpurun_out/time_g.jsonl; tail -2 gpurun_out/time_g.err
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_scat_g.csv python tools/ncu_target.py scatter 2 > /dev/null 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -m gpu -x --timeout 600 -k "scatter or graph" > gpurun_out/gpu_tests_g.log 2>&1; tail -2 gpurun_out/gpu_tests_g.log
+timeout 600 python tools/stress_scatter.py 20 i32_3 f64_2 > gpurun_out/stress_g.jsonl 2> gpurun_out/stress_g.err
+timeout 600 python tools/stress_scatter.py 4 full_f64 full_i32 >> gpurun_out/stress_g.jsonl 2>> gpurun_out/stress_g.err; cat gpurun_out/stress_g.jsonl
 for n in 1 2 4 8; do
   timeout 900 python bench.py --gpus $n --steps 3 --warmup 2 --no-extra --no-cpu-baseline > gpurun_out/bench_sp$n.json 2> gpurun_out/bench_sp$n.err
   tail -1 gpurun_out/bench_sp$n.err
