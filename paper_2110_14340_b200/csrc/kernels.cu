@@ -788,7 +788,7 @@ constexpr int SB_MAXB = 1024;    // max buckets
 constexpr int SA_CH = 4096;      // apply chunk (pairs)
 constexpr int SA_BPS = 3;        // apply CTAs of 256 threads per SM
 constexpr int SBITS_LB = 20;     // bits pass: 2^20 elements (128 KB of bits) per CTA item
-constexpr int SBITS_T = 512;     // bits CTA (co-resident with SA_BPS apply CTAs)
+constexpr int SBITS_T = 1024;    // bits CTA (co-resident with SA_BPS apply CTAs)
 
 __device__ __forceinline__ bool owned(int32_t k, int32_t lo, unsigned span) {
     return (unsigned)(k - lo) < span;
@@ -990,7 +990,7 @@ __global__ void __launch_bounds__(256, SA_BPS) scat_apply_kernel(const int32_t *
 // into L2 by the apply (no extra HBM pass).  The wait gives up after
 // SBITS_IDLE polls without apply progress (kernels serialised, e.g. under a
 // profiler): correctness never depends on it, only where the keys come from.
-constexpr int SBITS_IDLE = 2000;  // x ~100 ns
+constexpr int SBITS_IDLE = 200;   // x ~1 us
 __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__restrict__ pidx,
                                                             const u64 *__restrict__ base, int nb,
                                                             int shift, int64_t lo, int64_t hi,
@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__res
             const u64 need = (p1 + SA_CH - 1) / SA_CH;
             u64 last = *(volatile const u64 *)work;
             for (int idle = 0; last < need && idle < SBITS_IDLE;) {
-                __nanosleep(100);
+                __nanosleep(1000);  // polls stay off the apply's counter
                 const u64 w = *(volatile const u64 *)work;
                 if (w != last) {
                     last = w;
@@ -1558,46 +1558,72 @@ template <typename T>
 __global__ void __launch_bounds__(256) merge_bitmap_kernel(const T *__restrict__ src, PeerPtrs dsts,
                                                            const uint32_t *__restrict__ bitmap,
                                                            int64_t lo, int64_t hi) {
-    // One warp per group of 32 words (1024 elements); lane l holds word
-    // w0+l.  Sparse groups (<= 96 set bits): every lane copies its own
-    // word's elements (32 independent chains).  Dense groups: the warp walks
-    // the words 8 at a time, lane l moving element l of each, so the 8 loads
-    // are in flight together and each word goes out as one coalesced
+    // One warp per 4 groups of 32 words (4096 elements); lane l holds words
+    // w0 + l + 32u (u < 4, loaded together).  Sparse iterations (every lane
+    // <= 8 set bits in its 4 words): each lane gathers its elements' indices
+    // and issues all their loads before the stores.  Dense groups: the warp
+    // walks a group's words 8 at a time, lane l moving element l of each, so
+    // 8 loads are in flight per lane and each word goes out as one coalesced
     // 128/256-byte segment per peer.
+    constexpr int G = 4, SP = 8;
     const int lane = threadIdx.x & 31;
     const int64_t wlo = lo >> 5, whi = (hi + 31) >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w0 = wlo + gw * 32; w0 < whi; w0 += nw * 32) {
-        const uint32_t mine = (w0 + lane < whi) ? __ldg(bitmap + w0 + lane) : 0u;
-        const int tot = __reduce_add_sync(0xffffffffu, __popc(mine));
-        if (tot == 0) continue;
-        if (tot <= 96) {
-            uint32_t m = mine;
-            while (m) {
-                const int bp = __ffs(m) - 1;
-                m &= m - 1;
-                const int64_t e = ((w0 + lane) << 5) + bp;
-                const T v = src[e];
-                for (int d = 0; d < dsts.n; d++) static_cast<T *>(dsts.p[d])[e] = v;
+    for (int64_t w0 = wlo + gw * 32 * G; w0 < whi; w0 += nw * 32 * G) {
+        uint32_t m[G];
+        int cnt = 0;
+#pragma unroll
+        for (int u = 0; u < G; u++) {
+            const int64_t w = w0 + 32 * u + lane;
+            m[u] = w < whi ? __ldg(bitmap + w) : 0u;
+            cnt += __popc(m[u]);
+        }
+        if (__reduce_max_sync(0xffffffffu, (unsigned)cnt) <= SP) {
+            int64_t e[SP];
+            int k = 0;
+#pragma unroll
+            for (int u = 0; u < G; u++) {
+                uint32_t x = m[u];
+                while (x) {
+                    const int bp = __ffs(x) - 1;
+                    x &= x - 1;
+                    e[k < SP ? k : SP - 1] = ((w0 + 32 * u + lane) << 5) + bp;
+                    k++;
+                }
+            }
+            T v[SP];
+#pragma unroll
+            for (int j = 0; j < SP; j++)
+                if (j < k) v[j] = src[e[j]];
+            for (int d = 0; d < dsts.n; d++) {
+                T *dp = static_cast<T *>(dsts.p[d]);
+#pragma unroll
+                for (int j = 0; j < SP; j++)
+                    if (j < k) dp[e[j]] = v[j];
             }
             continue;
         }
 #pragma unroll 1
-        for (int j0 = 0; j0 < 32; j0 += 8) {
-            T v[8];
-            bool on[8];
+        for (int u = 0; u < G; u++) {
+            const int64_t g0 = w0 + 32 * u;
+            if (__ballot_sync(0xffffffffu, m[u] != 0u) == 0u) continue;
+#pragma unroll 1
+            for (int j0 = 0; j0 < 32; j0 += 8) {
+                T v[8];
+                bool on[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const uint32_t bits = __shfl_sync(0xffffffffu, mine, j0 + u);
-                on[u] = (bits >> lane) & 1u;
-                if (on[u]) v[u] = __ldcs(src + ((w0 + j0 + u) << 5) + lane);
-            }
-            for (int d = 0; d < dsts.n; d++) {
-                T *dp = static_cast<T *>(dsts.p[d]);
+                for (int q = 0; q < 8; q++) {
+                    const uint32_t bits = __shfl_sync(0xffffffffu, m[u], j0 + q);
+                    on[q] = (bits >> lane) & 1u;
+                    if (on[q]) v[q] = __ldcs(src + ((g0 + j0 + q) << 5) + lane);
+                }
+                for (int d = 0; d < dsts.n; d++) {
+                    T *dp = static_cast<T *>(dsts.p[d]);
 #pragma unroll
-                for (int u = 0; u < 8; u++)
-                    if (on[u]) dp[((w0 + j0 + u) << 5) + lane] = v[u];
+                    for (int q = 0; q < 8; q++)
+                        if (on[q]) dp[((g0 + j0 + q) << 5) + lane] = v[q];
+                }
             }
         }
     }
@@ -1906,12 +1932,13 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     const int smem = (int)((((int64_t)1 << pb) >> 5) + 2) * 4;
     cudaFuncSetAttribute(scat_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int64_t items = (int64_t)pl.nb << (pl.shift - pb);
-    const int g = (int)(items < nsm ? items : nsm);
     if (s2) {
+        const int g = (int)(items < nsm ? items : nsm);  // one per SM, beside the apply
         scat_bits_kernel<<<g, SBITS_T, smem, s2>>>(pidx, base, pl.nb, pl.shift, lo, hi, work, bitmap);
         cudaEventRecord(join, s2);
         cudaStreamWaitEvent(s, join, 0);
     } else {
+        const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
         scat_bits_kernel<<<g, SBITS_T, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, nullptr, bitmap);
     }
     return cudaGetLastError();
@@ -1964,7 +1991,7 @@ cudaError_t merge_bitmap(cudaStream_t s, const void *src, PeerPtrs dsts, const u
                          int64_t elem, int64_t lo, int64_t hi) {
     if (hi <= lo || dsts.n == 0) return cudaSuccess;
     const int64_t words = ((hi + 31) >> 5) - (lo >> 5);
-    const int g = grid_for(words, 8 * 32, 148 * 8);  // 8 warps x 32 words per block
+    const int g = grid_for(words, 8 * 32 * 4, 148 * 8);  // 8 warps x 4 x 32 words per block
     if (elem == 8)
         merge_bitmap_kernel<double><<<g, 256, 0, s>>>(static_cast<const double *>(src), dsts,
                                                       bitmap, lo, hi);

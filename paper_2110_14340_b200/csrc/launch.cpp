@@ -634,8 +634,10 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                         CK(cudaEventCreateWithFlags(&dv.fork, cudaEventDisableTiming));
                         CK(cudaEventCreateWithFlags(&dv.join, cudaEventDisableTiming));
                     }
+                    static const bool serial_bits = getenv("JACC_SCATTER_BITS_SERIAL") != nullptr;
                     CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
-                                              drec, sp, dv.scratch, dv.s2, dv.fork, dv.join));
+                                              drec, sp, dv.scratch, serial_bits ? nullptr : dv.s2,
+                                              dv.fork, dv.join));
                 } else if (f64) {
                     CK(jk::scatter_add_f64(dv.s, ix, reinterpret_cast<const double *>(b),
                                            reinterpret_cast<double *>(W->rep[d]), p.i1 - p.i0, lo,
