@@ -65,7 +65,9 @@ jacc_status jacc_init(int n_devices, const int *device_ids) {
                     else CK(e);
                     R.peer_pairs++;
                 }
-            if (n_devices > 1 && R.distinct && !getenv("JACC_NO_NCCL")) {
+            // JACC_FORCE_NCCL=1 builds the communicator for a single device too:
+            // the NCCL combine path then runs on a one-GPU box (tests)
+            if ((n_devices > 1 || getenv("JACC_FORCE_NCCL")) && R.distinct && !getenv("JACC_NO_NCCL")) {
                 // NCCL allreduce for the reduction combine.  A
                 // communicator that cannot be built is an error, not a silent
                 // switch to the peer-memory combine (JACC_NO_NCCL=1 selects

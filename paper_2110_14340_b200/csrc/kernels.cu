@@ -76,6 +76,10 @@ __device__ __forceinline__ void publish_dirty(u64 mn, u64 mx, u64 *dirty) {
             atomicMin(&dirty[1], ~b);
         }
     }
+    // smn/smx are reused by the next call in the same kernel (fig4 publishes
+    // two records): no warp may overwrite them before thread 0 has read them
+    // (WAR found by compute-sanitizer racecheck, round 2)
+    __syncthreads();
 }
 
 // ---------------------------------------------------------------------------

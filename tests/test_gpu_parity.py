@@ -1432,3 +1432,24 @@ def test_info_single_device(J):
         info = J.jacc_get_info()
     assert info == {"n_devices": 1, "distinct_gpus": 1, "combine": "peer", "peer_pairs": 0,
                     "multiprocess": 0, "rank": 0}
+
+
+def test_nccl_combine_path_single_gpu(J, monkeypatch):
+    """The NCCL allreduce combine executed on a one-GPU
+    box: JACC_FORCE_NCCL builds a one-rank communicator, so the reduction
+    goes through ncclAllReduce + the combine kernel; dyadic inputs, exact."""
+    monkeypatch.setenv("JACC_FORCE_NCCL", "1")
+    L = 1_000_003
+    x = synth.dyadic_f64(L, 118, 1)
+    y = synth.dyadic_f64(L, 118, 2)
+    with runtime(J, 1):
+        assert J.jacc_get_info()["combine"] == "nccl"
+        _create(J, x, y)
+        s = np.array([0.75])
+        J.jacc_launch(J.JACC_LOOP_DOT_F64, J.make_range(0, L),
+                      [_in(J, x), _in(J, y), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s)])
+        s2 = np.array([-1.0])
+        J.jacc_launch(J.JACC_LOOP_SUM_F64, J.make_range(0, L),
+                      [_in(J, x), J.arg(J.JACC_ARG_REDUCE_SUM_F64, s2)])
+    assert s[0] == orc.dot_f64(x, y, 0.75)
+    assert s2[0] == orc.sum_f64(x, -1.0)
