@@ -887,12 +887,15 @@ __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off,
     if (lane == 31) *total = inc;
 }
 
-// Partition.  Per tile: all keys of a thread, then the values of its owned
-// ones (two batches of independent loads), ranks by shared-memory atomics,
-// warp scan, one cursor reservation per non-empty bucket (global atomic;
-// gdst[b] = stream position of the tile's segment minus its staging offset),
-// staging in bucket order, bucket-contiguous write-out.
-template <typename T>
+// Partition.  Per tile: the keys and values of a thread (ALL: every value is
+// loaded together with its key, one latency round -- used when every
+// update is owned, n = 1 or duplicated; otherwise the values of the owned
+// keys only, after the keys), ranks by shared-memory atomics, warp scan, one
+// cursor reservation per non-empty bucket (global atomic, issued before the
+// staging so its round trip overlaps it), staging in bucket order,
+// bucket-contiguous write-out.
+constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;  // buckets per thread
+template <typename T, bool ALL>
 __global__ void __launch_bounds__(SB_T, 2) scat_part_kernel(const int32_t *__restrict__ idx,
                                                             const T *__restrict__ b, int64_t n,
                                                             int32_t lo, unsigned span, int shift,
@@ -915,10 +918,15 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_kernel(const int32_t *__res
         int32_t k[E];
         T v[E];
 #pragma unroll
-        for (int j = 0; j < E; j++) k[j] = j * SB_T < rem ? __ldcs(ti + j * SB_T) : lo - 1;
+        for (int j = 0; j < E; j++) {
+            k[j] = j * SB_T < rem ? __ldcs(ti + j * SB_T) : lo - 1;
+            if (ALL && j * SB_T < rem) v[j] = __ldcs(tb + j * SB_T);
+        }
+        if (!ALL) {
 #pragma unroll
-        for (int j = 0; j < E; j++)
-            if (owned(k[j], lo, span)) v[j] = __ldcs(tb + j * SB_T);
+            for (int j = 0; j < E; j++)
+                if (owned(k[j], lo, span)) v[j] = __ldcs(tb + j * SB_T);
+        }
         for (int i = tid; i < nb; i += SB_T) hist[i] = 0;
         __syncthreads();
         unsigned rk[E];
@@ -927,11 +935,14 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_kernel(const int32_t *__res
             if (owned(k[j], lo, span)) rk[j] = atomicAdd(&hist[(unsigned)(k[j] - lo) >> shift], 1u);
         __syncthreads();
         if (tid < 32) warp_exscan(hist, loff, nb, &total);
-        __syncthreads();
-        for (int i = tid; i < nb; i += SB_T) {
-            const unsigned c = hist[i];
-            if (c) gdst[i] = atomicAdd(&cursor[i], (u64)c) - loff[i];
+        u64 res[SB_RES];
+#pragma unroll
+        for (int r = 0; r < SB_RES; r++) {
+            const int i = tid + r * SB_T;
+            const unsigned c = i < nb ? hist[i] : 0u;
+            res[r] = c ? atomicAdd(&cursor[i], (u64)c) : 0;  // consumed after the staging
         }
+        __syncthreads();  // loff
 #pragma unroll
         for (int j = 0; j < E; j++)
             if (owned(k[j], lo, span)) {
@@ -939,6 +950,11 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_kernel(const int32_t *__res
                 sk[pos] = k[j];
                 sv[pos] = v[j];
             }
+#pragma unroll
+        for (int r = 0; r < SB_RES; r++) {
+            const int i = tid + r * SB_T;
+            if (i < nb && hist[i]) gdst[i] = res[r] - loff[i];
+        }
         __syncthreads();
         const unsigned cnt = total;
         for (unsigned pos = tid; pos < cnt; pos += SB_T) {
@@ -1862,7 +1878,7 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
     return cudaGetLastError();
 }
 
-ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
+ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_total) {
     ScatterPlan p{};
     const int64_t span = hi - lo;
     const char *force = getenv("JACC_SCATTER_BINNED");  // "0" never, "1" always (tests)
@@ -1877,6 +1893,7 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem) {
     p.binned = true;
     p.shift = shift;
     p.nb = (int)((span + ((int64_t)1 << shift) - 1) >> shift);
+    p.all_owned = lo == 0 && hi >= m_total;
     p.hdr = ((size_t)(3 * p.nb + 2) * 8 + 255) & ~(size_t)255;
     p.scratch = p.hdr + (((size_t)n * 4 + 255) & ~(size_t)255) + (size_t)n * elem;
     return p;
@@ -1906,12 +1923,16 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     const int64_t tile = (int64_t)SB_T * SB_E;
     const int pg = (int)std::min<int64_t>((n + tile - 1) / tile, (int64_t)nsm * 8);
     const int pdsm = (int)tile * ((is_f64 ? 8 : 4) + 4);
+    // every update owned (one device, or duplicated execution): load the
+    // values with the keys; else only the owned ones (the owner filter keeps
+    // a device's value reads at ~1/n)
+    const bool all = pl.all_owned;
     // attributes are per device: set on every call (host-side, cheap)
     if (is_f64) {
-        cudaFuncSetAttribute(scat_part_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-        scat_part_kernel<double><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo32, span,
-                                                        pl.shift, pl.nb, cursor, pidx,
-                                                        reinterpret_cast<double *>(pv));
+        auto kp = all ? scat_part_kernel<double, true> : scat_part_kernel<double, false>;
+        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+        kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo32, span, pl.shift, pl.nb,
+                                  cursor, pidx, reinterpret_cast<double *>(pv));
         if (s2) {  // the bits pass forks off here and runs beside the apply
             cudaEventRecord(fork, s);
             cudaStreamWaitEvent(s2, fork, 0);
@@ -1920,10 +1941,10 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
                                                                base, pl.nb, work, static_cast<double *>(a),
                                                                dirty);
     } else {
-        cudaFuncSetAttribute(scat_part_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-        scat_part_kernel<int32_t><<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32, span,
-                                                         pl.shift, pl.nb, cursor, pidx,
-                                                         reinterpret_cast<int32_t *>(pv));
+        auto kp = all ? scat_part_kernel<int32_t, true> : scat_part_kernel<int32_t, false>;
+        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+        kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32, span, pl.shift, pl.nb,
+                                  cursor, pidx, reinterpret_cast<int32_t *>(pv));
         if (s2) {
             cudaEventRecord(fork, s);
             cudaStreamWaitEvent(s2, fork, 0);

@@ -71,11 +71,12 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
 // range fused into (4).  is_f64: T = double, else int32.
 struct ScatterPlan {
     bool binned;
+    bool all_owned;     // [lo, hi) covers every element of a (one device / duplicated)
     int shift, nb;      // bucket = 2^shift elements, nb buckets
     size_t hdr;         // bytes of counters/bases at the start of the scratch
     size_t scratch;     // total scratch bytes (header + n keys + n values)
 };
-ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem);
+ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_total);
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
                                u64 *dirty, const ScatterPlan &pl, void *scratch, cudaStream_t s2,

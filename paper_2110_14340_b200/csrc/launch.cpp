@@ -417,7 +417,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
             if (!local(d) || !L.plan[d].active) continue;
             const DevPlan &p = L.plan[d];
             const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
-            const jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
+            const jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem, W->nelem);
             if (!sp.binned) continue;
             Device &dv = R.dev[d];
             set_dev(d);
@@ -624,7 +624,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 const bool f64 = id == JACC_LOOP_SCATTER_ADD_F64;
                 const char *b = L.a[1].reg->rep[d] + (L.a[1].off + p.i0) * (int64_t)W->elem;
                 const int64_t lo = L.dup ? 0 : p.own_lo, hi = L.dup ? W->nelem : p.own_hi;
-                jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem);
+                jk::ScatterPlan sp = jk::scatter_plan(p.i1 - p.i0, lo, hi, (int)W->elem, W->nelem);
                 if (R.nq > 1) sp.binned = false;     // per-device scratch is not per queue
                 if (sp.binned && dv.scratch_bytes < sp.scratch)
                     sp.binned = false;  // scratch could not be reserved up front: direct kernel
