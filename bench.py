@@ -711,11 +711,11 @@ def run_loops(J, C, n, peaks, args):
         "merge_ms": m * 1e3,
         "roofline": {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                      "frac": ach / pk, "traffic": traffic, "traffic_source": tsrc,
-                     "peak_source": (f"cuBLAS DGEMM 8192^3 measured on this pool ({dsrc})" if dg
+                     "peak_source": (f"cuBLAS DGEMM 8192^3: {dsrc}" if dg
                                      else "MEASURED_PEAKS bf16 burst x nominal fp64/bf16 ratio"),
                      "peak_bf16_scaled": scaled, "frac_of_bf16_scaled": ach / scaled if scaled else None,
                      "spec_peak": FP64_SPEC_TFLOPS, "frac_of_spec": ach / FP64_SPEC_TFLOPS,
-                     "kernel": "gemm_f64_kernel (DMMA)", "kernel_avg_ms": k * 1e3,
+                     "kernel": "gemm_tma_kernel (TMA + mbarrier ring, DMMA)", "kernel_avg_ms": k * 1e3,
                      "algo_flops_per_launch": fl // n},
         "e2e": {"value": fl / te / 1e12, "unit": "TFLOP/s", "seconds": te,
                 "h2d_bytes_per_step": Ag.nbytes + Bg.nbytes, "d2h_bytes_per_step": Cg.nbytes},
