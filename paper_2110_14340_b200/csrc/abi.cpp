@@ -146,9 +146,6 @@ jacc_status jacc_finalize(void) {
         for (void *p : dv.retired) cudaFree(p);
         dv.retired.clear();
         if (dv.pe) cudaEventDestroy(dv.pe);
-        if (dv.s2) cudaStreamDestroy(dv.s2);
-        if (dv.fork) cudaEventDestroy(dv.fork);
-        if (dv.join) cudaEventDestroy(dv.join);
         for (size_t q = 1; q < dv.qs.size(); q++) cudaStreamDestroy(dv.qs[q]);
         for (size_t q = 1; q < dv.qpartials.size(); q++) {
             cudaFree(dv.qpartials[q]);

@@ -792,7 +792,7 @@ constexpr int SB_MAXB = 1024;    // max buckets
 constexpr int SA_CH = 4096;      // apply chunk (pairs)
 constexpr int SA_BPS = 3;        // apply CTAs of 256 threads per SM
 constexpr int SBITS_LB = 20;     // bits pass: 2^20 elements (128 KB of bits) per CTA item
-constexpr int SBITS_T = 1024;    // bits CTA (co-resident with SA_BPS apply CTAs)
+constexpr int SBITS_T = 1024;    // bits CTA
 
 __device__ __forceinline__ bool owned(int32_t k, int32_t lo, unsigned span) {
     return (unsigned)(k - lo) < span;
@@ -1004,17 +1004,13 @@ __global__ void __launch_bounds__(256, SA_BPS) scat_apply_kernel(const int32_t *
 // scans the bucket's keys (16-byte loads), sets its bits with shared-memory
 // atomicOr and writes its words once (a part's first/last word may be
 // shared with the neighbour part when lo is not 32-aligned: atomicOr into
-// the zeroed bitmap).  It runs concurrently with the apply on a second
-// stream and follows it: before a bucket it waits until the apply has
-// dequeued the bucket's last chunk, so the keys it reads were just brought
-// into L2 by the apply (no extra HBM pass).  The wait gives up after
-// SBITS_IDLE polls without apply progress (kernels serialised, e.g. under a
-// profiler): correctness never depends on it, only where the keys come from.
-constexpr int SBITS_IDLE = 200;   // x ~1 us
+// the zeroed bitmap).  (Run on a second stream beside the apply, following
+// its chunk counter, it measured no faster and the range-replay DRAM total
+// of the launch was unchanged: profiles/scat_experiments_r02.txt.)
 __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__restrict__ pidx,
                                                             const u64 *__restrict__ base, int nb,
                                                             int shift, int64_t lo, int64_t hi,
-                                                            const u64 *work, uint32_t *bitmap) {
+                                                            uint32_t *bitmap) {
     extern __shared__ uint32_t sw[];
     const int lp = shift > SBITS_LB ? shift - SBITS_LB : 0;  // log2 parts per bucket
     const int pb = shift > SBITS_LB ? SBITS_LB : shift;      // log2 elements per part
@@ -1026,20 +1022,6 @@ __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__res
         const int64_t e1 = e0 + ((int64_t)1 << pb) < hi ? e0 + ((int64_t)1 << pb) : hi;
         const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
         const u64 p0 = base[bk], p1 = base[bk + 1];
-        if (work && threadIdx.x == 0) {
-            const u64 need = (p1 + SA_CH - 1) / SA_CH;
-            u64 last = *(volatile const u64 *)work;
-            for (int idle = 0; last < need && idle < SBITS_IDLE;) {
-                __nanosleep(1000);  // polls stay off the apply's counter
-                const u64 w = *(volatile const u64 *)work;
-                if (w != last) {
-                    last = w;
-                    idle = 0;
-                } else {
-                    idle++;
-                }
-            }
-        }
         for (int i = threadIdx.x; i < nw; i += SBITS_T) sw[i] = 0;
         __syncthreads();
         auto put = [&](int64_t k) {
@@ -1886,9 +1868,10 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_
     if (!(force && force[0] == '1') && (n < (1 << 22) || span * elem <= (int64_t)96 << 20))
         return p;  // a fits in L2: the direct kernel is already L2-resident
     if (hi > INT32_MAX) return p;  // keys are int32: never, kept for the 32-bit arithmetic
-    // buckets of 8 MiB of `a` (round 1: 8 MiB 4.18 ms vs 16 MiB 4.38, 4 MiB 5.73)
-    int shift = 0;
-    while (((int64_t)elem << shift) < ((int64_t)8 << 20)) shift++;
+    // buckets of 2^20 elements (8 MiB of fp64 -- round 1: 8 MiB 4.18 ms vs
+    // 16 MiB 4.38, 4 MiB 5.73 -- and 4 MiB of int32: one bits-pass part per
+    // bucket, so every key is read once there)
+    int shift = 20;
     while (((span + ((int64_t)1 << shift) - 1) >> shift) > SB_MAXB) shift++;
     p.binned = true;
     p.shift = shift;
@@ -1901,8 +1884,7 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_
 
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
-                               u64 *dirty, const ScatterPlan &pl, void *scratch, cudaStream_t s2,
-                               cudaEvent_t fork, cudaEvent_t join) {
+                               u64 *dirty, const ScatterPlan &pl, void *scratch) {
     char *sc = static_cast<char *>(scratch);
     u64 *counts = reinterpret_cast<u64 *>(sc);
     u64 *cursor = counts + pl.nb;
@@ -1933,10 +1915,6 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
         cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
         kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo32, span, pl.shift, pl.nb,
                                   cursor, pidx, reinterpret_cast<double *>(pv));
-        if (s2) {  // the bits pass forks off here and runs beside the apply
-            cudaEventRecord(fork, s);
-            cudaStreamWaitEvent(s2, fork, 0);
-        }
         scat_apply_kernel<double><<<nsm * SA_BPS, 256, 0, s>>>(pidx, reinterpret_cast<const double *>(pv),
                                                                base, pl.nb, work, static_cast<double *>(a),
                                                                dirty);
@@ -1945,10 +1923,6 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
         cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
         kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32, span, pl.shift, pl.nb,
                                   cursor, pidx, reinterpret_cast<int32_t *>(pv));
-        if (s2) {
-            cudaEventRecord(fork, s);
-            cudaStreamWaitEvent(s2, fork, 0);
-        }
         scat_apply_kernel<int32_t><<<nsm * SA_BPS, 256, 0, s>>>(pidx, reinterpret_cast<const int32_t *>(pv),
                                                                 base, pl.nb, work,
                                                                 static_cast<int32_t *>(a), dirty);
@@ -1957,15 +1931,8 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     const int smem = (int)((((int64_t)1 << pb) >> 5) + 2) * 4;
     cudaFuncSetAttribute(scat_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int64_t items = (int64_t)pl.nb << (pl.shift - pb);
-    if (s2) {
-        const int g = (int)(items < nsm ? items : nsm);  // one per SM, beside the apply
-        scat_bits_kernel<<<g, SBITS_T, smem, s2>>>(pidx, base, pl.nb, pl.shift, lo, hi, work, bitmap);
-        cudaEventRecord(join, s2);
-        cudaStreamWaitEvent(s, join, 0);
-    } else {
-        const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
-        scat_bits_kernel<<<g, SBITS_T, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, nullptr, bitmap);
-    }
+    const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
+    scat_bits_kernel<<<g, SBITS_T, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap);
     return cudaGetLastError();
 }
 

@@ -629,15 +629,8 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 if (sp.binned && dv.scratch_bytes < sp.scratch)
                     sp.binned = false;  // scratch could not be reserved up front: direct kernel
                 if (sp.binned) {
-                    if (!dv.s2) {
-                        CK(cudaStreamCreateWithFlags(&dv.s2, cudaStreamNonBlocking));
-                        CK(cudaEventCreateWithFlags(&dv.fork, cudaEventDisableTiming));
-                        CK(cudaEventCreateWithFlags(&dv.join, cudaEventDisableTiming));
-                    }
-                    static const bool serial_bits = getenv("JACC_SCATTER_BITS_SERIAL") != nullptr;
                     CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
-                                              drec, sp, dv.scratch, serial_bits ? nullptr : dv.s2,
-                                              dv.fork, dv.join));
+                                              drec, sp, dv.scratch));
                 } else if (f64) {
                     CK(jk::scatter_add_f64(dv.s, ix, reinterpret_cast<const double *>(b),
                                            reinterpret_cast<double *>(W->rep[d]), p.i1 - p.i0, lo,

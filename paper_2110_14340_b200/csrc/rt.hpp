@@ -254,8 +254,6 @@ struct Device {
     cudaEvent_t pe = nullptr;    // phase event (iteration-split scatter)
     u64 *scr_dirty = nullptr;    // scratch dirty record (phase-1 kernels)
     size_t scratch_bytes = 0;
-    cudaStream_t s2 = nullptr;   // binned scatter: bits pass beside the apply
-    cudaEvent_t fork = nullptr, join = nullptr;
     // profiling
     double kernel_s = 0, merge_s = 0;
     uint64_t launches = 0, bytes_merged = 0;
