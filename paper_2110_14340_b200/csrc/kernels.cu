@@ -894,15 +894,15 @@ __device__ __forceinline__ void warp_exscan(const unsigned *hist, unsigned *off,
 // cursor reservation per non-empty bucket (global atomic, issued before the
 // staging so its round trip overlaps it), staging in bucket order,
 // bucket-contiguous write-out.
-constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;  // buckets per thread
-template <typename T, bool ALL>
-__global__ void __launch_bounds__(SB_T, 2) scat_part_kernel(const int32_t *__restrict__ idx,
+template <typename T, bool ALL, int SB_T = ::jk::SB_T, int MINB = 2>
+__global__ void __launch_bounds__(SB_T, MINB) scat_part_kernel(const int32_t *__restrict__ idx,
                                                             const T *__restrict__ b, int64_t n,
                                                             int32_t lo, unsigned span, int shift,
                                                             int nb, u64 *cursor,
                                                             int32_t *__restrict__ pidx,
                                                             T *__restrict__ pval) {
     constexpr int E = SB_E, TILE = SB_T * E;
+    constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;  // buckets per thread
     __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB];
     __shared__ u64 gdst[SB_MAXB];
     __shared__ unsigned total;
