@@ -1290,6 +1290,47 @@ __global__ void __launch_bounds__(HT, MINB) himeno_stencil_kernel(
 
 // copy loop: one warp per (i, j) row of the box; the 16-byte-aligned body
 // as float4 (p and wrk2 share the layout), head / tail as scalars
+// Copy loop p = wrk2 over the box, a pure stream.  A warp owns rows (i, j)
+// with a static row stride; when the rows are 16-byte aligned along k (the
+// benchmark's grids: K % 4 == 0 or the aligned part of K = 4m+1 rows) it
+// moves HC rows per round, every lane issuing all its loads (up to 4
+// float4 chunks + one head/tail scalar per row) before any store, so
+// 2 x HC KB are in flight per warp.  HALO boundary planes are also stored
+// into the neighbours' replicas (push_top / push_bot).
+constexpr int HC = 2;  // rows per round
+__device__ __forceinline__ void himeno_copy_row_vec(const float *__restrict__ wrk2, float *__restrict__ p,
+                                                    float *tp, float *bp, int64_t rb, int64_t k0,
+                                                    int64_t k1, int lane, bool load, float4 *v,
+                                                    float &sv, int64_t &sk) {
+    // ka: first 16-byte aligned k >= k0; chunks [ka, kt) in float4
+    int64_t ka = k0 + ((4 - ((rb + k0) & 3)) & 3);
+    if (ka > k1) ka = k1;
+    const int64_t nch = (k1 - ka) >> 2, kt = ka + 4 * nch;
+    if (load) {
+        sk = -1;
+        if (lane < ka - k0) sk = k0 + lane;
+        else if (lane >= 8 && lane - 8 < k1 - kt) sk = kt + (lane - 8);
+        sv = sk >= 0 ? __ldcs(wrk2 + rb + sk) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (lane + 32 * u < nch) v[u] = __ldcs(reinterpret_cast<const float4 *>(wrk2 + rb + ka) + lane + 32 * u);
+        return;
+    }
+    if (sk >= 0) {
+        __stcs(p + rb + sk, sv);
+        if (tp) tp[rb + sk] = sv;
+        if (bp) bp[rb + sk] = sv;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+        if (lane + 32 * u < nch) {
+            const int64_t x = rb + ka + 4 * (lane + 32 * u);
+            __stcs(reinterpret_cast<float4 *>(p + x), v[u]);
+            if (tp) *reinterpret_cast<float4 *>(tp + x) = v[u];
+            if (bp) *reinterpret_cast<float4 *>(bp + x) = v[u];
+        }
+}
+
 __global__ void __launch_bounds__(HT) himeno_copy_kernel(
     const float *__restrict__ wrk2, float *__restrict__ p, int64_t J, int64_t K, int64_t i0,
     int64_t i1, int64_t j0, int64_t j1, int64_t k0, int64_t k1, u64 *dirty, float *push_top,
@@ -1301,86 +1342,53 @@ __global__ void __launch_bounds__(HT) himeno_copy_kernel(
     const int64_t nw = ((int64_t)gridDim.x * HT) >> 5;
     const bool vec = ((reinterpret_cast<uintptr_t>(wrk2) | reinterpret_cast<uintptr_t>(p) |
                        reinterpret_cast<uintptr_t>(push_top) | reinterpret_cast<uintptr_t>(push_bot)) &
-                      15) == 0;
+                      15) == 0 &&
+                     (k1 - k0) <= 128 * 4 + 6;  // one round of <= 4 float4 per lane per row
     u64 mn = kU64Max, mx = 0;
-    // a pure stream (no neighbour reuse): static row stride; a shared row
-    // counter would serialise on its atomics (rows are only 2 KB of work)
-    (void)ticket;
-    for (int64_t r = wg; r < rows; r += nw) {
-        const int64_t i = i0 + r / nj, j = j0 + r % nj;
-        const int64_t rb = i * P + j * K;
-        float *tp = (i == i0) ? push_top : nullptr;
-        float *bp = (i == i1 - 1) ? push_bot : nullptr;
-        int64_t ka = vec ? k0 + ((4 - ((rb + k0) & 3)) & 3) : k1;
-        if (ka > k1) ka = k1;
-        const int64_t nch = (k1 - ka) >> 2, kt = ka + 4 * nch;
-        if (vec) {
-            // one latency round per row: the <= 3 + 3 scalar head/tail
-            // points and up to 4 float4 chunks per lane are all loaded
-            // before any store
-            int64_t sk = -1;
-            if (lane < ka - k0) sk = k0 + lane;
-            else if (lane >= 8 && lane - 8 < k1 - kt) sk = kt + (lane - 8);
-            const float sv = sk >= 0 ? __ldcs(wrk2 + rb + sk) : 0.f;
-            bool sdone = false;
-            for (int64_t c0 = 0; c0 < nch || !sdone; c0 += 128) {
-                float4 v[4];
+    (void)ticket;  // a pure stream: static row stride (a shared row counter serialised)
+    if (vec) {
+        for (int64_t r0 = wg; r0 < rows; r0 += nw * HC) {
+            float4 v[HC][4];
+            float sv[HC];
+            int64_t sk[HC], rb[HC];
+            float *tp[HC], *bp[HC];
 #pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (c0 + lane + 32 * u < nch)
-                        v[u] = __ldcs(reinterpret_cast<const float4 *>(wrk2 + rb + ka) + c0 + lane + 32 * u);
-                if (!sdone && sk >= 0) {
-                    __stcs(p + rb + sk, sv);
-                    if (tp) tp[rb + sk] = sv;
-                    if (bp) bp[rb + sk] = sv;
+            for (int h = 0; h < HC; h++) {
+                const int64_t r = r0 + h * nw;
+                rb[h] = -1;
+                if (r >= rows) continue;
+                const int64_t i = i0 + r / nj, j = j0 + r % nj;
+                rb[h] = i * P + j * K;
+                tp[h] = (i == i0) ? push_top : nullptr;
+                bp[h] = (i == i1 - 1) ? push_bot : nullptr;
+                himeno_copy_row_vec(wrk2, p, tp[h], bp[h], rb[h], k0, k1, lane, true, v[h], sv[h], sk[h]);
+            }
+#pragma unroll
+            for (int h = 0; h < HC; h++) {
+                if (rb[h] < 0) continue;
+                himeno_copy_row_vec(wrk2, p, tp[h], bp[h], rb[h], k0, k1, lane, false, v[h], sv[h], sk[h]);
+                if (k1 > k0) {
+                    mn = (u64)(rb[h] + k0) < mn ? (u64)(rb[h] + k0) : mn;
+                    mx = (u64)(rb[h] + k1 - 1) > mx ? (u64)(rb[h] + k1 - 1) : mx;
                 }
-                sdone = true;
-#pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (c0 + lane + 32 * u < nch) {
-                        const int64_t x = rb + ka + 4 * (c0 + lane + 32 * u);
-                        __stcs(reinterpret_cast<float4 *>(p + x), v[u]);
-                        if (tp) *reinterpret_cast<float4 *>(tp + x) = v[u];
-                        if (bp) *reinterpret_cast<float4 *>(bp + x) = v[u];
-                    }
+            }
+        }
+    } else {
+        for (int64_t r = wg; r < rows; r += nw) {
+            const int64_t i = i0 + r / nj, j = j0 + r % nj;
+            const int64_t rb = i * P + j * K;
+            float *tp = (i == i0) ? push_top : nullptr;
+            float *bp = (i == i1 - 1) ? push_bot : nullptr;
+            for (int64_t k = k0 + lane; k < k1; k += 32) {
+                const float x = __ldcs(wrk2 + rb + k);
+                __stcs(p + rb + k, x);
+                if (tp) tp[rb + k] = x;
+                if (bp) bp[rb + k] = x;
             }
             if (k1 > k0) {
                 mn = (u64)(rb + k0) < mn ? (u64)(rb + k0) : mn;
                 mx = (u64)(rb + k1 - 1) > mx ? (u64)(rb + k1 - 1) : mx;
             }
-            continue;
-        }
-        // scalar head [k0, ka) and tail [kt, k1)
-        for (int64_t k = k0 + lane; k < ka; k += 32) {
-            const float v = __ldcs(wrk2 + rb + k);
-            __stcs(p + rb + k, v);
-            if (tp) tp[rb + k] = v;
-            if (bp) bp[rb + k] = v;
-        }
-        for (int64_t k = kt + lane; k < k1; k += 32) {
-            const float v = __ldcs(wrk2 + rb + k);
-            __stcs(p + rb + k, v);
-            if (tp) tp[rb + k] = v;
-            if (bp) bp[rb + k] = v;
-        }
-        for (int64_t ch = lane; ch < nch; ch += 64) {
-            float4 v[2];
-#pragma unroll
-            for (int u = 0; u < 2; u++)
-                if (ch + 32 * u < nch)
-                    v[u] = __ldcs(reinterpret_cast<const float4 *>(wrk2 + rb + ka) + ch + 32 * u);
-#pragma unroll
-            for (int u = 0; u < 2; u++)
-                if (ch + 32 * u < nch) {
-                    const int64_t x = rb + ka + 4 * (ch + 32 * u);
-                    __stcs(reinterpret_cast<float4 *>(p + x), v[u]);
-                    if (tp) *reinterpret_cast<float4 *>(tp + x) = v[u];
-                    if (bp) *reinterpret_cast<float4 *>(bp + x) = v[u];
-                }
-        }
-        if (k1 > k0) {
-            mn = (u64)(rb + k0) < mn ? (u64)(rb + k0) : mn;
-            mx = (u64)(rb + k1 - 1) > mx ? (u64)(rb + k1 - 1) : mx;
         }
     }
     publish_dirty_flat(mn, mx, dirty);

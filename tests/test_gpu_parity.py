@@ -395,7 +395,9 @@ def _gemm_bound(A, B):
 
 
 @pytest.mark.parametrize("shape", [(64, 64, 64), (37, 53, 71), (130, 67, 16), (1, 1, 1),
-                                   (200, 256, 33)])
+                                   (200, 256, 33),
+                                   # TMA path (K, N even) with ragged M, N and K tiles
+                                   (300, 258, 130), (129, 130, 18), (513, 384, 2)])
 @pytest.mark.parametrize("n", [1, 2, 3])
 def test_gemm_random_tolerance(J, shape, n):
     M, N, K = shape

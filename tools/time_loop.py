@@ -51,6 +51,23 @@ def main():
         arrs = (A, B, C)
         args = [J.arg(IN, A), J.arg(IN, B), J.arg(OUT, C)]
         loop, rng, work, unit = J.JACC_LOOP_GEMM_F64, None, 2 * G**3, "TFLOP/s"
+    elif which in ("himeno", "himeno_copy"):
+        I, Jd, K = 1024, 512, 512
+        hp, ha, hb, hc, hw1, hbd = synth.himeno_init(I, Jd, K)
+        hw2 = np.zeros_like(hp)
+        arrs = (hp, ha, hb, hc, hw1, hbd, hw2)
+        g = np.zeros(1)
+        if which == "himeno":
+            args = [J.arg(IN, hp), J.arg(IN, ha), J.arg(IN, hb), J.arg(IN, hc), J.arg(IN, hw1),
+                    J.arg(IN, hbd), J.arg(OUT, hw2), J.arg(J.JACC_ARG_REDUCE_SUM_F64, g),
+                    J.arg(J.JACC_ARG_SCALAR_F64, f64=0.8)]
+            loop = J.JACC_LOOP_HIMENO_F32
+            work = 56 * (I - 2) * (Jd - 2) * (K - 2)
+        else:
+            args = [J.arg(IN, hw2), J.arg(OUT, hp)]
+            loop = J.JACC_LOOP_HIMENO_COPY_F32
+            work = 8 * (I - 2) * (Jd - 2) * (K - 2)
+        rng, unit = None, "GB/s"
     else:
         A, B = synth.polybench_jacobi2d(16384)
         arrs = (A, B)
@@ -64,7 +81,7 @@ def main():
     J.jacc_set_profiling(1)
     J.jacc_profile_reset()
     for _ in range(reps):
-        J.jacc_launch(loop, rng, args, 0 if which != "dot" else -1)
+        J.jacc_launch(loop, rng, args, 0 if which not in ("dot", "himeno") else -1)
     J.jacc_wait()
     k, m, nl, _ = J.jacc_profile_totals(0)
     J.jacc_finalize()
