@@ -1527,7 +1527,7 @@ __global__ void __launch_bounds__(256) merge_range_kernel(const char *__restrict
         for (int d = 0; d < dsts.n; d++) {
             int4 *d4 = reinterpret_cast<int4 *>(static_cast<char *>(dsts.p[d]) + vs);
 #pragma unroll
-            for (int u = 0; u < 8; u++) d4[q + u * nth] = v[u];
+            for (int u = 0; u < 8; u++) __stcs(d4 + q + u * nth, v[u]);
         }
     }
     for (; q < nv; q += nth) {
