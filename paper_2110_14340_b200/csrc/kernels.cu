@@ -967,6 +967,109 @@ __global__ void __launch_bounds__(SB_T, MINB) scat_part_kernel(const int32_t *__
     }
 }
 
+// Partition with the next tile's keys and values prefetched into shared
+// memory by cp.async while the current tile is processed (every update
+// owned, 16-byte aligned idx and b): the loads never stall the tile's
+// processing.  The tile is moved from the raw buffer into registers at the
+// top of the iteration, the buffer is refilled with the next tile, and the
+// rest is scat_part_kernel.
+template <typename T>
+__global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__restrict__ idx,
+                                                               const T *__restrict__ b, int64_t n,
+                                                               int32_t lo, unsigned span, int shift,
+                                                               int nb, u64 *cursor,
+                                                               int32_t *__restrict__ pidx,
+                                                               T *__restrict__ pval) {
+    constexpr int E = SB_E, TILE = SB_T * E;
+    constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;
+    __shared__ unsigned total;
+    // dynamic: staging [TILE] T, [TILE] i32; raw [TILE] T, [TILE] i32;
+    // gdst u64[nb], hist u32[nb2], loff u32[nb2] (per-bucket state sized by
+    // nb so two CTAs fit an SM)
+    extern __shared__ __align__(16) unsigned char sdyn[];
+    T *sv = reinterpret_cast<T *>(sdyn);
+    int32_t *sk = reinterpret_cast<int32_t *>(sdyn + TILE * sizeof(T));
+    T *rv = reinterpret_cast<T *>(sdyn + TILE * (sizeof(T) + 4));
+    int32_t *rk = reinterpret_cast<int32_t *>(sdyn + TILE * (2 * sizeof(T) + 4));
+    const int nb2 = (nb + 1) & ~1;
+    u64 *gdst = reinterpret_cast<u64 *>(sdyn + TILE * (2 * sizeof(T) + 8));
+    unsigned *hist = reinterpret_cast<unsigned *>(gdst + nb);
+    unsigned *loff = hist + nb2;
+    const int tid = threadIdx.x;
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    auto prefetch = [&](int64_t t) {
+        if (t < ntiles) {
+            const int64_t e0 = t * TILE;
+            const int64_t left = n - e0 < TILE ? n - e0 : TILE;  // elements in this tile
+            constexpr int KC = TILE * 4 / 16, VC = TILE * (int)sizeof(T) / 16;  // 16-byte chunks
+            for (int c = tid; c < KC; c += SB_T) {
+                const int64_t el = (int64_t)c * 4;
+                const int bytes = el + 4 <= left ? 16 : (el < left ? (int)(left - el) * 4 : 0);
+                cp_async16(rk + 4 * c, bytes ? idx + e0 + el : idx, bytes);
+            }
+            constexpr int EPC = 16 / (int)sizeof(T);
+            for (int c = tid; c < VC; c += SB_T) {
+                const int64_t el = (int64_t)c * EPC;
+                const int bytes = el + EPC <= left ? 16 : (el < left ? (int)(left - el) * (int)sizeof(T) : 0);
+                cp_async16(rv + EPC * c, bytes ? b + e0 + el : b, bytes);
+            }
+        }
+        cp_commit();
+    };
+    prefetch(blockIdx.x);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int rem = (int)(n - t * TILE < TILE ? n - t * TILE : TILE) - tid;  // valid: j*SB_T < rem
+        cp_wait<0>();
+        __syncthreads();
+        int32_t k[E];
+        T v[E];
+#pragma unroll
+        for (int j = 0; j < E; j++) {
+            k[j] = j * SB_T < rem ? rk[j * SB_T + tid] : lo - 1;
+            v[j] = rv[j * SB_T + tid];
+        }
+        for (int i = tid; i < nb; i += SB_T) hist[i] = 0;
+        __syncthreads();  // raw buffer read by every thread: refill it
+        prefetch(t + gridDim.x);
+        unsigned rkk[E];
+#pragma unroll
+        for (int j = 0; j < E; j++)
+            if (owned(k[j], lo, span)) rkk[j] = atomicAdd(&hist[(unsigned)(k[j] - lo) >> shift], 1u);
+        __syncthreads();
+        if (tid < 32) warp_exscan(hist, loff, nb, &total);
+        u64 res[SB_RES];
+#pragma unroll
+        for (int r = 0; r < SB_RES; r++) {
+            const int i = tid + r * SB_T;
+            const unsigned c = i < nb ? hist[i] : 0u;
+            res[r] = c ? atomicAdd(&cursor[i], (u64)c) : 0;
+        }
+        __syncthreads();  // loff
+#pragma unroll
+        for (int j = 0; j < E; j++)
+            if (owned(k[j], lo, span)) {
+                const unsigned pos = loff[(unsigned)(k[j] - lo) >> shift] + rkk[j];
+                sk[pos] = k[j];
+                sv[pos] = v[j];
+            }
+#pragma unroll
+        for (int r = 0; r < SB_RES; r++) {
+            const int i = tid + r * SB_T;
+            if (i < nb && hist[i]) gdst[i] = res[r] - loff[i];
+        }
+        __syncthreads();
+        const unsigned cnt = total;
+        for (unsigned pos = tid; pos < cnt; pos += SB_T) {
+            const int32_t kk = sk[pos];
+            const u64 g = gdst[(unsigned)(kk - lo) >> shift] + pos;
+            pidx[g] = kk;
+            pval[g] = sv[pos];
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+}
+
 // Apply: pairs in stream (bucket) order through a dynamic chunk counter, so
 // the chunks in flight span ~one bucket of `a` and its read-modify-writes
 // hit L2.  (Loading all of a thread's pairs before its REDs measured slower:
@@ -1917,20 +2020,39 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     // values with the keys; else only the owned ones (the owner filter keeps
     // a device's value reads at ~1/n)
     const bool all = pl.all_owned;
+    // ... and, with 16-byte aligned idx and b, prefetched a tile ahead by
+    // cp.async (JACC_SCATTER_PF=0: the register-load partition)
+    static const bool pf_off = getenv("JACC_SCATTER_PF") && getenv("JACC_SCATTER_PF")[0] == '0';
+    const bool pf = all && !pf_off && ((uintptr_t)idx % 16 == 0) && ((uintptr_t)b % 16 == 0);
+    const int pfsm = 2 * pdsm + pl.nb * 8 + ((pl.nb + 1) & ~1) * 8;
     // attributes are per device: set on every call (host-side, cheap)
     if (is_f64) {
-        auto kp = all ? scat_part_kernel<double, true> : scat_part_kernel<double, false>;
-        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-        kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo32, span, pl.shift, pl.nb,
-                                  cursor, pidx, reinterpret_cast<double *>(pv));
+        if (pf) {
+            cudaFuncSetAttribute(scat_part_pf_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, pfsm);
+            scat_part_pf_kernel<double><<<pg, SB_T, pfsm, s>>>(idx, static_cast<const double *>(b), n, lo32,
+                                                                   span, pl.shift, pl.nb, cursor, pidx,
+                                                                   reinterpret_cast<double *>(pv));
+        } else {
+            auto kp = all ? scat_part_kernel<double, true> : scat_part_kernel<double, false>;
+            cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+            kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo32, span, pl.shift, pl.nb,
+                                      cursor, pidx, reinterpret_cast<double *>(pv));
+        }
         scat_apply_kernel<double><<<nsm * SA_BPS, 256, 0, s>>>(pidx, reinterpret_cast<const double *>(pv),
                                                                base, pl.nb, work, static_cast<double *>(a),
                                                                dirty);
     } else {
-        auto kp = all ? scat_part_kernel<int32_t, true> : scat_part_kernel<int32_t, false>;
-        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-        kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32, span, pl.shift, pl.nb,
-                                  cursor, pidx, reinterpret_cast<int32_t *>(pv));
+        if (pf) {
+            cudaFuncSetAttribute(scat_part_pf_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, pfsm);
+            scat_part_pf_kernel<int32_t><<<pg, SB_T, pfsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32,
+                                                                    span, pl.shift, pl.nb, cursor, pidx,
+                                                                    reinterpret_cast<int32_t *>(pv));
+        } else {
+            auto kp = all ? scat_part_kernel<int32_t, true> : scat_part_kernel<int32_t, false>;
+            cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+            kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32, span, pl.shift, pl.nb,
+                                      cursor, pidx, reinterpret_cast<int32_t *>(pv));
+        }
         scat_apply_kernel<int32_t><<<nsm * SA_BPS, 256, 0, s>>>(pidx, reinterpret_cast<const int32_t *>(pv),
                                                                 base, pl.nb, work,
                                                                 static_cast<int32_t *>(a), dirty);
