@@ -982,7 +982,7 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__
                                                                T *__restrict__ pval) {
     constexpr int E = SB_E, TILE = SB_T * E;
     constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;
-    __shared__ unsigned total;
+    __shared__ unsigned total, wsum[SB_T / 32];
     // dynamic: staging [TILE] T, [TILE] i32; raw [TILE] T, [TILE] i32;
     // gdst u64[nb], hist u32[nb2], loff u32[nb2] (per-bucket state sized by
     // nb so two CTAs fit an SM)
@@ -1036,13 +1036,40 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__
         for (int j = 0; j < E; j++)
             if (owned(k[j], lo, span)) rkk[j] = atomicAdd(&hist[(unsigned)(k[j] - lo) >> shift], 1u);
         __syncthreads();
-        if (tid < 32) warp_exscan(hist, loff, nb, &total);
         u64 res[SB_RES];
+        if (nb <= SB_T) {
+            // one bucket per thread: block-wide scan (every warp busy)
+            const unsigned c = tid < nb ? hist[tid] : 0u;
+            unsigned inc = c;
 #pragma unroll
-        for (int r = 0; r < SB_RES; r++) {
-            const int i = tid + r * SB_T;
-            const unsigned c = i < nb ? hist[i] : 0u;
-            res[r] = c ? atomicAdd(&cursor[i], (u64)c) : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned x = __shfl_up_sync(0xffffffffu, inc, o);
+                if ((tid & 31) >= o) inc += x;
+            }
+            if ((tid & 31) == 31) wsum[tid >> 5] = inc;
+            res[0] = c ? atomicAdd(&cursor[tid], (u64)c) : 0;  // consumed after the staging
+            __syncthreads();
+            if (tid < 32) {
+                const unsigned x = tid < SB_T / 32 ? wsum[tid] : 0u;
+                unsigned y = x;
+#pragma unroll
+                for (int o = 1; o < SB_T / 32; o <<= 1) {
+                    const unsigned z = __shfl_up_sync(0xffffffffu, y, o);
+                    if (tid >= o) y += z;
+                }
+                if (tid < SB_T / 32) wsum[tid] = y - x;
+                if (tid == SB_T / 32 - 1) total = y;
+            }
+            __syncthreads();
+            if (tid < nb) loff[tid] = wsum[tid >> 5] + inc - c;
+        } else {
+            if (tid < 32) warp_exscan(hist, loff, nb, &total);
+#pragma unroll
+            for (int r = 0; r < SB_RES; r++) {
+                const int i = tid + r * SB_T;
+                const unsigned c = i < nb ? hist[i] : 0u;
+                res[r] = c ? atomicAdd(&cursor[i], (u64)c) : 0;
+            }
         }
         __syncthreads();  // loff
 #pragma unroll
