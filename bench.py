@@ -837,8 +837,11 @@ def merge_probes(J):
         del A, B
     finally:
         J.jacc_finalize()
-    # merge_bitmap: scatter whose targets all fall in device 0's slice
+    # merge_bitmap: scatter whose targets all fall in device 0's slice, with
+    # the direct scatter kernel (the binned pipeline fuses the push into its
+    # bits pass, measured below)
     M = SCAT_N
+    os.environ["JACC_SCATTER_BINNED"] = "0"
     for name, nupd in (("merge_bitmap_dense", 2**27), ("merge_bitmap_sparse", 2**20)):
         J.jacc_init(2, [0, 0])
         try:
@@ -866,6 +869,46 @@ def merge_probes(J):
             del idx, b, a
         finally:
             J.jacc_finalize()
+    del os.environ["JACC_SCATTER_BINNED"]
+    # binned scatter with the EAGER push fused into its bits pass: device 0's
+    # launch time under EAGER (bits pass also stores the 0.68 GB of dirty
+    # elements into the peer) minus the same launch under HALO (no push)
+    J.jacc_init(2, [0, 0])
+    try:
+        nupd = 2**27
+        idx = synth.index_i32(nupd, M // 2, 4, synth.AID["idx"])
+        b = synth.dyadic_f64(nupd, 4, synth.AID["b"])
+        a = synth.dyadic_f64(M, 4, synth.AID["a0"])
+        for arr in (idx, b, a):
+            J.jacc_data_create(arr)
+            J.jacc_update_device(arr)
+        sargs = [J.arg(IN, idx), J.arg(IN, b), J.arg(INOUT, a)]
+        tk = {}
+        for pol in (J.JACC_MERGE_HALO, J.JACC_MERGE_EAGER):
+            J.jacc_set_merge_policy(pol)
+            fn = lambda: J.jacc_launch(J.JACC_LOOP_SCATTER_ADD_F64, J.make_range(0, nupd), sargs, 0)  # noqa: E731
+            fn()
+            J.jacc_wait()
+            J.jacc_set_profiling(1)
+            J.jacc_profile_reset()
+            for _ in range(4):
+                fn()
+            J.jacc_wait()
+            k, m, nl, _ = J.jacc_profile_totals(0)
+            J.jacc_set_profiling(0)
+            tk[pol] = (k + m) / max(nl, 1)
+        bm = J.jacc_get_dirty_bitmap(a, 0, M)
+        moved = 8 * int(np.unpackbits(bm.view(np.uint8)).sum())
+        extra = tk[J.JACC_MERGE_EAGER] - tk[J.JACC_MERGE_HALO]
+        out["binned_scatter_fused_push"] = {
+            "kernel": "scat_bits_kernel (EAGER push fused)", "launch_us_halo": tk[J.JACC_MERGE_HALO] * 1e6,
+            "launch_us_eager": tk[J.JACC_MERGE_EAGER] * 1e6, "push_cost_us": extra * 1e6,
+            "bytes_pushed": moved, "push_gbs": 2 * moved / extra / 1e9 if extra > 0 else None,
+            "vs_separate_merge_bitmap_us": out.get("merge_bitmap_dense", {}).get("us"),
+            "nvlink_time_at_770_us": moved / (NVLINK_GBS * 1e9) * 1e6}
+        del idx, b, a
+    finally:
+        J.jacc_finalize()
     return out
 
 

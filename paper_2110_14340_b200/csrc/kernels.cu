@@ -1169,17 +1169,26 @@ __global__ void __launch_bounds__(256, 2) scat_apply_kernel(const int32_t *__res
 // scans the bucket's keys (16-byte loads), sets its bits with shared-memory
 // atomicOr and writes its words once (a part's first/last word may be
 // shared with the neighbour part when lo is not 32-aligned: atomicOr into
-// the zeroed bitmap).  (Run on a second stream beside the apply, following
-// its chunk counter, it measured no faster and the range-replay DRAM total
-// of the launch was unchanged: profiles/scat_experiments_r02.txt.)
+// the zeroed bitmap).  Under EAGER with peers (push.n > 0) the same pass is
+// the merge: the part's dirty elements, final after the apply, are stored
+// into every peer replica straight from the shared-memory words (one warp
+// per word, lane l moving element l: a coalesced 128/256-byte segment per
+// word and peer) -- tracking and merge fused, no separate merge kernel and
+// no re-read of the bitmap.  (Run on a second stream beside the apply,
+// following its chunk counter, the pass measured no faster and the
+// range-replay DRAM total of the launch was unchanged:
+// profiles/scat_experiments_r02.txt.)
+template <typename T>
 __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__restrict__ pidx,
                                                             const u64 *__restrict__ base, int nb,
                                                             int shift, int64_t lo, int64_t hi,
-                                                            uint32_t *bitmap) {
+                                                            uint32_t *bitmap, const T *__restrict__ a,
+                                                            PeerPtrs push) {
     extern __shared__ uint32_t sw[];
     const int lp = shift > SBITS_LB ? shift - SBITS_LB : 0;  // log2 parts per bucket
     const int pb = shift > SBITS_LB ? SBITS_LB : shift;      // log2 elements per part
     const int64_t items = (int64_t)nb << lp;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int bk = (int)(it >> lp), q = (int)(it & ((1 << lp) - 1));
         const int64_t e0 = lo + ((int64_t)bk << shift) + ((int64_t)q << pb);
@@ -1213,6 +1222,27 @@ __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__res
                 if (v) atomicOr(bitmap + w0 + i, v);
             } else {
                 bitmap[w0 + i] = v;
+            }
+        }
+        if (push.n > 0) {
+            // fused EAGER merge: 4 words per warp per round (4 loads in
+            // flight per lane), element l of word i by lane l
+            constexpr int NWP = SBITS_T / 32;
+            for (int64_t i0 = warp; i0 < nw; i0 += 4 * NWP) {
+                T v[4];
+                bool on[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int64_t i = i0 + u * NWP;
+                    on[u] = i < nw && ((sw[i < nw ? i : 0] >> lane) & 1u);
+                    if (on[u]) v[u] = a[((w0 + i) << 5) + lane];
+                }
+                for (int d = 0; d < push.n; d++) {
+                    T *dp = static_cast<T *>(push.p[d]);
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        if (on[u]) dp[((w0 + i0 + u * NWP) << 5) + lane] = v[u];
+                }
             }
         }
         __syncthreads();
@@ -2057,7 +2087,7 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_
 
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
-                               u64 *dirty, const ScatterPlan &pl, void *scratch) {
+                               u64 *dirty, const ScatterPlan &pl, void *scratch, PeerPtrs push) {
     char *sc = static_cast<char *>(scratch);
     u64 *counts = reinterpret_cast<u64 *>(sc);
     u64 *cursor = counts + pl.nb;
@@ -2124,10 +2154,18 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     }
     const int pb = pl.shift > SBITS_LB ? SBITS_LB : pl.shift;
     const int smem = (int)((((int64_t)1 << pb) >> 5) + 2) * 4;
-    cudaFuncSetAttribute(scat_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (is_f64)
+        cudaFuncSetAttribute(scat_bits_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    else
+        cudaFuncSetAttribute(scat_bits_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int64_t items = (int64_t)pl.nb << (pl.shift - pb);
     const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
-    scat_bits_kernel<<<g, SBITS_T, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap);
+    if (is_f64)
+        scat_bits_kernel<double><<<g, SBITS_T, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap,
+                                                          static_cast<const double *>(a), push);
+    else
+        scat_bits_kernel<int32_t><<<g, SBITS_T, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap,
+                                                           static_cast<const int32_t *>(a), push);
     return cudaGetLastError();
 }
 
