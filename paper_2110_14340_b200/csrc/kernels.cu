@@ -338,6 +338,19 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem, int byte
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+// 16 bytes into shared memory: a full chunk by cp.async; a partial chunk
+// (the end of an array) by plain element loads, zero-filled, so nothing past
+// the last element is ever read (T = the array's element type)
+template <typename T>
+__device__ __forceinline__ void cp_async16_tail(T *smem, const T *gmem, int bytes) {
+    if (bytes == 16) {
+        cp_async16(smem, gmem, 16);
+        return;
+    }
+    constexpr int EPC = 16 / (int)sizeof(T);
+#pragma unroll
+    for (int e = 0; e < EPC; e++) smem[e] = e * (int)sizeof(T) < bytes ? gmem[e] : T(0);
+}
 template <int N>
 __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
@@ -1004,13 +1017,13 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__
             for (int c = tid; c < KC; c += SB_T) {
                 const int64_t el = (int64_t)c * 4;
                 const int bytes = el + 4 <= left ? 16 : (el < left ? (int)(left - el) * 4 : 0);
-                cp_async16(rk + 4 * c, bytes ? idx + e0 + el : idx, bytes);
+                cp_async16_tail(rk + 4 * c, idx + e0 + el, bytes);
             }
             constexpr int EPC = 16 / (int)sizeof(T);
             for (int c = tid; c < VC; c += SB_T) {
                 const int64_t el = (int64_t)c * EPC;
                 const int bytes = el + EPC <= left ? 16 : (el < left ? (int)(left - el) * (int)sizeof(T) : 0);
-                cp_async16(rv + EPC * c, bytes ? b + e0 + el : b, bytes);
+                cp_async16_tail(rv + EPC * c, b + e0 + el, bytes);
             }
         }
         cp_commit();
@@ -1122,13 +1135,13 @@ __global__ void __launch_bounds__(256, 2) scat_apply_kernel(const int32_t *__res
             for (int q = tid; q < SA_CH / 4; q += 256) {
                 const int64_t el = (int64_t)q * 4;
                 const int bytes = el + 4 <= left ? 16 : (el < left ? (int)(left - el) * 4 : 0);
-                cp_async16(sk + st * SA_CH + 4 * q, bytes ? pidx + p0 + el : pidx, bytes);
+                cp_async16_tail(sk + st * SA_CH + 4 * q, pidx + p0 + el, bytes);
             }
             constexpr int EPC = 16 / (int)sizeof(T);
             for (int q = tid; q < SA_CH / EPC; q += 256) {
                 const int64_t el = (int64_t)q * EPC;
                 const int bytes = el + EPC <= left ? 16 : (el < left ? (int)(left - el) * (int)sizeof(T) : 0);
-                cp_async16(sv + st * SA_CH + EPC * q, bytes ? pval + p0 + el : pval, bytes);
+                cp_async16_tail(sv + st * SA_CH + EPC * q, pval + p0 + el, bytes);
             }
         }
         cp_commit();
