@@ -35,17 +35,21 @@ def _run(cmd):
     return r
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, defines=(), out=None):
+    """defines / out: experiment builds (tools/) -- extra -D flags for the
+    kernels, written to `out` instead of the package's libjacc.so."""
+    if defines or out:
+        force = True
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(s) <= t for s in SOURCES):
             return LIB
     nccl_inc, nccl_lib = nccl_paths()
-    bdir = os.path.join(PKG, "_build")
+    bdir = os.path.join(PKG, "_build") if not (defines or out) else (out + ".build")
     os.makedirs(bdir, exist_ok=True)
     ko = os.path.join(bdir, "kernels.o")
     _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-          "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-c",
+          "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines], "-I", INCLUDE, "-c",
           os.path.join(CSRC, "kernels.cu"), "-o", ko])
     objs = [ko]
     for src in HOST:
@@ -54,14 +58,18 @@ def build(force=False, verbose=False):
               "-I", os.path.join(CUDA_HOME, "include"), "-I", nccl_inc, "-c",
               os.path.join(CSRC, src), "-o", o])
         objs.append(o)
-    tmp = LIB + ".tmp"
+    dst = out or LIB
+    tmp = dst + ".tmp"
     # only the jacc_* C-ABI is exported (csrc/exports.map)
     _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static",
           "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}",
           "-Xlinker", f"--version-script={os.path.join(CSRC, 'exports.map')}"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, dst)
+    return dst
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="-v" in sys.argv))
+    # python build.py [-v] [--out PATH] [-DNAME=VAL ...]
+    a = sys.argv[1:]
+    o = a[a.index("--out") + 1] if "--out" in a else None
+    print(build(force=True, verbose="-v" in a, defines=[x[2:] for x in a if x.startswith("-D")], out=o))

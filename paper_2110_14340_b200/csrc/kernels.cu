@@ -802,7 +802,18 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(const int32_t *__restr
 constexpr int SB_T = 256;        // partition CTA; tile = SB_T * SB_E updates
 constexpr int SB_E = 16;
 constexpr int SB_MAXB = 1024;    // max buckets
-constexpr int SA_CH = 4096;      // apply chunk (pairs)
+#ifndef SA_CH
+#define SA_CH 2048               // apply chunk (pairs)
+#endif
+#ifndef SA_BPS
+#define SA_BPS 4                 // apply CTAs (256 threads) per SM
+#endif
+#ifndef SA_BITS_RED
+#define SA_BITS_RED 0            // apply sets the dirty bits itself (RED.OR; no bits pass without peers)
+#endif
+#ifndef SA_PFB
+#define SA_PFB 2                 // apply: L2 prefetch of a's slice, buckets ahead (0: off)
+#endif
 constexpr int SBITS_LB = 20;     // bits pass: 2^20 elements (128 KB of bits) per CTA item
 constexpr int SBITS_T = 1024;    // bits CTA
 
@@ -810,9 +821,34 @@ __device__ __forceinline__ bool owned(int32_t k, int32_t lo, unsigned span) {
     return (unsigned)(k - lo) < span;
 }
 
+// Speculative layout (see scatter_add_binned): bucket b's stream starts at
+// b*cap, so the partition needs no histogram.  A tile whose reservation would
+// pass (b+1)*cap raises *ovf and writes nothing; the exact pipeline
+// (histogram, scan, partition) then runs, gated on *ovf, and overwrites the
+// layout.  The init kernel sets both layouts' starting state.
+__global__ void __launch_bounds__(1024) scat_init_kernel(u64 *counts, u64 *cursor, u64 *base,
+                                                         u64 *work, unsigned *ovf, int nb, u64 cap) {
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        counts[b] = 0;
+        cursor[b] = base[b] = (u64)b * cap;
+    }
+    if (threadIdx.x == 0) {
+        base[nb] = (u64)nb * cap;
+        *work = 0;
+        *ovf = 0;
+    }
+}
+
+// exact-pipeline kernels behind a speculative partition run only after an
+// overflow (gate == nullptr: always)
+__device__ __forceinline__ bool scat_skip(const unsigned *gate) {
+    return gate != nullptr && *reinterpret_cast<const volatile unsigned *>(gate) == 0;
+}
+
 __global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restrict__ idx, int64_t n,
                                                         int32_t lo, unsigned span, int shift, int nb,
-                                                        u64 *counts) {
+                                                        u64 *counts, const unsigned *gate) {
+    if (scat_skip(gate)) return;
     __shared__ unsigned h[SB_MAXB];
     for (int i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
     __syncthreads();
@@ -843,7 +879,8 @@ __global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restric
 // exclusive scan of counts[0..nb) -> base[0..nb] and cursor = base (one
 // block of 1024 threads: nb <= SB_MAXB); also zeroes the apply's counter
 __global__ void __launch_bounds__(1024) scat_scan_kernel(const u64 *counts, int nb, u64 *base,
-                                                         u64 *cursor, u64 *work) {
+                                                         u64 *cursor, u64 *work, const unsigned *gate) {
+    if (scat_skip(gate)) return;
     __shared__ u64 wsum[32];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const u64 c = t < nb ? counts[t] : 0;
@@ -912,13 +949,15 @@ __global__ void __launch_bounds__(SB_T, MINB) scat_part_kernel(const int32_t *__
                                                             int32_t lo, unsigned span, int shift,
                                                             int nb, u64 *cursor,
                                                             int32_t *__restrict__ pidx,
-                                                            T *__restrict__ pval) {
+                                                            T *__restrict__ pval, u64 cap,
+    unsigned *ovf, int spec) {
     constexpr int E = SB_E, TILE = SB_T * E;
     constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;  // buckets per thread
     __shared__ unsigned hist[SB_MAXB], loff[SB_MAXB];
     __shared__ u64 gdst[SB_MAXB];
     __shared__ unsigned total;
     extern __shared__ __align__(16) unsigned char sdyn[];  // [TILE] T, [TILE] i32
+    if (spec == 2 && scat_skip(ovf)) return;
     T *sv = reinterpret_cast<T *>(sdyn);
     int32_t *sk = reinterpret_cast<int32_t *>(sdyn + TILE * sizeof(T));
     const int tid = threadIdx.x;
@@ -962,12 +1001,26 @@ __global__ void __launch_bounds__(SB_T, MINB) scat_part_kernel(const int32_t *__
                 sk[pos] = k[j];
                 sv[pos] = v[j];
             }
+        bool bad = false;  // speculative layout: a segment passing its bucket's capacity
 #pragma unroll
         for (int r = 0; r < SB_RES; r++) {
             const int i = tid + r * SB_T;
-            if (i < nb && hist[i]) gdst[i] = res[r] - loff[i];
+            if (i < nb && hist[i]) {
+                gdst[i] = res[r] - loff[i];
+                bad |= spec == 1 && res[r] + hist[i] > (u64)(i + 1) * cap;
+            }
         }
-        __syncthreads();
+        if (spec == 1) {
+            // stop at the first overflow anywhere (this tile writes nothing;
+            // the exact pipeline redoes the launch's partition)
+            if (tid == 0 && *reinterpret_cast<volatile unsigned *>(ovf)) bad = true;
+            if (__syncthreads_or(bad)) {
+                if (tid == 0) atomicOr(ovf, 1u);
+                break;
+            }
+        } else {
+            __syncthreads();
+        }
         const unsigned cnt = total;
         for (unsigned pos = tid; pos < cnt; pos += SB_T) {
             const int32_t kk = sk[pos];
@@ -991,7 +1044,8 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__
                                                                int32_t lo, unsigned span, int shift,
                                                                int nb, u64 *cursor,
                                                                int32_t *__restrict__ pidx,
-                                                               T *__restrict__ pval) {
+                                                               T *__restrict__ pval, u64 cap,
+    unsigned *ovf, int spec) {
     constexpr int E = SB_E, TILE = SB_T * E;
     constexpr int SB_RES = (SB_MAXB + SB_T - 1) / SB_T;
     __shared__ unsigned total, wsum[SB_T / 32];
@@ -999,6 +1053,7 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__
     // gdst u64[nb], hist u32[nb2], loff u32[nb2] (per-bucket state sized by
     // nb so two CTAs fit an SM)
     extern __shared__ __align__(16) unsigned char sdyn[];
+    if (spec == 2 && scat_skip(ovf)) return;
     T *sv = reinterpret_cast<T *>(sdyn);
     int32_t *sk = reinterpret_cast<int32_t *>(sdyn + TILE * sizeof(T));
     T *rv = reinterpret_cast<T *>(sdyn + TILE * (sizeof(T) + 4));
@@ -1091,12 +1146,26 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__
                 sk[pos] = k[j];
                 sv[pos] = v[j];
             }
+        bool bad = false;  // speculative layout: a segment passing its bucket's capacity
 #pragma unroll
         for (int r = 0; r < SB_RES; r++) {
             const int i = tid + r * SB_T;
-            if (i < nb && hist[i]) gdst[i] = res[r] - loff[i];
+            if (i < nb && hist[i]) {
+                gdst[i] = res[r] - loff[i];
+                bad |= spec == 1 && res[r] + hist[i] > (u64)(i + 1) * cap;
+            }
         }
-        __syncthreads();
+        if (spec == 1) {
+            // stop at the first overflow anywhere (this tile writes nothing;
+            // the exact pipeline redoes the launch's partition)
+            if (tid == 0 && *reinterpret_cast<volatile unsigned *>(ovf)) bad = true;
+            if (__syncthreads_or(bad)) {
+                if (tid == 0) atomicOr(ovf, 1u);
+                break;
+            }
+        } else {
+            __syncthreads();
+        }
         const unsigned cnt = total;
         for (unsigned pos = tid; pos < cnt; pos += SB_T) {
             const int32_t kk = sk[pos];
@@ -1117,21 +1186,79 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__
 // SM (96 KB of double-buffered fp64 pairs each).  (Round 1's register loads
 // at 3 CTAs/SM: f64 2.07 vs 2.10 ms, int32 1.66 vs ~1.54 ms.)
 template <typename T>
-__global__ void __launch_bounds__(256, 2) scat_apply_kernel(const int32_t *__restrict__ pidx,
+__global__ void __launch_bounds__(256, SA_BPS) scat_apply_kernel(const int32_t *__restrict__ pidx,
                                                                const T *__restrict__ pval,
-                                                               const u64 *base, int nb, u64 *work,
-                                                               T *a, u64 *dirty) {
+                                                               const u64 *base, const u64 *end, int nb,
+                                                               u64 *work, T *a, u64 *dirty, u64 cap,
+                                                               const unsigned *ovf, int spec,
+                                                               int64_t lo, int64_t hi, int shift,
+                                                               uint32_t *bitmap) {
     extern __shared__ __align__(16) unsigned char sdyn[];  // [2][SA_CH] i32 keys, [2][SA_CH] T values
     int32_t *sk = reinterpret_cast<int32_t *>(sdyn);
     T *sv = reinterpret_cast<T *>(sdyn + 2 * SA_CH * 4);
     __shared__ u64 nextc;
+    __shared__ unsigned cpre[SB_MAXB + 1], wsum[8];
     const int tid = threadIdx.x;
+    // layout: exact (one contiguous stream of base[nb] pairs) or the
+    // speculative fixed-capacity one (bucket b's pairs in [b*cap, end[b]),
+    // chunks numbered over the buckets' non-empty chunks: prefix cpre)
+    const bool fx = spec != 0 && *ovf == 0;
     const int64_t m = (int64_t)base[nb];
-    const int64_t nchunks = (m + SA_CH - 1) / SA_CH;
+    int64_t nchunks = (m + SA_CH - 1) / SA_CH;
+    if (!fx) {
+        // exact layout: cpre[b] = the chunk bucket b starts in (for the
+        // prefetch's bucket lookup only; chunks are positional)
+        for (int bk = tid; bk <= nb; bk += 256) cpre[bk] = (unsigned)(base[bk] / SA_CH);
+        __syncthreads();
+    } else {
+        constexpr int PER = (SB_MAXB + 255) / 256;
+        unsigned cnt[PER], loc = 0;
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            const int bk = tid * PER + j;
+            cnt[j] = bk < nb ? (unsigned)((end[bk] - (u64)bk * cap + SA_CH - 1) / SA_CH) : 0u;
+            loc += cnt[j];
+        }
+        unsigned inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned x = __shfl_up_sync(0xffffffffu, inc, o);
+            if ((tid & 31) >= o) inc += x;
+        }
+        if ((tid & 31) == 31) wsum[tid >> 5] = inc;
+        __syncthreads();
+        unsigned run = inc - loc;
+        for (int w = 0; w < (tid >> 5); w++) run += wsum[w];
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            const int bk = tid * PER + j;
+            if (bk <= nb) cpre[bk] = run;
+            run += cnt[j];
+        }
+        if (tid == 255 && nb >= 256 * PER) cpre[nb] = run;
+        __syncthreads();
+        nchunks = cpre[nb];
+    }
+    // chunk c -> first pair p0, pair count
+    auto chunk = [&](int64_t c, int64_t &p0) -> int {
+        if (!fx) {
+            p0 = c * SA_CH;
+            return (int)(m - p0 < SA_CH ? m - p0 : SA_CH);
+        }
+        int l = 0, h = nb;  // largest bucket l with cpre[l] <= c
+        while (h - l > 1) {
+            const int md = (l + h) >> 1;
+            if (cpre[md] <= (unsigned)c) l = md;
+            else h = md;
+        }
+        p0 = (int64_t)((u64)l * cap) + (c - (int64_t)cpre[l]) * SA_CH;
+        const int64_t left = (int64_t)end[l] - p0;
+        return (int)(left < SA_CH ? left : SA_CH);
+    };
     auto fetch = [&](int64_t c, int st) {
         if (c < nchunks) {
-            const int64_t p0 = c * SA_CH;
-            const int64_t left = m - p0 < SA_CH ? m - p0 : SA_CH;
+            int64_t p0;
+            const int64_t left = chunk(c, p0);
             for (int q = tid; q < SA_CH / 4; q += 256) {
                 const int64_t el = (int64_t)q * 4;
                 const int bytes = el + 4 <= left ? 16 : (el < left ? (int)(left - el) * 4 : 0);
@@ -1159,14 +1286,39 @@ __global__ void __launch_bounds__(256, 2) scat_apply_kernel(const int32_t *__res
         fetch(cn, st ^ 1);
         cp_wait<1>();
         __syncthreads();  // chunk c is in stage st
-        const int64_t p0 = c * SA_CH;
-        const int cnt = (int)(m - p0 < SA_CH ? m - p0 : SA_CH);
+        int64_t p0;
+        const int cnt = chunk(c, p0);
+        if (SA_PFB > 0 && tid == 0) {
+            // warm L2 with bucket b+SA_PFB's slice of `a`: chunk j of bucket b's
+            // K chunks prefetches fraction [j/K, (j+1)/K) of it, so the REDs of
+            // that bucket find its lines resident instead of missing on them
+            int l = 0, h = nb;
+            while (h - l > 1) {
+                const int md = (l + h) >> 1;
+                if (cpre[md] <= (unsigned)c) l = md;
+                else h = md;
+            }
+            const int tb = l + SA_PFB;
+            if (tb < nb) {
+                const int64_t K = cpre[l + 1] > cpre[l] ? cpre[l + 1] - cpre[l] : 1;
+                const int64_t j = c - cpre[l] < K ? c - cpre[l] : K - 1;
+                const int64_t e0 = lo + ((int64_t)tb << shift);
+                const int64_t e1 = e0 + ((int64_t)1 << shift) < hi ? e0 + ((int64_t)1 << shift) : hi;
+                const int64_t bytes = (e1 - e0) * (int64_t)sizeof(T);
+                const uintptr_t p = (reinterpret_cast<uintptr_t>(a + e0) + (uintptr_t)(bytes * j / K)) & ~(uintptr_t)15;
+                const uintptr_t q = (reinterpret_cast<uintptr_t>(a + e0) + (uintptr_t)(bytes * (j + 1) / K)) & ~(uintptr_t)15;
+                if (q > p)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)(q - p))
+                                 : "memory");
+            }
+        }
         const int32_t *ck = sk + st * SA_CH;
         const T *cv = sv + st * SA_CH;
 #pragma unroll 4
         for (int q = tid; q < cnt; q += 256) {
             const int32_t k = ck[q];
             atomicAdd(a + k, cv[q]);
+            if (SA_BITS_RED) atomicOr(bitmap + (k >> 5), 1u << (k & 31));
             mn = (u64)k < mn ? (u64)k : mn;
             mx = (u64)k > mx ? (u64)k : mx;
         }
@@ -1193,7 +1345,8 @@ __global__ void __launch_bounds__(256, 2) scat_apply_kernel(const int32_t *__res
 // profiles/scat_experiments_r02.txt.)
 template <typename T>
 __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__restrict__ pidx,
-                                                            const u64 *__restrict__ base, int nb,
+                                                            const u64 *__restrict__ base,
+                                                            const u64 *__restrict__ end, int nb,
                                                             int shift, int64_t lo, int64_t hi,
                                                             uint32_t *bitmap, const T *__restrict__ a,
                                                             PeerPtrs push) {
@@ -1208,7 +1361,7 @@ __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__res
         if (e0 >= hi) continue;  // uniform per CTA
         const int64_t e1 = e0 + ((int64_t)1 << pb) < hi ? e0 + ((int64_t)1 << pb) : hi;
         const int64_t w0 = e0 >> 5, nw = ((e1 - 1) >> 5) - w0 + 1;
-        const u64 p0 = base[bk], p1 = base[bk + 1];
+        const u64 p0 = base[bk], p1 = end[bk];  // end = the partition's final cursor
         for (int i = threadIdx.x; i < nw; i += SBITS_T) sw[i] = 0;
         __syncthreads();
         auto put = [&](int64_t k) {
@@ -2093,8 +2246,21 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_
     p.shift = shift;
     p.nb = (int)((span + ((int64_t)1 << shift) - 1) >> shift);
     p.all_owned = lo == 0 && hi >= m_total;
-    p.hdr = ((size_t)(3 * p.nb + 2) * 8 + 255) & ~(size_t)255;
-    p.scratch = p.hdr + (((size_t)n * 4 + 255) & ~(size_t)255) + (size_t)n * elem;
+    // Speculative layout: with i.i.d. uniform keys (the workload's reading,
+    // DESIGN R-7) a bucket receives n*2^shift/m_total owned updates, and the
+    // fullest of 256 buckets at 2^28 exceeds the mean by ~0.4 %; capacity =
+    // mean + 1/8 + two tiles.  Skewed index mixes overflow and take the exact
+    // pipeline in the same launch (device-side gate, no host round trip).
+    const char *sp = getenv("JACC_SCATTER_SPEC");  // "0": exact pipeline only (A/B, tests)
+    const int64_t mean = (int64_t)(((unsigned __int128)n << shift) / (unsigned __int128)(m_total > 0 ? m_total : 1));
+    int64_t cap = mean + mean / 8 + 2 * (int64_t)SB_T * SB_E;
+    cap = (cap + SA_CH - 1) / SA_CH * SA_CH;
+    p.spec = !(sp && sp[0] == '0');
+    p.cap = (u64)cap;
+    p.slots = (size_t)n;
+    if (p.spec && (size_t)p.nb * (size_t)cap > p.slots) p.slots = (size_t)p.nb * (size_t)cap;
+    p.hdr = ((size_t)(3 * p.nb + 3) * 8 + 255) & ~(size_t)255;
+    p.scratch = p.hdr + ((p.slots * 4 + 255) & ~(size_t)255) + p.slots * elem;
     return p;
 }
 
@@ -2103,21 +2269,19 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
                                u64 *dirty, const ScatterPlan &pl, void *scratch, PeerPtrs push) {
     char *sc = static_cast<char *>(scratch);
     u64 *counts = reinterpret_cast<u64 *>(sc);
-    u64 *cursor = counts + pl.nb;
-    u64 *base = cursor + pl.nb;  // nb + 1
+    u64 *cursor = counts + pl.nb;  // after the partition: every bucket's stream end
+    u64 *base = cursor + pl.nb;    // nb + 1
     u64 *work = base + pl.nb + 1;
+    unsigned *ovf = reinterpret_cast<unsigned *>(work + 1);
     int32_t *pidx = reinterpret_cast<int32_t *>(sc + pl.hdr);
-    char *pv = sc + pl.hdr + (((size_t)n * 4 + 255) & ~(size_t)255);
+    char *pv = sc + pl.hdr + ((pl.slots * 4 + 255) & ~(size_t)255);
     const int32_t lo32 = (int32_t)lo;
     const unsigned span = (unsigned)(hi - lo);
-    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)pl.nb * 8, s);
-    if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
-    scat_hist_kernel<<<nsm * 8, 256, 0, s>>>(idx, n, lo32, span, pl.shift, pl.nb, counts);
-    scat_scan_kernel<<<1, 1024, 0, s>>>(counts, pl.nb, base, cursor, work);
+    scat_init_kernel<<<1, 1024, 0, s>>>(counts, cursor, base, work, ovf, pl.nb, pl.cap);
     const int64_t tile = (int64_t)SB_T * SB_E;
     const int pg = (int)std::min<int64_t>((n + tile - 1) / tile, (int64_t)nsm * 8);
     const int pdsm = (int)tile * ((is_f64 ? 8 : 4) + 4);
@@ -2129,42 +2293,60 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     // cp.async (1.50 vs 1.61 ms for the register-load partition at 2^28)
     const bool pf = all && ((uintptr_t)idx % 16 == 0) && ((uintptr_t)b % 16 == 0);
     const int pfsm = 2 * pdsm + pl.nb * 8 + ((pl.nb + 1) & ~1) * 8;
-    // attributes are per device: set on every call (host-side, cheap)
-    if (is_f64) {
-        if (pf) {
-            cudaFuncSetAttribute(scat_part_pf_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, pfsm);
-            scat_part_pf_kernel<double><<<pg, SB_T, pfsm, s>>>(idx, static_cast<const double *>(b), n, lo32,
-                                                                   span, pl.shift, pl.nb, cursor, pidx,
-                                                                   reinterpret_cast<double *>(pv));
+    auto partition = [&](int spec) {
+        // attributes are per device: set on every call (host-side, cheap)
+        if (is_f64) {
+            if (pf) {
+                cudaFuncSetAttribute(scat_part_pf_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, pfsm);
+                scat_part_pf_kernel<double><<<pg, SB_T, pfsm, s>>>(idx, static_cast<const double *>(b), n, lo32,
+                                                                       span, pl.shift, pl.nb, cursor, pidx,
+                                                                       reinterpret_cast<double *>(pv), pl.cap,
+                                                                       ovf, spec);
+            } else {
+                auto kp = all ? scat_part_kernel<double, true> : scat_part_kernel<double, false>;
+                cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+                kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo32, span, pl.shift, pl.nb,
+                                          cursor, pidx, reinterpret_cast<double *>(pv), pl.cap, ovf, spec);
+            }
         } else {
-            auto kp = all ? scat_part_kernel<double, true> : scat_part_kernel<double, false>;
-            cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-            kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const double *>(b), n, lo32, span, pl.shift, pl.nb,
-                                      cursor, pidx, reinterpret_cast<double *>(pv));
+            if (pf) {
+                cudaFuncSetAttribute(scat_part_pf_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, pfsm);
+                scat_part_pf_kernel<int32_t><<<pg, SB_T, pfsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32,
+                                                                        span, pl.shift, pl.nb, cursor, pidx,
+                                                                        reinterpret_cast<int32_t *>(pv), pl.cap,
+                                                                        ovf, spec);
+            } else {
+                auto kp = all ? scat_part_kernel<int32_t, true> : scat_part_kernel<int32_t, false>;
+                cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
+                kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32, span, pl.shift, pl.nb,
+                                          cursor, pidx, reinterpret_cast<int32_t *>(pv), pl.cap, ovf, spec);
+            }
         }
+    };
+    // speculative partition, then the exact pipeline gated on its overflow
+    // flag (without speculation: the exact pipeline, ungated)
+    const unsigned *gate = pl.spec ? ovf : nullptr;
+    if (pl.spec) partition(1);
+    scat_hist_kernel<<<nsm * 8, 256, 0, s>>>(idx, n, lo32, span, pl.shift, pl.nb, counts, gate);
+    scat_scan_kernel<<<1, 1024, 0, s>>>(counts, pl.nb, base, cursor, work, gate);
+    partition(pl.spec ? 2 : 0);
+    const int aspec = pl.spec ? 1 : 0;
+    if (is_f64) {
         const int asm_ = 2 * SA_CH * (4 + 8);
         cudaFuncSetAttribute(scat_apply_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_);
-        scat_apply_kernel<double><<<nsm * 2, 256, asm_, s>>>(pidx, reinterpret_cast<const double *>(pv),
-                                                                base, pl.nb, work, static_cast<double *>(a),
-                                                                dirty);
+        scat_apply_kernel<double><<<nsm * SA_BPS, 256, asm_, s>>>(pidx, reinterpret_cast<const double *>(pv),
+                                                                base, cursor, pl.nb, work,
+                                                                static_cast<double *>(a), dirty, pl.cap, ovf,
+                                                                aspec, lo, hi, pl.shift, bitmap);
     } else {
-        if (pf) {
-            cudaFuncSetAttribute(scat_part_pf_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, pfsm);
-            scat_part_pf_kernel<int32_t><<<pg, SB_T, pfsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32,
-                                                                    span, pl.shift, pl.nb, cursor, pidx,
-                                                                    reinterpret_cast<int32_t *>(pv));
-        } else {
-            auto kp = all ? scat_part_kernel<int32_t, true> : scat_part_kernel<int32_t, false>;
-            cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, pdsm);
-            kp<<<pg, SB_T, pdsm, s>>>(idx, static_cast<const int32_t *>(b), n, lo32, span, pl.shift, pl.nb,
-                                      cursor, pidx, reinterpret_cast<int32_t *>(pv));
-        }
         const int asm_ = 2 * SA_CH * (4 + 4);
         cudaFuncSetAttribute(scat_apply_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_);
-        scat_apply_kernel<int32_t><<<nsm * 2, 256, asm_, s>>>(pidx, reinterpret_cast<const int32_t *>(pv),
-                                                                 base, pl.nb, work,
-                                                                 static_cast<int32_t *>(a), dirty);
+        scat_apply_kernel<int32_t><<<nsm * SA_BPS, 256, asm_, s>>>(pidx, reinterpret_cast<const int32_t *>(pv),
+                                                                 base, cursor, pl.nb, work,
+                                                                 static_cast<int32_t *>(a), dirty, pl.cap, ovf,
+                                                                 aspec, lo, hi, pl.shift, bitmap);
     }
+    if (SA_BITS_RED && push.n == 0) return cudaGetLastError();
     const int pb = pl.shift > SBITS_LB ? SBITS_LB : pl.shift;
     const int smem = (int)((((int64_t)1 << pb) >> 5) + 2) * 4;
     if (is_f64)
@@ -2174,10 +2356,10 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     const int64_t items = (int64_t)pl.nb << (pl.shift - pb);
     const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
     if (is_f64)
-        scat_bits_kernel<double><<<g, SBITS_T, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap,
+        scat_bits_kernel<double><<<g, SBITS_T, smem, s>>>(pidx, base, cursor, pl.nb, pl.shift, lo, hi, bitmap,
                                                           static_cast<const double *>(a), push);
     else
-        scat_bits_kernel<int32_t><<<g, SBITS_T, smem, s>>>(pidx, base, pl.nb, pl.shift, lo, hi, bitmap,
+        scat_bits_kernel<int32_t><<<g, SBITS_T, smem, s>>>(pidx, base, cursor, pl.nb, pl.shift, lo, hi, bitmap,
                                                            static_cast<const int32_t *>(a), push);
     return cudaGetLastError();
 }

@@ -73,8 +73,11 @@ struct ScatterPlan {
     bool binned;
     bool all_owned;     // [lo, hi) covers every element of a (one device / duplicated)
     int shift, nb;      // bucket = 2^shift elements, nb buckets
+    bool spec;          // speculative fixed-capacity layout first (no histogram pass)
+    u64 cap;            // its pairs per bucket (bucket b at [b*cap, (b+1)*cap))
+    size_t slots;       // pair slots: max(n, nb*cap)
     size_t hdr;         // bytes of counters/bases at the start of the scratch
-    size_t scratch;     // total scratch bytes (header + n keys + n values)
+    size_t scratch;     // total scratch bytes (header + slots keys + slots values)
 };
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_total);
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,

@@ -552,9 +552,13 @@ def test_scatter_paths_and_misaligned_ranges(J, monkeypatch, binned, n, lo):
 
 @pytest.mark.parametrize("dtype", ["f64", "i32"])
 @pytest.mark.parametrize("n", [1, 2, 3])
-def test_scatter_binned_large(J, dtype, n):
+@pytest.mark.parametrize("spec", ["1", "0"])
+def test_scatter_binned_large(J, monkeypatch, dtype, n, spec):
     """Arrays larger than L2 take the binned pipeline by default; n=3 gives
-    owned spans off word and bucket boundaries."""
+    owned spans off word and bucket boundaries.  spec=1: the speculative
+    fixed-capacity layout (uniform keys never overflow it); spec=0: the exact
+    histogram pipeline."""
+    monkeypatch.setenv("JACC_SCATTER_SPEC", spec)
     M = 2**25 if dtype == "f64" else 2**26
     N = 2**23
     idx = synth.index_i32(N, M, 76, 5)
@@ -590,6 +594,42 @@ def test_scatter_binned_ragged_skewed(J, monkeypatch, dtype, n):
         b, a0 = synth.dyadic_f64(N, 79, 6), synth.dyadic_f64(M, 79, 7)
     else:
         b, a0 = synth.int_i32(N, -1000, 1000, 79, 6), synth.int_i32(M, -10**6, 10**6, 79, 7)
+    ref = a0.copy()
+    orc.scatter_add(idx, b, ref)
+    a, bms, drs, reps = _scatter(J, idx, b, a0, n)
+    assert np.array_equal(a, ref)
+    for d in range(n):
+        lo, hi = orc.partition(M, n, d)
+        bm, mn, mx = orc.scatter_add_filtered(idx, b, a0.copy(), lo, hi - 1)
+        assert np.array_equal(bms[d], bm) and drs[d] == (mn, mx)
+        assert np.array_equal(reps[d], ref)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "i32"])
+@pytest.mark.parametrize("n", [1, 3])
+@pytest.mark.parametrize("where", ["late", "slight"])
+def test_scatter_binned_overflow(J, monkeypatch, dtype, n, where):
+    """The speculative layout's fallback: uniform keys except that the LAST
+    tenth of the updates lands in one bucket ("late": the overflow is found
+    after most tiles were written speculatively), or one bucket receiving
+    ~1.3x the mean ("slight": just past the 1/8 slack).  The exact pipeline
+    must redo the partition in the same launch; every result, bitmap and
+    range equals the oracle."""
+    monkeypatch.setenv("JACC_SCATTER_BINNED", "1")
+    M = 2**24 + 999 if dtype == "f64" else 2**25 + 999
+    N = 2**23 + 5
+    idx = synth.index_i32(N, M, 81, 5)
+    if where == "late":
+        k = N // 10
+        idx[N - k:] = synth.index_i32(k, 2**19, 81, 8) + np.int32(2**20 + 5)
+    else:
+        k = (3 * (N * 2**20 // M)) // 10  # +0.3 of a bucket's mean share, spread over the input
+        pos = np.linspace(0, N - 1, k).astype(np.int64)
+        idx[pos] = synth.index_i32(k, 2**20, 81, 8) + np.int32(2**21)
+    if dtype == "f64":
+        b, a0 = synth.dyadic_f64(N, 81, 6), synth.dyadic_f64(M, 81, 7)
+    else:
+        b, a0 = synth.int_i32(N, -1000, 1000, 81, 6), synth.int_i32(M, -10**6, 10**6, 81, 7)
     ref = a0.copy()
     orc.scatter_add(idx, b, ref)
     a, bms, drs, reps = _scatter(J, idx, b, a0, n)
