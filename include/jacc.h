@@ -405,7 +405,7 @@ jacc_status jacc_get_info(jacc_info *out);
  * the caller's own replica coherent and copies it to the caller's host
  * buffer.  Introspection calls accept only the caller's device. */
 #define JACC_UNIQUE_ID_BYTES 128
-#define JACC_RUNTIME_HANDLE_BYTES 192
+#define JACC_RUNTIME_HANDLE_BYTES 256
 #define JACC_REGION_HANDLE_BYTES 64
 
 /* NCCL unique id for the reduction communicator (out: >= 128 bytes). */
@@ -420,8 +420,9 @@ jacc_status jacc_unique_id(void *out, size_t bytes);
 jacc_status jacc_init_rank(int rank, int world, int cuda_ordinal, const void *unique_id,
                            const char *shm_name);
 
-/* Opaque handle blob of this rank's events and reduction buffer
- * (>= JACC_RUNTIME_HANDLE_BYTES) / import a peer's. */
+/* Opaque handle blob of this rank's events, reduction buffer and GPU UUID
+ * (>= JACC_RUNTIME_HANDLE_BYTES) / import a peer's (a peer on the same GPU
+ * makes jacc_get_info report distinct_gpus = 0). */
 jacc_status jacc_export_runtime(void *out, size_t bytes);
 jacc_status jacc_import_runtime(int peer, const void *in, size_t bytes);
 

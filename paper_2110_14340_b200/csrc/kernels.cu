@@ -808,9 +808,6 @@ constexpr int SB_MAXB = 1024;    // max buckets
 #ifndef SA_BPS
 #define SA_BPS 4                 // apply CTAs (256 threads) per SM
 #endif
-#ifndef SA_BITS_RED
-#define SA_BITS_RED 0            // apply sets the dirty bits itself (RED.OR; no bits pass without peers)
-#endif
 #ifndef SA_PFB
 #define SA_PFB 2                 // apply: L2 prefetch of a's slice, buckets ahead (0: off)
 #endif
@@ -1191,8 +1188,7 @@ __global__ void __launch_bounds__(256, SA_BPS) scat_apply_kernel(const int32_t *
                                                                const u64 *base, const u64 *end, int nb,
                                                                u64 *work, T *a, u64 *dirty, u64 cap,
                                                                const unsigned *ovf, int spec,
-                                                               int64_t lo, int64_t hi, int shift,
-                                                               uint32_t *bitmap) {
+                                                               int64_t lo, int64_t hi, int shift) {
     extern __shared__ __align__(16) unsigned char sdyn[];  // [2][SA_CH] i32 keys, [2][SA_CH] T values
     int32_t *sk = reinterpret_cast<int32_t *>(sdyn);
     T *sv = reinterpret_cast<T *>(sdyn + 2 * SA_CH * 4);
@@ -1318,7 +1314,6 @@ __global__ void __launch_bounds__(256, SA_BPS) scat_apply_kernel(const int32_t *
         for (int q = tid; q < cnt; q += 256) {
             const int32_t k = ck[q];
             atomicAdd(a + k, cv[q]);
-            if (SA_BITS_RED) atomicOr(bitmap + (k >> 5), 1u << (k & 31));
             mn = (u64)k < mn ? (u64)k : mn;
             mx = (u64)k > mx ? (u64)k : mx;
         }
@@ -2337,16 +2332,15 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
         scat_apply_kernel<double><<<nsm * SA_BPS, 256, asm_, s>>>(pidx, reinterpret_cast<const double *>(pv),
                                                                 base, cursor, pl.nb, work,
                                                                 static_cast<double *>(a), dirty, pl.cap, ovf,
-                                                                aspec, lo, hi, pl.shift, bitmap);
+                                                                aspec, lo, hi, pl.shift);
     } else {
         const int asm_ = 2 * SA_CH * (4 + 4);
         cudaFuncSetAttribute(scat_apply_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_);
         scat_apply_kernel<int32_t><<<nsm * SA_BPS, 256, asm_, s>>>(pidx, reinterpret_cast<const int32_t *>(pv),
                                                                  base, cursor, pl.nb, work,
                                                                  static_cast<int32_t *>(a), dirty, pl.cap, ovf,
-                                                                 aspec, lo, hi, pl.shift, bitmap);
+                                                                 aspec, lo, hi, pl.shift);
     }
-    if (SA_BITS_RED && push.n == 0) return cudaGetLastError();
     const int pb = pl.shift > SBITS_LB ? SBITS_LB : pl.shift;
     const int smem = (int)((((int64_t)1 << pb) >> 5) + 2) * 4;
     if (is_f64)

@@ -81,7 +81,7 @@ jacc_status jacc_init_rank(int rank, int world, int cuda_ordinal, const void *un
 jacc_status jacc_export_runtime(void *out, size_t bytes) {
     return guard([&]() -> jacc_status {
         if (!R.mp || !out || bytes < JACC_RUNTIME_HANDLE_BYTES) return JACC_ERR_INVALID;
-        static_assert(3 * sizeof(cudaIpcMemHandle_t) <= JACC_RUNTIME_HANDLE_BYTES, "handle size");
+        static_assert(3 * sizeof(cudaIpcMemHandle_t) + 16 <= JACC_RUNTIME_HANDLE_BYTES, "handle size");
         Device &dv = R.dev[R.me];
         set_dev(R.me);
         char *o = static_cast<char *>(out);
@@ -94,6 +94,10 @@ jacc_status jacc_export_runtime(void *out, size_t bytes) {
         memcpy(o, &e0, sizeof(e0));
         memcpy(o + 64, &e1, sizeof(e1));
         memcpy(o + 128, &mp, sizeof(mp));
+        // the GPU's UUID: importers learn whether two ranks share a GPU
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, dv.ord));
+        memcpy(o + 192, &prop.uuid, 16);
         return JACC_OK;
     });
 }
@@ -117,6 +121,9 @@ jacc_status jacc_import_runtime(int peer, const void *in, size_t bytes) {
         CK(cudaIpcOpenMemHandle(&ptr, mp, cudaIpcMemLazyEnablePeerAccess));
         pv.part = static_cast<double *>(ptr);
         pv.ord = -1;
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, R.dev[R.me].ord));
+        if (!memcmp(p + 192, &prop.uuid, 16)) R.distinct = false;  // reported by jacc_get_info
         return JACC_OK;
     });
 }

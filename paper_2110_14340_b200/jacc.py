@@ -64,7 +64,7 @@ JACC_MAX_QUEUES = 32
 JACC_ASYNC_AUTO = -2
 JACC_MODE_ADAPTIVE = 2
 JACC_UNIQUE_ID_BYTES = 128
-JACC_RUNTIME_HANDLE_BYTES = 192
+JACC_RUNTIME_HANDLE_BYTES = 256
 JACC_REGION_HANDLE_BYTES = 64
 
 

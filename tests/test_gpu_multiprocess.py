@@ -69,6 +69,11 @@ def test_multiprocess_parity(tmp_path, world, policy):
     for rank in range(world):
         z = np.load(tmp_path / f"rank{rank}.npz")
         assert int(z["world"]) == world
+        # the ranks share this box's GPU: the runtime must say so (GPU UUIDs
+        # in the exchanged runtime handles) and combine over peer memory
+        import torch
+        if torch.cuda.device_count() < world:
+            assert z["info"].tolist() == [world, 0, 0]
         assert np.array_equal(z["A"], A) and np.array_equal(z["B"], B), rank
         lo, hi = orc.partition(N, world, rank)
         # dirty range of the last A-writing sweep == oracle write log

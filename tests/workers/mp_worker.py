@@ -118,6 +118,8 @@ def main():
     J.jacc_update_host(fa)
     J.jacc_update_host(fb)
     res["fig4_a"], res["fig4_b"] = fa, fb
+    info = J.jacc_get_info()
+    res["info"] = np.array([info["n_devices"], info["distinct_gpus"], info["combine"] == "nccl"])
     jd.finalize()
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), world=world, **res)
     dist.destroy_process_group()
