@@ -744,7 +744,7 @@ def run_loops(J, C, n, peaks, args):
         t, k, m = _time_loop(J, C, launch, 5)
         byts = S * per
         te = _e2e(J, C, [idx, b, a], launch, [a], reps=1)
-        tk = [f"scat_{p}" + ("" if dt == "f64" else "_i32") for p in ("hist", "part", "apply", "bits")]
+        tk = [f"scat_{p}" + ("" if dt == "f64" else "_i32") for p in ("part", "apply", "bits")]
         ach = byts / k / 1e9 if n == 1 else None
         out[f"scatter_{dt}_2^28"] = {
             "workload": f"SCAT: a[idx[i]] += b[i], {dt}, 2^28 updates into 2^28 elements, "

@@ -1653,6 +1653,9 @@ __global__ void __launch_bounds__(HT, MINB) himeno_stencil_kernel(
 // float4 chunks + one head/tail scalar per row) before any store, so
 // 2 x HC KB are in flight per warp.  HALO boundary planes are also stored
 // into the neighbours' replicas (push_top / push_bot).
+#ifndef HIMENO_COPY_MINB
+#define HIMENO_COPY_MINB 3      // copy CTAs per SM (3: 0.447 vs 0.454 ms at 1 -- 2 by registers)
+#endif
 constexpr int HC = 2;  // rows per round
 __device__ __forceinline__ void himeno_copy_row_vec(const float *__restrict__ wrk2, float *__restrict__ p,
                                                     float *tp, float *bp, int64_t rb, int64_t k0,
@@ -1687,7 +1690,7 @@ __device__ __forceinline__ void himeno_copy_row_vec(const float *__restrict__ wr
         }
 }
 
-__global__ void __launch_bounds__(HT) himeno_copy_kernel(
+__global__ void __launch_bounds__(HT, HIMENO_COPY_MINB) himeno_copy_kernel(
     const float *__restrict__ wrk2, float *__restrict__ p, int64_t J, int64_t K, int64_t i0,
     int64_t i1, int64_t j0, int64_t j1, int64_t k0, int64_t k1, u64 *dirty, float *push_top,
     float *push_bot, unsigned *ticket) {

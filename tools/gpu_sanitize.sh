@@ -9,7 +9,7 @@ mkdir -p gpurun_out
 TAG=${ROUND_TAG:-r02}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 T=tests/test_gpu_parity.py
-K='J256 or test_jacobi_multi_device and 17- or test_scatter_exact and 100- or test_square_multi and 1000- or test_dot_sum_dyadic_exact and 4096 or test_gemm_random_tolerance or himeno_multi_device and shape1 or test_fig4_chain and 257 or test_scatter_iteration_split and sizes0 or test_iteration_split_back_to_back_halo or test_graph_capture or async_queues or test_scatter_paths_and_misaligned_ranges or test_scatter_binned_extreme_skew or test_jacobi_column_split'
+K='J256 or test_jacobi_multi_device and 17- or test_scatter_exact and 100- or test_square_multi and 1000- or test_dot_sum_dyadic_exact and 4096 or test_gemm_random_tolerance or himeno_multi_device and shape1 or test_fig4_chain and 257 or test_scatter_iteration_split and sizes0 or test_iteration_split_back_to_back_halo or test_graph_capture or async_queues or test_scatter_paths_and_misaligned_ranges or test_scatter_binned_extreme_skew or test_scatter_binned_overflow and late or test_jacobi_column_split'
 for tool in memcheck racecheck synccheck; do
   extra=""
   [ $tool = memcheck ] && extra="--leak-check no"
