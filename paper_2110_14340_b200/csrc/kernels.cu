@@ -1644,6 +1644,185 @@ __global__ void __launch_bounds__(HT, MINB) himeno_stencil_kernel(
     publish_dirty_flat(mn, mx, dirty);
 }
 
+// Plane-marching stencil (rows 16-byte aligned: K % 4 == 0 and aligned
+// bases -- the benchmark's grids).  A tile is 8 rows (j) x 128 points (k) x
+// up to 32 planes (i); a CTA (8 warps, warp = row, lane = 4 consecutive k)
+// marches its tile along i with the p rows j-1..j+8 of planes i-1, i, i+1 in
+// a 4-slot shared-memory ring, plane i+2 arriving by cp.async while plane i
+// is computed.  p comes from HBM once per tile (+2 halo rows of 10, +2 halo
+// planes of 32) instead of being re-read for every neighbour row: the
+// row-per-warp kernel read p ~3.5x from DRAM (a build without the
+// coefficient loads still read 2.7 GB for the 1.07 GB p, profiles/
+// himeno_experiments_r01.txt).  Tiles are handed out in (k, j, i) order by
+// an atomic counter, so tiles in flight share their halo rows in L2.
+// Arithmetic per point exactly as himeno_point (fp32 as written).
+#ifndef HIMENO_PM
+#define HIMENO_PM 1
+#endif
+constexpr int H5_JB = 8, H5_KW = 128, H5_IS = 32;
+constexpr int H5_RS = H5_KW + 8;              // smem row: k halo of 4 on each side
+constexpr int H5_PL = (H5_JB + 2) * H5_RS;    // floats per plane slot
+__global__ void __launch_bounds__(256, 2) himeno_stencil_pm_kernel(
+    const float *__restrict__ p, const float *__restrict__ a, const float *__restrict__ b,
+    const float *__restrict__ c, const float *__restrict__ wrk1, const float *__restrict__ bnd,
+    float *__restrict__ wrk2, int64_t I, int64_t J, int64_t K, int64_t i0, int64_t i1, int64_t j0,
+    int64_t j1, int64_t k0, int64_t k1, float omega, double *partials, unsigned *ticket,
+    double *out, u64 *dirty) {
+    __shared__ __align__(16) float sp[4 * H5_PL];
+    __shared__ double sh[8];
+    __shared__ bool last;
+    __shared__ long long stile;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t P = J * K, V = I * J * K;
+    const float *co[12] = {a, a + V, a + 2 * V, a + 3 * V, b, b + V, b + 2 * V,
+                           c, c + V, c + 2 * V, wrk1, bnd};
+    const int64_t kb0 = k0 & ~(int64_t)3;
+    const int64_t nks = (k1 - kb0 + H5_KW - 1) / H5_KW;
+    const int64_t njb = (j1 - j0 + H5_JB - 1) / H5_JB;
+    const int64_t nis = (i1 - i0 + H5_IS - 1) / H5_IS;
+    const int64_t ntiles = nks * njb * nis;
+    u64 *ctr = reinterpret_cast<u64 *>(ticket + 8);
+    double g = 0.0;
+    u64 mn = kU64Max, mx = 0;
+    // p rows jb-1 .. jb+8, k kb-4 .. kb+131 of plane i into ring slot i & 3
+    // (outside the array: zero-filled, never read as a neighbour of a point
+    // of the box)
+    auto load_plane = [&](int64_t i, int64_t jb, int64_t kb) {
+        float *dst = sp + (int)(i & 3) * H5_PL;
+        for (int q = tid; q < (H5_JB + 2) * (H5_RS / 4); q += 256) {
+            const int r = q / (H5_RS / 4), c4 = q - r * (H5_RS / 4);
+            const int64_t j = jb - 1 + r, k = kb - 4 + 4 * c4;
+            const bool ok = i >= 0 && i < I && j >= 0 && j < J && k >= 0 && k < K;
+            cp_async16(dst + r * H5_RS + 4 * c4, ok ? p + i * P + j * K + k : p, ok ? 16 : 0);
+        }
+    };
+    for (;;) {
+        __syncthreads();  // the previous tile's planes are no longer read; stile consumed
+        if (tid == 0) stile = (long long)atomicAdd(ctr, 1ull);
+        __syncthreads();
+        const int64_t t = stile;
+        if (t >= ntiles) break;
+        const int64_t ks = t % nks, jbi = (t / nks) % njb, isg = t / (nks * njb);
+        const int64_t kb = kb0 + ks * H5_KW, jb = j0 + jbi * H5_JB;
+        const int64_t is = i0 + isg * H5_IS, ie = is + H5_IS < i1 ? is + H5_IS : i1;
+        load_plane(is - 1, jb, kb);
+        load_plane(is, jb, kb);
+        cp_commit();
+        load_plane(is + 1, jb, kb);
+        cp_commit();
+        const int64_t j = jb + w, k = kb + 4 * lane;
+        // points k .. k+3 of row j: valid ones are in [k0, k1); a chunk with
+        // none skips its loads (k < k1 <= K keeps the float4 inside the row)
+        const bool any = j < j1 && k + 3 >= k0 && k < k1;
+        const bool full = j < j1 && k >= k0 && k + 4 <= k1;
+        for (int64_t i = is; i < ie; i++) {
+            cp_wait<0>();
+            __syncthreads();  // plane i+1 is in; every warp is past plane i-1 (slot of i+2 free)
+            if (i + 2 <= ie) load_plane(i + 2, jb, kb);
+            cp_commit();
+            if (!any) continue;
+            const int64_t x = i * P + j * K + k;
+            const float4 A0 = __ldcs(reinterpret_cast<const float4 *>(co[0] + x));
+            const float4 A1 = __ldcs(reinterpret_cast<const float4 *>(co[1] + x));
+            const float4 A2 = __ldcs(reinterpret_cast<const float4 *>(co[2] + x));
+            const float4 A3 = __ldcs(reinterpret_cast<const float4 *>(co[3] + x));
+            const float4 B0 = __ldcs(reinterpret_cast<const float4 *>(co[4] + x));
+            const float4 B1 = __ldcs(reinterpret_cast<const float4 *>(co[5] + x));
+            const float4 B2 = __ldcs(reinterpret_cast<const float4 *>(co[6] + x));
+            const float4 C0 = __ldcs(reinterpret_cast<const float4 *>(co[7] + x));
+            const float4 C1 = __ldcs(reinterpret_cast<const float4 *>(co[8] + x));
+            const float4 C2 = __ldcs(reinterpret_cast<const float4 *>(co[9] + x));
+            const float4 W1 = __ldcs(reinterpret_cast<const float4 *>(co[10] + x));
+            const float4 BD = __ldcs(reinterpret_cast<const float4 *>(co[11] + x));
+            const float *s0p = sp + (int)(i & 3) * H5_PL + (w + 1) * H5_RS + 4 * lane + 4;
+            const float *sPp = sp + (int)((i + 1) & 3) * H5_PL + (w + 1) * H5_RS + 4 * lane + 4;
+            const float *sMp = sp + (int)((i - 1) & 3) * H5_PL + (w + 1) * H5_RS + 4 * lane + 4;
+            auto row = [](const float *q) {
+                PRow o;
+                o.v = *reinterpret_cast<const float4 *>(q);
+                o.l = q[-1];
+                o.r = q[4];
+                return o;
+            };
+            const PRow C = row(s0p), JP = row(s0p + H5_RS), JM = row(s0p - H5_RS);
+            const PRow IP = row(sPp), IM = row(sMp);
+            const float4 pp = *reinterpret_cast<const float4 *>(sPp + H5_RS);
+            const float4 pm = *reinterpret_cast<const float4 *>(sPp - H5_RS);
+            const float4 mp = *reinterpret_cast<const float4 *>(sMp + H5_RS);
+            const float4 mm = *reinterpret_cast<const float4 *>(sMp - H5_RS);
+            float res[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                float s0 = __fmul_rn(f4(A0, e), f4(IP.v, e));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(A1, e), f4(JP.v, e)));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(A2, e), kp(C, e)));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(B0, e),
+                                             __fadd_rn(__fsub_rn(__fsub_rn(f4(pp, e), f4(pm, e)), f4(mp, e)),
+                                                       f4(mm, e))));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(B1, e),
+                                             __fadd_rn(__fsub_rn(__fsub_rn(kp(JP, e), kp(JM, e)), km(JP, e)),
+                                                       km(JM, e))));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(B2, e),
+                                             __fadd_rn(__fsub_rn(__fsub_rn(kp(IP, e), kp(IM, e)), km(IP, e)),
+                                                       km(IM, e))));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(C0, e), f4(IM.v, e)));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(C1, e), f4(JM.v, e)));
+                s0 = __fadd_rn(s0, __fmul_rn(f4(C2, e), km(C, e)));
+                s0 = __fadd_rn(s0, f4(W1, e));
+                const float p0 = f4(C.v, e);
+                const float ss = __fmul_rn(__fsub_rn(__fmul_rn(s0, f4(A3, e)), p0), f4(BD, e));
+                if (full || (k + e >= k0 && k + e < k1)) g += (double)__fmul_rn(ss, ss);
+                res[e] = __fadd_rn(p0, __fmul_rn(omega, ss));
+            }
+            if (full) {
+                __stcs(reinterpret_cast<float4 *>(wrk2 + x), make_float4(res[0], res[1], res[2], res[3]));
+                mn = (u64)x < mn ? (u64)x : mn;
+                mx = (u64)(x + 3) > mx ? (u64)(x + 3) : mx;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; e++)
+                    if (k + e >= k0 && k + e < k1) {
+                        __stcs(wrk2 + x + e, res[e]);
+                        mn = (u64)(x + e) < mn ? (u64)(x + e) : mn;
+                        mx = (u64)(x + e) > mx ? (u64)(x + e) : mx;
+                    }
+            }
+        }
+    }
+    cp_wait<0>();
+    // fixed-order reduction: warp, block, then the last block over the grid
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g += __shfl_down_sync(0xffffffffu, g, o);
+    if (lane == 0) sh[w] = g;
+    __syncthreads();
+    if (tid == 0) {
+        double v = 0.0;
+        for (int q = 0; q < 8; q++) v += sh[q];
+        partials[blockIdx.x] = v;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double v = 0.0;
+        for (unsigned q = tid; q < gridDim.x; q += 256) v += __ldcg(partials + q);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if (lane == 0) sh[w] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int q = 0; q < 8; q++) tot += sh[q];
+            *out = tot;
+            *ticket = 0u;
+            *ctr = 0ull;  // every CTA has left the tile loop
+        }
+    }
+    publish_dirty<8>(mn, mx, dirty);
+}
+
 // copy loop: one warp per (i, j) row of the box; the 16-byte-aligned body
 // as float4 (p and wrk2 share the layout), head / tail as scalars
 // Copy loop p = wrk2 over the box, a pure stream.  A warp owns rows (i, j)
@@ -2211,6 +2390,21 @@ cudaError_t himeno_stencil(cudaStream_t s, const float *p, const float *a, const
                            unsigned *ticket, double *out, u64 *dirty) {
     if (i1 <= i0 || j1 <= j0 || k1 <= k0) return cudaErrorInvalidValue;
     static_assert(kHimenoGrid <= kHimenoPartials, "partials buffer");
+    const uintptr_t al = reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(a) |
+                         reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(c) |
+                         reinterpret_cast<uintptr_t>(wrk1) | reinterpret_cast<uintptr_t>(bnd) |
+                         reinterpret_cast<uintptr_t>(wrk2);
+    if (HIMENO_PM && K % 4 == 0 && (al & 15) == 0) {
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int grid = 2 * (nsm > 0 ? nsm : 148);
+        if (grid <= kHimenoPartials) {
+            himeno_stencil_pm_kernel<<<grid, 256, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0, i1, j0, j1,
+                                                          k0, k1, omega, partials, ticket, out, dirty);
+            return cudaGetLastError();
+        }
+    }
     himeno_stencil_kernel<2><<<kHimenoGrid, HT, 0, s>>>(p, a, b, c, wrk1, bnd, wrk2, I, J, K, i0, i1, j0,
                                                         j1, k0, k1, omega, partials, ticket, out, dirty);
     return cudaGetLastError();

@@ -838,10 +838,14 @@ def _himeno_gpu(J, arrs, nn, n, policy, omega=0.8, rng=None):
     return p, wrk2, gosas, dirt
 
 
-@pytest.mark.parametrize("shape", [(3, 3, 3), (9, 5, 7), (17, 12, 21), (34, 33, 35), (66, 40, 70)])
+@pytest.mark.parametrize("shape", [(3, 3, 3), (9, 5, 7), (17, 12, 21), (34, 33, 35), (66, 40, 70),
+                                   (40, 21, 132), (70, 37, 64), (9, 260, 12)])
 @pytest.mark.parametrize("n", [1, 2, 3, 8])
 @pytest.mark.parametrize("policy", [0, 1])
 def test_himeno_multi_device(J, shape, n, policy):
+    """K % 4 == 0 shapes take the plane-marching kernel (several k strips, a
+    partial last strip, several j blocks and i segments, ragged ends), the
+    others the row-per-warp kernel."""
     I, Jd, K = shape
     arrs = synth.himeno_random(I, Jd, K, 95)
     nn = 3
@@ -869,8 +873,11 @@ def test_himeno_multi_device(J, shape, n, policy):
         assert dirt[1][d] == cl
 
 
-def test_himeno_subrange(J):
-    I, Jd, K = 20, 18, 22
+@pytest.mark.parametrize("K", [22, 24])
+def test_himeno_subrange(J, K):
+    """A launch box off the interior (k from 5: partial float4 chunks; K = 24
+    takes the plane-marching kernel)."""
+    I, Jd = 20, 18
     arrs = synth.himeno_random(I, Jd, K, 96)
     rng = J.make_range([3, 2, 5], [15, 17, 20])
     gp, gw, gosas, _ = _himeno_gpu(J, arrs, 1, 2, 0, rng=rng)
