@@ -859,8 +859,21 @@ __global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restric
         if (owned(k, lo, span)) atomicAdd(&h[(unsigned)(k - lo) >> shift], 1u);
     };
     if (tid < hd) put(idx[tid]);
-#pragma unroll 4
-    for (int64_t q = tid; q < n4; q += nth) {
+    // 4 key loads in flight before their shared atomics (not hoisted by the compiler)
+    int64_t q = tid;
+    for (; q + 3 * nth < n4; q += 4 * nth) {
+        int4 k[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) k[u] = __ldcs(idx4 + q + u * nth);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            put(k[u].x);
+            put(k[u].y);
+            put(k[u].z);
+            put(k[u].w);
+        }
+    }
+    for (; q < n4; q += nth) {
         const int4 k = __ldcs(idx4 + q);
         put(k.x);
         put(k.y);
@@ -1368,8 +1381,24 @@ __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__res
         if (threadIdx.x < pa - p0) put(pidx[p0 + threadIdx.x]);
         if (threadIdx.x < p1 - pt) put(pidx[pt + threadIdx.x]);
         const int4 *k4 = reinterpret_cast<const int4 *>(pidx + pa);
-#pragma unroll 4
-        for (u64 q4 = threadIdx.x; q4 < n4; q4 += SBITS_T) {
+        // SB_U 16-byte loads in flight per thread before their atomics (the
+        // compiler does not hoist global loads above shared atomics itself)
+        // (measured: int32 3.16 -> 3.01 ms per launch with 4; fp64 best with 2)
+        constexpr int SB_U = sizeof(T) == 4 ? 4 : 2;
+        u64 q4 = threadIdx.x;
+        for (; q4 + (SB_U - 1) * SBITS_T < n4; q4 += SB_U * SBITS_T) {
+            int4 k[SB_U];
+#pragma unroll
+            for (int u = 0; u < SB_U; u++) k[u] = __ldcs(k4 + q4 + u * SBITS_T);
+#pragma unroll
+            for (int u = 0; u < SB_U; u++) {
+                put(k[u].x);
+                put(k[u].y);
+                put(k[u].z);
+                put(k[u].w);
+            }
+        }
+        for (; q4 < n4; q4 += SBITS_T) {
             const int4 k = __ldcs(k4 + q4);
             put(k.x);
             put(k.y);
