@@ -858,10 +858,10 @@ def merge_probes(J):
             bm = J.jacc_get_dirty_bitmap(a, 0, M)
             dirty = int(np.unpackbits(bm.view(np.uint8)).sum())
             words = (M // 2 + 31) // 32
-            moved = 8 * dirty
+            moved = 8 * _pushed_elements(bm, 0, M // 2)
             out[name] = {"kernel": "merge_bitmap_kernel", "us": mt * 1e6, "updates": nupd,
                          "dirty_elements": dirty, "bitmap_words_scanned": words,
-                         "bytes_pushed": moved,
+                         "bytes_pushed": moved, "dense_word_rule": DENSE_RULE,
                          "hbm_bytes": 2 * moved + 4 * words,
                          "gbs": (2 * moved + 4 * words) / mt / 1e9,
                          "frac_of_hbm_copy": (2 * moved + 4 * words) / mt / 1e9 / peak,
@@ -898,7 +898,7 @@ def merge_probes(J):
             J.jacc_set_profiling(0)
             tk[pol] = (k + m) / max(nl, 1)
         bm = J.jacc_get_dirty_bitmap(a, 0, M)
-        moved = 8 * int(np.unpackbits(bm.view(np.uint8)).sum())
+        moved = 8 * _pushed_elements(bm, 0, M // 2)
         extra = tk[J.JACC_MERGE_EAGER] - tk[J.JACC_MERGE_HALO]
         out["binned_scatter_fused_push"] = {
             "kernel": "scat_bits_kernel (EAGER push fused)", "launch_us_halo": tk[J.JACC_MERGE_HALO] * 1e6,
@@ -910,6 +910,19 @@ def merge_probes(J):
     finally:
         J.jacc_finalize()
     return out
+
+
+DENSE_RULE = ("a bitmap word with >= 8 of its 32 elements dirty and inside the device's slice "
+              "is pushed whole (kernels.cu merge_dense)")
+
+
+def _pushed_elements(bm, lo, hi, dense_t=8):
+    """Elements a bitmap merge stores into each peer for device slice [lo, hi):
+    dense words whole, the others element by element (merge_dense)."""
+    pop = np.unpackbits(bm.view(np.uint8)).reshape(-1, 32).sum(axis=1).astype(np.int64)
+    w = np.arange(pop.size, dtype=np.int64)
+    whole = (pop >= dense_t) & (w * 32 >= lo) & (w * 32 + 32 <= hi)
+    return int(np.where(whole, 32, pop).sum())
 
 
 def main():

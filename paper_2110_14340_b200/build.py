@@ -54,7 +54,7 @@ def build(force=False, verbose=False, defines=(), out=None):
     objs = [ko]
     for src in HOST:
         o = os.path.join(bdir, src.replace(".cpp", ".o"))
-        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE,
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", *[f"-D{d}" for d in defines], "-I", INCLUDE,
               "-I", os.path.join(CUDA_HOME, "include"), "-I", nccl_inc, "-c",
               os.path.join(CSRC, src), "-o", o])
         objs.append(o)

@@ -813,6 +813,26 @@ constexpr int SB_MAXB = 1024;    // max buckets
 #endif
 constexpr int SBITS_LB = 20;     // bits pass: 2^20 elements (128 KB of bits) per CTA item
 constexpr int SBITS_T = 1024;    // bits CTA
+#ifndef SBITS_PW
+#define SBITS_PW 4               // bits pass EAGER push: words per warp per round
+#endif
+
+// Dense words of a bitmap merge move whole: a word with >= MERGE_DENSE_T of
+// its 32 elements dirty touches (nearly) every 32-byte sector of its
+// elements anyway, and element-masked stores of partly dirty sectors are
+// read-modify-written by the memory side (merge_bitmap measured 3.0 GB of
+// DRAM for 0.68 GB of dirty elements) and cross NVLink as masked partial
+// writes.  Storing the word's clean elements too is exact: the word lies
+// inside the source device's owned slice [lo, hi), where the source replica
+// is valid (the launch pulled its read footprint) and no other device
+// writes, so a clean element's value equals every peer's copy-to-be -- the
+// same argument as the range merge, which moves the whole [min, max] span.
+#ifndef MERGE_DENSE_T
+#define MERGE_DENSE_T 8
+#endif
+__device__ __forceinline__ bool merge_dense(uint32_t bits, int64_t w, int64_t lo, int64_t hi) {
+    return MERGE_DENSE_T > 0 && __popc(bits) >= MERGE_DENSE_T && (w << 5) >= lo && (w << 5) + 32 <= hi;
+}
 
 __device__ __forceinline__ bool owned(int32_t k, int32_t lo, unsigned span) {
     return (unsigned)(k - lo) < span;
@@ -1415,22 +1435,23 @@ __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__res
             }
         }
         if (push.n > 0) {
-            // fused EAGER merge: 4 words per warp per round (4 loads in
+            // fused EAGER merge: PW words per warp per round (PW loads in
             // flight per lane), element l of word i by lane l
-            constexpr int NWP = SBITS_T / 32;
-            for (int64_t i0 = warp; i0 < nw; i0 += 4 * NWP) {
-                T v[4];
-                bool on[4];
+            constexpr int NWP = SBITS_T / 32, PW = SBITS_PW;
+            for (int64_t i0 = warp; i0 < nw; i0 += PW * NWP) {
+                T v[PW];
+                bool on[PW];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < PW; u++) {
                     const int64_t i = i0 + u * NWP;
-                    on[u] = i < nw && ((sw[i < nw ? i : 0] >> lane) & 1u);
+                    const uint32_t bits = i < nw ? sw[i] : 0u;
+                    on[u] = ((bits >> lane) & 1u) || (i < nw && merge_dense(bits, w0 + i, lo, hi));
                     if (on[u]) v[u] = a[((w0 + i) << 5) + lane];
                 }
                 for (int d = 0; d < push.n; d++) {
                     T *dp = static_cast<T *>(push.p[d]);
 #pragma unroll
-                    for (int u = 0; u < 4; u++)
+                    for (int u = 0; u < PW; u++)
                         if (on[u]) dp[((w0 + i0 + u * NWP) << 5) + lane] = v[u];
                 }
             }
@@ -2193,6 +2214,8 @@ __global__ void __launch_bounds__(256) merge_bitmap_kernel(const T *__restrict__
                 for (int q = 0; q < 8; q++) {
                     const uint32_t bits = __shfl_sync(0xffffffffu, m[u], j0 + q);
                     on[q] = (bits >> lane) & 1u;
+                    // dense word inside the slice: the whole word (see merge_dense)
+                    if (merge_dense(bits, g0 + j0 + q, lo, hi)) on[q] = true;
                     if (on[q]) v[q] = __ldcs(src + ((g0 + j0 + q) << 5) + lane);
                 }
                 for (int d = 0; d < dsts.n; d++) {

@@ -2,6 +2,12 @@
 //  tracking, merges, reduction combine (a3-a6, a8)
 #include "rt.hpp"
 
+// binned scatter under EAGER: the bits pass pushes the dirty elements itself
+// (1) or the separate merge_bitmap kernel does (0)
+#ifndef SCAT_FUSED_PUSH
+#define SCAT_FUSED_PUSH 1
+#endif
+
 namespace jrt {
 
 // Feed completed adaptive observations (FIFO) to their controllers.  An
@@ -633,7 +639,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                     // EAGER: the bits pass also pushes the dirty elements to
                     // every peer (merge fused into the tracking pass)
                     jk::PeerPtrs push{};
-                    if (writes && R.policy == JACC_MERGE_EAGER && n > 1) {
+                    if (SCAT_FUSED_PUSH && writes && R.policy == JACC_MERGE_EAGER && n > 1) {
                         for (int q = 0; q < n; q++)
                             if (q != d) push.p[push.n++] = W->rep[q];
                         scat_fused_push = true;
