@@ -870,9 +870,9 @@ def merge_probes(J):
         finally:
             J.jacc_finalize()
     del os.environ["JACC_SCATTER_BINNED"]
-    # binned scatter with the EAGER push fused into its bits pass: device 0's
-    # launch time under EAGER (bits pass also stores the 0.68 GB of dirty
-    # elements into the peer) minus the same launch under HALO (no push)
+    # binned scatter under EAGER: device 0's launch time (binned pipeline +
+    # merge_bitmap of its dirty words into the peer) minus the same launch
+    # under HALO (no push)
     J.jacc_init(2, [0, 0])
     try:
         nupd = 2**27
@@ -900,11 +900,11 @@ def merge_probes(J):
         bm = J.jacc_get_dirty_bitmap(a, 0, M)
         moved = 8 * _pushed_elements(bm, 0, M // 2)
         extra = tk[J.JACC_MERGE_EAGER] - tk[J.JACC_MERGE_HALO]
-        out["binned_scatter_fused_push"] = {
-            "kernel": "scat_bits_kernel (EAGER push fused)", "launch_us_halo": tk[J.JACC_MERGE_HALO] * 1e6,
+        out["binned_scatter_eager_merge"] = {
+            "kernel": "merge_bitmap_kernel after the binned scatter", "launch_us_halo": tk[J.JACC_MERGE_HALO] * 1e6,
             "launch_us_eager": tk[J.JACC_MERGE_EAGER] * 1e6, "push_cost_us": extra * 1e6,
             "bytes_pushed": moved, "push_gbs": 2 * moved / extra / 1e9 if extra > 0 else None,
-            "vs_separate_merge_bitmap_us": out.get("merge_bitmap_dense", {}).get("us"),
+            "merge_bitmap_dense_us": out.get("merge_bitmap_dense", {}).get("us"),
             "nvlink_time_at_770_us": moved / (NVLINK_GBS * 1e9) * 1e6}
         del idx, b, a
     finally:

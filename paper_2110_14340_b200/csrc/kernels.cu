@@ -813,9 +813,6 @@ constexpr int SB_MAXB = 1024;    // max buckets
 #endif
 constexpr int SBITS_LB = 20;     // bits pass: 2^20 elements (128 KB of bits) per CTA item
 constexpr int SBITS_T = 1024;    // bits CTA
-#ifndef SBITS_PW
-#define SBITS_PW 4               // bits pass EAGER push: words per warp per round
-#endif
 
 // Dense words of a bitmap merge move whole: a word with >= MERGE_DENSE_T of
 // its 32 elements dirty touches (nearly) every 32-byte sector of its
@@ -1362,27 +1359,20 @@ __global__ void __launch_bounds__(256, SA_BPS) scat_apply_kernel(const int32_t *
 // scans the bucket's keys (16-byte loads), sets its bits with shared-memory
 // atomicOr and writes its words once (a part's first/last word may be
 // shared with the neighbour part when lo is not 32-aligned: atomicOr into
-// the zeroed bitmap).  Under EAGER with peers (push.n > 0) the same pass is
-// the merge: the part's dirty elements, final after the apply, are stored
-// into every peer replica straight from the shared-memory words (one warp
-// per word, lane l moving element l: a coalesced 128/256-byte segment per
-// word and peer) -- tracking and merge fused, no separate merge kernel and
-// no re-read of the bitmap.  (Run on a second stream beside the apply,
-// following its chunk counter, the pass measured no faster and the
-// range-replay DRAM total of the launch was unchanged:
-// profiles/scat_experiments_r02.txt.)
+// the zeroed bitmap).  Under EAGER the separate merge_bitmap kernel then
+// pushes the dirty words (a push fused into this pass, from the
+// shared-memory words, measured 559 vs 358 us at 2^27 dense updates:
+// profiles/scat_experiments_r02.txt item 16).
 template <typename T>
 __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__restrict__ pidx,
                                                             const u64 *__restrict__ base,
                                                             const u64 *__restrict__ end, int nb,
                                                             int shift, int64_t lo, int64_t hi,
-                                                            uint32_t *bitmap, const T *__restrict__ a,
-                                                            PeerPtrs push) {
+                                                            uint32_t *bitmap) {
     extern __shared__ uint32_t sw[];
     const int lp = shift > SBITS_LB ? shift - SBITS_LB : 0;  // log2 parts per bucket
     const int pb = shift > SBITS_LB ? SBITS_LB : shift;      // log2 elements per part
     const int64_t items = (int64_t)nb << lp;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int bk = (int)(it >> lp), q = (int)(it & ((1 << lp) - 1));
         const int64_t e0 = lo + ((int64_t)bk << shift) + ((int64_t)q << pb);
@@ -1432,28 +1422,6 @@ __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__res
                 if (v) atomicOr(bitmap + w0 + i, v);
             } else {
                 bitmap[w0 + i] = v;
-            }
-        }
-        if (push.n > 0) {
-            // fused EAGER merge: PW words per warp per round (PW loads in
-            // flight per lane), element l of word i by lane l
-            constexpr int NWP = SBITS_T / 32, PW = SBITS_PW;
-            for (int64_t i0 = warp; i0 < nw; i0 += PW * NWP) {
-                T v[PW];
-                bool on[PW];
-#pragma unroll
-                for (int u = 0; u < PW; u++) {
-                    const int64_t i = i0 + u * NWP;
-                    const uint32_t bits = i < nw ? sw[i] : 0u;
-                    on[u] = ((bits >> lane) & 1u) || (i < nw && merge_dense(bits, w0 + i, lo, hi));
-                    if (on[u]) v[u] = a[((w0 + i) << 5) + lane];
-                }
-                for (int d = 0; d < push.n; d++) {
-                    T *dp = static_cast<T *>(push.p[d]);
-#pragma unroll
-                    for (int u = 0; u < PW; u++)
-                        if (on[u]) dp[((w0 + i0 + u * NWP) << 5) + lane] = v[u];
-                }
             }
         }
         __syncthreads();
@@ -2510,7 +2478,7 @@ ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_
 
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
-                               u64 *dirty, const ScatterPlan &pl, void *scratch, PeerPtrs push) {
+                               u64 *dirty, const ScatterPlan &pl, void *scratch) {
     char *sc = static_cast<char *>(scratch);
     u64 *counts = reinterpret_cast<u64 *>(sc);
     u64 *cursor = counts + pl.nb;  // after the partition: every bucket's stream end
@@ -2599,11 +2567,11 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
     const int64_t items = (int64_t)pl.nb << (pl.shift - pb);
     const int g = (int)(items < 2 * nsm ? items : 2 * nsm);
     if (is_f64)
-        scat_bits_kernel<double><<<g, SBITS_T, smem, s>>>(pidx, base, cursor, pl.nb, pl.shift, lo, hi, bitmap,
-                                                          static_cast<const double *>(a), push);
+        scat_bits_kernel<double><<<g, SBITS_T, smem, s>>>(pidx, base, cursor, pl.nb, pl.shift, lo, hi,
+                                                          bitmap);
     else
-        scat_bits_kernel<int32_t><<<g, SBITS_T, smem, s>>>(pidx, base, cursor, pl.nb, pl.shift, lo, hi, bitmap,
-                                                           static_cast<const int32_t *>(a), push);
+        scat_bits_kernel<int32_t><<<g, SBITS_T, smem, s>>>(pidx, base, cursor, pl.nb, pl.shift, lo, hi,
+                                                           bitmap);
     return cudaGetLastError();
 }
 

@@ -65,10 +65,9 @@ cudaError_t scatter_add_i32(cudaStream_t s, const int32_t *idx, const int32_t *b
 // streams through shared-memory staging (coalesced, full-line writes),
 // (4) apply the pairs in stream order, so the read-modify-writes of a hit
 // L2 and every line of a moves to/from HBM about once, (5) dirty bits per
-// bucket part in shared memory, each bitmap word written once; with peers
-// in `push` (EAGER), (5) also stores the dirty elements into every peer
-// replica -- the merge fused into the tracking pass.  Dirty range fused
-// into (4).  is_f64: T = double, else int32.
+// bucket part in shared memory, each bitmap word written once (EAGER:
+// merge_bitmap follows).  Dirty range fused into (4).  is_f64: T = double,
+// else int32.
 struct ScatterPlan {
     bool binned;
     bool all_owned;     // [lo, hi) covers every element of a (one device / duplicated)
@@ -82,7 +81,7 @@ struct ScatterPlan {
 ScatterPlan scatter_plan(int64_t n, int64_t lo, int64_t hi, int elem, int64_t m_total);
 cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, const void *b,
                                void *a, int64_t n, int64_t lo, int64_t hi, uint32_t *bitmap,
-                               u64 *dirty, const ScatterPlan &pl, void *scratch, PeerPtrs push);
+                               u64 *dirty, const ScatterPlan &pl, void *scratch);
 
 // NEXT-2  Himeno benchmark (DESIGN R-17), fp32, row-major
 // [I][J][K] arrays (a: 4, b and c: 3 stacked arrays).  Stencil loop over

@@ -2,12 +2,6 @@
 //  tracking, merges, reduction combine (a3-a6, a8)
 #include "rt.hpp"
 
-// binned scatter under EAGER: the bits pass pushes the dirty elements itself
-// (1) or the separate merge_bitmap kernel does (0)
-#ifndef SCAT_FUSED_PUSH
-#define SCAT_FUSED_PUSH 1
-#endif
-
 namespace jrt {
 
 // Feed completed adaptive observations (FIFO) to their controllers.  An
@@ -502,7 +496,6 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                                (size_t)(pl.hi - pl.lo) * e, cudaMemcpyDefault, dv.s));
             merged_bytes += (uint64_t)(pl.hi - pl.lo) * e;
         }
-        bool scat_fused_push = false;  // binned scatter pushed its dirty elements itself
         ProfRec pr{d, nullptr, nullptr, nullptr};
         if (prof) {
             pr.k0 = pool_event();
@@ -636,16 +629,8 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 if (sp.binned && dv.scratch_bytes < sp.scratch)
                     sp.binned = false;  // scratch could not be reserved up front: direct kernel
                 if (sp.binned) {
-                    // EAGER: the bits pass also pushes the dirty elements to
-                    // every peer (merge fused into the tracking pass)
-                    jk::PeerPtrs push{};
-                    if (SCAT_FUSED_PUSH && writes && R.policy == JACC_MERGE_EAGER && n > 1) {
-                        for (int q = 0; q < n; q++)
-                            if (q != d) push.p[push.n++] = W->rep[q];
-                        scat_fused_push = true;
-                    }
                     CK(jk::scatter_add_binned(dv.s, f64, ix, b, W->rep[d], p.i1 - p.i0, lo, hi, bm,
-                                              drec, sp, dv.scratch, push));
+                                              drec, sp, dv.scratch));
                 } else if (f64) {
                     CK(jk::scatter_add_f64(dv.s, ix, reinterpret_cast<const double *>(b),
                                            reinterpret_cast<double *>(W->rep[d]), p.i1 - p.i0, lo,
@@ -687,8 +672,7 @@ jacc_status do_launch(int loop_id, const jacc_range *range, const jacc_arg *args
                 const jk::Box2D bx = make_box2d(W, nbox, p.blo, p.bhi);
                 CK(jk::merge_box(dv.s, W->rep[d], pp, bx, drec, (int64_t)W->elem));
             } else if (id == JACC_LOOP_SCATTER_ADD_F64 || id == JACC_LOOP_SCATTER_ADD_I32) {
-                if (!scat_fused_push)
-                    CK(jk::merge_bitmap(dv.s, W->rep[d], pp, W->bitmap[d], (int64_t)W->elem, p.wlo, p.whi));
+                CK(jk::merge_bitmap(dv.s, W->rep[d], pp, W->bitmap[d], (int64_t)W->elem, p.wlo, p.whi));
             } else {
                 CK(jk::merge_range(dv.s, W->rep[d], pp, drec, (int64_t)W->elem, p.wlo, p.whi));
             }
