@@ -2197,6 +2197,104 @@ __global__ void __launch_bounds__(256) merge_bitmap_kernel(const T *__restrict__
     }
 }
 
+// Himeno copy by the bulk-copy engine (rows 16-byte aligned: K % 4 == 0).
+// A warp owns rows (i, j) with a static stride; its elected lane moves each
+// row's 16-byte-aligned body [ka, kt) global -> shared -> global with
+// cp.async.bulk (completion of the load on a per-slot mbarrier, the store
+// in a bulk group), HCT_R rows of loads in flight per warp in a slot ring;
+// the other lanes copy the <= 3 + 3 unaligned head / tail elements.  HALO
+// boundary planes are also bulk-stored into the neighbours' replicas.
+#ifndef HIMENO_COPY_BULK
+#define HIMENO_COPY_BULK 1
+#endif
+#ifndef HIMENO_CB_GRID
+#define HIMENO_CB_GRID 16         // bulk copy CTAs (4 warps) per SM
+#endif
+#ifndef HIMENO_CB_R
+#define HIMENO_CB_R 4
+#endif
+constexpr int HCT_R = HIMENO_CB_R, HCT_W = 4;
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, u64 *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst), "r"(smem_u32(src)), "r"(bytes) : "memory");
+}
+__global__ void __launch_bounds__(HCT_W * 32) himeno_copy_bulk_kernel(
+    const float *__restrict__ wrk2, float *__restrict__ p, int64_t J, int64_t K, int64_t i0,
+    int64_t i1, int64_t j0, int64_t j1, int64_t k0, int64_t k1, u64 *dirty, float *push_top,
+    float *push_bot) {
+    extern __shared__ __align__(128) unsigned char hsm[];
+    __shared__ __align__(8) u64 bar[HCT_W][HCT_R];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t P = J * K, nj = j1 - j0, rows = (i1 - i0) * nj;
+    const int64_t ka = (k0 + 3) & ~(int64_t)3, kt = k1 & ~(int64_t)3;  // body [ka, kt), kt > ka
+    const unsigned bbytes = (unsigned)(4 * (kt - ka));
+    const int64_t slot_f = (4 * K + 127) / 128 * 32;                      // floats per slot
+    float *slots = reinterpret_cast<float *>(hsm) + (int64_t)warp * HCT_R * slot_f;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (lane == 0) {
+        for (int u = 0; u < HCT_R; u++) mbar_init(&bar[warp][u], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto rowbase = [&](int64_t r, int64_t &i) {
+        i = i0 + r / nj;
+        return i * P + (j0 + r % nj) * K;
+    };
+    auto issue = [&](int64_t it) {  // lane 0: bulk load of the it-th row of this warp
+        const int64_t r = wg + it * nw;
+        if (r >= rows) return;
+        int64_t i;
+        const int64_t rb = rowbase(r, i);
+        u64 *b = &bar[warp][it % HCT_R];
+        mbar_expect_tx(b, bbytes);
+        bulk_g2s(slots + (it % HCT_R) * slot_f, wrk2 + rb + ka, bbytes, b);
+    };
+    if (lane == 0)
+        for (int it = 0; it < HCT_R; it++) issue(it);
+    u64 mn = kU64Max, mx = 0;
+    for (int64_t it = 0;; it++) {
+        const int64_t r = wg + it * nw;
+        if (r >= rows) break;
+        int64_t i;
+        const int64_t rb = rowbase(r, i);
+        float *tp = (i == i0) ? push_top : nullptr;
+        float *bp = (i == i1 - 1) ? push_bot : nullptr;
+        // head [k0, ka) and tail [kt, k1): lanes 0..2 and 8..10
+        int64_t k = -1;
+        if (lane < ka - k0) k = k0 + lane;
+        else if (lane >= 8 && lane - 8 < k1 - kt) k = kt + (lane - 8);
+        if (k >= 0) {
+            const float x = __ldcs(wrk2 + rb + k);
+            __stcs(p + rb + k, x);
+            if (tp) tp[rb + k] = x;
+            if (bp) bp[rb + k] = x;
+        }
+        if (lane == 0) {
+            const int sl = (int)(it % HCT_R);
+            mbar_wait(&bar[warp][sl], (unsigned)((it / HCT_R) & 1));
+            const float *src = slots + sl * slot_f;
+            bulk_s2g(p + rb + ka, src, bbytes);
+            if (tp) bulk_s2g(tp + rb + ka, src, bbytes);
+            if (bp) bulk_s2g(bp + rb + ka, src, bbytes);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            // the previous row's slot is free once its stores have read it
+            if (it > 0) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                issue(it - 1 + HCT_R);
+            }
+            mn = (u64)(rb + k0) < mn ? (u64)(rb + k0) : mn;
+            mx = (u64)(rb + k1 - 1) > mx ? (u64)(rb + k1 - 1) : mx;
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    publish_dirty<HCT_W>(mn, mx, dirty);
+}
+
 inline int grid_for(int64_t work, int per_block, int max_blocks) {
     int64_t g = (work + per_block - 1) / per_block;
     if (g < 1) g = 1;
@@ -2436,6 +2534,18 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
                         unsigned *ticket) {
     (void)I;
     if (i1 <= i0 || j1 <= j0 || k1 <= k0) return cudaErrorInvalidValue;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(wrk2) | reinterpret_cast<uintptr_t>(p) |
+                         reinterpret_cast<uintptr_t>(push_top) | reinterpret_cast<uintptr_t>(push_bot);
+    const int64_t ka = (k0 + 3) & ~(int64_t)3, kt = k1 & ~(int64_t)3;
+    const int64_t smem = (int64_t)HCT_W * HCT_R * ((4 * K + 127) / 128 * 128);
+    if (HIMENO_COPY_BULK && K % 4 == 0 && (al & 15) == 0 && kt - ka >= 4 && smem <= 48 * 1024) {
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        himeno_copy_bulk_kernel<<<(nsm > 0 ? nsm : 148) * HIMENO_CB_GRID, HCT_W * 32, (size_t)smem, s>>>(
+            wrk2, p, J, K, i0, i1, j0, j1, k0, k1, dirty, push_top, push_bot);
+        return cudaGetLastError();
+    }
     himeno_copy_kernel<<<kHimenoGrid, HT, 0, s>>>(wrk2, p, J, K, i0, i1, j0, j1, k0, k1, dirty,
                                                   push_top, push_bot, ticket);
     return cudaGetLastError();
