@@ -2207,8 +2207,8 @@ __global__ void __launch_bounds__(256) merge_bitmap_kernel(const T *__restrict__
 #ifndef HIMENO_COPY_BULK
 #define HIMENO_COPY_BULK 1
 #endif
-#ifndef HIMENO_CB_GRID
-#define HIMENO_CB_GRID 16         // bulk copy CTAs (4 warps) per SM
+#ifndef HIMENO_CB_RPW
+#define HIMENO_CB_RPW 4           // bulk copy: rows per warp
 #endif
 #ifndef HIMENO_CB_R
 #define HIMENO_CB_R 4
@@ -2293,6 +2293,71 @@ __global__ void __launch_bounds__(HCT_W * 32) himeno_copy_bulk_kernel(
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     publish_dirty<HCT_W>(mn, mx, dirty);
+}
+
+// Range merge by the bulk-copy engine: the recorded span's 16-byte-aligned
+// body in 2 KB chunks, global -> shared (cp.async.bulk, mbarrier) ->
+// every peer replica (bulk stores), a warp's elected lane keeping
+// MRB_R chunks of loads in flight in a slot ring (the structure of
+// himeno_copy_bulk_kernel); the unaligned head and tail bytes by threads.
+#ifndef MERGE_RANGE_BULK
+#define MERGE_RANGE_BULK 1
+#endif
+constexpr int MRB_R = 4, MRB_W = 4, MRB_CH = 2048;
+__global__ void __launch_bounds__(MRB_W * 32) merge_range_bulk_kernel(const char *__restrict__ src,
+                                                                     PeerPtrs dsts, const u64 *dirty,
+                                                                     int64_t elem, int64_t lo, int64_t hi) {
+    __shared__ __align__(128) char slots_all[MRB_W * MRB_R * MRB_CH];
+    __shared__ __align__(8) u64 bar[MRB_W][MRB_R];
+    const u64 dmin = dirty[0], dmax = ~dirty[1];
+    if (dmin > dmax) return;
+    const int64_t a = (int64_t)dmin > lo ? (int64_t)dmin : lo;
+    const int64_t b = (int64_t)dmax + 1 < hi ? (int64_t)dmax + 1 : hi;
+    if (a >= b) return;
+    const int64_t s = a * elem, e = b * elem;  // byte span
+    int64_t vs = (s + 15) & ~(int64_t)15, ve = e & ~(int64_t)15;
+    if (vs > ve) vs = ve = e;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = s + tid; q < vs; q += nth)
+        for (int d = 0; d < dsts.n; d++) static_cast<char *>(dsts.p[d])[q] = src[q];
+    for (int64_t q = ve + tid; q < e; q += nth)
+        for (int d = 0; d < dsts.n; d++) static_cast<char *>(dsts.p[d])[q] = src[q];
+    if (lane != 0) return;  // the bulk part is one lane per warp
+    const int64_t nch = (ve - vs + MRB_CH - 1) / MRB_CH;
+    const int64_t wg = tid >> 5, nw = nth >> 5;
+    char *slots = slots_all + warp * MRB_R * MRB_CH;
+    for (int u = 0; u < MRB_R; u++) mbar_init(&bar[warp][u], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    auto bytes_of = [&](int64_t c) {
+        const int64_t o = vs + c * MRB_CH;
+        return (unsigned)(ve - o < MRB_CH ? ve - o : MRB_CH);
+    };
+    auto issue = [&](int64_t it) {
+        const int64_t c = wg + it * nw;
+        if (c >= nch) return;
+        u64 *br = &bar[warp][it % MRB_R];
+        const unsigned n = bytes_of(c);
+        mbar_expect_tx(br, n);
+        bulk_g2s(slots + (it % MRB_R) * MRB_CH, src + vs + c * MRB_CH, n, br);
+    };
+    for (int it = 0; it < MRB_R; it++) issue(it);
+    for (int64_t it = 0;; it++) {
+        const int64_t c = wg + it * nw;
+        if (c >= nch) break;
+        const int sl = (int)(it % MRB_R);
+        mbar_wait(&bar[warp][sl], (unsigned)((it / MRB_R) & 1));
+        const unsigned n = bytes_of(c);
+        for (int d = 0; d < dsts.n; d++)
+            bulk_s2g(static_cast<char *>(dsts.p[d]) + vs + c * MRB_CH, slots + sl * MRB_CH, n);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (it > 0) {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            issue(it - 1 + MRB_R);
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 inline int grid_for(int64_t work, int per_block, int max_blocks) {
@@ -2538,11 +2603,13 @@ cudaError_t himeno_copy(cudaStream_t s, const float *wrk2, float *p, int64_t I, 
                          reinterpret_cast<uintptr_t>(push_top) | reinterpret_cast<uintptr_t>(push_bot);
     const int64_t ka = (k0 + 3) & ~(int64_t)3, kt = k1 & ~(int64_t)3;
     const int64_t smem = (int64_t)HCT_W * HCT_R * ((4 * K + 127) / 128 * 128);
-    if (HIMENO_COPY_BULK && K % 4 == 0 && (al & 15) == 0 && kt - ka >= 4 && smem <= 48 * 1024) {
-        int dev = 0, nsm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        himeno_copy_bulk_kernel<<<(nsm > 0 ? nsm : 148) * HIMENO_CB_GRID, HCT_W * 32, (size_t)smem, s>>>(
+    if (HIMENO_COPY_BULK && K % 4 == 0 && (al & 15) == 0 && kt - ka >= 4 && smem <= 40 * 1024) {
+        // a few rows per warp (HIMENO_CB_RPW), many CTAs: the block
+        // scheduler balances them (0.350 ms at 4 rows per warp, 0.358 at 8,
+        // 0.396 at 55)
+        const int64_t rows = (i1 - i0) * (j1 - j0);
+        const int64_t g = std::max<int64_t>(1, (rows + HCT_W * HIMENO_CB_RPW - 1) / (HCT_W * HIMENO_CB_RPW));
+        himeno_copy_bulk_kernel<<<(unsigned)std::min<int64_t>(g, INT32_MAX), HCT_W * 32, (size_t)smem, s>>>(
             wrk2, p, J, K, i0, i1, j0, j1, k0, k1, dirty, push_top, push_bot);
         return cudaGetLastError();
     }
@@ -2688,6 +2755,19 @@ cudaError_t scatter_add_binned(cudaStream_t s, bool is_f64, const int32_t *idx, 
 cudaError_t merge_range(cudaStream_t s, const void *src, PeerPtrs dsts, const u64 *dirty,
                         int64_t elem, int64_t lo, int64_t hi) {
     if (hi <= lo || dsts.n == 0) return cudaSuccess;
+    if (MERGE_RANGE_BULK) {
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        // enough warps that every one moves a few chunks of the host-side
+        // upper bound of the span (the recorded span may be shorter)
+        const int64_t warps = ((hi - lo) * elem + 4 * MRB_CH - 1) / (4 * MRB_CH);
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>((warps + MRB_W - 1) / MRB_W,
+                                                                 (int64_t)(nsm > 0 ? nsm : 148) * 32));
+        merge_range_bulk_kernel<<<(unsigned)g, MRB_W * 32, 0, s>>>(static_cast<const char *>(src), dsts, dirty,
+                                                                   elem, lo, hi);
+        return cudaGetLastError();
+    }
     merge_range_kernel<<<grid_for((hi - lo) * elem, 256 * 16 * 8, 148 * 16), 256, 0, s>>>(
         static_cast<const char *>(src), dsts, dirty, elem, lo, hi);
     return cudaGetLastError();
