@@ -830,7 +830,7 @@ def merge_probes(J):
         mt = prof(lambda: J.jacc_launch(J.JACC_LOOP_JACOBI2D_F64, rng, args_ab, 0), 6)
         span = ((hi - 1) * N + N - 2) - ((lo + 1) * N + 1) + 1
         byts = 8 * span
-        out["merge_range"] = {"kernel": "merge_range_kernel", "us": mt * 1e6,
+        out["merge_range"] = {"kernel": "merge_range_bulk_kernel", "us": mt * 1e6,
                               "dirty_bytes": byts, "copy_gbs": 2 * byts / mt / 1e9,
                               "frac_of_hbm_copy": 2 * byts / mt / 1e9 / peak,
                               "nvlink_time_at_770_us": byts / (NVLINK_GBS * 1e9) * 1e6}
