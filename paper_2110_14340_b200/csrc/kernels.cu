@@ -892,6 +892,7 @@ __global__ void __launch_bounds__(256) scat_hist_kernel(const int32_t *__restric
         int4 k[4];
 #pragma unroll
         for (int u = 0; u < 4; u++) k[u] = __ldcs(idx4 + q + u * nth);
+        // (the owned test reads every key before any atomic is issued)
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             put(k[u].x);
@@ -1451,12 +1452,21 @@ __global__ void __launch_bounds__(SBITS_T) scat_bits_kernel(const int32_t *__res
             int4 k[SB_U];
 #pragma unroll
             for (int u = 0; u < SB_U; u++) k[u] = __ldcs(k4 + q4 + u * SBITS_T);
+            // the atomics are control-dependent on every key of the batch
+            // (keys are non-negative element indices, so the test always
+            // passes): the scheduler cannot sink later loads below earlier
+            // atomics (it did: 1 load per 4 atomics, bits pass 0.25 -> 0.33 ms)
+            int all = 0;
 #pragma unroll
-            for (int u = 0; u < SB_U; u++) {
-                put(k[u].x);
-                put(k[u].y);
-                put(k[u].z);
-                put(k[u].w);
+            for (int u = 0; u < SB_U; u++) all |= k[u].x | k[u].y | k[u].z | k[u].w;
+            if (all >= 0) {
+#pragma unroll
+                for (int u = 0; u < SB_U; u++) {
+                    put(k[u].x);
+                    put(k[u].y);
+                    put(k[u].z);
+                    put(k[u].w);
+                }
             }
         }
         for (; q4 < n4; q4 += SBITS_T) {
