@@ -1076,7 +1076,13 @@ __global__ void __launch_bounds__(SB_T, MINB) scat_part_kernel(const int32_t *__
 // processing.  The tile is moved from the raw buffer into registers at the
 // top of the iteration, the buffer is refilled with the next tile, and the
 // rest is scat_part_kernel.
-template <typename T, bool BULK = sizeof(T) == 4>
+#ifndef SCAT_PF_PIECE
+#define SCAT_PF_PIECE 65536u      // bulk prefetch piece (bytes)
+#endif
+#ifndef SCAT_PF_BULK_F64
+#define SCAT_PF_BULK_F64 0
+#endif
+template <typename T, bool BULK = (sizeof(T) == 4 || SCAT_PF_BULK_F64)>
 __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__restrict__ idx,
                                                                const T *__restrict__ b, int64_t n,
                                                                int32_t lo, unsigned span, int shift,
@@ -1122,8 +1128,13 @@ __global__ void __launch_bounds__(SB_T, 2) scat_part_pf_kernel(const int32_t *__
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads of raw
             mbar_expect_tx(&pbar, kb + vb);
-            if (kb) bulk_g2s(rk, idx + e0, kb, &pbar);
-            if (vb) bulk_g2s(rv, b + e0, vb, &pbar);
+            // in pieces of at most SCAT_PF_PIECE bytes (several copies in flight)
+            for (unsigned o = 0; o < kb; o += SCAT_PF_PIECE)
+                bulk_g2s(reinterpret_cast<char *>(rk) + o, reinterpret_cast<const char *>(idx + e0) + o,
+                         kb - o < SCAT_PF_PIECE ? kb - o : SCAT_PF_PIECE, &pbar);
+            for (unsigned o = 0; o < vb; o += SCAT_PF_PIECE)
+                bulk_g2s(reinterpret_cast<char *>(rv) + o, reinterpret_cast<const char *>(b + e0) + o,
+                         vb - o < SCAT_PF_PIECE ? vb - o : SCAT_PF_PIECE, &pbar);
         }
         for (int64_t el = kb / 4 + tid; el < left; el += SB_T) rk[el] = idx[e0 + el];
         for (int64_t el = vb / sizeof(T) + tid; el < left; el += SB_T) rv[el] = b[e0 + el];
