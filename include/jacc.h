@@ -77,7 +77,10 @@ int jacc_num_devices(void);
  *   JACC_MERGE_EAGER: after each launch every device pushes its recorded
  *     dirty region of every written array to all other replicas
  *     ("Updated data are sent to all other GPUs after each kernel
- *     execution"; sync at start and end).
+ *     execution"; sync at start and end): a range record
+ *     moves its [min, max] span, a bitmap record its dirty elements, with
+ *     32-element words holding >= 8 dirty elements inside the device's
+ *     owned block moved whole (same values, full sectors; DESIGN R-22).
  *   JACC_MERGE_HALO: push only the dirty rows the neighbouring devices read
  *     in a launch of the same loop shape (the config's boundary-row
  *     dirty-range merge; the paper's manual halo comparison P:909,

@@ -90,3 +90,20 @@ def test_exchange_plan_covers_exactly_the_owned_slice(J, seed):
             assert a % elem == 0 and b % elem == 0
             got.extend(range(a // elem, b // elem))
         assert sorted(got) == want and len(got) == len(set(got))
+
+
+def test_bench_pushed_elements_dense_rule():
+    """bench.py counts the bytes a bitmap merge stores (DESIGN R-22): words
+    with >= 8 dirty elements inside the owned slice move whole, the others
+    element by element, and words straddling the slice edge never whole."""
+    import numpy as np
+    import bench
+    bm = np.zeros(4, dtype=np.uint32)
+    bm[0] = 0xFF          # 8 dirty, inside [0, 100): whole -> 32
+    bm[1] = 0x7F          # 7 dirty: element by element -> 7
+    bm[2] = 0xFFFF        # 16 dirty but word 2 = [64, 96) inside -> 32
+    bm[3] = 0xFFFFFFFF    # 32 dirty, word [96, 128) straddles hi = 100 -> 32 bits counted, not "whole"
+    assert bench._pushed_elements(bm, 0, 100) == 32 + 7 + 32 + 32
+    bm[3] = 0x0F0F        # 8 dirty, straddling: element by element
+    assert bench._pushed_elements(bm, 0, 100) == 32 + 7 + 32 + 8
+    assert bench._pushed_elements(bm, 1, 128) == 8 + 7 + 32 + 32  # word 0 starts before lo
