@@ -143,6 +143,9 @@ __device__ __forceinline__ void jload(JRow<V> &o, const double *__restrict__ src
     o.r = (ok && lane == 31 && cs + 32 * V < N) ? __ldg(p + cs + 32 * V) : 0.0;
 }
 
+#ifndef JACOBI_FAST
+#define JACOBI_FAST 1
+#endif
 template <int V, int JW, int JR, int JPF, int MINB, bool CS = true>
 __global__ void __launch_bounds__(JW * 32, MINB)
     jacobi2d_kernel(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t r0,
@@ -153,17 +156,73 @@ __global__ void __launch_bounds__(JW * 32, MINB)
     const int64_t cs = cs_base + ((int64_t)blockIdx.x * JW + warp) * (32 * V);
     const int64_t j0 = cs + lane * V;
     u64 mn = kU64Max, mx = 0;
+    // Full bands (JR rows) of slabs whose every column is written take an
+    // unrolled path without per-row validity, column, push or dirty
+    // bookkeeping; partial bands and edge slabs take the general loop,
+    // kept rolled so the kernel's code stays small (a second unrolled copy
+    // doubled it past the instruction cache: 0.86-0.99 vs 0.70 ms,
+    // profiles/jacobi_experiments_r02.txt).  Warp-uniform choice.
+    const bool slab_full = JACOBI_FAST && V == 2 && __all_sync(0xffffffffu, j0 >= c0 && j0 + V <= c1);
+    const bool eL = lane == 0 && cs >= 1 && cs < N, eR = lane == 31 && cs + 32 * V < N;
 
     for (int64_t ty = blockIdx.y; ty < ntiles_y; ty += gridDim.y) {
         const int64_t rs = r0 + ty * JR;
         const int64_t re = rs + JR < r1 ? rs + JR : r1;
+        if (slab_full && re - rs == JR) {
+            const double *__restrict__ sp = src + (rs - 1) * N;
+            double *__restrict__ dp = dst + rs * N + j0;
+            JRow<V> q[JPF + 3];
+#pragma unroll
+            for (int t = 0; t < JPF + 3; t++) {
+                const double *p = sp + t * N;
+                const double2 w = __ldg(reinterpret_cast<const double2 *>(p + j0));
+                q[t].v[0] = w.x;
+                q[t].v[V - 1] = w.y;
+                q[t].l = eL ? __ldg(p + cs - 1) : 0.0;
+                q[t].r = eR ? __ldg(p + cs + 32 * V) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < JR; k++) {
+                const JRow<V> &U = q[0], &C = q[1], &D = q[2];
+                const double fromL = __shfl_up_sync(0xffffffffu, C.v[V - 1], 1);
+                const double fromR = __shfl_down_sync(0xffffffffu, C.v[0], 1);
+                double a0 = __dadd_rn(C.v[0], lane > 0 ? fromL : C.l);  // PolyBench order
+                a0 = __dadd_rn(a0, C.v[V - 1]);
+                a0 = __dadd_rn(a0, D.v[0]);
+                a0 = __dadd_rn(a0, U.v[0]);
+                double a1 = __dadd_rn(C.v[V - 1], C.v[0]);
+                a1 = __dadd_rn(a1, lane < 31 ? fromR : C.r);
+                a1 = __dadd_rn(a1, D.v[V - 1]);
+                a1 = __dadd_rn(a1, U.v[V - 1]);
+                const double2 o2 = make_double2(__dmul_rn(0.2, a0), __dmul_rn(0.2, a1));
+                double *dq = dp + (int64_t)k * N;
+                if constexpr (CS) __stcs(reinterpret_cast<double2 *>(dq), o2);
+                else *reinterpret_cast<double2 *>(dq) = o2;
+                if (k == 0 && push_top && rs == r0) *reinterpret_cast<double2 *>(push_top + (dq - dst)) = o2;
+                if (k == JR - 1 && push_bot && re == r1) *reinterpret_cast<double2 *>(push_bot + (dq - dst)) = o2;
+#pragma unroll
+                for (int t = 0; t < JPF + 2; t++) q[t] = q[t + 1];
+                if (k + JPF + 2 <= JR) {
+                    const double *p = sp + (int64_t)(k + JPF + 3) * N;
+                    const double2 w = __ldg(reinterpret_cast<const double2 *>(p + j0));
+                    q[JPF + 2].v[0] = w.x;
+                    q[JPF + 2].v[V - 1] = w.y;
+                    q[JPF + 2].l = eL ? __ldg(p + cs - 1) : 0.0;
+                    q[JPF + 2].r = eR ? __ldg(p + cs + 32 * V) : 0.0;
+                }
+            }
+            const u64 f0 = (u64)(rs * N + j0), f1 = (u64)((re - 1) * N + j0 + V - 1);
+            mn = f0 < mn ? f0 : mn;
+            mx = f1 > mx ? f1 : mx;
+            continue;
+        }
         // rows needed: rs-1 .. re (re <= r1 <= N-1 exists)
         JRow<V> q[JPF + 3];
 #pragma unroll
         for (int t = 0; t < JPF + 3; t++)
             jload<V>(q[t], src, N, rs - 1 + t, j0, cs, lane, rs - 1 + t <= re);
 
-#pragma unroll
+#pragma unroll 1
         for (int k = 0; k < JR; k++) {
             const int64_t i = rs + k;
             if (i >= re) break;
