@@ -104,5 +104,8 @@ def test_multiprocess_random_programs(world):
            os.path.join(ROOT, "tests", "workers", "mp_random.py"), "--seeds", "24",
            "--first", str(5000 + 100 * world)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    # the first failing rank's own error (the others then time out waiting
+    # for it): every line that names an error, before the tail
+    first = [l for l in r.stderr.splitlines() if "Error" in l or "assert" in l or "mismatch" in l][:40]
+    assert r.returncode == 0, "\n".join(first) + "\n...\n" + r.stdout[-2000:] + r.stderr[-2000:]
     assert r.stdout.count("ok 24") == world
